@@ -1,0 +1,153 @@
+/*
+ * pcf_sort.h -- C ABI of libpcfsort.so, the B200 (sm_100a) PCF Learned Sort.
+ *
+ * The library sorts an array of 8-byte keys on one GPU with PCF Learned Sort
+ * (Sato & Matsui, arXiv 2405.07122): Algorithm 1 "Learned-Sort"
+ * with the piecewise-constant CDF model of §3.2
+ * and alpha = beta = gamma = delta = floor(n^{3/4})
+ * (Theorems 1-2).  Silent points of the paper are resolved
+ * as listed in DESIGN.md §2 (readings R1-R16); the result is bit-identical to
+ * the CPU oracle in oracle/ (tests/test_gpu_parity.py), including every
+ * per-node bucket histogram when the pass log is enabled.
+ *
+ * Signatures use plain pointers and sizes only.  "device" pointers are CUDA
+ * device (or managed) memory of the current device; "host" pointers are
+ * ordinary host memory.  `stream` is a cudaStream_t passed as void* (NULL =
+ * the legacy default stream).  All functions are thread-safe for distinct
+ * streams; the library keeps no global state besides a thread-local error
+ * string.
+ */
+#ifndef PCF_SORT_H
+#define PCF_SORT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCF_ABI_VERSION 1
+
+/* ---- status codes (every entry point returns one) ---------------------- */
+#define PCF_OK 0
+#define PCF_ERR_INVALID_ARG 1          /* NULL with n>0, tau<2, bad overlap, n > 2^40, bad struct_size */
+#define PCF_ERR_NAN 2                  /* f64 input contains a NaN (domain error)         */
+#define PCF_ERR_WORKSPACE_TOO_SMALL 3  /* caller workspace smaller than pcf_workspace_bytes()          */
+#define PCF_ERR_OOM 4                  /* device allocation failed                                     */
+#define PCF_ERR_CUDA 5                 /* a CUDA runtime call failed (see pcf_last_error())            */
+#define PCF_ERR_LOG_OVERFLOW 6         /* pass log capacity exceeded (records beyond capacity dropped) */
+#define PCF_ERR_INTERNAL 7             /* internal capacity bound violated (bug)                       */
+
+/* ---- key types ---------------------------------------------------------- */
+#define PCF_KEY_F64 0   /* IEEE binary64, ascending under IEEE-754 totalOrder (-0.0 before +0.0) */
+#define PCF_KEY_U64 1   /* uint64_t, ascending numeric order                                      */
+
+/* ---- flags -------------------------------------------------------------- */
+#define PCF_FLAG_SYNC       1u  /* synchronise the stream before returning and report NaN/overflow */
+#define PCF_FLAG_SAMPLE_ALL 2u  /* test mode (reading R14): sample = whole segment, alpha = m      */
+#define PCF_FLAG_TIMING     4u  /* record CUDA events per phase into stats->phase_ms (implies SYNC) */
+
+/* One record per bucketing node, i.e. per call of Alg. 1 that reaches its
+ * model-based bucketing step.  Identical layout to the
+ * oracle's record; compared after sorting by (level, offset). */
+typedef struct pcf_node_record {
+    uint32_t level;       /* recursion level, 1 = whole array                       */
+    uint32_t alpha;       /* sample size alpha (= beta = gamma = delta unless R14)   */
+    uint64_t offset;      /* global offset of the segment in the array               */
+    uint64_t m;           /* segment length                                          */
+    uint64_t xmin_bits;   /* bit pattern of x_min, totalOrder min     */
+    uint64_t xmax_bits;   /* bit pattern of x_max                                    */
+    uint64_t digest_b;    /* digest of b[1..beta+1]               */
+    uint64_t digest_h;    /* digest of H[1..gamma+1]  (bucket sizes |c_j|)           */
+    uint32_t n_fallback;  /* non-empty buckets with |c_j| >= delta    */
+    uint32_t n_small;     /* non-empty buckets with |c_j| < delta and < tau          */
+    uint32_t n_recurse;   /* non-empty buckets with tau <= |c_j| < delta             */
+    uint32_t reserved;
+} pcf_node_record;        /* 72 bytes */
+
+/* Optional pass log (parity / debugging).  All buffers are DEVICE memory
+ * owned by the caller.  Off when params->log == NULL. */
+typedef struct pcf_pass_log {
+    pcf_node_record *records;  /* device array of `capacity` records, unordered      */
+    uint64_t capacity;
+    uint64_t *count;           /* device u64, set to the number of records produced  */
+    uint32_t *level1_b;        /* device, level-1 b[1..beta+1] (0-based), or NULL    */
+    uint32_t *level1_h;        /* device, level-1 H[1..gamma+1] (0-based), or NULL   */
+    uint64_t level1_capacity;  /* entries available in level1_b / level1_h           */
+} pcf_pass_log;
+
+/* Host-side statistics, filled when params->stats != NULL and the call is
+ * synchronous (PCF_FLAG_SYNC or PCF_FLAG_TIMING). */
+#define PCF_PHASES 8
+typedef struct pcf_stats {
+    uint32_t kernel_launches;  /* kernels this call launched                                  */
+    uint32_t rounds;           /* device work rounds (global bucketing / split waves)        */
+    uint32_t host_syncs;       /* stream synchronisations performed inside the call          */
+    uint32_t reserved;
+    uint64_t groups_smem;      /* bucket groups finished in shared memory (K7 tasks)         */
+    uint64_t split_tasks;      /* oversized groups re-partitioned in global memory            */
+    uint64_t global_nodes;     /* bucketing nodes run by the global (multi-CTA) path          */
+    uint64_t fallback_keys_global; /* keys sorted by the global fallback sort               */
+    /* PCF_FLAG_TIMING: milliseconds per phase, CUDA events on `stream`:
+     * [0] min/max  [1] sample+fit  [2] classify+histogram  [3] stable scatter
+     * [4] smem subtree (K7)  [5] global fallback sort  [6] other  [7] total */
+    float phase_ms[PCF_PHASES];
+    uint64_t phase_bytes[PCF_PHASES];  /* algorithmic bytes per phase */
+} pcf_stats;
+
+typedef struct pcf_params {
+    uint32_t struct_size;      /* = sizeof(pcf_params); set by pcf_params_init             */
+    uint32_t tau;              /* base-case threshold tau (reading R1), >= 2; default 64   */
+    uint64_t seed;             /* sampler seed (reading R3); default 0                     */
+    uint32_t flags;            /* PCF_FLAG_*; default PCF_FLAG_SYNC                        */
+    uint32_t reserved0;
+    void *workspace;           /* device scratch, >= pcf_workspace_bytes(); NULL = the      */
+    size_t workspace_bytes;    /*   library allocates stream-ordered (cudaMallocAsync)     */
+    pcf_pass_log *log;         /* host struct pointing at device buffers, or NULL          */
+    pcf_stats *stats;          /* host struct, or NULL                                     */
+} pcf_params;
+
+/* Fill *p with the defaults above.  Never fails. */
+void pcf_params_init(pcf_params *p);
+
+/* Upper bound on the device scratch one sort of n keys of `key_type` needs
+ * with parameters p (NULL = defaults): one n-key buffer plus the PCF tables,
+ * histograms and work queues.  Pure host arithmetic; no CUDA call. */
+size_t pcf_workspace_bytes(size_t n, int key_type, const pcf_params *p);
+
+/* Sort n keys.  in/out: DEVICE pointers to n contiguous keys, 8-byte aligned.
+ * `in` is never written unless in == out (in-place is allowed); any other
+ * overlap of [in, in+n) and [out, out+n) is PCF_ERR_INVALID_ARG.  `out` is
+ * fully overwritten with the ascending permutation of `in`.
+ * Errors: argument errors return before any launch.  NaN (f64) is detected on
+ * the device by the first pass; later kernels do no work; with PCF_FLAG_SYNC the
+ * call returns PCF_ERR_NAN (out unspecified), otherwise PCF_OK is returned
+ * after enqueueing and the NaN is only visible through a later synchronous call
+ * (asynchronous error reporting is not provided in ABI v1).
+ * Without PCF_FLAG_SYNC the call may still synchronise internally when the
+ * input needs more than one global bucketing round (skewed data); see
+ * DESIGN.md §5. */
+int pcf_sort_f64(const double *in, double *out, size_t n, const pcf_params *p, void *stream);
+int pcf_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const pcf_params *p, void *stream);
+
+/* End-to-end entry: HOST pointers (pinned memory recommended).  Copies the n
+ * keys to the device, sorts them with pcf_sort_*, copies the result back and
+ * synchronises `stream`.  Device buffers are stream-ordered allocations freed
+ * before return.  in_host == out_host is allowed. */
+int pcf_sort_f64_host(const double *in_host, double *out_host, size_t n, const pcf_params *p, void *stream);
+int pcf_sort_u64_host(const uint64_t *in_host, uint64_t *out_host, size_t n, const pcf_params *p, void *stream);
+
+/* Human-readable name of a status code (static storage). */
+const char *pcf_status_string(int status);
+
+/* Detail of the last error on the calling thread (static thread-local storage). */
+const char *pcf_last_error(void);
+
+/* ABI version of the loaded library (PCF_ABI_VERSION it was built with). */
+int pcf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCF_SORT_H */

@@ -1,0 +1,224 @@
+"""paper_2405_07122_b200 -- B200-native PCF Learned Sort (arXiv 2405.07122).
+
+Thin ctypes binding over ``libpcfsort.so`` (C ABI in ``include/pcf_sort.h``).
+Argument marshalling only: every step of the sort runs in the library's CUDA
+kernels.  PyTorch is used for device memory and streams.  There is no CPU
+fallback: if the extension is missing or no GPU is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from ._build import LIB_PATH, build  # noqa: F401
+
+__all__ = ["build", "lib", "sort", "sort_host", "workspace_bytes", "PCFError", "KEY_F64", "KEY_U64",
+           "FLAG_SYNC", "FLAG_SAMPLE_ALL", "FLAG_TIMING", "PHASES"]
+
+KEY_F64, KEY_U64 = 0, 1
+FLAG_SYNC, FLAG_SAMPLE_ALL, FLAG_TIMING = 1, 2, 4
+PHASES = ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "total"]
+STATUS = {0: "PCF_OK", 1: "PCF_ERR_INVALID_ARG", 2: "PCF_ERR_NAN", 3: "PCF_ERR_WORKSPACE_TOO_SMALL",
+          4: "PCF_ERR_OOM", 5: "PCF_ERR_CUDA", 6: "PCF_ERR_LOG_OVERFLOW", 7: "PCF_ERR_INTERNAL"}
+
+
+class NodeRecord(ctypes.Structure):
+    _fields_ = [("level", ctypes.c_uint32), ("alpha", ctypes.c_uint32),
+                ("offset", ctypes.c_uint64), ("m", ctypes.c_uint64),
+                ("xmin_bits", ctypes.c_uint64), ("xmax_bits", ctypes.c_uint64),
+                ("digest_b", ctypes.c_uint64), ("digest_h", ctypes.c_uint64),
+                ("n_fallback", ctypes.c_uint32), ("n_small", ctypes.c_uint32),
+                ("n_recurse", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+class PassLog(ctypes.Structure):
+    _fields_ = [("records", ctypes.c_void_p), ("capacity", ctypes.c_uint64),
+                ("count", ctypes.c_void_p), ("level1_b", ctypes.c_void_p),
+                ("level1_h", ctypes.c_void_p), ("level1_capacity", ctypes.c_uint64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("kernel_launches", ctypes.c_uint32), ("rounds", ctypes.c_uint32),
+                ("host_syncs", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("groups_smem", ctypes.c_uint64), ("split_tasks", ctypes.c_uint64),
+                ("global_nodes", ctypes.c_uint64), ("fallback_keys_global", ctypes.c_uint64),
+                ("phase_ms", ctypes.c_float * 8), ("phase_bytes", ctypes.c_uint64 * 8)]
+
+    def as_dict(self):
+        return {"kernel_launches": self.kernel_launches, "rounds": self.rounds,
+                "host_syncs": self.host_syncs, "groups_smem": self.groups_smem,
+                "split_tasks": self.split_tasks, "global_nodes": self.global_nodes,
+                "fallback_keys_global": self.fallback_keys_global,
+                "phase_ms": {PHASES[i]: float(self.phase_ms[i]) for i in range(8)},
+                "phase_bytes": {PHASES[i]: int(self.phase_bytes[i]) for i in range(8)}}
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("tau", ctypes.c_uint32),
+                ("seed", ctypes.c_uint64), ("flags", ctypes.c_uint32), ("reserved0", ctypes.c_uint32),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("log", ctypes.POINTER(PassLog)), ("stats", ctypes.POINTER(Stats))]
+
+
+class PCFError(RuntimeError):
+    def __init__(self, status: int, detail: str = ""):
+        super().__init__(f"{STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+_lib = None
+SYMBOLS = ["pcf_params_init", "pcf_workspace_bytes", "pcf_sort_f64", "pcf_sort_u64", "pcf_sort_f64_host",
+           "pcf_sort_u64_host", "pcf_status_string", "pcf_last_error", "pcf_abi_version"]
+
+
+def lib():
+    """Load libpcfsort.so (built in-tree by ``build()``); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run __graft_entry__.build() "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, sz, i32, u32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32
+        PP = ctypes.POINTER(Params)
+        L.pcf_params_init.argtypes = [PP]; L.pcf_params_init.restype = None
+        L.pcf_workspace_bytes.argtypes = [sz, i32, PP]; L.pcf_workspace_bytes.restype = sz
+        for name in ["pcf_sort_f64", "pcf_sort_u64", "pcf_sort_f64_host", "pcf_sort_u64_host"]:
+            f = getattr(L, name)
+            f.argtypes = [vp, vp, sz, PP, vp]
+            f.restype = i32
+        L.pcf_status_string.argtypes = [i32]; L.pcf_status_string.restype = ctypes.c_char_p
+        L.pcf_last_error.argtypes = []; L.pcf_last_error.restype = ctypes.c_char_p
+        L.pcf_abi_version.argtypes = []; L.pcf_abi_version.restype = i32
+        _ = u32
+        _lib = L
+    return _lib
+
+
+def make_params(tau: int = 64, seed: int = 0, flags: int = FLAG_SYNC, workspace=None, workspace_bytes=0):
+    p = Params()
+    lib().pcf_params_init(ctypes.byref(p))
+    p.tau, p.seed, p.flags = tau, seed, flags
+    if workspace is not None:
+        p.workspace, p.workspace_bytes = workspace, workspace_bytes
+    return p
+
+
+def workspace_bytes(n: int, key_type: int = KEY_F64) -> int:
+    return int(lib().pcf_workspace_bytes(n, key_type, None))
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise PCFError(rc, lib().pcf_last_error().decode())
+
+
+class SortInfo:
+    """Pass log (node records, level-1 b/H) and statistics of one sort."""
+
+    def __init__(self):
+        self.nodes = None
+        self.level1_b = None
+        self.level1_h = None
+        self.stats = None
+
+
+def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False, log: bool = False,
+         timing: bool = False, stats: bool = False, sync: bool = True, workspace=None, node_capacity=None,
+         stream=None):
+    """Sort a 1-D CUDA tensor of float64 or uint64 keys ascending (totalOrder for f64).
+
+    Returns ``out`` (a new tensor unless given; ``out is x`` sorts in place), or
+    ``(out, SortInfo)`` when ``log``/``timing``/``stats`` is requested.
+    """
+    import torch
+
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError("x must be a CUDA tensor (no CPU fallback)")
+    if x.dtype == torch.float64:
+        fn, kt = lib().pcf_sort_f64, KEY_F64
+    elif x.dtype == torch.uint64:
+        fn, kt = lib().pcf_sort_u64, KEY_U64
+    else:
+        raise TypeError(f"keys must be float64 or uint64, got {x.dtype}")
+    if x.dim() != 1 or not x.is_contiguous():
+        raise ValueError("x must be a contiguous 1-D tensor")
+    n = x.numel()
+    if out is None:
+        out = torch.empty_like(x)
+    flags = (FLAG_SYNC if sync else 0) | (FLAG_SAMPLE_ALL if sample_all else 0) | (FLAG_TIMING if timing else 0)
+    p = make_params(tau, seed, flags)
+    if workspace is not None:
+        p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    info = SortInfo() if (log or timing or stats) else None
+    keep = []
+    if log:
+        cap = node_capacity if node_capacity is not None else max(64, n // 8 + 64)
+        recs = torch.zeros(cap * 9, dtype=torch.int64, device=x.device)   # 72-byte records
+        cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
+        from math import isqrt
+        l1 = 2
+        if n:
+            # floor(n^{3/4}) + 2 upper bound without the library: isqrt(isqrt(n^3)) + 2
+            l1 = isqrt(isqrt(n ** 3)) + 2
+        b = torch.zeros(l1, dtype=torch.int32, device=x.device)
+        h = torch.zeros(l1, dtype=torch.int32, device=x.device)
+        pl = PassLog(recs.data_ptr(), cap, cnt.data_ptr(), b.data_ptr(), h.data_ptr(), l1)
+        p.log = ctypes.pointer(pl)
+        keep += [recs, cnt, b, h, pl]
+    st = Stats()
+    if info is not None:
+        p.stats = ctypes.pointer(st)
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    with torch.cuda.device(x.device):
+        rc = fn(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), n, ctypes.byref(p),
+                ctypes.c_void_p(s.cuda_stream))
+    _check(rc)
+    if info is None:
+        return out
+    info.stats = st.as_dict()
+    if log:
+        import numpy as np
+        k = int(cnt.item())
+        arr = recs.view(torch.uint8).cpu().numpy().view(np.uint8)[: k * 72]
+        info.nodes = np.frombuffer(arr.tobytes(), dtype=NODE_DTYPE()).copy()
+        info.level1_b = b.cpu().numpy().view(np.uint32)
+        info.level1_h = h.cpu().numpy().view(np.uint32)
+    return out, info
+
+
+def NODE_DTYPE():
+    import numpy as np
+    return np.dtype([("level", "<u4"), ("alpha", "<u4"), ("offset", "<u8"), ("m", "<u8"),
+                     ("xmin_bits", "<u8"), ("xmax_bits", "<u8"), ("digest_b", "<u8"),
+                     ("digest_h", "<u8"), ("n_fallback", "<u4"), ("n_small", "<u4"),
+                     ("n_recurse", "<u4"), ("reserved", "<u4")])
+
+
+def sort_host(x, out=None, *, tau: int = 64, seed: int = 0, stream=None):
+    """End-to-end sort of HOST keys (numpy array or CPU tensor; pinned recommended)
+    through ``pcf_sort_*_host``: H2D copy, device sort, D2H copy, synchronise."""
+    import numpy as np
+    import torch
+
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda:
+            raise TypeError("sort_host expects host memory")
+        ptr, n, dt = x.data_ptr(), x.numel(), x.dtype
+        is_f64 = dt == torch.float64
+        if out is None:
+            out = torch.empty_like(x)
+        optr = out.data_ptr()
+    else:
+        x = np.ascontiguousarray(x)
+        ptr, n = x.ctypes.data, x.size
+        is_f64 = x.dtype == np.float64
+        if out is None:
+            out = np.empty_like(x)
+        optr = out.ctypes.data
+    fn = lib().pcf_sort_f64_host if is_f64 else lib().pcf_sort_u64_host
+    p = make_params(tau, seed, FLAG_SYNC)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    rc = fn(ctypes.c_void_p(ptr), ctypes.c_void_p(optr), n, ctypes.byref(p), ctypes.c_void_p(s.cuda_stream))
+    _check(rc)
+    return out

@@ -1,0 +1,585 @@
+// pcf_api.cu -- host orchestration and the C ABI of libpcfsort.so (include/pcf_sort.h).
+//
+// Call structure for one sort of n keys:
+//   n <= S_CAP          one K7 task: the whole Algorithm 1 in one CTA's shared memory.
+//   n >  S_CAP          level-1 node on the global path: k_minmax -> k_node_model ->
+//                       k_fit_sample -> k_fit_scan, then split rounds (count, scan,
+//                       scatter, taskgen) until every group fits a K7 CTA; oversized
+//                       recursing buckets become new global nodes (next round);
+//                       then one persistent K7 launch over all groups; K8 for buckets
+//                       that Alg. 1 sends to Standard-Sort and that exceed S_CAP.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pcf_sort.h"
+#include "pcf_common.cuh"
+#include "pcf_global.cuh"
+#include "pcf_k7.cuh"
+#include "pcf_k8.cuh"
+
+namespace pcf {
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            return fail(PCF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+        }                                                                                          \
+    } while (0)
+
+static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- capacities
+struct Caps {
+    u64 n;
+    u32 P;            // iroot34(n)
+    u32 node_cap;
+    u64 arena_u32;
+    u32 k7_cap;
+    u32 split_cap;
+    u32 items_cap;
+    u64 cmat_cap;     // entries of the C / P count matrices
+    u64 bsum_cap;
+};
+
+static Caps caps_for(u64 n) {
+    Caps c;
+    c.n = n;
+    c.P = (u32)iroot34(n);
+    c.node_cap = (u32)(n / S_CAP + 2);
+    // root tables + every oversized node: sum of 3*(m^{3/4}+2) over disjoint m > S_CAP
+    // is <= 3*(n^{3/4} + n / S_CAP^{1/4} + 2*node_cap)  (S_CAP^{1/4} > 9.5)
+    c.arena_u32 = 3ull * ((u64)c.P + 2) + 3ull * (n * 2 / 19 + 2ull * c.node_cap) + 64;
+    c.k7_cap = (u32)std::min<u64>(n / 32 + 65536, 0xffffffffull);
+    c.split_cap = (u32)(n / 1024 + 4096);
+    c.items_cap = (u32)(n / S_CAP + 64);
+    c.cmat_cap = (n / SPLIT_TILE + 64) * (u64)GMAX;
+    c.bsum_cap = c.cmat_cap / SCAN_CHUNK + 2;
+    return c;
+}
+
+struct Counters {             // zeroed at the start of every call
+    u32 nan_flag, err_flag, k7_count, k7_next;
+    u32 nsplits_out, nitems, pad0, pad1;
+    unsigned long long rec_count, k7_keys;
+};
+
+struct Layout {
+    size_t ctx, counters, tmp, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
+};
+
+static Layout layout_for(const Caps &c) {
+    Layout L;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    L.ctx = take(sizeof(DevCtx));
+    L.counters = take(sizeof(Counters));
+    L.tmp = take(c.n * 8);
+    L.nodes = take((size_t)c.node_cap * sizeof(GNode));
+    L.acc = take((size_t)c.node_cap * sizeof(NodeAcc));
+    L.arena = take(c.arena_u32 * 4);
+    L.k7 = take((size_t)c.k7_cap * sizeof(K7Task));
+    L.splits_a = take((size_t)c.split_cap * sizeof(SplitTask));
+    L.splits_b = take((size_t)c.split_cap * sizeof(SplitTask));
+    L.items = take((size_t)c.items_cap * sizeof(SegItem));
+    L.cmat = take(c.cmat_cap * 4);
+    L.pmat = take(c.cmat_cap * 4);
+    L.bsum = take(c.bsum_cap * 4);
+    L.total = off;
+    return L;
+}
+
+static size_t small_layout_bytes() {
+    // n <= S_CAP: ctx + counters + one K7 task
+    return align_up(sizeof(DevCtx), 256) + align_up(sizeof(Counters), 256) + align_up(sizeof(K7Task), 256);
+}
+
+static size_t workspace_bytes_impl(size_t n) {
+    if (n == 0) return 0;
+    if (n <= (size_t)S_CAP) return small_layout_bytes();
+    return layout_for(caps_for(n)).total;
+}
+
+// ---------------------------------------------------------------- phase timer
+struct PhaseTimer {
+    bool on = false;
+    cudaStream_t st;
+    struct Ev { int phase; cudaEvent_t a, b; };
+    std::vector<Ev> evs;
+    int cur = -1;
+    cudaEvent_t cur_a = nullptr;
+    void begin(int phase) {
+        if (!on) return;
+        cudaEvent_t a;
+        cudaEventCreate(&a);
+        cudaEventRecord(a, st);
+        cur = phase;
+        cur_a = a;
+    }
+    void end() {
+        if (!on || cur < 0) return;
+        cudaEvent_t b;
+        cudaEventCreate(&b);
+        cudaEventRecord(b, st);
+        evs.push_back({cur, cur_a, b});
+        cur = -1;
+    }
+    void collect(float *ms) {
+        for (auto &e : evs) {
+            float t = 0;
+            cudaEventElapsedTime(&t, e.a, e.b);
+            ms[e.phase] += t;
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        evs.clear();
+    }
+};
+
+enum { PH_MINMAX = 0, PH_FIT = 1, PH_COUNT = 2, PH_SCATTER = 3, PH_K7 = 4, PH_K8 = 5, PH_OTHER = 6, PH_TOTAL = 7 };
+
+static int k7_smem_bytes() { return (int)sizeof(K7Smem); }
+static int split_smem_bytes() { return (int)sizeof(SplitScatterSmem); }
+
+template <class K>
+static int configure_kernels() {
+    static thread_local bool done = false;
+    if (done) return PCF_OK;
+    CK(cudaFuncSetAttribute(k7_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7_smem_bytes()));
+    CK(cudaFuncSetAttribute(k_split_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
+    done = true;
+    return PCF_OK;
+}
+
+// ---------------------------------------------------------------- the sort
+template <class K>
+static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, cudaStream_t st) {
+    pcf_params p;
+    pcf_params_init(&p);
+    if (pp) {
+        if (pp->struct_size < sizeof(pcf_params)) return fail(PCF_ERR_INVALID_ARG, "pcf_params.struct_size too small");
+        p = *pp;
+    }
+    if (p.tau < 2) return fail(PCF_ERR_INVALID_ARG, "tau must be >= 2");
+    if (n == 0) return PCF_OK;
+    if (!in || !out) return fail(PCF_ERR_INVALID_ARG, "NULL key pointer with n > 0");
+    if (n >= (1ull << 32)) return fail(PCF_ERR_INVALID_ARG, "n must be < 2^32 in ABI v1");
+    if (((uintptr_t)in & 7) || ((uintptr_t)out & 7)) return fail(PCF_ERR_INVALID_ARG, "keys must be 8-byte aligned");
+    if (in != out) {
+        uintptr_t a0 = (uintptr_t)in, a1 = a0 + n * 8, b0 = (uintptr_t)out, b1 = b0 + n * 8;
+        if (a0 < b1 && b0 < a1) return fail(PCF_ERR_INVALID_ARG, "in and out overlap (only in == out is allowed)");
+    }
+    int rc = configure_kernels<K>();
+    if (rc) return rc;
+
+    const bool timing = (p.flags & PCF_FLAG_TIMING) != 0;
+    const bool sync = timing || (p.flags & PCF_FLAG_SYNC) != 0;
+    const bool logging = p.log != nullptr;
+    pcf_stats stats;
+    memset(&stats, 0, sizeof stats);
+    PhaseTimer tm;
+    tm.on = timing;
+    tm.st = st;
+    cudaEvent_t ev_total0 = nullptr, ev_total1 = nullptr;
+    if (timing) {
+        cudaEventCreate(&ev_total0);
+        cudaEventCreate(&ev_total1);
+        cudaEventRecord(ev_total0, st);
+    }
+
+    const size_t need = workspace_bytes_impl(n);
+    char *ws = (char *)p.workspace;
+    bool own = false;
+    if (ws) {
+        if (p.workspace_bytes < need) return fail(PCF_ERR_WORKSPACE_TOO_SMALL, "workspace smaller than pcf_workspace_bytes()");
+        if ((uintptr_t)ws & 255) return fail(PCF_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+    } else {
+        cudaError_t e = cudaMallocAsync((void **)&ws, need, st);
+        if (e != cudaSuccess) { cudaGetLastError(); return fail(PCF_ERR_OOM, "cudaMallocAsync workspace failed"); }
+        own = true;
+    }
+    struct Freer {
+        bool own; char *ws; cudaStream_t st;
+        ~Freer() { if (own) cudaFreeAsync(ws, st); }
+    } freer{own, ws, st};
+
+    DevCtx hc;
+    memset(&hc, 0, sizeof hc);
+    hc.buf[0] = const_cast<u64 *>(in);
+    hc.buf[2] = out;
+    hc.n = n;
+    hc.seed = p.seed;
+    hc.tau = p.tau;
+    hc.flags = p.flags;
+    if (logging) {
+        hc.rec = reinterpret_cast<NodeRec *>(p.log->records);
+        hc.rec_cap = p.log->records ? p.log->capacity : 0;
+        hc.l1_b = p.log->level1_b;
+        hc.l1_h = p.log->level1_h;
+        hc.l1_cap = p.log->level1_capacity;
+        if (!p.log->count) return fail(PCF_ERR_INVALID_ARG, "pass log needs a count pointer");
+        hc.rec_count = reinterpret_cast<unsigned long long *>(p.log->count);
+        if (!hc.rec) hc.rec = reinterpret_cast<NodeRec *>(1);   // non-null marks logging on; cap 0
+        CK(cudaMemsetAsync(p.log->count, 0, 8, st));
+    }
+
+    const bool small = n <= (size_t)S_CAP;
+    DevCtx *d_ctx;
+    Counters *d_cnt;
+    Caps caps;
+    Layout L;
+    memset(&L, 0, sizeof L);
+    if (small) {
+        d_ctx = (DevCtx *)ws;
+        d_cnt = (Counters *)(ws + align_up(sizeof(DevCtx), 256));
+        K7Task *d_task = (K7Task *)(ws + align_up(sizeof(DevCtx), 256) + align_up(sizeof(Counters), 256));
+        hc.k7 = d_task;
+        hc.k7_cap = 1;
+        hc.buf[1] = nullptr;
+    } else {
+        caps = caps_for(n);
+        L = layout_for(caps);
+        d_ctx = (DevCtx *)(ws + L.ctx);
+        d_cnt = (Counters *)(ws + L.counters);
+        hc.buf[1] = (u64 *)(ws + L.tmp);
+        hc.nodes = (GNode *)(ws + L.nodes);
+        hc.k7 = (K7Task *)(ws + L.k7);
+        hc.k7_cap = caps.k7_cap;
+        hc.splits_out = (SplitTask *)(ws + L.splits_b);
+        hc.splits_cap = caps.split_cap;
+        hc.items = (SegItem *)(ws + L.items);
+        hc.items_cap = caps.items_cap;
+    }
+    hc.nan_flag = &d_cnt->nan_flag;
+    hc.err_flag = &d_cnt->err_flag;
+    hc.k7_count = &d_cnt->k7_count;
+    hc.k7_next = &d_cnt->k7_next;
+    hc.nsplits_out = &d_cnt->nsplits_out;
+    hc.nitems = &d_cnt->nitems;
+    hc.k7_keys = &d_cnt->k7_keys;
+    if (!logging) hc.rec_count = &d_cnt->rec_count;
+    CK(cudaMemcpyAsync(d_ctx, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d_cnt, 0, sizeof(Counters), st));
+
+    const bool sample_all = (p.flags & PCF_FLAG_SAMPLE_ALL) != 0;
+    u32 launches = 0;
+    int status = PCF_OK;
+    std::vector<SegItem> fallbacks;
+    u64 k7_tasks = 0;
+    u64 bytes[PCF_PHASES] = {0};
+    std::vector<u32> global_nodes;   // indices (for the pass-log finalisation)
+
+    if (small) {
+        K7Task t;
+        memset(&t, 0, sizeof t);
+        t.off = 0; t.size = (u32)n; t.kind = K7_NODE; t.src = 0; t.level = 1;
+        CK(cudaMemcpyAsync(hc.k7, &t, sizeof t, cudaMemcpyHostToDevice, st));
+        u32 one = 1;
+        CK(cudaMemcpyAsync(&d_cnt->k7_count, &one, 4, cudaMemcpyHostToDevice, st));
+        tm.begin(PH_K7);
+        k7_kernel<K><<<1, K7_THREADS, k7_smem_bytes(), st>>>(d_ctx);
+        CK(cudaGetLastError());
+        tm.end();
+        launches++;
+        k7_tasks = 1;
+        bytes[PH_K7] += 16ull * n;
+    } else {
+        // ------------------------------------------------ global nodes
+        u64 arena_used = 0;
+        u32 *arena = (u32 *)(ws + L.arena);
+        u32 node_count = 0;
+        std::vector<SplitTask> list;
+        auto add_node = [&](u64 off, u32 m, u32 level, u32 src) -> int {
+            if (node_count >= caps.node_cap) return fail(PCF_ERR_INTERNAL, "global node capacity exceeded");
+            GNode g;
+            memset(&g, 0, sizeof g);
+            u32 P = (u32)iroot34(m);
+            g.off = off; g.m = m; g.level = level;
+            g.kmin = ~0ull; g.kmax = 0;
+            g.alpha = sample_all ? m : P; g.beta = P; g.gamma = P; g.delta = P;
+            g.src = src;
+            u64 need_u32 = 3ull * ((u64)P + 2);
+            if (arena_used + need_u32 > caps.arena_u32) return fail(PCF_ERR_INTERNAL, "node table arena exceeded");
+            g.cnt = arena + arena_used;
+            g.T = g.cnt + (P + 2);
+            g.H = g.T + (P + 2);
+            arena_used += need_u32;
+            u32 idx = node_count++;
+            CK(cudaMemcpyAsync(hc.nodes + idx, &g, sizeof g, cudaMemcpyHostToDevice, st));
+            CK(cudaMemsetAsync(g.cnt, 0, need_u32 * 4, st));
+            const DevCtx *dc = d_ctx;
+            tm.begin(PH_MINMAX);
+            u64 nvec = m / 2 + 1;
+            u32 grid = (u32)std::min<u64>(148ull * 8, (nvec + MM_THREADS * MM_UNROLL - 1) / (MM_THREADS * MM_UNROLL));
+            k_minmax<K><<<grid, MM_THREADS, 0, st>>>(dc, idx);
+            tm.end();
+            tm.begin(PH_FIT);
+            k_node_model<K><<<1, 1, 0, st>>>(dc, idx);
+            u32 alpha = g.alpha;
+            k_fit_sample<K><<<(alpha + 255) / 256, 256, 0, st>>>(dc, idx);
+            k_fit_scan<<<1, 1024, 0, st>>>(dc, idx);
+            tm.end();
+            CK(cudaGetLastError());
+            launches += 4;
+            bytes[PH_MINMAX] += 8ull * m;
+            bytes[PH_FIT] += 8ull * alpha + 8ull * (P + 2);
+            stats.global_nodes++;
+            global_nodes.push_back(idx);
+            SplitTask s;
+            memset(&s, 0, sizeof s);
+            s.off = off; s.m = m; s.node = idx; s.jlo = 1; s.jhi = P + 2;
+            s.shift = choose_shift(P + 1, m);
+            s.G = (P + 1 + (1u << s.shift) - 1) >> s.shift;
+            s.src = src; s.dst = src == 1 ? 2 : 1;
+            list.push_back(s);
+            return PCF_OK;
+        };
+        rc = add_node(0, (u32)n, 1, 0);
+        if (rc) return rc;
+
+        SplitTask *d_list = (SplitTask *)(ws + L.splits_a);
+        u32 *d_C = (u32 *)(ws + L.cmat), *d_P = (u32 *)(ws + L.pmat), *d_bsum = (u32 *)(ws + L.bsum);
+        u32 round = 0;
+        while (!list.empty()) {
+            round++;
+            // launch the list in batches whose count matrices fit
+            size_t i0 = 0;
+            while (i0 < list.size()) {
+                u64 ctot = 0, mtot = 0;
+                u32 tiles = 0;
+                size_t i1 = i0;
+                while (i1 < list.size()) {
+                    SplitTask &s = list[i1];
+                    u32 nt = (s.m + SPLIT_TILE - 1) / SPLIT_TILE;
+                    u64 need_c = (u64)nt * s.G;
+                    if (i1 > i0 && ctot + need_c > caps.cmat_cap) break;
+                    if (need_c > caps.cmat_cap) return fail(PCF_ERR_INTERNAL, "split count matrix too large");
+                    s.tile_begin = tiles; s.ntiles = nt; s.cbase = ctot; s.mbase = mtot;
+                    tiles += nt; ctot += need_c; mtot += s.m;
+                    if (i1 - i0 + 1 >= caps.split_cap) { i1++; break; }
+                    i1++;
+                }
+                u32 ns = (u32)(i1 - i0);
+                CK(cudaMemcpyAsync(d_list, list.data() + i0, ns * sizeof(SplitTask), cudaMemcpyHostToDevice, st));
+                tm.begin(PH_COUNT);
+                k_split_count<K><<<tiles, SPLIT_THREADS, 0, st>>>(d_ctx, d_list, ns, d_C);
+                tm.end();
+                tm.begin(PH_OTHER);
+                u32 nblk = (u32)((ctot + SCAN_CHUNK - 1) / SCAN_CHUNK);
+                k_scan_partials<<<nblk, SCAN_THREADS, 0, st>>>(d_C, ctot, d_bsum);
+                k_scan_bsums<<<1, SCAN_THREADS, 0, st>>>(d_bsum, nblk);
+                k_scan_final<<<nblk, SCAN_THREADS, 0, st>>>(d_C, ctot, d_bsum, d_P);
+                tm.end();
+                tm.begin(PH_SCATTER);
+                k_split_scatter<K><<<tiles, SPLIT_THREADS, split_smem_bytes(), st>>>(d_ctx, d_list, ns, d_P);
+                tm.end();
+                tm.begin(PH_OTHER);
+                k_split_taskgen<<<ns, 256, 0, st>>>(d_ctx, d_list, d_P);
+                tm.end();
+                CK(cudaGetLastError());
+                launches += 6;
+                bytes[PH_COUNT] += 8ull * mtot;
+                bytes[PH_SCATTER] += 16ull * mtot;
+                stats.split_tasks += ns;
+                i0 = i1;
+            }
+            // read back what the round produced
+            Counters hcnt;
+            CK(cudaMemcpyAsync(&hcnt, d_cnt, sizeof hcnt, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            stats.host_syncs++;
+            if (hcnt.nan_flag) { status = PCF_ERR_NAN; break; }
+            if (hcnt.err_flag) return fail(PCF_ERR_INTERNAL, "device work-queue capacity exceeded (err_flag=" + std::to_string(hcnt.err_flag) + ")");
+            std::vector<SplitTask> next(hcnt.nsplits_out);
+            if (hcnt.nsplits_out)
+                CK(cudaMemcpyAsync(next.data(), hc.splits_out, hcnt.nsplits_out * sizeof(SplitTask), cudaMemcpyDeviceToHost, st));
+            std::vector<SegItem> items(hcnt.nitems);
+            if (hcnt.nitems)
+                CK(cudaMemcpyAsync(items.data(), hc.items, hcnt.nitems * sizeof(SegItem), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            CK(cudaMemsetAsync(&d_cnt->nsplits_out, 0, 8, st));   // nsplits_out and nitems
+            list.swap(next);
+            for (const SegItem &it : items) {
+                if (it.kind == 0) { rc = add_node(it.off, it.m, it.level, it.src); if (rc) return rc; }
+                else fallbacks.push_back(it);
+            }
+        }
+        stats.rounds = round;
+        if (status == PCF_OK) {
+            Counters hcnt;
+            CK(cudaMemcpyAsync(&hcnt, d_cnt, sizeof hcnt, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            stats.host_syncs++;
+            k7_tasks = hcnt.k7_count;
+            bytes[PH_K7] += 16ull * hcnt.k7_keys;
+            if (k7_tasks) {
+                int dev = 0, nsm = 148;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                u32 grid = (u32)std::min<u64>(k7_tasks, (u64)nsm);
+                tm.begin(PH_K7);
+                k7_kernel<K><<<grid, K7_THREADS, k7_smem_bytes(), st>>>(d_ctx);
+                tm.end();
+                CK(cudaGetLastError());
+                launches++;
+            }
+            // K8: global Standard-Sort of large buckets
+            for (const SegItem &it : fallbacks) {
+                const u64 m = it.m;
+                u64 *src = (it.src == 0 ? const_cast<u64 *>(in) : it.src == 1 ? hc.buf[1] : out) + it.off;
+                u64 *bo = out + it.off, *bt = hc.buf[1] + it.off;
+                u32 npass = 1;
+                for (u64 w = K8_TILE; w < m; w *= 2) npass++;
+                // pass k writes `out` iff (npass - 1 - k) is even, so the last pass lands in out
+                u64 *dst0 = ((npass - 1) % 2 == 0) ? bo : bt;
+                u32 nblk = (u32)((m + K8_TILE - 1) / K8_TILE);
+                tm.begin(PH_K8);
+                k8_blocksort<K><<<nblk, K8_THREADS, 0, st>>>(src, dst0, m);
+                u64 *cur = dst0;
+                for (u64 w = K8_TILE; w < m; w *= 2) {
+                    u64 *nxt = cur == bo ? bt : bo;
+                    k8_merge<K><<<nblk, K8_THREADS, 0, st>>>(cur, nxt, m, w);
+                    cur = nxt;
+                    launches++;
+                }
+                tm.end();
+                launches++;
+                CK(cudaGetLastError());
+                bytes[PH_K8] += 16ull * m * npass;
+                stats.fallback_keys_global += m;
+            }
+            // pass log: records of the global nodes (need the complete H)
+            if (logging) {
+                NodeAcc *acc = (NodeAcc *)(ws + L.acc);
+                CK(cudaMemsetAsync(acc, 0, sizeof(NodeAcc) * node_count, st));
+                for (u32 idx : global_nodes) {
+                    k_node_finalize_acc<<<64, 256, 0, st>>>(d_ctx, idx, acc + idx);
+                    k_node_finalize_rec<K><<<1, 1, 0, st>>>(d_ctx, idx, acc + idx);
+                    launches += 2;
+                }
+                CK(cudaGetLastError());
+            }
+        }
+    }
+    stats.groups_smem = k7_tasks;
+    if (timing) cudaEventRecord(ev_total1, st);
+    if (sync) {
+        Counters hcnt;
+        CK(cudaMemcpyAsync(&hcnt, d_cnt, sizeof hcnt, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        stats.host_syncs++;
+        if (hcnt.nan_flag) status = PCF_ERR_NAN;
+        else if (hcnt.err_flag) status = fail(PCF_ERR_INTERNAL, "device capacity exceeded (err_flag=" + std::to_string(hcnt.err_flag) + ")");
+        if (status == PCF_OK && logging) {
+            unsigned long long cnt = 0;
+            CK(cudaMemcpy(&cnt, p.log->count, 8, cudaMemcpyDeviceToHost));
+            if (cnt > p.log->capacity) status = fail(PCF_ERR_LOG_OVERFLOW, "pass log capacity exceeded");
+        }
+        if (status == PCF_ERR_NAN) fail(PCF_ERR_NAN, "input contains NaN");
+    }
+    stats.kernel_launches = launches;
+    if (timing) {
+        tm.collect(stats.phase_ms);
+        float tot = 0;
+        cudaEventElapsedTime(&tot, ev_total0, ev_total1);
+        stats.phase_ms[PH_TOTAL] = tot;
+        cudaEventDestroy(ev_total0);
+        cudaEventDestroy(ev_total1);
+    }
+    for (int i = 0; i < PCF_PHASES; ++i) stats.phase_bytes[i] = bytes[i];
+    if (p.stats) *p.stats = stats;
+    return status;
+}
+
+template <class K>
+static int sort_host(const u64 *in_h, u64 *out_h, size_t n, const pcf_params *pp, cudaStream_t st) {
+    if (n == 0) return PCF_OK;
+    if (!in_h || !out_h) return fail(PCF_ERR_INVALID_ARG, "NULL host pointer with n > 0");
+    u64 *d = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&d, n * 8, st);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(PCF_ERR_OOM, "cudaMallocAsync keys failed"); }
+    int rc = PCF_OK;
+    e = cudaMemcpyAsync(d, in_h, n * 8, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
+    if (!rc) rc = sort_device<K>(d, d, n, pp, st);
+    if (!rc) {
+        e = cudaMemcpyAsync(out_h, d, n * 8, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
+    }
+    cudaFreeAsync(d, st);
+    e = cudaStreamSynchronize(st);
+    if (!rc && e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
+    return rc;
+}
+
+}  // namespace pcf
+
+// ---------------------------------------------------------------- C ABI
+extern "C" {
+
+void pcf_params_init(pcf_params *p) {
+    if (!p) return;
+    memset(p, 0, sizeof *p);
+    p->struct_size = sizeof(pcf_params);
+    p->tau = 64;
+    p->seed = 0;
+    p->flags = PCF_FLAG_SYNC;
+}
+
+size_t pcf_workspace_bytes(size_t n, int key_type, const pcf_params *p) {
+    (void)key_type;
+    (void)p;
+    return pcf::workspace_bytes_impl(n);
+}
+
+int pcf_sort_f64(const double *in, double *out, size_t n, const pcf_params *p, void *stream) {
+    return pcf::sort_device<pcf::KeyF64>(reinterpret_cast<const pcf::u64 *>(in), reinterpret_cast<pcf::u64 *>(out), n, p,
+                                         (cudaStream_t)stream);
+}
+
+int pcf_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const pcf_params *p, void *stream) {
+    return pcf::sort_device<pcf::KeyU64>(reinterpret_cast<const pcf::u64 *>(in), reinterpret_cast<pcf::u64 *>(out), n, p,
+                                         (cudaStream_t)stream);
+}
+
+int pcf_sort_f64_host(const double *in_host, double *out_host, size_t n, const pcf_params *p, void *stream) {
+    return pcf::sort_host<pcf::KeyF64>(reinterpret_cast<const pcf::u64 *>(in_host), reinterpret_cast<pcf::u64 *>(out_host),
+                                       n, p, (cudaStream_t)stream);
+}
+
+int pcf_sort_u64_host(const uint64_t *in_host, uint64_t *out_host, size_t n, const pcf_params *p, void *stream) {
+    return pcf::sort_host<pcf::KeyU64>(reinterpret_cast<const pcf::u64 *>(in_host), reinterpret_cast<pcf::u64 *>(out_host),
+                                       n, p, (cudaStream_t)stream);
+}
+
+const char *pcf_status_string(int s) {
+    switch (s) {
+        case PCF_OK: return "PCF_OK";
+        case PCF_ERR_INVALID_ARG: return "PCF_ERR_INVALID_ARG";
+        case PCF_ERR_NAN: return "PCF_ERR_NAN";
+        case PCF_ERR_WORKSPACE_TOO_SMALL: return "PCF_ERR_WORKSPACE_TOO_SMALL";
+        case PCF_ERR_OOM: return "PCF_ERR_OOM";
+        case PCF_ERR_CUDA: return "PCF_ERR_CUDA";
+        case PCF_ERR_LOG_OVERFLOW: return "PCF_ERR_LOG_OVERFLOW";
+        case PCF_ERR_INTERNAL: return "PCF_ERR_INTERNAL";
+        default: return "PCF_ERR_UNKNOWN";
+    }
+}
+
+const char *pcf_last_error(void) { return pcf::g_last_error.c_str(); }
+
+int pcf_abi_version(void) { return PCF_ABI_VERSION; }
+
+}  // extern "C"

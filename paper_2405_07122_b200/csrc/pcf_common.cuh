@@ -1,0 +1,224 @@
+// pcf_common.cuh -- shared device definitions of the B200 PCF Learned Sort.
+//
+// Implements, independently of oracle/ (no shared code), the written specs of
+// the ordered-key transform for IEEE totalOrder (R11), i(x) with
+// explicitly rounded binary64 ops (R6, R15), floor(m^{3/4}) in exact 128-bit
+// integers (R5), the counter-based sampler (R3, R4), the bucket table
+// T[i] = floor(b_i*gamma/alpha)+1 (R7) and the order-independent digest (§3.4).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pcf {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+typedef unsigned short u16;
+
+// ---------------------------------------------------------------- tunables
+constexpr int K7_THREADS = 512;          // smem-subtree kernel block
+constexpr int K7_WARPS = K7_THREADS / 32;
+constexpr int S_CAP = 8192;              // keys a K7 CTA holds (two 64 KB buffers)
+constexpr int NB_CAP = 1024;             // max buckets of one K7 CTA-level partition
+constexpr int WMAX = 1024;               // largest segment a single warp runs Alg. 1 on
+constexpr int WNB = 184;                 // >= iroot34(WMAX) + 2 (warp scratch bins)
+constexpr int WSTACK = 320;              // warp DFS stack entries (bound: DESIGN.md §5.3)
+constexpr int GMAX = 1024;               // digits per global split pass
+constexpr int SPLIT_THREADS = 512;
+constexpr int SPLIT_TILE = 16384;        // keys per split tile (per-tile counts fit u16? no: u32)
+constexpr u64 GOLDEN = 0x9E3779B97F4A7C15ull;
+
+// ---------------------------------------------------------------- key transforms
+// totalOrder on binary64 == unsigned order of the "flipped" bits: set the sign
+// bit of non-negative patterns, complement negative ones (R11).
+struct KeyF64 {
+    static constexpr bool is_f64 = true;
+    __host__ __device__ static inline u64 to_okey(u64 raw) {
+        return raw ^ ((u64)((long long)raw >> 63) | 0x8000000000000000ull);
+    }
+    __host__ __device__ static inline u64 from_okey(u64 k) {
+        return (k >> 63) ? (k ^ 0x8000000000000000ull) : ~k;
+    }
+};
+struct KeyU64 {
+    static constexpr bool is_f64 = false;
+    __host__ __device__ static inline u64 to_okey(u64 raw) { return raw; }
+    __host__ __device__ static inline u64 from_okey(u64 k) { return k; }
+};
+
+// ---------------------------------------------------------------- model of one bucketing node
+// i(x) = floor((x - x_min) / (x_max - x_min) * beta) + 1
+struct Model {
+    double xmin;    // f64: x_min as a double
+    double r;       // fl(x_max - x_min)  (f64)  or  RN(x_max - x_min) (u64, R15)
+    double betad;   // (double)beta, exact
+    u64 umin;       // u64: x_min
+    u32 beta;
+    u32 pad;
+};
+
+template <class K>
+__device__ __forceinline__ u32 interval_index(u64 okey, const Model &md) {
+    double d;
+    if (K::is_f64) {
+        double x = __longlong_as_double((long long)K::from_okey(okey));
+        d = __dsub_rn(x, md.xmin);
+    } else {
+        d = __ull2double_rn(okey - md.umin);
+    }
+    double q = __ddiv_rn(d, md.r);
+    double t = __dmul_rn(q, md.betad);
+    return __double2uint_rz(t) + 1u;   // t in [0, beta]  (R6: no clamp needed)
+}
+
+// Build the model from the node's ordered min/max keys.  Returns false when
+// the range is degenerate (not 0 < r < inf, R9/R10): Standard-Sort instead.
+template <class K>
+__device__ inline bool make_model(u64 kmin, u64 kmax, u32 beta, Model &md) {
+    md.beta = beta;
+    md.betad = (double)beta;
+    md.pad = 0;
+    if (K::is_f64) {
+        double xa = __longlong_as_double((long long)K::from_okey(kmin));
+        double xb = __longlong_as_double((long long)K::from_okey(kmax));
+        md.xmin = xa;
+        md.umin = 0;
+        md.r = __dsub_rn(xb, xa);
+        return (md.r > 0.0) && (md.r <= 1.7976931348623157e308);
+    } else {
+        md.xmin = 0.0;
+        md.umin = kmin;
+        md.r = __ull2double_rn(kmax - kmin);
+        return kmax > kmin;
+    }
+}
+
+// ---------------------------------------------------------------- floor(m^{3/4})  (R5)
+__host__ __device__ inline u64 iroot34(u64 m) {
+    if (m == 0) return 0;
+    unsigned __int128 m3 = (unsigned __int128)m * m * m;   // m < 2^32 here
+    u64 c = (u64)pow((double)m, 0.75);
+    auto p4 = [](u64 c) -> unsigned __int128 {
+        unsigned __int128 c2 = (unsigned __int128)c * c;
+        return c2 * c2;
+    };
+    while (c > 0 && p4(c) > m3) --c;
+    while (p4(c + 1) <= m3) ++c;
+    return c;
+}
+
+// ---------------------------------------------------------------- sampler (R3, R4)
+__host__ __device__ __forceinline__ u64 mix64(u64 z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ u64 node_key(u64 seed, u32 level, u64 o) {
+    return mix64(seed ^ mix64(o + (u64)level * GOLDEN));
+}
+__device__ __forceinline__ u64 sample_pos(u64 nkey, u64 k, u64 m) {
+    return __umul64hi(mix64(nkey + (k + 1) * GOLDEN), m);
+}
+// digest term of v_i at 1-based index i
+__host__ __device__ __forceinline__ u64 digest_term(u64 i1, u32 v) { return mix64((i1 << 32) ^ (u64)v); }
+
+// T[i] = floor(b_i * gamma / alpha) + 1   (R7; = b_i + 1 when alpha == gamma)
+__host__ __device__ __forceinline__ u32 bucket_of(u32 b, u32 alpha, u32 gamma) {
+    if (alpha == gamma) return b + 1;
+    return (u32)(((u64)b * gamma) / alpha) + 1;
+}
+
+// ---------------------------------------------------------------- device records
+struct NodeRec {   // == pcf_node_record (72 bytes)
+    u32 level, alpha;
+    u64 offset, m;
+    u64 xmin_bits, xmax_bits;
+    u64 digest_b, digest_h;
+    u32 n_fallback, n_small, n_recurse, reserved;
+};
+
+// A bucketing node run by the global (multi-CTA) path.
+struct GNode {
+    u64 off;        // global offset of the segment (= its position in every buffer)
+    u32 m;          // segment length
+    u32 level;
+    u64 kmin, kmax; // ordered keys (atomicMin/atomicMax targets)
+    u32 alpha, beta, gamma, delta;
+    u32 src;        // buffer holding the segment (0 in, 1 tmp, 2 out)
+    u32 degenerate; // 1: range not in (0, inf) -> Standard-Sort
+    Model md;
+    u32 *cnt;       // [beta+2]  per-bin sample counts, then b (inclusive prefix), 1-based
+    u32 *T;         // [beta+2]  bucket table, 1-based
+    u32 *H;         // [gamma+2] bucket sizes, 1-based (written by the split/K7 leaves)
+    u64 digest_b;
+};
+
+// Work item of the smem-subtree kernel (K7).
+enum : u32 { K7_GROUP = 0, K7_NODE = 1, K7_SORT = 2 };
+struct K7Task {
+    u64 off;        // global offset == buffer position of the first key
+    u32 size;
+    u32 kind;       // K7_GROUP: buckets [jlo, jhi) of global node `node`
+    u32 src;        // buffer holding the keys
+    u32 level;      // K7_NODE: level of this node; K7_GROUP: level of `node`
+    u32 node;
+    u32 jlo, jhi;
+    u32 pad;
+};
+
+// A global split: stable partition of a segment by digit (j - jlo) >> shift.
+struct SplitTask {
+    u64 off;
+    u32 m;
+    u32 node;
+    u32 jlo, jhi;   // bucket range of the segment (1-based, half-open)
+    u32 shift, G;   // G = ceil((jhi - jlo) / 2^shift) <= GMAX
+    u32 src, dst;
+    u32 tile_begin, ntiles;  // filled by the host plan
+    u64 cbase;      // offset of this split's digit-major count matrix
+    u64 mbase;      // sum of m over earlier splits of the same launch
+};
+
+// Items the split leaves for the host (large recursing buckets / fallback).
+struct SegItem {
+    u64 off;
+    u32 m;
+    u32 level;      // level the segment would be processed at
+    u32 src;
+    u32 kind;       // 0 = recurse (new global node), 1 = fallback sort
+};
+
+struct DevCtx {
+    u64 *buf[3];            // in (const, never written unless in==out), tmp, out
+    u64 n;
+    u64 seed;
+    u32 tau;
+    u32 flags;
+    GNode *nodes;
+    // K7 queue
+    K7Task *k7;
+    u32 *k7_count;
+    u32 k7_cap;
+    u32 *k7_next;
+    // next-round splits / segments
+    SplitTask *splits_out;
+    u32 *nsplits_out;
+    u32 splits_cap;
+    SegItem *items;
+    u32 *nitems;
+    u32 items_cap;
+    // status
+    u32 *nan_flag;
+    u32 *err_flag;          // bit0 capacity overflow, bit1 internal
+    unsigned long long *k7_keys;   // keys handed to K7 (for the byte accounting)
+    // pass log
+    NodeRec *rec;
+    unsigned long long *rec_count;
+    u64 rec_cap;
+    u32 *l1_b, *l1_h;
+    u64 l1_cap;
+};
+
+constexpr u32 FLAG_SAMPLE_ALL = 2u;
+
+}  // namespace pcf

@@ -1,0 +1,453 @@
+// pcf_global.cuh -- multi-CTA kernels for bucketing nodes larger than one CTA's
+// shared memory (the level-1 array and oversized recursing buckets).
+//
+//   k_minmax        x_min / x_max of the segment under totalOrder, NaN flag
+//   k_node_model    i(x) parameters, degenerate-range test (R9, R10)
+//   k_fit_sample    alpha seeded sample positions, i(a_k), per-bin counts
+//   k_fit_scan      b = prefix of counts, T[i] = floor(b_i*gamma/alpha)+1    (R7)
+//   k_split_count   per-tile digit counts of d(x) = (T[i(x)] - jlo) >> shift (digit-major matrix)
+//   k_scan_*        exclusive scan of the count matrix -> per-(digit, tile) output offsets
+//   k_split_scatter stable placement by digit (Append order)
+//   k_split_taskgen one task per non-empty digit group (K7 group / node / sort,
+//                   deeper split, or an item for the host: large node / fallback)
+// A "split" is a stable partition of a segment by a digit of its bucket index
+// j; composing splits with a final in-smem placement by j (K7) equals the
+// paper's single stable placement by j because stable partitions compose.
+#pragma once
+#include "pcf_common.cuh"
+
+namespace pcf {
+
+constexpr int MM_THREADS = 256;
+constexpr int MM_UNROLL = 4;
+
+__device__ __forceinline__ ulonglong2 ld_stream(const ulonglong2 *p) {
+    ulonglong2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+    return r;
+}
+
+template <class K>
+__device__ __forceinline__ void mm_acc(u64 raw, u64 &mn, u64 &mx, bool &nan) {
+    if (K::is_f64) nan |= (raw & 0x7fffffffffffffffull) > 0x7ff0000000000000ull;
+    u64 k = K::to_okey(raw);
+    mn = k < mn ? k : mn;
+    mx = k > mx ? k : mx;
+}
+
+template <class K>
+__global__ void __launch_bounds__(MM_THREADS) k_minmax(const DevCtx *__restrict__ c, u32 node) {
+    GNode &g = c->nodes[node];
+    const u64 *x = c->buf[g.src] + g.off;
+    const u64 m = g.m;
+    u64 mn = ~0ull, mx = 0;
+    bool nan = false;
+    const u64 head = (((uintptr_t)x & 15) && m) ? 1 : 0;
+    const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(x + head);
+    const u64 nv = (m - head) / 2;
+    const u64 gtid = (u64)blockIdx.x * MM_THREADS + threadIdx.x;
+    const u64 stride = (u64)gridDim.x * MM_THREADS;
+    u64 i = gtid;
+    for (; i + (MM_UNROLL - 1) * stride < nv; i += MM_UNROLL * stride) {
+        ulonglong2 r[MM_UNROLL];
+#pragma unroll
+        for (int u = 0; u < MM_UNROLL; ++u) r[u] = ld_stream(v + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < MM_UNROLL; ++u) { mm_acc<K>(r[u].x, mn, mx, nan); mm_acc<K>(r[u].y, mn, mx, nan); }
+    }
+    for (; i < nv; i += stride) { ulonglong2 r = ld_stream(v + i); mm_acc<K>(r.x, mn, mx, nan); mm_acc<K>(r.y, mn, mx, nan); }
+    if (gtid == 0) {
+        if (head) mm_acc<K>(x[0], mn, mx, nan);
+        if ((m - head) & 1) mm_acc<K>(x[m - 1], mn, mx, nan);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        u64 a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn; mx = b > mx ? b : mx;
+    }
+    __shared__ u64 smn[MM_THREADS / 32], smx[MM_THREADS / 32];
+    __shared__ int snan;
+    if (threadIdx.x == 0) snan = 0;
+    __syncthreads();
+    if (nan) snan = 1;
+    if ((threadIdx.x & 31) == 0) { smn[threadIdx.x >> 5] = mn; smx[threadIdx.x >> 5] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < MM_THREADS / 32; ++w) { mn = smn[w] < mn ? smn[w] : mn; mx = smx[w] > mx ? smx[w] : mx; }
+        atomicMin(&g.kmin, mn);
+        atomicMax(&g.kmax, mx);
+        if (snan) atomicOr(c->nan_flag, 1u);
+    }
+}
+
+__device__ __forceinline__ void push_item(const DevCtx *c, u64 off, u32 m, u32 level, u32 src, u32 kind) {
+    u32 slot = atomicAdd(c->nitems, 1u);
+    if (slot < c->items_cap) {
+        SegItem it; it.off = off; it.m = m; it.level = level; it.src = src; it.kind = kind;
+        c->items[slot] = it;
+    } else {
+        atomicOr(c->err_flag, 1u);
+    }
+}
+
+template <class K>
+__global__ void k_node_model(const DevCtx *__restrict__ c, u32 node) {
+    if (*c->nan_flag) return;
+    GNode &g = c->nodes[node];
+    Model md;
+    bool ok = make_model<K>(g.kmin, g.kmax, g.beta, md);
+    g.md = md;
+    g.degenerate = ok ? 0u : 1u;
+    if (!ok) push_item(c, g.off, g.m, g.level, g.src, 1u);   // Standard-Sort the whole segment
+}
+
+template <class K>
+__global__ void k_fit_sample(const DevCtx *__restrict__ c, u32 node) {
+    if (*c->nan_flag) return;
+    const GNode &g = c->nodes[node];
+    if (g.degenerate) return;
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= g.alpha) return;
+    const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
+    const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, g.off), k, g.m);
+    const u64 raw = c->buf[g.src][g.off + pos];
+    const Model md = g.md;
+    atomicAdd(&g.cnt[interval_index<K>(K::to_okey(raw), md)], 1u);
+}
+
+// One CTA: b[i] = sum_{i'<=i} cnt[i'] for i = 1..beta+1 in place; T[i] = bucket_of(b_i).
+__global__ void __launch_bounds__(1024) k_fit_scan(const DevCtx *__restrict__ c, u32 node) {
+    if (*c->nan_flag) return;
+    GNode &g = c->nodes[node];
+    if (g.degenerate) return;
+    const u32 nb = g.beta + 1;
+    const bool logging = c->rec != nullptr;
+    const bool copy_l1 = g.level == 1 && c->l1_b != nullptr;
+    __shared__ u32 wsum[32];
+    __shared__ u32 carry_s;
+    __shared__ u64 dsum[32];
+    if (threadIdx.x == 0) carry_s = 0;
+    u64 db = 0;
+    const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (u32 base = 1; base <= nb; base += 1024) {
+        __syncthreads();
+        u32 i = base + threadIdx.x;
+        u32 v = i <= nb ? g.cnt[i] : 0;
+        u32 x = v;
+        for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= (u32)o) x += y; }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            u32 s = wsum[lane];
+            u32 t = s;
+            for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, t, o); if (lane >= (u32)o) t += y; }
+            wsum[lane] = t - s;
+        }
+        __syncthreads();
+        u32 carry = carry_s;
+        u32 b = carry + wsum[w] + x;
+        if (i <= nb) {
+            g.cnt[i] = b;
+            g.T[i] = bucket_of(b, g.alpha, g.gamma);
+            if (logging) db += digest_term(i, b);
+            if (copy_l1 && i - 1 < c->l1_cap) c->l1_b[i - 1] = b;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) carry_s = b;
+    }
+    if (logging) {
+        for (int o = 16; o > 0; o >>= 1) db += __shfl_xor_sync(0xffffffffu, db, o);
+        if (lane == 0) dsum[w] = db;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            u64 s = 0;
+            for (int k = 0; k < 32; ++k) s += dsum[k];
+            g.digest_b = s;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ splits
+__device__ __forceinline__ u32 find_split(const SplitTask *L, u32 ns, u32 tile) {
+    u32 lo = 0, hi = ns - 1;
+    while (lo < hi) {
+        u32 mid = (lo + hi + 1) >> 1;
+        if (L[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <class K>
+__device__ __forceinline__ u32 digit_of(u64 okey, const Model &md, const u32 *__restrict__ T, u32 jlo, u32 shift) {
+    u32 j = __ldg(&T[interval_index<K>(okey, md)]);
+    return (j - jlo) >> shift;
+}
+
+template <class K>
+__global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__restrict__ c, const SplitTask *__restrict__ L,
+                                                               u32 ns, u32 *__restrict__ C) {
+    __shared__ u32 hist[GMAX];
+    if (*c->nan_flag) return;
+    const u32 s = find_split(L, ns, blockIdx.x);
+    const SplitTask st = L[s];
+    const u32 lt = blockIdx.x - st.tile_begin;
+    const GNode &g = c->nodes[st.node];
+    for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) hist[d] = 0;
+    __syncthreads();
+    const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
+    if (g.degenerate) {
+        if (threadIdx.x == 0) hist[0] = k1 - k0;
+    } else {
+        const Model md = g.md;
+        const u64 *x = c->buf[st.src] + st.off;
+        for (u32 k = k0 + threadIdx.x; k < k1; k += SPLIT_THREADS) {
+            u32 d = digit_of<K>(K::to_okey(x[k]), md, g.T, st.jlo, st.shift);
+            atomicAdd(&hist[d], 1u);
+        }
+    }
+    __syncthreads();
+    for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
+}
+
+// --- exclusive scan of a u32 array (3 phases)
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
+
+__device__ __forceinline__ u32 block_excl_scan_1024(u32 v, u32 *wsum, u32 &total) {
+    const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u32 x = v;
+    for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= (u32)o) x += y; }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        u32 s = wsum[lane];
+        u32 t = s;
+        for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, t, o); if (lane >= (u32)o) t += y; }
+        wsum[lane] = t - s;
+        if (lane == 31) wsum[32] = t;
+    }
+    __syncthreads();
+    u32 r = wsum[w] + x - v;
+    total = wsum[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(const u32 *__restrict__ in, u64 n, u32 *__restrict__ bsum) {
+    __shared__ u32 wsum[33];
+    u64 base = (u64)blockIdx.x * SCAN_CHUNK + (u64)threadIdx.x * SCAN_ITEMS;
+    u32 s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) if (base + k < n) s += in[base + k];
+    u32 total;
+    block_excl_scan_1024(s, wsum, total);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_bsums(u32 *__restrict__ bsum, u32 nb) {
+    __shared__ u32 wsum[33];
+    u32 carry = 0;
+    for (u32 base = 0; base < nb; base += SCAN_THREADS) {
+        u32 i = base + threadIdx.x;
+        u32 v = i < nb ? bsum[i] : 0;
+        u32 total;
+        u32 e = block_excl_scan_1024(v, wsum, total);
+        if (i < nb) bsum[i] = carry + e;
+        carry += total;
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const u32 *__restrict__ in, u64 n, const u32 *__restrict__ bsum,
+                                                             u32 *__restrict__ out) {
+    __shared__ u32 wsum[33];
+    u64 base = (u64)blockIdx.x * SCAN_CHUNK + (u64)threadIdx.x * SCAN_ITEMS;
+    u32 v[SCAN_ITEMS];
+    u32 s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) { v[k] = base + k < n ? in[base + k] : 0; s += v[k]; }
+    u32 total;
+    u32 e = block_excl_scan_1024(s, wsum, total) + bsum[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) { if (base + k < n) out[base + k] = e; e += v[k]; }
+}
+
+// --- stable scatter by digit
+struct SplitScatterSmem {
+    u32 wc[SPLIT_THREADS / 32][GMAX];
+    u16 dig[SPLIT_TILE];
+};
+
+template <class K>
+__global__ void __launch_bounds__(SPLIT_THREADS) k_split_scatter(const DevCtx *__restrict__ c, const SplitTask *__restrict__ L,
+                                                                 u32 ns, const u32 *__restrict__ P) {
+    extern __shared__ __align__(16) unsigned char sc_smem_raw[];
+    SplitScatterSmem &S = *reinterpret_cast<SplitScatterSmem *>(sc_smem_raw);
+    if (*c->nan_flag) return;
+    const u32 s = find_split(L, ns, blockIdx.x);
+    const SplitTask st = L[s];
+    const u32 lt = blockIdx.x - st.tile_begin;
+    const GNode &g = c->nodes[st.node];
+    if (g.degenerate) return;
+    const Model md = g.md;
+    const u32 *T = g.T;
+    const u64 *x = c->buf[st.src] + st.off;
+    u64 *y = c->buf[st.dst] + st.off;
+    const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr u32 NW = SPLIT_THREADS / 32;
+    const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
+    const u32 R = (k1 - k0 + NW - 1) / NW;
+    const u32 r0 = min(k0 + w * R, k1), r1 = min(r0 + R, k1);
+    for (u32 d = lane; d < st.G; d += 32) S.wc[w][d] = 0;
+    __syncwarp();
+    for (u32 kb = r0; kb < r1; kb += 32) {
+        u32 k = kb + lane;
+        bool act = k < r1;
+        u32 d = 0xffffffffu;
+        if (act) { d = digit_of<K>(K::to_okey(x[k]), md, T, st.jlo, st.shift); S.dig[k - k0] = (u16)d; }
+        u32 peers = __match_any_sync(0xffffffffu, d);
+        if (act && (peers & ((1u << lane) - 1)) == 0) S.wc[w][d] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) {
+        u32 run = P[st.cbase + (u64)d * st.ntiles + lt] - (u32)st.mbase;
+        for (u32 ww = 0; ww < NW; ++ww) { u32 cc = S.wc[ww][d]; S.wc[ww][d] = run; run += cc; }
+    }
+    __syncthreads();
+    for (u32 kb = r0; kb < r1; kb += 32) {
+        u32 k = kb + lane;
+        bool act = k < r1;
+        u32 d = act ? (u32)S.dig[k - k0] : 0xffffffffu;
+        u64 raw = act ? x[k] : 0;
+        u32 peers = __match_any_sync(0xffffffffu, d);
+        u32 base = act ? S.wc[w][d] : 0;
+        __syncwarp();
+        if (act) {
+            u32 rank = __popc(peers & ((1u << lane) - 1));
+            y[base + rank] = raw;
+            if (rank == 0) S.wc[w][d] = base + __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
+__host__ __device__ inline u32 ceil_log2_u32(u32 v) {   // v >= 1
+    u32 r = 0;
+    while ((1ull << r) < v) ++r;
+    return r;
+}
+__host__ __device__ inline u32 floor_log2_u64(u64 v) {  // v >= 1
+    u32 r = 0;
+    while (v >> (r + 1)) ++r;
+    return r;
+}
+// Digit shift for splitting W >= 2 consecutive buckets holding c keys:
+// G = ceil(W / 2^s) <= GMAX, expected group ~ S_CAP/2 keys, G >= 2.
+__host__ __device__ inline u32 choose_shift(u32 W, u32 c) {
+    u32 cl = ceil_log2_u32(W);
+    u32 smin = cl > 10 ? cl - 10 : 0;
+    u64 q = ((u64)(S_CAP / 2) * W) / (c ? c : 1);
+    u32 st = floor_log2_u64(q ? q : 1);
+    u32 s = st < 10 ? st : 10;
+    if (s < smin) s = smin;
+    if (s > cl - 1) s = cl - 1;
+    return s;
+}
+
+__device__ __forceinline__ void push_k7(const DevCtx *c, const K7Task &t) {
+    u32 slot = atomicAdd(c->k7_count, 1u);
+    atomicAdd(c->k7_keys, (unsigned long long)t.size);
+    if (slot < c->k7_cap) c->k7[slot] = t;
+    else atomicOr(c->err_flag, 1u);
+}
+
+__global__ void k_split_taskgen(const DevCtx *__restrict__ c, const SplitTask *__restrict__ L, const u32 *__restrict__ P) {
+    if (*c->nan_flag) return;
+    const SplitTask st = L[blockIdx.x];
+    GNode &g = c->nodes[st.node];
+    if (g.degenerate) return;
+    const u32 tau = c->tau;
+    for (u32 d = threadIdx.x; d < st.G; d += blockDim.x) {
+        u32 start = P[st.cbase + (u64)d * st.ntiles] - (u32)st.mbase;
+        u32 end = d + 1 < st.G ? P[st.cbase + (u64)(d + 1) * st.ntiles] - (u32)st.mbase : st.m;
+        u32 cnt = end - start;
+        if (cnt == 0) continue;
+        u32 jlo = st.jlo + (d << st.shift);
+        u32 jhi = min(jlo + (1u << st.shift), st.jhi);
+        u32 W = jhi - jlo;
+        u64 goff = st.off + start;
+        if (W == 1) {
+            g.H[jlo] = cnt;
+            bool sort = cnt >= g.delta || cnt < tau;   // Alg. 1
+            if (cnt <= (u32)S_CAP) {
+                K7Task t; t.off = goff; t.size = cnt; t.kind = sort ? K7_SORT : K7_NODE; t.src = st.dst;
+                t.level = g.level + 1; t.node = st.node; t.jlo = jlo; t.jhi = jhi; t.pad = 0;
+                push_k7(c, t);
+            } else {
+                push_item(c, goff, cnt, g.level + 1, st.dst, sort ? 1u : 0u);
+            }
+        } else if (cnt <= (u32)S_CAP && W <= (u32)NB_CAP) {
+            K7Task t; t.off = goff; t.size = cnt; t.kind = K7_GROUP; t.src = st.dst;
+            t.level = g.level; t.node = st.node; t.jlo = jlo; t.jhi = jhi; t.pad = 0;
+            push_k7(c, t);
+        } else {
+            SplitTask nt;
+            nt.off = goff; nt.m = cnt; nt.node = st.node; nt.jlo = jlo; nt.jhi = jhi;
+            nt.shift = choose_shift(W, cnt);
+            nt.G = (W + (1u << nt.shift) - 1) >> nt.shift;
+            nt.src = st.dst; nt.dst = st.dst == 1 ? 2 : 1;
+            nt.tile_begin = 0; nt.ntiles = 0; nt.cbase = 0; nt.mbase = 0;
+            u32 slot = atomicAdd(c->nsplits_out, 1u);
+            if (slot < c->splits_cap) c->splits_out[slot] = nt;
+            else atomicOr(c->err_flag, 1u);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ pass-log finalisation of a global node
+struct NodeAcc {
+    unsigned long long dh;
+    u32 nf, ns, nr, pad;
+};
+
+__global__ void k_node_finalize_acc(const DevCtx *__restrict__ c, u32 node, NodeAcc *acc) {
+    const GNode &g = c->nodes[node];
+    if (g.degenerate || *c->nan_flag) return;
+    const u32 tau = c->tau;
+    u64 dh = 0;
+    u32 nf = 0, ns = 0, nr = 0;
+    const bool copy_l1 = g.level == 1 && c->l1_h != nullptr;
+    for (u32 u = blockIdx.x * blockDim.x + threadIdx.x; u <= g.gamma; u += gridDim.x * blockDim.x) {
+        u32 h = g.H[u + 1];
+        dh += digest_term(u + 1, h);
+        if (h) { if (h >= g.delta) nf++; else if (h < tau) ns++; else nr++; }
+        if (copy_l1 && u < c->l1_cap) c->l1_h[u] = h;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        dh += __shfl_xor_sync(0xffffffffu, dh, o);
+        nf += __shfl_xor_sync(0xffffffffu, nf, o);
+        ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        nr += __shfl_xor_sync(0xffffffffu, nr, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&acc->dh, dh);
+        atomicAdd(&acc->nf, nf); atomicAdd(&acc->ns, ns); atomicAdd(&acc->nr, nr);
+    }
+}
+
+template <class K>
+__global__ void k_node_finalize_rec(const DevCtx *__restrict__ c, u32 node, const NodeAcc *acc) {
+    const GNode &g = c->nodes[node];
+    if (g.degenerate || *c->nan_flag) return;
+    unsigned long long slot = atomicAdd(c->rec_count, 1ull);
+    if (slot < c->rec_cap) {
+        NodeRec r;
+        r.level = g.level; r.alpha = g.alpha; r.offset = g.off; r.m = g.m;
+        r.xmin_bits = K::from_okey(g.kmin); r.xmax_bits = K::from_okey(g.kmax);
+        r.digest_b = g.digest_b; r.digest_h = acc->dh;
+        r.n_fallback = acc->nf; r.n_small = acc->ns; r.n_recurse = acc->nr; r.reserved = 0;
+        c->rec[slot] = r;
+    }
+}
+
+}  // namespace pcf

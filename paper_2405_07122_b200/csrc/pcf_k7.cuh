@@ -1,0 +1,713 @@
+// pcf_k7.cuh -- K7: run the whole remaining Algorithm-1 subtree of a segment
+// in shared memory, one CTA per task, persistent.
+//
+// A task is one of
+//   K7_GROUP : buckets [jlo, jhi) of a global bucketing node whose keys lie,
+//              in stable (Append) order, in one contiguous range.  The CTA
+//              finishes the node's model-based bucketing for those buckets
+//              (stable placement by j) and then processes
+//              every bucket per Alg. 1 lines 160-167.
+//   K7_NODE  : a segment that is a fresh Learned-Sort call (level L, offset o).
+//   K7_SORT  : a bucket that Alg. 1 sends to Standard-Sort (|c_j| >= delta or
+//              n < tau): sorted and written out.
+// The task's keys are loaded once (HBM read), every deeper level runs in
+// shared memory, and each finished run of buckets is written once to `out`.
+//
+// Segments > WMAX keys are processed by the whole CTA (cta_node); segments of
+// <= WMAX keys by one warp each (warp_node), with an explicit DFS stack.
+// Stable placement uses per-warp counters over warp-contiguous key ranges
+// (CTA) or in-order 32-key chunks with __match_any_sync (warp), so the order of
+// every bucket equals the Append order and the next level samples the same
+// keys as the oracle (readings R4, R16).
+#pragma once
+#include "pcf_common.cuh"
+
+namespace pcf {
+
+struct WarpScratch {
+    u16 cnt[WNB];    // per-bin sample counts -> b (inclusive prefix), 1-based
+    u16 T[WNB];      // bucket table, 1-based
+    u16 H[WNB];      // bucket sizes, 0-based bucket index u = j-1
+    u16 C[WNB];      // running cursors / bucket ends
+    u32 stack[WSTACK];
+};
+
+struct BigItem {
+    u32 pos, size, level, buf, kind;   // kind: 0 node, 1 sort
+};
+
+constexpr int BIG_CAP = 48;
+
+struct K7Smem {
+    u64 A[S_CAP];
+    u64 B[S_CAP];
+    u16 U[S_CAP];
+    u32 Hc[NB_CAP + 1];
+    u32 Bs[NB_CAP + 1];
+    union {
+        u16 wcnt[K7_WARPS][NB_CAP];               // CTA partition per-warp counters
+        struct { u32 cnt[S_CAP / 8 + 8]; u32 T[S_CAP / 8 + 8]; } fit;   // CTA fit (beta+2 <= 863)
+        WarpScratch w[K7_WARPS];
+    } u;
+    BigItem big[BIG_CAP];
+    u64 red[2 * K7_WARPS];
+    u32 redu[4 * K7_WARPS];
+    u32 scan_tmp[K7_WARPS + 1];
+    K7Task task;
+    u32 task_idx;
+    u32 nbig;
+    u32 chunk_next;
+    u32 nchunks;
+    u32 chunk_sz;
+    u32 gnode_beta, gnode_delta, gnode_level;
+    Model gmd;
+    const u32 *gT;
+    u32 *gH;
+};
+
+// ------------------------------------------------------------------ small helpers
+__device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ u32 warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ u32 lanemask_lt() {
+    u32 r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ u32 next_pow2(u32 v) { return v <= 1 ? 1 : 1u << (32 - __clz(v - 1)); }
+
+__device__ __forceinline__ u64 warp_min_u64(u64 v) {
+    for (int o = 16; o > 0; o >>= 1) { u64 w = __shfl_xor_sync(0xffffffffu, v, o); v = w < v ? w : v; }
+    return v;
+}
+__device__ __forceinline__ u64 warp_max_u64(u64 v) {
+    for (int o = 16; o > 0; o >>= 1) { u64 w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
+    return v;
+}
+__device__ __forceinline__ u64 warp_sum_u64(u64 v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ u32 warp_sum_u32(u32 v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// inclusive warp scan
+__device__ __forceinline__ u32 warp_incl_scan(u32 v) {
+    u32 lane = lane_id();
+    for (int o = 1; o < 32; o <<= 1) {
+        u32 w = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= (u32)o) v += w;
+    }
+    return v;
+}
+
+// ------------------------------------------------------------------ node record (pass log)
+__device__ __forceinline__ void write_record(const DevCtx *c, u32 level, u32 alpha, u64 off, u64 m,
+                                             u64 xmin_bits, u64 xmax_bits, u64 db, u64 dh, u32 nf,
+                                             u32 ns, u32 nr) {
+    unsigned long long slot = atomicAdd(c->rec_count, 1ull);
+    if (slot < c->rec_cap) {
+        NodeRec r;
+        r.level = level; r.alpha = alpha; r.offset = off; r.m = m;
+        r.xmin_bits = xmin_bits; r.xmax_bits = xmax_bits;
+        r.digest_b = db; r.digest_h = dh;
+        r.n_fallback = nf; r.n_small = ns; r.n_recurse = nr; r.reserved = 0;
+        c->rec[slot] = r;
+    }
+}
+
+// ------------------------------------------------------------------ sorting ("Standard-Sort", R2)
+// Bitonic network over ordered keys; all merges ascending (first step of each
+// stage compares i with its mirror), so virtual +inf padding never moves.
+__device__ void warp_bitonic_smem(u64 *a, u32 n) {
+    if (n <= 1) return;
+    u32 P = next_pow2(n);
+    u32 lane = lane_id();
+    u32 lgP = 31 - __clz(P);
+    for (u32 lk = 1; lk <= lgP; ++lk) {
+        u32 k = 1u << lk, lh = lk - 1;
+        for (u32 t = lane; t < (P >> 1); t += 32) {
+            u32 blk = t >> lh, w = t & ((1u << lh) - 1);
+            u32 lo = (blk << lk) + w, hi = (blk << lk) + k - 1 - w;
+            if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
+        }
+        __syncwarp();
+        for (int lj = (int)lh - 1; lj >= 0; --lj) {
+            u32 j = 1u << lj;
+            for (u32 t = lane; t < (P >> 1); t += 32) {
+                u32 lo = ((t >> lj) << (lj + 1)) + (t & (j - 1)), hi = lo + j;
+                if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Register bitonic for n <= 64: lane l holds elements l and l+32.
+__device__ void warp_sort64_write(const u64 *a, u32 n, u64 *gout_raw, bool f64) {
+    u32 lane = lane_id();
+    u64 v0 = lane < n ? a[lane] : ~0ull;
+    u64 v1 = lane + 32 < n ? a[lane + 32] : ~0ull;
+    if (n > 32) {
+        for (u32 k = 2; k <= 64; k <<= 1) {
+            for (u32 j = k >> 1; j > 0; j >>= 1) {
+                if (j == 32) {
+                    // partner of element i=lane is i+32 (same lane), ascending since (i & 64) == 0
+                    u64 lo = v0 < v1 ? v0 : v1, hi = v0 < v1 ? v1 : v0;
+                    v0 = lo; v1 = hi;
+                } else {
+                    u64 p0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                    u64 p1 = __shfl_xor_sync(0xffffffffu, v1, j);
+                    u32 i0 = lane, i1 = lane + 32;
+                    bool up0 = (i0 & k) == 0, up1 = (i1 & k) == 0;
+                    bool low0 = (i0 & j) == 0, low1 = (i1 & j) == 0;
+                    v0 = (low0 == up0) ? (v0 < p0 ? v0 : p0) : (v0 > p0 ? v0 : p0);
+                    v1 = (low1 == up1) ? (v1 < p1 ? v1 : p1) : (v1 > p1 ? v1 : p1);
+                }
+            }
+        }
+    } else {
+        for (u32 k = 2; k <= 32; k <<= 1) {
+            for (u32 j = k >> 1; j > 0; j >>= 1) {
+                u64 p0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                bool up = (lane & k) == 0, low = (lane & j) == 0;
+                v0 = (low == up) ? (v0 < p0 ? v0 : p0) : (v0 > p0 ? v0 : p0);
+            }
+        }
+    }
+    if (lane < n) gout_raw[lane] = f64 ? KeyF64::from_okey(v0) : v0;
+    if (lane + 32 < n) gout_raw[lane + 32] = f64 ? KeyF64::from_okey(v1) : v1;
+}
+
+template <class K>
+__device__ void warp_sort_write(u64 *a, u32 n, u64 *gout_raw) {
+    if (n == 0) return;
+    if (n <= 64) {
+        warp_sort64_write(a, n, gout_raw, K::is_f64);
+    } else {
+        warp_bitonic_smem(a, n);
+        for (u32 k = lane_id(); k < n; k += 32) gout_raw[k] = K::from_okey(a[k]);
+    }
+    __syncwarp();
+}
+
+template <class K>
+__device__ void cta_sort_write(u64 *a, u32 n, u64 *gout_raw) {
+    if (n > 1) {
+        u32 P = next_pow2(n);
+        u32 lgP = 31 - __clz(P);
+        for (u32 lk = 1; lk <= lgP; ++lk) {
+            u32 k = 1u << lk, lh = lk - 1;
+            for (u32 t = threadIdx.x; t < (P >> 1); t += K7_THREADS) {
+                u32 blk = t >> lh, w = t & ((1u << lh) - 1);
+                u32 lo = (blk << lk) + w, hi = (blk << lk) + k - 1 - w;
+                if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
+            }
+            __syncthreads();
+            for (int lj = (int)lh - 1; lj >= 0; --lj) {
+                u32 j = 1u << lj;
+                for (u32 t = threadIdx.x; t < (P >> 1); t += K7_THREADS) {
+                    u32 lo = ((t >> lj) << (lj + 1)) + (t & (j - 1)), hi = lo + j;
+                    if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    for (u32 k = threadIdx.x; k < n; k += K7_THREADS) gout_raw[k] = K::from_okey(a[k]);
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ warp window of sorted buckets
+// Consecutive buckets sent to Standard-Sort are sorted together: by the order
+// property sorting their concatenation equals
+// concatenating the individually sorted buckets.
+struct Window {
+    u32 start, len;
+};
+
+template <class K>
+__device__ __forceinline__ void window_flush(Window &w, u64 *Y, u64 *gout) {
+    if (w.len) warp_sort_write<K>(Y + w.start, w.len, gout + w.start);
+    w.len = 0;
+}
+template <class K>
+__device__ __forceinline__ void window_add(Window &w, u64 *Y, u64 *gout, u32 pos, u32 h) {
+    if (w.len && (w.len + h > 64 || pos != w.start + w.len)) window_flush<K>(w, Y, gout);
+    if (w.len == 0) w.start = pos;
+    w.len += h;
+    if (w.len > 64) window_flush<K>(w, Y, gout);
+}
+
+// ------------------------------------------------------------------ warp-level Alg. 1
+// Learned-Sort of the segment X[p, p+m) (m <= WMAX, m >= tau) at level L, global
+// offset gbase + p, and all its descendants; finished runs go to gout[pos].
+// Stack entries: pos(13) | size(11) | depth(4) | buf(1).
+template <class K>
+__device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, u32 L0, u64 gbase,
+                          u64 *gout) {
+    WarpScratch &ws = S.u.w[warp_id()];
+    const u32 lane = lane_id();
+    const u32 tau = c->tau;
+    const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
+    const bool logging = c->rec != nullptr;
+    u32 sp = 0;
+    if (lane == 0) ws.stack[0] = p0 | (m0 << 13) | (0u << 24) | (buf0 << 28);
+    sp = 1;
+    __syncwarp();
+    while (sp > 0) {
+        u32 e = ws.stack[--sp];
+        __syncwarp();
+        u32 p = e & 0x1fffu, m = (e >> 13) & 0x7ffu, d = (e >> 24) & 0xfu, bi = e >> 28;
+        if (m == 0) m = 2048;   // never: sizes are <= WMAX = 1024 (< 2048)
+        u64 *X = bi ? S.B : S.A;
+        u64 *Y = bi ? S.A : S.B;
+        u32 L = L0 + d;
+        Window win; win.len = 0; win.start = 0;
+        if (m < tau) { window_add<K>(win, X, gout, p, m); window_flush<K>(win, X, gout); continue; }
+        // x_min, x_max over the segment
+        u64 mn = ~0ull, mx = 0;
+        for (u32 k = lane; k < m; k += 32) { u64 v = X[p + k]; mn = v < mn ? v : mn; mx = v > mx ? v : mx; }
+        mn = warp_min_u64(mn); mx = warp_max_u64(mx);
+        Model md;
+        u32 P = (u32)iroot34(m);
+        if (!make_model<K>(mn, mx, P, md)) {   // R9/R10: Standard-Sort
+            warp_sort_write<K>(X + p, m, gout + p);
+            continue;
+        }
+        const u32 alpha = sample_all ? m : P, beta = P, gamma = P, delta = P;
+        for (u32 i = lane; i <= beta + 1; i += 32) ws.cnt[i] = 0;
+        __syncwarp();
+        // sample (R3, R4) and count per interval
+        const u64 nkey = node_key(c->seed, L, gbase + p);
+        for (u32 k0 = 0; k0 < alpha; k0 += 32) {
+            u32 k = k0 + lane;
+            bool act = k < alpha;
+            u32 i = 0xffffffffu;
+            if (act) {
+                u32 pos = sample_all ? k : (u32)sample_pos(nkey, k, m);
+                i = interval_index<K>(X[p + pos], md);
+            }
+            u32 peers = __match_any_sync(0xffffffffu, i);
+            if (act && (peers & lanemask_lt()) == 0) ws.cnt[i] += (u16)__popc(peers);
+            __syncwarp();
+        }
+        // b = inclusive prefix of the counts, T = floor(b*gamma/alpha)+1
+        {
+            u32 nb = beta + 1;                       // entries 1..beta+1
+            u32 per = (nb + 31) / 32;
+            u32 s0 = 1 + lane * per, s1 = min(s0 + per, nb + 1);
+            u32 loc = 0;
+            for (u32 i = s0; i < s1; ++i) loc += ws.cnt[i];
+            u32 incl = warp_incl_scan(loc);
+            u32 run = incl - loc;
+            u64 db = 0;
+            for (u32 i = s0; i < s1; ++i) {
+                run += ws.cnt[i];
+                ws.cnt[i] = (u16)run;
+                ws.T[i] = (u16)bucket_of(run, alpha, gamma);
+                if (logging) db += digest_term(i, run);
+            }
+            if (logging) db = warp_sum_u64(db);
+            __syncwarp();
+            // classify every key: u = T[i(x)] - 1; histogram H[u]
+            for (u32 u = lane; u <= gamma; u += 32) ws.H[u] = 0;
+            __syncwarp();
+            for (u32 k0 = 0; k0 < m; k0 += 32) {
+                u32 k = k0 + lane;
+                bool act = k < m;
+                u32 u = 0xffffffffu;
+                if (act) { u = ws.T[interval_index<K>(X[p + k], md)] - 1u; S.U[p + k] = (u16)u; }
+                u32 peers = __match_any_sync(0xffffffffu, u);
+                if (act && (peers & lanemask_lt()) == 0) ws.H[u] += (u16)__popc(peers);
+                __syncwarp();
+            }
+            // exclusive prefix of H -> cursors
+            u32 ng = gamma + 1;
+            u32 perg = (ng + 31) / 32;
+            u32 g0 = lane * perg, g1 = min(g0 + perg, ng);
+            u32 locg = 0;
+            for (u32 u = g0; u < g1; ++u) locg += ws.H[u];
+            u32 inclg = warp_incl_scan(locg);
+            u32 rg = inclg - locg;
+            for (u32 u = g0; u < g1; ++u) { ws.C[u] = (u16)rg; rg += ws.H[u]; }
+            __syncwarp();
+            // stable scatter (Append in index order)
+            for (u32 k0 = 0; k0 < m; k0 += 32) {
+                u32 k = k0 + lane;
+                bool act = k < m;
+                u32 u = act ? (u32)S.U[p + k] : 0xffffffffu;
+                u32 peers = __match_any_sync(0xffffffffu, u);
+                u32 base = act ? ws.C[u] : 0;
+                __syncwarp();
+                if (act) {
+                    u32 rank = __popc(peers & lanemask_lt());
+                    Y[p + base + rank] = X[p + k];
+                    if (rank == 0) ws.C[u] = (u16)(base + __popc(peers));
+                }
+                __syncwarp();
+            }
+            // node record (pass log) and child dispatch
+            u32 nf = 0, ns = 0, nr = 0;
+            u64 dh = 0;
+            for (u32 u = lane; u <= gamma; u += 32) {
+                u32 h = ws.H[u];
+                if (logging) dh += digest_term(u + 1, h);
+                if (h) { if (h >= delta) nf++; else if (h < tau) ns++; else nr++; }
+            }
+            if (logging) {
+                dh = warp_sum_u64(dh);
+                nf = warp_sum_u32(nf); ns = warp_sum_u32(ns); nr = warp_sum_u32(nr);
+                if (lane == 0)
+                    write_record(c, L, alpha, gbase + p, m, K::from_okey(mn), K::from_okey(mx), db, dh, nf,
+                                 ns, nr);
+            }
+        }
+        // children in bucket order: windows of Standard-Sort buckets, pushes of recursions
+        for (u32 u = 0; u <= gamma; ++u) {
+            u32 h = ws.H[u];
+            if (h == 0) continue;
+            u32 start = p + ws.C[u] - h;
+            if (h >= delta || h < tau) {
+                window_add<K>(win, Y, gout, start, h);
+            } else {
+                window_flush<K>(win, Y, gout);
+                if (lane == 0) {
+                    if (sp < WSTACK && d + 1 < 16) ws.stack[sp] = start | (h << 13) | ((d + 1) << 24) | ((bi ^ 1u) << 28);
+                    else atomicOr(c->err_flag, 2u);
+                }
+                sp++;
+                __syncwarp();
+            }
+        }
+        window_flush<K>(win, Y, gout);
+        if (sp > WSTACK) sp = WSTACK;
+    }
+}
+
+// Process the buckets [u0, u1) of a CTA-level partition whose keys are in Y:
+// sort runs of Standard-Sort buckets, run warp_node on recursing ones (<= WMAX).
+template <class K>
+__device__ void warp_range(const DevCtx *c, K7Smem &S, u32 ybuf, u32 u0, u32 u1, u32 delta, u32 Lc,
+                           u64 gbase, u64 *gout) {
+    u64 *Y = ybuf ? S.B : S.A;
+    const u32 tau = c->tau;
+    Window win; win.len = 0; win.start = 0;
+    for (u32 u = u0; u < u1; ++u) {
+        u32 h = S.Hc[u];
+        if (h == 0) continue;
+        u32 pos = S.Bs[u];
+        if (h > WMAX) { window_flush<K>(win, Y, gout); continue; }   // CTA big list
+        if (h >= delta || h < tau) {
+            window_add<K>(win, Y, gout, pos, h);
+        } else {
+            window_flush<K>(win, Y, gout);
+            warp_node<K>(c, S, ybuf, pos, h, Lc, gbase, gout);
+        }
+    }
+    window_flush<K>(win, Y, gout);
+}
+
+// ------------------------------------------------------------------ CTA-level primitives
+__device__ __forceinline__ u64 cta_reduce_min(K7Smem &S, u64 v) {
+    v = warp_min_u64(v);
+    if (lane_id() == 0) S.red[warp_id()] = v;
+    __syncthreads();
+    if (warp_id() == 0) {
+        u64 w = lane_id() < K7_WARPS ? S.red[lane_id()] : ~0ull;
+        w = warp_min_u64(w);
+        if (lane_id() == 0) S.red[K7_WARPS] = w;
+    }
+    __syncthreads();
+    u64 r = S.red[K7_WARPS];
+    __syncthreads();
+    return r;
+}
+__device__ __forceinline__ u64 cta_reduce_max(K7Smem &S, u64 v) {
+    v = warp_max_u64(v);
+    if (lane_id() == 0) S.red[warp_id()] = v;
+    __syncthreads();
+    if (warp_id() == 0) {
+        u64 w = lane_id() < K7_WARPS ? S.red[lane_id()] : 0ull;
+        w = warp_max_u64(w);
+        if (lane_id() == 0) S.red[K7_WARPS] = w;
+    }
+    __syncthreads();
+    u64 r = S.red[K7_WARPS];
+    __syncthreads();
+    return r;
+}
+__device__ __forceinline__ u64 cta_reduce_sum64(K7Smem &S, u64 v) {
+    v = warp_sum_u64(v);
+    if (lane_id() == 0) S.red[warp_id()] = v;
+    __syncthreads();
+    if (warp_id() == 0) {
+        u64 w = lane_id() < K7_WARPS ? S.red[lane_id()] : 0ull;
+        w = warp_sum_u64(w);
+        if (lane_id() == 0) S.red[K7_WARPS] = w;
+    }
+    __syncthreads();
+    u64 r = S.red[K7_WARPS];
+    __syncthreads();
+    return r;
+}
+
+// exclusive scan of a[0..n) (n <= 2*K7_THREADS) in place; returns the total
+__device__ u32 cta_excl_scan(K7Smem &S, u32 *a, u32 n) {
+    u32 t = threadIdx.x;
+    u32 i0 = 2 * t, i1 = 2 * t + 1;
+    u32 v0 = i0 < n ? a[i0] : 0, v1 = i1 < n ? a[i1] : 0;
+    u32 loc = v0 + v1;
+    u32 incl = warp_incl_scan(loc);
+    if (lane_id() == 31) S.scan_tmp[warp_id()] = incl;
+    __syncthreads();
+    if (warp_id() == 0) {
+        u32 w = lane_id() < K7_WARPS ? S.scan_tmp[lane_id()] : 0;
+        u32 wi = warp_incl_scan(w);
+        if (lane_id() < K7_WARPS) S.scan_tmp[lane_id()] = wi - w;
+        if (lane_id() == K7_WARPS - 1) S.scan_tmp[K7_WARPS] = wi;
+    }
+    __syncthreads();
+    u32 base = S.scan_tmp[warp_id()] + incl - loc;
+    if (i0 < n) a[i0] = base;
+    if (i1 < n) a[i1] = base + v0;
+    u32 total = S.scan_tmp[K7_WARPS];
+    __syncthreads();
+    return total;
+}
+
+// Stable partition X[0..m) -> Y[0..m) by U[k] in [0, nb): per-warp contiguous
+// ranges, per-warp counters, bucket sizes to Hc, bucket starts to Bs.
+__device__ void cta_partition(K7Smem &S, const u64 *X, u64 *Y, u32 m, u32 nb) {
+    const u32 w = warp_id(), lane = lane_id();
+    const u32 R = (m + K7_WARPS - 1) / K7_WARPS;
+    const u32 r0 = min(w * R, m), r1 = min(r0 + R, m);
+    for (u32 u = lane; u < nb; u += 32) S.u.wcnt[w][u] = 0;
+    __syncwarp();
+    for (u32 k0 = r0; k0 < r1; k0 += 32) {
+        u32 k = k0 + lane;
+        bool act = k < r1;
+        u32 u = act ? (u32)S.U[k] : 0xffffffffu;
+        u32 peers = __match_any_sync(0xffffffffu, u);
+        if (act && (peers & lanemask_lt()) == 0) S.u.wcnt[w][u] += (u16)__popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
+        u32 tot = 0;
+        for (u32 ww = 0; ww < K7_WARPS; ++ww) tot += S.u.wcnt[ww][u];
+        S.Hc[u] = tot;
+        S.Bs[u] = tot;
+    }
+    __syncthreads();
+    cta_excl_scan(S, S.Bs, nb);
+    for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
+        u32 run = S.Bs[u];
+        for (u32 ww = 0; ww < K7_WARPS; ++ww) { u32 cc = S.u.wcnt[ww][u]; S.u.wcnt[ww][u] = (u16)run; run += cc; }
+    }
+    __syncthreads();
+    for (u32 k0 = r0; k0 < r1; k0 += 32) {
+        u32 k = k0 + lane;
+        bool act = k < r1;
+        u32 u = act ? (u32)S.U[k] : 0xffffffffu;
+        u32 peers = __match_any_sync(0xffffffffu, u);
+        u32 base = act ? S.u.wcnt[w][u] : 0;
+        __syncwarp();
+        if (act) {
+            u32 rank = __popc(peers & lanemask_lt());
+            Y[base + rank] = X[k];
+            if (rank == 0) S.u.wcnt[w][u] = (u16)(base + __popc(peers));
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+}
+
+// After a CTA-level partition into Y (Hc/Bs valid for nb buckets): push big
+// children (> WMAX) to the CTA stack, hand the rest to warps in chunks.
+template <class K>
+__device__ void cta_dispatch(const DevCtx *c, K7Smem &S, u32 ybuf, u32 base_pos, u32 m, u32 nb,
+                             u32 delta, u32 Lc, u64 gbase, u64 *gout) {
+    const u32 tau = c->tau;
+    for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
+        u32 h = S.Hc[u];
+        if (h > WMAX) {
+            u32 slot = atomicAdd(&S.nbig, 1u);
+            if (slot < BIG_CAP) {
+                BigItem it;
+                it.pos = base_pos + S.Bs[u]; it.size = h; it.level = Lc; it.buf = ybuf;
+                it.kind = (h >= delta || h < tau) ? 1u : 0u;
+                S.big[slot] = it;
+            } else {
+                atomicOr(c->err_flag, 2u);
+            }
+        }
+    }
+    // Bs are relative to the partitioned range; make them absolute buffer positions
+    for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) S.Bs[u] += base_pos;
+    if (threadIdx.x == 0) {
+        u32 cs = max(64u, (m + 2 * K7_WARPS - 1) / (2 * K7_WARPS));
+        S.chunk_sz = cs;
+        S.nchunks = (m + cs - 1) / cs;
+        S.chunk_next = 0;
+    }
+    __syncthreads();
+    const u32 lane = lane_id();
+    for (;;) {
+        u32 ch = 0;
+        if (lane == 0) ch = atomicAdd(&S.chunk_next, 1u);
+        ch = __shfl_sync(0xffffffffu, ch, 0);
+        if (ch >= S.nchunks) break;
+        // buckets whose start lies in [ch*cs, (ch+1)*cs) (relative): lower bounds over Bs
+        u32 lo_key = base_pos + ch * S.chunk_sz, hi_key = base_pos + (ch + 1) * S.chunk_sz;
+        u32 a = 0, b = nb;
+        while (a < b) { u32 mid = (a + b) >> 1; if (S.Bs[mid] < lo_key) a = mid + 1; else b = mid; }
+        u32 u0 = a;
+        b = nb;
+        while (a < b) { u32 mid = (a + b) >> 1; if (S.Bs[mid] < hi_key) a = mid + 1; else b = mid; }
+        u32 u1 = a;
+        if (u0 < u1) warp_range<K>(c, S, ybuf, u0, u1, delta, Lc, gbase, gout);
+    }
+    __syncthreads();
+}
+
+// CTA-level Alg. 1 on X[p, p+m) (WMAX < m <= S_CAP), level L, global offset
+// gbase + p.  Leaves sorted or partitions into the other buffer and dispatches.
+template <class K>
+__device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32 L, u64 gbase, u64 *gout) {
+    u64 *X = xbuf ? S.B : S.A;
+    u64 *Y = xbuf ? S.A : S.B;
+    const u32 tau = c->tau;
+    const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
+    const bool logging = c->rec != nullptr;
+    if (m < tau) { cta_sort_write<K>(X + p, m, gout + p); return; }
+    u64 mn = ~0ull, mx = 0;
+    for (u32 k = threadIdx.x; k < m; k += K7_THREADS) { u64 v = X[p + k]; mn = v < mn ? v : mn; mx = v > mx ? v : mx; }
+    mn = cta_reduce_min(S, mn);
+    mx = cta_reduce_max(S, mx);
+    Model md;
+    u32 P = (u32)iroot34(m);
+    if (!make_model<K>(mn, mx, P, md)) { cta_sort_write<K>(X + p, m, gout + p); return; }
+    const u32 alpha = sample_all ? m : P, beta = P, gamma = P, delta = P;
+    u32 *cnt = S.u.fit.cnt, *T = S.u.fit.T;
+    for (u32 i = threadIdx.x; i <= beta + 1; i += K7_THREADS) cnt[i] = 0;
+    __syncthreads();
+    const u64 nkey = node_key(c->seed, L, gbase + p);
+    for (u32 k = threadIdx.x; k < alpha; k += K7_THREADS) {
+        u32 pos = sample_all ? k : (u32)sample_pos(nkey, k, m);
+        atomicAdd(&cnt[interval_index<K>(X[p + pos], md)], 1u);
+    }
+    __syncthreads();
+    // inclusive prefix over cnt[1..beta+1]: exclusive scan of cnt[1..] then add own
+    for (u32 i = threadIdx.x; i <= beta; i += K7_THREADS) T[i] = cnt[i + 1];
+    __syncthreads();
+    cta_excl_scan(S, T, beta + 1);
+    u64 db = 0;
+    for (u32 i = threadIdx.x; i <= beta; i += K7_THREADS) {
+        u32 b = T[i] + cnt[i + 1];
+        if (logging) db += digest_term(i + 1, b);
+        cnt[i + 1] = b;
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i <= beta; i += K7_THREADS) T[i + 1] = bucket_of(cnt[i + 1], alpha, gamma);
+    __syncthreads();
+    if (logging) db = cta_reduce_sum64(S, db);
+    for (u32 k = threadIdx.x; k < m; k += K7_THREADS) S.U[k] = (u16)(T[interval_index<K>(X[p + k], md)] - 1u);
+    __syncthreads();
+    // partition X[p..] -> Y[p..]: cta_partition works on positions 0..m of U, so shift U
+    cta_partition(S, X + p, Y + p, m, gamma + 1);
+    if (logging) {
+        u64 dh = 0;
+        u32 nf = 0, ns = 0, nr = 0;
+        for (u32 u = threadIdx.x; u <= gamma; u += K7_THREADS) {
+            u32 h = S.Hc[u];
+            dh += digest_term(u + 1, h);
+            if (h) { if (h >= delta) nf++; else if (h < tau) ns++; else nr++; }
+        }
+        dh = cta_reduce_sum64(S, dh);
+        u64 cnts = cta_reduce_sum64(S, (u64)nf | ((u64)ns << 21) | ((u64)nr << 42));
+        if (threadIdx.x == 0)
+            write_record(c, L, alpha, gbase + p, m, K::from_okey(mn), K::from_okey(mx), db, dh,
+                         (u32)(cnts & 0x1fffff), (u32)((cnts >> 21) & 0x1fffff), (u32)(cnts >> 42));
+    }
+    cta_dispatch<K>(c, S, xbuf ^ 1u, p, m, gamma + 1, delta, L + 1, gbase, gout);
+}
+
+// ------------------------------------------------------------------ the kernel
+template <class K>
+__global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restrict__ c) {
+    extern __shared__ __align__(16) unsigned char k7_smem_raw[];
+    K7Smem &S = *reinterpret_cast<K7Smem *>(k7_smem_raw);
+    if (*c->nan_flag) return;
+    const u32 ntasks = *c->k7_count;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            S.task_idx = atomicAdd(c->k7_next, 1u);
+            if (S.task_idx < ntasks) S.task = c->k7[S.task_idx];
+            S.nbig = 0;
+        }
+        __syncthreads();
+        if (S.task_idx >= ntasks) break;
+        const K7Task task = S.task;
+        const u64 *src = c->buf[task.src] + task.off;
+        u64 *gout = c->buf[2] + task.off;
+        const u32 m = task.size;
+        bool nan_here = false;
+        for (u32 k = threadIdx.x; k < m; k += K7_THREADS) {
+            u64 raw = src[k];
+            if (K::is_f64 && (raw & 0x7fffffffffffffffull) > 0x7ff0000000000000ull) nan_here = true;
+            S.A[k] = K::to_okey(raw);
+        }
+        if (K::is_f64 && task.level == 1 && __syncthreads_or(nan_here)) {
+            if (threadIdx.x == 0) atomicOr(c->nan_flag, 1u);
+            return;
+        }
+        __syncthreads();
+        if (task.kind == K7_SORT) {
+            cta_sort_write<K>(S.A, m, gout);
+        } else if (task.kind == K7_NODE) {
+            if (m <= WMAX) {
+                if (warp_id() == 0) warp_node<K>(c, S, 0u, 0u, m, task.level, task.off, gout);
+                __syncthreads();
+            } else {
+                if (threadIdx.x == 0) {
+                    BigItem it; it.pos = 0; it.size = m; it.level = task.level; it.buf = 0; it.kind = 0;
+                    S.big[0] = it; S.nbig = 1;
+                }
+                __syncthreads();
+            }
+        } else {  // K7_GROUP: finish the global node's placement for buckets [jlo, jhi)
+            if (threadIdx.x == 0) {
+                const GNode &g = c->nodes[task.node];
+                S.gmd = g.md; S.gT = g.T; S.gH = g.H;
+                S.gnode_delta = g.delta; S.gnode_level = g.level;
+            }
+            __syncthreads();
+            const Model md = S.gmd;
+            const u32 *gT = S.gT;
+            for (u32 k = threadIdx.x; k < m; k += K7_THREADS)
+                S.U[k] = (u16)(__ldg(&gT[interval_index<K>(S.A[k], md)]) - task.jlo);
+            __syncthreads();
+            const u32 nb = task.jhi - task.jlo;
+            cta_partition(S, S.A, S.B, m, nb);
+            for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) S.gH[task.jlo + u] = S.Hc[u];
+            cta_dispatch<K>(c, S, 1u, 0u, m, nb, S.gnode_delta, S.gnode_level + 1, task.off, gout);
+        }
+        // big items (> WMAX): processed by the whole CTA, LIFO
+        for (;;) {
+            __syncthreads();
+            u32 nb_ = S.nbig;
+            if (nb_ == 0 || nb_ > BIG_CAP) break;
+            BigItem it = S.big[nb_ - 1];
+            __syncthreads();
+            if (threadIdx.x == 0) S.nbig = nb_ - 1;
+            __syncthreads();
+            u64 *X = it.buf ? S.B : S.A;
+            if (it.kind == 1) cta_sort_write<K>(X + it.pos, it.size, gout + it.pos);
+            else cta_node<K>(c, S, it.buf, it.pos, it.size, it.level, task.off, gout);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace pcf

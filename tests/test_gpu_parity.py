@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+The bar (integer/index work): bit-exact sorted output AND bit-exact per-node
+records -- (level, offset, m, alpha, x_min/x_max bits, digest of b, digest of H,
+#fallback/#small/#recurse buckets) -- plus the full level-1 b and H arrays.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pcf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2405_07122_b200 as m
+    m.build()
+    m.lib()
+    return m
+
+
+DEV = "cuda:0"
+
+
+def compare(pcf, x, tau=64, seed=0, sample_all=False, check_nodes=True, inplace=False):
+    flags = oracle.FLAG_SAMPLE_ALL if sample_all else 0
+    ref = oracle.learned_sort(x, tau=tau, seed=seed, flags=flags, log=check_nodes, check=True)
+    xt = torch.from_numpy(x.copy()).to(DEV)
+    if inplace:
+        out, info = pcf.sort(xt, xt, tau=tau, seed=seed, sample_all=sample_all, log=check_nodes, stats=True)
+        assert out.data_ptr() == xt.data_ptr()
+    else:
+        out, info = pcf.sort(xt, tau=tau, seed=seed, sample_all=sample_all, log=check_nodes, stats=True)
+        assert np.array_equal(xt.cpu().numpy().view(np.uint64), x.view(np.uint64)), "input was modified"
+    got = out.cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), ref.out.view(np.uint64)), "sorted output differs"
+    if check_nodes:
+        a = oracle.sort_nodes(ref.nodes)
+        b = np.sort(info.nodes, order=["level", "offset"])
+        assert len(a) == len(b), f"node count {len(b)} != oracle {len(a)}"
+        for f in a.dtype.names:
+            if not np.array_equal(a[f], b[f]):
+                bad = np.nonzero(a[f] != b[f])[0][:5]
+                raise AssertionError(f"node field {f} differs at {bad}: gpu {b[bad]} oracle {a[bad]}")
+        if ref.l1_b is not None and len(ref.l1_b):
+            assert np.array_equal(info.level1_b[: len(ref.l1_b)], ref.l1_b), "level-1 b differs"
+            assert np.array_equal(info.level1_h[: len(ref.l1_h)], ref.l1_h), "level-1 H differs"
+    return ref, info
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 63, 64, 65, 100, 1000, 1024, 1025, 4097, 8191, 8192, 8193,
+                               10_000, 50_000, 100_000, 1_000_000, 3_000_000])
+def test_n_sweep_uniform(pcf, n):
+    compare(pcf, synth.generate("uniform", n, 17))
+
+
+@pytest.mark.parametrize("name,n", [("c1", None), ("c2", 2_000_000), ("c3", 2_000_000), ("c4", 2_000_000),
+                                    ("c5f", 2_000_000), ("c5u", 2_000_000)])
+def test_configs_reduced(pcf, name, n):
+    compare(pcf, synth.config(name, n=n))
+
+
+@pytest.mark.parametrize("dist", ["normal", "exponential", "lognormal", "gauss_mix8", "exp700u4", "u64"])
+@pytest.mark.parametrize("n", [5_000, 20_000, 300_000])
+def test_distributions(pcf, dist, n):
+    compare(pcf, synth.generate(dist, n, 3))
+
+
+@pytest.mark.parametrize("tau", [2, 3, 16, 300, 5000])
+def test_tau(pcf, tau):
+    compare(pcf, synth.generate("lognormal", 200_000, 5), tau=tau)
+    compare(pcf, synth.generate("uniform", 3000, 5), tau=tau)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 12345678901234567])
+def test_seeds(pcf, seed):
+    compare(pcf, synth.generate("exponential", 100_000, 8), seed=seed)
+
+
+@pytest.mark.parametrize("n", [500, 6000, 100_000])
+def test_sample_all_mode(pcf, n):
+    compare(pcf, synth.generate("normal", n, 4), sample_all=True)
+
+
+def _patterns(n, rng):
+    base = rng.normal(0, 1, n)
+    out = {
+        "sorted": np.sort(base),
+        "reverse": np.sort(base)[::-1].copy(),
+        "all_equal": np.full(n, 3.25),
+        "two_values": np.where(rng.random(n) < 0.5, -1.0, 2.0),
+        "mixed_zero": np.where(rng.random(n) < 0.5, -0.0, 0.0),
+        "zeros_and_values": np.where(rng.random(n) < 0.3, rng.choice([-0.0, 0.0], n), base),
+        "overflow_range": np.where(rng.random(n) < 0.5, -1e308, 1e308) * rng.random(n),
+        "with_inf": np.where(rng.random(n) < 0.01, np.inf, base),
+        "with_neg_inf": np.where(rng.random(n) < 0.01, -np.inf, base),
+        "subnormal": rng.random(n) * 5e-320,
+        "dup_heavy": np.round(base * 3) / 3,
+        "few_distinct": rng.integers(0, 5, n).astype(np.float64),
+        "ties_at_edges": np.concatenate([np.zeros(n // 3), np.ones(n - n // 3)]),
+    }
+    return out
+
+
+@pytest.mark.parametrize("n", [50, 3000, 9000, 120_000])
+def test_patterns(pcf, n):
+    rng = np.random.default_rng(n)
+    for name, x in _patterns(n, rng).items():
+        try:
+            compare(pcf, np.ascontiguousarray(x, dtype=np.float64))
+        except AssertionError as e:
+            raise AssertionError(f"pattern {name}: {e}")
+
+
+def test_u64_patterns(pcf):
+    rng = np.random.default_rng(9)
+    for x in [np.arange(100_000, dtype=np.uint64)[::-1].copy(),
+              np.full(20_000, 7, dtype=np.uint64),
+              (synth.generate("u64", 200_000, 1) >> np.uint64(40)).astype(np.uint64),
+              np.array([0, 2 ** 64 - 1] * 5000, dtype=np.uint64),
+              rng.integers(0, 3, 50_000).astype(np.uint64)]:
+        compare(pcf, x)
+
+
+def test_inplace(pcf):
+    compare(pcf, synth.generate("lognormal", 500_000, 11), inplace=True)
+    compare(pcf, synth.generate("uniform", 3000, 11), inplace=True)
+
+
+@pytest.mark.parametrize("n", [10, 5000, 100_000])
+def test_nan_is_error(pcf, n):
+    x = synth.generate("uniform", n, 1)
+    x[n // 2] = np.nan
+    with pytest.raises(pcf.PCFError) as e:
+        pcf.sort(torch.from_numpy(x).to(DEV))
+    assert e.value.status == 2
+
+
+def test_determinism(pcf):
+    x = torch.from_numpy(synth.generate("lognormal", 1_000_000, 2)).to(DEV)
+    outs = [pcf.sort(x, log=True) for _ in range(5)]
+    for o, info in outs[1:]:
+        assert torch.equal(o, outs[0][0])
+        assert np.array_equal(np.sort(info.nodes, order=["level", "offset"]),
+                              np.sort(outs[0][1].nodes, order=["level", "offset"]))
+
+
+def test_host_entry(pcf):
+    x = synth.generate("exponential", 200_000, 6)
+    got = pcf.sort_host(x)
+    assert np.array_equal(got.view(np.uint64), oracle.learned_sort(x).out.view(np.uint64))
+    u = synth.generate("u64", 100_000, 6)
+    assert np.array_equal(pcf.sort_host(u), np.sort(u))
+
+
+def test_full_size_c2_exact(pcf):
+    """configs[1] at its BASELINE.json size (1e7): full output and all node records."""
+    compare(pcf, synth.config("c2"))
+
+
+def test_full_size_c1_exact(pcf):
+    compare(pcf, synth.config("c1"))
