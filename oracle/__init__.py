@@ -236,7 +236,8 @@ def learned_sort(x: np.ndarray, tau: int = 64, seed: int = 0, flags: int = 0, lo
     ctx.tau, ctx.flags, ctx.seed, ctx.check = tau, flags, seed, 1 if check else 0
     nodes = l1b = l1h = None
     if log:
-        cap = node_cap if node_cap is not None else max(16, n // 8 + 16)
+        # every node has >= tau keys and nodes of one level are disjoint; <= ~12 levels
+        cap = node_cap if node_cap is not None else min(n, 12 * (n // max(tau, 1))) + 16
         nodes = np.zeros(cap, dtype=NODE_DTYPE)
         ctx.nodes, ctx.nodes_cap = nodes.ctypes.data, cap
         l1cap = iroot34(n) + 2 if n else 2

@@ -153,7 +153,7 @@ def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False,
     info = SortInfo() if (log or timing or stats) else None
     keep = []
     if log:
-        cap = node_capacity if node_capacity is not None else max(64, n // 8 + 64)
+        cap = node_capacity if node_capacity is not None else min(n, 12 * (n // max(tau, 1))) + 64
         recs = torch.zeros(cap * 9, dtype=torch.int64, device=x.device)   # 72-byte records
         cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
         from math import isqrt

@@ -361,6 +361,10 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
                 if (lane == 0)
                     write_record(c, L, alpha, gbase + p, m, K::from_okey(mn), K::from_okey(mx), db, dh, nf,
                                  ns, nr);
+                if (L == 1 && c->l1_b) {
+                    for (u32 i = lane; i <= beta && i < c->l1_cap; i += 32) c->l1_b[i] = ws.cnt[i + 1];
+                    for (u32 u = lane; u <= gamma && u < c->l1_cap; u += 32) c->l1_h[u] = ws.H[u];
+                }
             }
         }
         // children in bucket order: windows of Standard-Sort buckets, pushes of recursions
@@ -609,7 +613,10 @@ __device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32
         cnt[i + 1] = b;
     }
     __syncthreads();
-    for (u32 i = threadIdx.x; i <= beta; i += K7_THREADS) T[i + 1] = bucket_of(cnt[i + 1], alpha, gamma);
+    for (u32 i = threadIdx.x; i <= beta; i += K7_THREADS) {
+        T[i + 1] = bucket_of(cnt[i + 1], alpha, gamma);
+        if (logging && L == 1 && c->l1_b && i < c->l1_cap) c->l1_b[i] = cnt[i + 1];
+    }
     __syncthreads();
     if (logging) db = cta_reduce_sum64(S, db);
     for (u32 k = threadIdx.x; k < m; k += K7_THREADS) S.U[k] = (u16)(T[interval_index<K>(X[p + k], md)] - 1u);
@@ -629,6 +636,8 @@ __device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32
         if (threadIdx.x == 0)
             write_record(c, L, alpha, gbase + p, m, K::from_okey(mn), K::from_okey(mx), db, dh,
                          (u32)(cnts & 0x1fffff), (u32)((cnts >> 21) & 0x1fffff), (u32)(cnts >> 42));
+        if (L == 1 && c->l1_h)
+            for (u32 u = threadIdx.x; u <= gamma && u < c->l1_cap; u += K7_THREADS) c->l1_h[u] = S.Hc[u];
     }
     cta_dispatch<K>(c, S, xbuf ^ 1u, p, m, gamma + 1, delta, L + 1, gbase, gout);
 }
