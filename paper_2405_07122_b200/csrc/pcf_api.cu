@@ -329,10 +329,17 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             k_node_model<K><<<1, 1, 0, st>>>(dc, idx);
             u32 alpha = g.alpha;
             k_fit_sample<K><<<(alpha + 255) / 256, 256, 0, st>>>(dc, idx);
-            k_fit_scan<<<1, 1024, 0, st>>>(dc, idx);
+            {
+                u64 nbins = (u64)P + 1;
+                u32 nblk = (u32)((nbins + SCAN_CHUNK - 1) / SCAN_CHUNK);
+                u32 *bs = (u32 *)(ws + L.bsum);
+                k_scan_partials<<<nblk, SCAN_THREADS, 0, st>>>(g.cnt + 1, nbins, bs);
+                k_scan_bsums<<<1, SCAN_THREADS, 0, st>>>(bs, nblk);
+                k_fit_final<<<nblk, SCAN_THREADS, 0, st>>>(dc, idx, bs);
+            }
             tm.end();
             CK(cudaGetLastError());
-            launches += 4;
+            launches += 6;
             bytes[PH_MINMAX] += 8ull * m;
             bytes[PH_FIT] += 8ull * alpha + 8ull * (P + 2);
             stats.global_nodes++;

@@ -14,6 +14,7 @@ namespace pcf {
 typedef unsigned long long u64;
 typedef unsigned int u32;
 typedef unsigned short u16;
+typedef unsigned char u8;
 
 // ---------------------------------------------------------------- tunables
 constexpr int K7_THREADS = 512;          // smem-subtree kernel block

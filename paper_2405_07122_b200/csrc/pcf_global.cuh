@@ -114,58 +114,6 @@ __global__ void k_fit_sample(const DevCtx *__restrict__ c, u32 node) {
     atomicAdd(&g.cnt[interval_index<K>(K::to_okey(raw), md)], 1u);
 }
 
-// One CTA: b[i] = sum_{i'<=i} cnt[i'] for i = 1..beta+1 in place; T[i] = bucket_of(b_i).
-__global__ void __launch_bounds__(1024) k_fit_scan(const DevCtx *__restrict__ c, u32 node) {
-    if (*c->nan_flag) return;
-    GNode &g = c->nodes[node];
-    if (g.degenerate) return;
-    const u32 nb = g.beta + 1;
-    const bool logging = c->rec != nullptr;
-    const bool copy_l1 = g.level == 1 && c->l1_b != nullptr;
-    __shared__ u32 wsum[32];
-    __shared__ u32 carry_s;
-    __shared__ u64 dsum[32];
-    if (threadIdx.x == 0) carry_s = 0;
-    u64 db = 0;
-    const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (u32 base = 1; base <= nb; base += 1024) {
-        __syncthreads();
-        u32 i = base + threadIdx.x;
-        u32 v = i <= nb ? g.cnt[i] : 0;
-        u32 x = v;
-        for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= (u32)o) x += y; }
-        if (lane == 31) wsum[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            u32 s = wsum[lane];
-            u32 t = s;
-            for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, t, o); if (lane >= (u32)o) t += y; }
-            wsum[lane] = t - s;
-        }
-        __syncthreads();
-        u32 carry = carry_s;
-        u32 b = carry + wsum[w] + x;
-        if (i <= nb) {
-            g.cnt[i] = b;
-            g.T[i] = bucket_of(b, g.alpha, g.gamma);
-            if (logging) db += digest_term(i, b);
-            if (copy_l1 && i - 1 < c->l1_cap) c->l1_b[i - 1] = b;
-        }
-        __syncthreads();
-        if (threadIdx.x == 1023) carry_s = b;
-    }
-    if (logging) {
-        for (int o = 16; o > 0; o >>= 1) db += __shfl_xor_sync(0xffffffffu, db, o);
-        if (lane == 0) dsum[w] = db;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            u64 s = 0;
-            for (int k = 0; k < 32; ++k) s += dsum[k];
-            g.digest_b = s;
-        }
-    }
-}
-
 // ------------------------------------------------------------------ splits
 __device__ __forceinline__ u32 find_split(const SplitTask *L, u32 ns, u32 tile) {
     u32 lo = 0, hi = ns - 1;
@@ -199,10 +147,20 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__r
     } else {
         const Model md = g.md;
         const u64 *x = c->buf[st.src] + st.off;
-        for (u32 k = k0 + threadIdx.x; k < k1; k += SPLIT_THREADS) {
-            u32 d = digit_of<K>(K::to_okey(x[k]), md, g.T, st.jlo, st.shift);
-            atomicAdd(&hist[d], 1u);
+        const u32 *T = g.T;
+        constexpr u32 UB = 4;
+        u32 k = k0 + threadIdx.x;
+        for (; k + (UB - 1) * SPLIT_THREADS < k1; k += UB * SPLIT_THREADS) {
+            u64 raw[UB];
+            u32 ix[UB];
+#pragma unroll
+            for (u32 q = 0; q < UB; ++q) raw[q] = x[k + q * SPLIT_THREADS];
+#pragma unroll
+            for (u32 q = 0; q < UB; ++q) ix[q] = __ldg(&T[interval_index<K>(K::to_okey(raw[q]), md)]);
+#pragma unroll
+            for (u32 q = 0; q < UB; ++q) atomicAdd(&hist[(ix[q] - st.jlo) >> st.shift], 1u);
         }
+        for (; k < k1; k += SPLIT_THREADS) atomicAdd(&hist[digit_of<K>(K::to_okey(x[k]), md, T, st.jlo, st.shift)], 1u);
     }
     __syncthreads();
     for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
@@ -271,6 +229,47 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const u32 *__restri
     for (int k = 0; k < SCAN_ITEMS; ++k) { if (base + k < n) out[base + k] = e; e += v[k]; }
 }
 
+// b[i] = inclusive prefix of cnt[1..beta+1] (exclusive block offsets from the
+// k_scan_partials/k_scan_bsums pass over cnt+1), T[i] = floor(b_i*gamma/alpha)+1
+// (R7), digest of b and the level-1 dump for the pass log.
+__global__ void __launch_bounds__(SCAN_THREADS) k_fit_final(const DevCtx *__restrict__ c, u32 node, const u32 *__restrict__ bsum) {
+    __shared__ u32 wsum[33];
+    __shared__ unsigned long long dsum;
+    if (*c->nan_flag) return;
+    GNode &g = c->nodes[node];
+    if (g.degenerate) return;
+    const u64 n = g.beta + 1;
+    const bool logging = c->rec != nullptr;
+    const bool copy_l1 = g.level == 1 && c->l1_b != nullptr;
+    u32 *in = g.cnt + 1;
+    if (threadIdx.x == 0) dsum = 0;
+    const u64 base = (u64)blockIdx.x * SCAN_CHUNK + (u64)threadIdx.x * SCAN_ITEMS;
+    u32 v[SCAN_ITEMS];
+    u32 s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) { v[k] = base + k < n ? in[base + k] : 0; s += v[k]; }
+    u32 total;
+    u32 e = block_excl_scan_1024(s, wsum, total) + bsum[blockIdx.x];
+    u64 db = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        e += v[k];
+        if (base + k < n) {
+            const u64 i = base + k + 1;   // 1-based interval index
+            in[base + k] = e;
+            g.T[i] = bucket_of(e, g.alpha, g.gamma);
+            if (logging) db += digest_term(i, e);
+            if (copy_l1 && i - 1 < c->l1_cap) c->l1_b[i - 1] = e;
+        }
+    }
+    if (logging) {
+        for (int o = 16; o > 0; o >>= 1) db += __shfl_xor_sync(0xffffffffu, db, o);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&dsum, (unsigned long long)db);
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd((unsigned long long *)&g.digest_b, dsum);
+    }
+}
+
 // --- stable scatter by digit
 struct SplitScatterSmem {
     u32 wc[SPLIT_THREADS / 32][GMAX];
@@ -299,35 +298,57 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_scatter(const DevCtx *_
     const u32 r0 = min(k0 + w * R, k1), r1 = min(r0 + R, k1);
     for (u32 d = lane; d < st.G; d += 32) S.wc[w][d] = 0;
     __syncwarp();
-    for (u32 kb = r0; kb < r1; kb += 32) {
-        u32 k = kb + lane;
-        bool act = k < r1;
-        u32 d = 0xffffffffu;
-        if (act) { d = digit_of<K>(K::to_okey(x[k]), md, T, st.jlo, st.shift); S.dig[k - k0] = (u16)d; }
-        u32 peers = __match_any_sync(0xffffffffu, d);
-        if (act && (peers & ((1u << lane) - 1)) == 0) S.wc[w][d] += __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-    for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) {
-        u32 run = P[st.cbase + (u64)d * st.ntiles + lt] - (u32)st.mbase;
-        for (u32 ww = 0; ww < NW; ++ww) { u32 cc = S.wc[ww][d]; S.wc[ww][d] = run; run += cc; }
-    }
-    __syncthreads();
-    for (u32 kb = r0; kb < r1; kb += 32) {
-        u32 k = kb + lane;
-        bool act = k < r1;
-        u32 d = act ? (u32)S.dig[k - k0] : 0xffffffffu;
-        u64 raw = act ? x[k] : 0;
-        u32 peers = __match_any_sync(0xffffffffu, d);
-        u32 base = act ? S.wc[w][d] : 0;
-        __syncwarp();
-        if (act) {
-            u32 rank = __popc(peers & ((1u << lane) - 1));
-            y[base + rank] = raw;
-            if (rank == 0) S.wc[w][d] = base + __popc(peers);
+    constexpr u32 UB = 4;
+    for (u32 kb = r0; kb < r1; kb += 32 * UB) {
+        u64 raw[UB];
+        u32 d[UB];
+#pragma unroll
+        for (u32 q = 0; q < UB; ++q) { u32 k = kb + q * 32 + lane; raw[q] = k < r1 ? x[k] : 0; }
+#pragma unroll
+        for (u32 q = 0; q < UB; ++q) {
+            u32 k = kb + q * 32 + lane;
+            d[q] = k < r1 ? interval_index<K>(K::to_okey(raw[q]), md) : 0u;
         }
-        __syncwarp();
+#pragma unroll
+        for (u32 q = 0; q < UB; ++q) {
+            u32 k = kb + q * 32 + lane;
+            d[q] = k < r1 ? (__ldg(&T[d[q]]) - st.jlo) >> st.shift : 0xffffffffu;
+        }
+#pragma unroll
+        for (u32 q = 0; q < UB; ++q) {
+            u32 k = kb + q * 32 + lane;
+            bool act = k < r1;
+            if (act) S.dig[k - k0] = (u16)d[q];
+            u32 peers = __match_any_sync(0xffffffffu, d[q]);
+            if (act && (peers & ((1u << lane) - 1)) == 0) S.wc[w][d[q]] += __popc(peers);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (u32 dd = threadIdx.x; dd < st.G; dd += SPLIT_THREADS) {
+        u32 run = P[st.cbase + (u64)dd * st.ntiles + lt] - (u32)st.mbase;
+        for (u32 ww = 0; ww < NW; ++ww) { u32 cc = S.wc[ww][dd]; S.wc[ww][dd] = run; run += cc; }
+    }
+    __syncthreads();
+    for (u32 kb = r0; kb < r1; kb += 32 * UB) {
+        u64 raw[UB];
+#pragma unroll
+        for (u32 q = 0; q < UB; ++q) { u32 k = kb + q * 32 + lane; raw[q] = k < r1 ? x[k] : 0; }
+#pragma unroll
+        for (u32 q = 0; q < UB; ++q) {
+            u32 k = kb + q * 32 + lane;
+            bool act = k < r1;
+            u32 d = act ? (u32)S.dig[k - k0] : 0xffffffffu;
+            u32 peers = __match_any_sync(0xffffffffu, d);
+            u32 base = act ? S.wc[w][d] : 0;
+            __syncwarp();
+            if (act) {
+                u32 rank = __popc(peers & ((1u << lane) - 1));
+                y[base + rank] = raw[q];
+                if (rank == 0) S.wc[w][d] = base + __popc(peers);
+            }
+            __syncwarp();
+        }
     }
 }
 

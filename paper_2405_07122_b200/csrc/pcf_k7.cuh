@@ -11,14 +11,17 @@
 //   K7_SORT  : a bucket that Alg. 1 sends to Standard-Sort (|c_j| >= delta or
 //              n < tau): sorted and written out.
 // The task's keys are loaded once (HBM read), every deeper level runs in
-// shared memory, and each finished run of buckets is written once to `out`.
+// shared memory, and each finished bucket is written once to `out`.
 //
-// Segments > WMAX keys are processed by the whole CTA (cta_node); segments of
-// <= WMAX keys by one warp each (warp_node), with an explicit DFS stack.
-// Stable placement uses per-warp counters over warp-contiguous key ranges
-// (CTA) or in-order 32-key chunks with __match_any_sync (warp), so the order of
-// every bucket equals the Append order and the next level samples the same
-// keys as the oracle (readings R4, R16).
+// After every partition the children are classified in parallel (one thread
+// or lane per bucket): buckets Alg. 1 sends to Standard-Sort with <= 64 keys
+// are sorted by a key-parallel rank pass (each key counts the smaller keys of
+// its own bucket -- O(|c_j|) per key); larger sorted buckets use a bitonic
+// network; recursing buckets become warp items (<= WMAX keys, warp_node with an
+// explicit DFS stack) or CTA items (> WMAX, cta_node).  Stable placement uses
+// per-warp counters over warp-contiguous key ranges (CTA) or in-order 32-key
+// chunks with __match_any_sync (warp), so every bucket keeps the Append order
+// and the next level samples the same keys as the oracle (readings R4, R16).
 #pragma once
 #include "pcf_common.cuh"
 
@@ -26,9 +29,9 @@ namespace pcf {
 
 struct WarpScratch {
     u16 cnt[WNB];    // per-bin sample counts -> b (inclusive prefix), 1-based
-    u16 T[WNB];      // bucket table, 1-based
+    u16 T[WNB];      // bucket table, 1-based; reused for the child kinds
     u16 H[WNB];      // bucket sizes, 0-based bucket index u = j-1
-    u16 C[WNB];      // running cursors / bucket ends
+    u16 C[WNB];      // running cursors -> bucket ends
     u32 stack[WSTACK];
 };
 
@@ -37,13 +40,17 @@ struct BigItem {
 };
 
 constexpr int BIG_CAP = 48;
+constexpr int ITEM_CAP = NB_CAP + 64;
+enum : u32 { CK_EMPTY = 0, CK_RANK = 1, CK_RECURSE = 2, CK_BITONIC = 3 };
 
 struct K7Smem {
     u64 A[S_CAP];
     u64 B[S_CAP];
-    u16 U[S_CAP];
-    u32 Hc[NB_CAP + 1];
-    u32 Bs[NB_CAP + 1];
+    u16 U[S_CAP];            // bucket index per buffer position
+    u32 Hc[NB_CAP + 1];      // CTA-level bucket sizes
+    u32 Bs[NB_CAP + 1];      // CTA-level bucket starts (absolute buffer positions)
+    u8 kindc[NB_CAP + 4];
+    u32 items[ITEM_CAP];     // warp items: pos(13) | size(11) << 13 | kind(1) << 24 (0 node, 1 sort)
     union {
         u16 wcnt[K7_WARPS][NB_CAP];               // CTA partition per-warp counters
         struct { u32 cnt[S_CAP / 8 + 8]; u32 T[S_CAP / 8 + 8]; } fit;   // CTA fit (beta+2 <= 863)
@@ -51,15 +58,12 @@ struct K7Smem {
     } u;
     BigItem big[BIG_CAP];
     u64 red[2 * K7_WARPS];
-    u32 redu[4 * K7_WARPS];
     u32 scan_tmp[K7_WARPS + 1];
     K7Task task;
     u32 task_idx;
     u32 nbig;
-    u32 chunk_next;
-    u32 nchunks;
-    u32 chunk_sz;
-    u32 gnode_beta, gnode_delta, gnode_level;
+    u32 nitems, item_next;
+    u32 gnode_delta, gnode_level;
     Model gmd;
     const u32 *gT;
     u32 *gH;
@@ -91,7 +95,6 @@ __device__ __forceinline__ u32 warp_sum_u32(u32 v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
-// inclusive warp scan
 __device__ __forceinline__ u32 warp_incl_scan(u32 v) {
     u32 lane = lane_id();
     for (int o = 1; o < 32; o <<= 1) {
@@ -99,6 +102,16 @@ __device__ __forceinline__ u32 warp_incl_scan(u32 v) {
         if (lane >= (u32)o) v += w;
     }
     return v;
+}
+
+// floor(m^{3/4}) for m <= S_CAP (m^3 < 2^40): float estimate + exact u64 fix-up (R5)
+__device__ __forceinline__ u32 iroot34_small(u32 m) {
+    u64 m3 = (u64)m * m * m;
+    u32 c = (u32)sqrtf(sqrtf((float)m3));
+    auto p4 = [](u64 x) { return x * x * x * x; };
+    while (c > 0 && p4(c) > m3) --c;
+    while (p4((u64)c + 1) <= m3) ++c;
+    return c;
 }
 
 // ------------------------------------------------------------------ node record (pass log)
@@ -143,50 +156,20 @@ __device__ void warp_bitonic_smem(u64 *a, u32 n) {
     }
 }
 
-// Register bitonic for n <= 64: lane l holds elements l and l+32.
-__device__ void warp_sort64_write(const u64 *a, u32 n, u64 *gout_raw, bool f64) {
-    u32 lane = lane_id();
-    u64 v0 = lane < n ? a[lane] : ~0ull;
-    u64 v1 = lane + 32 < n ? a[lane + 32] : ~0ull;
-    if (n > 32) {
-        for (u32 k = 2; k <= 64; k <<= 1) {
-            for (u32 j = k >> 1; j > 0; j >>= 1) {
-                if (j == 32) {
-                    // partner of element i=lane is i+32 (same lane), ascending since (i & 64) == 0
-                    u64 lo = v0 < v1 ? v0 : v1, hi = v0 < v1 ? v1 : v0;
-                    v0 = lo; v1 = hi;
-                } else {
-                    u64 p0 = __shfl_xor_sync(0xffffffffu, v0, j);
-                    u64 p1 = __shfl_xor_sync(0xffffffffu, v1, j);
-                    u32 i0 = lane, i1 = lane + 32;
-                    bool up0 = (i0 & k) == 0, up1 = (i1 & k) == 0;
-                    bool low0 = (i0 & j) == 0, low1 = (i1 & j) == 0;
-                    v0 = (low0 == up0) ? (v0 < p0 ? v0 : p0) : (v0 > p0 ? v0 : p0);
-                    v1 = (low1 == up1) ? (v1 < p1 ? v1 : p1) : (v1 > p1 ? v1 : p1);
-                }
-            }
-        }
-    } else {
-        for (u32 k = 2; k <= 32; k <<= 1) {
-            for (u32 j = k >> 1; j > 0; j >>= 1) {
-                u64 p0 = __shfl_xor_sync(0xffffffffu, v0, j);
-                bool up = (lane & k) == 0, low = (lane & j) == 0;
-                v0 = (low == up) ? (v0 < p0 ? v0 : p0) : (v0 > p0 ? v0 : p0);
-            }
-        }
-    }
-    if (lane < n) gout_raw[lane] = f64 ? KeyF64::from_okey(v0) : v0;
-    if (lane + 32 < n) gout_raw[lane + 32] = f64 ? KeyF64::from_okey(v1) : v1;
-}
-
+// Whole segment a[0, n) sorted by one warp and written (raw keys) to gout[0, n).
 template <class K>
 __device__ void warp_sort_write(u64 *a, u32 n, u64 *gout_raw) {
-    if (n == 0) return;
-    if (n <= 64) {
-        warp_sort64_write(a, n, gout_raw, K::is_f64);
+    const u32 lane = lane_id();
+    if (n <= 64) {   // rank sort: each key counts the keys before it in sorted order
+        for (u32 i = lane; i < n; i += 32) {
+            u64 v = a[i];
+            u32 r = 0;
+            for (u32 j = 0; j < n; ++j) { u64 w = a[j]; r += (w < v) | ((w == v) & (j < i)); }
+            gout_raw[r] = K::from_okey(v);
+        }
     } else {
         warp_bitonic_smem(a, n);
-        for (u32 k = lane_id(); k < n; k += 32) gout_raw[k] = K::from_okey(a[k]);
+        for (u32 k = lane; k < n; k += 32) gout_raw[k] = K::from_okey(a[k]);
     }
     __syncwarp();
 }
@@ -218,30 +201,18 @@ __device__ void cta_sort_write(u64 *a, u32 n, u64 *gout_raw) {
     __syncthreads();
 }
 
-// ------------------------------------------------------------------ warp window of sorted buckets
-// Consecutive buckets sent to Standard-Sort are sorted together: by the order
-// property sorting their concatenation equals
-// concatenating the individually sorted buckets.
-struct Window {
-    u32 start, len;
-};
-
+// Rank-sort the key at buffer position i of a small bucket [s, e) and write it.
 template <class K>
-__device__ __forceinline__ void window_flush(Window &w, u64 *Y, u64 *gout) {
-    if (w.len) warp_sort_write<K>(Y + w.start, w.len, gout + w.start);
-    w.len = 0;
-}
-template <class K>
-__device__ __forceinline__ void window_add(Window &w, u64 *Y, u64 *gout, u32 pos, u32 h) {
-    if (w.len && (w.len + h > 64 || pos != w.start + w.len)) window_flush<K>(w, Y, gout);
-    if (w.len == 0) w.start = pos;
-    w.len += h;
-    if (w.len > 64) window_flush<K>(w, Y, gout);
+__device__ __forceinline__ void rank_place(const u64 *Y, u32 i, u32 s, u32 e, u64 *gout) {
+    const u64 v = Y[i];
+    u32 r = 0;
+    for (u32 j = s; j < e; ++j) { u64 w = Y[j]; r += (w < v) | ((w == v) & (j < i)); }
+    gout[s + r] = K::from_okey(v);
 }
 
 // ------------------------------------------------------------------ warp-level Alg. 1
-// Learned-Sort of the segment X[p, p+m) (m <= WMAX, m >= tau) at level L, global
-// offset gbase + p, and all its descendants; finished runs go to gout[pos].
+// Learned-Sort of the segment X[p, p+m) (m <= WMAX) at level L, global offset
+// gbase + p, and all its descendants; finished buckets go to gout[pos].
 // Stack entries: pos(13) | size(11) | depth(4) | buf(1).
 template <class K>
 __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, u32 L0, u64 gbase,
@@ -251,165 +222,150 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
     const u32 tau = c->tau;
     const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
     const bool logging = c->rec != nullptr;
-    u32 sp = 0;
-    if (lane == 0) ws.stack[0] = p0 | (m0 << 13) | (0u << 24) | (buf0 << 28);
-    sp = 1;
+    if (lane == 0) ws.stack[0] = p0 | (m0 << 13) | (buf0 << 28);
+    u32 sp = 1;
     __syncwarp();
     while (sp > 0) {
-        u32 e = ws.stack[--sp];
+        const u32 e = ws.stack[--sp];
         __syncwarp();
-        u32 p = e & 0x1fffu, m = (e >> 13) & 0x7ffu, d = (e >> 24) & 0xfu, bi = e >> 28;
-        if (m == 0) m = 2048;   // never: sizes are <= WMAX = 1024 (< 2048)
+        const u32 p = e & 0x1fffu, m = (e >> 13) & 0x7ffu, d = (e >> 24) & 0xfu, bi = e >> 28;
         u64 *X = bi ? S.B : S.A;
         u64 *Y = bi ? S.A : S.B;
-        u32 L = L0 + d;
-        Window win; win.len = 0; win.start = 0;
-        if (m < tau) { window_add<K>(win, X, gout, p, m); window_flush<K>(win, X, gout); continue; }
+        const u32 L = L0 + d;
+        if (m < tau) { warp_sort_write<K>(X + p, m, gout + p); continue; }
         // x_min, x_max over the segment
         u64 mn = ~0ull, mx = 0;
         for (u32 k = lane; k < m; k += 32) { u64 v = X[p + k]; mn = v < mn ? v : mn; mx = v > mx ? v : mx; }
-        mn = warp_min_u64(mn); mx = warp_max_u64(mx);
+        mn = warp_min_u64(mn);
+        mx = warp_max_u64(mx);
         Model md;
-        u32 P = (u32)iroot34(m);
-        if (!make_model<K>(mn, mx, P, md)) {   // R9/R10: Standard-Sort
-            warp_sort_write<K>(X + p, m, gout + p);
-            continue;
-        }
+        const u32 P = iroot34_small(m);
+        if (!make_model<K>(mn, mx, P, md)) { warp_sort_write<K>(X + p, m, gout + p); continue; }   // R9/R10
         const u32 alpha = sample_all ? m : P, beta = P, gamma = P, delta = P;
+        const u32 ng = gamma + 1;
         for (u32 i = lane; i <= beta + 1; i += 32) ws.cnt[i] = 0;
+        for (u32 u = lane; u < ng; u += 32) ws.H[u] = 0;
         __syncwarp();
         // sample (R3, R4) and count per interval
         const u64 nkey = node_key(c->seed, L, gbase + p);
         for (u32 k0 = 0; k0 < alpha; k0 += 32) {
-            u32 k = k0 + lane;
-            bool act = k < alpha;
+            const u32 k = k0 + lane;
+            const bool act = k < alpha;
             u32 i = 0xffffffffu;
-            if (act) {
-                u32 pos = sample_all ? k : (u32)sample_pos(nkey, k, m);
-                i = interval_index<K>(X[p + pos], md);
-            }
-            u32 peers = __match_any_sync(0xffffffffu, i);
+            if (act) i = interval_index<K>(X[p + (sample_all ? k : (u32)sample_pos(nkey, k, m))], md);
+            const u32 peers = __match_any_sync(0xffffffffu, i);
             if (act && (peers & lanemask_lt()) == 0) ws.cnt[i] += (u16)__popc(peers);
             __syncwarp();
         }
         // b = inclusive prefix of the counts, T = floor(b*gamma/alpha)+1
+        u64 db = 0;
         {
-            u32 nb = beta + 1;                       // entries 1..beta+1
-            u32 per = (nb + 31) / 32;
-            u32 s0 = 1 + lane * per, s1 = min(s0 + per, nb + 1);
+            const u32 nb = beta + 1;
+            const u32 per = (nb + 31) / 32;
+            const u32 s0 = 1 + lane * per, s1 = min(s0 + per, nb + 1);
             u32 loc = 0;
             for (u32 i = s0; i < s1; ++i) loc += ws.cnt[i];
-            u32 incl = warp_incl_scan(loc);
-            u32 run = incl - loc;
-            u64 db = 0;
+            u32 run = warp_incl_scan(loc) - loc;
             for (u32 i = s0; i < s1; ++i) {
                 run += ws.cnt[i];
                 ws.cnt[i] = (u16)run;
                 ws.T[i] = (u16)bucket_of(run, alpha, gamma);
                 if (logging) db += digest_term(i, run);
             }
-            if (logging) db = warp_sum_u64(db);
+        }
+        __syncwarp();
+        // classify every key: u = T[i(x)] - 1; histogram H[u]
+        for (u32 k0 = 0; k0 < m; k0 += 32) {
+            const u32 k = k0 + lane;
+            const bool act = k < m;
+            u32 u = 0xffffffffu;
+            if (act) { u = ws.T[interval_index<K>(X[p + k], md)] - 1u; S.U[p + k] = (u16)u; }
+            const u32 peers = __match_any_sync(0xffffffffu, u);
+            if (act && (peers & lanemask_lt()) == 0) ws.H[u] += (u16)__popc(peers);
             __syncwarp();
-            // classify every key: u = T[i(x)] - 1; histogram H[u]
-            for (u32 u = lane; u <= gamma; u += 32) ws.H[u] = 0;
-            __syncwarp();
-            for (u32 k0 = 0; k0 < m; k0 += 32) {
-                u32 k = k0 + lane;
-                bool act = k < m;
-                u32 u = 0xffffffffu;
-                if (act) { u = ws.T[interval_index<K>(X[p + k], md)] - 1u; S.U[p + k] = (u16)u; }
-                u32 peers = __match_any_sync(0xffffffffu, u);
-                if (act && (peers & lanemask_lt()) == 0) ws.H[u] += (u16)__popc(peers);
-                __syncwarp();
-            }
-            // exclusive prefix of H -> cursors
-            u32 ng = gamma + 1;
-            u32 perg = (ng + 31) / 32;
-            u32 g0 = lane * perg, g1 = min(g0 + perg, ng);
+        }
+        // exclusive prefix of H -> cursors
+        {
+            const u32 perg = (ng + 31) / 32;
+            const u32 g0 = lane * perg, g1 = min(g0 + perg, ng);
             u32 locg = 0;
             for (u32 u = g0; u < g1; ++u) locg += ws.H[u];
-            u32 inclg = warp_incl_scan(locg);
-            u32 rg = inclg - locg;
+            u32 rg = warp_incl_scan(locg) - locg;
             for (u32 u = g0; u < g1; ++u) { ws.C[u] = (u16)rg; rg += ws.H[u]; }
+        }
+        __syncwarp();
+        // stable scatter (Append in index order)
+        for (u32 k0 = 0; k0 < m; k0 += 32) {
+            const u32 k = k0 + lane;
+            const bool act = k < m;
+            const u32 u = act ? (u32)S.U[p + k] : 0xffffffffu;
+            const u32 peers = __match_any_sync(0xffffffffu, u);
+            const u32 base = act ? ws.C[u] : 0;
             __syncwarp();
-            // stable scatter (Append in index order)
-            for (u32 k0 = 0; k0 < m; k0 += 32) {
-                u32 k = k0 + lane;
-                bool act = k < m;
-                u32 u = act ? (u32)S.U[p + k] : 0xffffffffu;
-                u32 peers = __match_any_sync(0xffffffffu, u);
-                u32 base = act ? ws.C[u] : 0;
-                __syncwarp();
-                if (act) {
-                    u32 rank = __popc(peers & lanemask_lt());
-                    Y[p + base + rank] = X[p + k];
-                    if (rank == 0) ws.C[u] = (u16)(base + __popc(peers));
-                }
-                __syncwarp();
+            if (act) {
+                const u32 rank = __popc(peers & lanemask_lt());
+                Y[p + base + rank] = X[p + k];
+                if (rank == 0) ws.C[u] = (u16)(base + __popc(peers));
             }
-            // node record (pass log) and child dispatch
+            __syncwarp();
+        }
+        // ws.C[u] = end of bucket u (relative to p).  Node record (pass log).
+        if (logging) {
             u32 nf = 0, ns = 0, nr = 0;
             u64 dh = 0;
-            for (u32 u = lane; u <= gamma; u += 32) {
-                u32 h = ws.H[u];
-                if (logging) dh += digest_term(u + 1, h);
+            for (u32 u = lane; u < ng; u += 32) {
+                const u32 h = ws.H[u];
+                dh += digest_term(u + 1, h);
                 if (h) { if (h >= delta) nf++; else if (h < tau) ns++; else nr++; }
             }
-            if (logging) {
-                dh = warp_sum_u64(dh);
-                nf = warp_sum_u32(nf); ns = warp_sum_u32(ns); nr = warp_sum_u32(nr);
-                if (lane == 0)
-                    write_record(c, L, alpha, gbase + p, m, K::from_okey(mn), K::from_okey(mx), db, dh, nf,
-                                 ns, nr);
-                if (L == 1 && c->l1_b) {
-                    for (u32 i = lane; i <= beta && i < c->l1_cap; i += 32) c->l1_b[i] = ws.cnt[i + 1];
-                    for (u32 u = lane; u <= gamma && u < c->l1_cap; u += 32) c->l1_h[u] = ws.H[u];
-                }
+            db = warp_sum_u64(db);
+            dh = warp_sum_u64(dh);
+            nf = warp_sum_u32(nf); ns = warp_sum_u32(ns); nr = warp_sum_u32(nr);
+            if (lane == 0)
+                write_record(c, L, alpha, gbase + p, m, K::from_okey(mn), K::from_okey(mx), db, dh, nf, ns, nr);
+            if (L == 1 && c->l1_b) {
+                for (u32 i = lane; i <= beta && i < c->l1_cap; i += 32) c->l1_b[i] = ws.cnt[i + 1];
+                for (u32 u = lane; u < ng && u < c->l1_cap; u += 32) c->l1_h[u] = ws.H[u];
             }
         }
-        // children in bucket order: windows of Standard-Sort buckets, pushes of recursions
-        for (u32 u = 0; u <= gamma; ++u) {
-            u32 h = ws.H[u];
-            if (h == 0) continue;
-            u32 start = p + ws.C[u] - h;
-            if (h >= delta || h < tau) {
-                window_add<K>(win, Y, gout, start, h);
-            } else {
-                window_flush<K>(win, Y, gout);
-                if (lane == 0) {
-                    if (sp < WSTACK && d + 1 < 16) ws.stack[sp] = start | (h << 13) | ((d + 1) << 24) | ((bi ^ 1u) << 28);
-                    else atomicOr(c->err_flag, 2u);
-                }
-                sp++;
-                __syncwarp();
+        // children, one lane per bucket
+        for (u32 u0 = 0; u0 < ng; u0 += 32) {
+            const u32 u = u0 + lane;
+            u32 kind = CK_EMPTY, h = 0, s = 0;
+            if (u < ng) {
+                h = ws.H[u];
+                s = ws.C[u] - h;
+                if (h) kind = (h >= delta || h < tau) ? (h <= 64 ? CK_RANK : CK_BITONIC) : CK_RECURSE;
+                ws.T[u] = (u16)kind;
+                if (kind == CK_RANK)
+                    for (u32 i = s; i < s + h; ++i) S.U[p + i] = (u16)u;
+            }
+            const u32 rmask = __ballot_sync(0xffffffffu, kind == CK_RECURSE);
+            if (kind == CK_RECURSE) {
+                const u32 slot = sp + __popc(rmask & lanemask_lt());
+                if (slot < WSTACK && d + 1 < 16) ws.stack[slot] = (p + s) | (h << 13) | ((d + 1) << 24) | ((bi ^ 1u) << 28);
+                else atomicOr(c->err_flag, 2u);
+            }
+            sp = min(sp + __popc(rmask), (u32)WSTACK);
+            u32 bmask = __ballot_sync(0xffffffffu, kind == CK_BITONIC);
+            while (bmask) {
+                const int b = __ffs(bmask) - 1;
+                bmask &= bmask - 1;
+                const u32 hs = __shfl_sync(0xffffffffu, h, b), ss = __shfl_sync(0xffffffffu, s, b);
+                warp_sort_write<K>(Y + p + ss, hs, gout + p + ss);
             }
         }
-        window_flush<K>(win, Y, gout);
-        if (sp > WSTACK) sp = WSTACK;
-    }
-}
-
-// Process the buckets [u0, u1) of a CTA-level partition whose keys are in Y:
-// sort runs of Standard-Sort buckets, run warp_node on recursing ones (<= WMAX).
-template <class K>
-__device__ void warp_range(const DevCtx *c, K7Smem &S, u32 ybuf, u32 u0, u32 u1, u32 delta, u32 Lc,
-                           u64 gbase, u64 *gout) {
-    u64 *Y = ybuf ? S.B : S.A;
-    const u32 tau = c->tau;
-    Window win; win.len = 0; win.start = 0;
-    for (u32 u = u0; u < u1; ++u) {
-        u32 h = S.Hc[u];
-        if (h == 0) continue;
-        u32 pos = S.Bs[u];
-        if (h > WMAX) { window_flush<K>(win, Y, gout); continue; }   // CTA big list
-        if (h >= delta || h < tau) {
-            window_add<K>(win, Y, gout, pos, h);
-        } else {
-            window_flush<K>(win, Y, gout);
-            warp_node<K>(c, S, ybuf, pos, h, Lc, gbase, gout);
+        __syncwarp();
+        // key-parallel rank sort of the small Standard-Sort buckets
+        for (u32 i = lane; i < m; i += 32) {
+            const u32 u = S.U[p + i];
+            if (u < ng && ws.T[u] == CK_RANK) {
+                const u32 en = ws.C[u], st = en - ws.H[u];
+                if (i >= st && i < en) rank_place<K>(Y + p, i, st, en, gout + p);
+            }
         }
+        __syncwarp();
     }
-    window_flush<K>(win, Y, gout);
 }
 
 // ------------------------------------------------------------------ CTA-level primitives
@@ -480,19 +436,19 @@ __device__ u32 cta_excl_scan(K7Smem &S, u32 *a, u32 n) {
     return total;
 }
 
-// Stable partition X[0..m) -> Y[0..m) by U[k] in [0, nb): per-warp contiguous
-// ranges, per-warp counters, bucket sizes to Hc, bucket starts to Bs.
-__device__ void cta_partition(K7Smem &S, const u64 *X, u64 *Y, u32 m, u32 nb) {
+// Stable partition X[p..p+m) -> Y[p..p+m) by U[p+k] in [0, nb): per-warp
+// contiguous ranges, per-warp counters.  Hc = bucket sizes, Bs = absolute starts.
+__device__ void cta_partition(K7Smem &S, const u64 *X, u64 *Y, u32 p, u32 m, u32 nb) {
     const u32 w = warp_id(), lane = lane_id();
     const u32 R = (m + K7_WARPS - 1) / K7_WARPS;
-    const u32 r0 = min(w * R, m), r1 = min(r0 + R, m);
+    const u32 r0 = p + min(w * R, m), r1 = p + min(w * R + R, m);
     for (u32 u = lane; u < nb; u += 32) S.u.wcnt[w][u] = 0;
     __syncwarp();
     for (u32 k0 = r0; k0 < r1; k0 += 32) {
-        u32 k = k0 + lane;
-        bool act = k < r1;
-        u32 u = act ? (u32)S.U[k] : 0xffffffffu;
-        u32 peers = __match_any_sync(0xffffffffu, u);
+        const u32 k = k0 + lane;
+        const bool act = k < r1;
+        const u32 u = act ? (u32)S.U[k] : 0xffffffffu;
+        const u32 peers = __match_any_sync(0xffffffffu, u);
         if (act && (peers & lanemask_lt()) == 0) S.u.wcnt[w][u] += (u16)__popc(peers);
         __syncwarp();
     }
@@ -506,19 +462,20 @@ __device__ void cta_partition(K7Smem &S, const u64 *X, u64 *Y, u32 m, u32 nb) {
     __syncthreads();
     cta_excl_scan(S, S.Bs, nb);
     for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
-        u32 run = S.Bs[u];
+        u32 run = p + S.Bs[u];
+        S.Bs[u] = run;
         for (u32 ww = 0; ww < K7_WARPS; ++ww) { u32 cc = S.u.wcnt[ww][u]; S.u.wcnt[ww][u] = (u16)run; run += cc; }
     }
     __syncthreads();
     for (u32 k0 = r0; k0 < r1; k0 += 32) {
-        u32 k = k0 + lane;
-        bool act = k < r1;
-        u32 u = act ? (u32)S.U[k] : 0xffffffffu;
-        u32 peers = __match_any_sync(0xffffffffu, u);
-        u32 base = act ? S.u.wcnt[w][u] : 0;
+        const u32 k = k0 + lane;
+        const bool act = k < r1;
+        const u32 u = act ? (u32)S.U[k] : 0xffffffffu;
+        const u32 peers = __match_any_sync(0xffffffffu, u);
+        const u32 base = act ? S.u.wcnt[w][u] : 0;
         __syncwarp();
         if (act) {
-            u32 rank = __popc(peers & lanemask_lt());
+            const u32 rank = __popc(peers & lanemask_lt());
             Y[base + rank] = X[k];
             if (rank == 0) S.u.wcnt[w][u] = (u16)(base + __popc(peers));
         }
@@ -527,56 +484,66 @@ __device__ void cta_partition(K7Smem &S, const u64 *X, u64 *Y, u32 m, u32 nb) {
     __syncthreads();
 }
 
-// After a CTA-level partition into Y (Hc/Bs valid for nb buckets): push big
-// children (> WMAX) to the CTA stack, hand the rest to warps in chunks.
+// Children of a CTA-level partition into Y (Hc/Bs valid for nb buckets of the
+// range [p, p+m)): rank-sort small Standard-Sort buckets, queue the rest.
 template <class K>
-__device__ void cta_dispatch(const DevCtx *c, K7Smem &S, u32 ybuf, u32 base_pos, u32 m, u32 nb,
-                             u32 delta, u32 Lc, u64 gbase, u64 *gout) {
+__device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m, u32 nb, u32 delta, u32 Lc,
+                             u64 gbase, u64 *gout) {
     const u32 tau = c->tau;
+    u64 *Y = ybuf ? S.B : S.A;
+    if (threadIdx.x == 0) { S.nitems = 0; S.item_next = 0; }
+    __syncthreads();
     for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
-        u32 h = S.Hc[u];
-        if (h > WMAX) {
-            u32 slot = atomicAdd(&S.nbig, 1u);
-            if (slot < BIG_CAP) {
-                BigItem it;
-                it.pos = base_pos + S.Bs[u]; it.size = h; it.level = Lc; it.buf = ybuf;
-                it.kind = (h >= delta || h < tau) ? 1u : 0u;
-                S.big[slot] = it;
+        const u32 h = S.Hc[u], s = S.Bs[u];
+        u32 kind = CK_EMPTY;
+        if (h) kind = (h >= delta || h < tau) ? (h <= 64 ? CK_RANK : CK_BITONIC) : CK_RECURSE;
+        S.kindc[u] = (u8)kind;
+        if (kind == CK_RANK) {
+            for (u32 i = s; i < s + h; ++i) S.U[i] = (u16)u;
+        } else if (kind != CK_EMPTY) {
+            if (h > WMAX) {
+                const u32 slot = atomicAdd(&S.nbig, 1u);
+                if (slot < BIG_CAP) {
+                    BigItem it;
+                    it.pos = s; it.size = h; it.level = Lc; it.buf = ybuf; it.kind = kind == CK_RECURSE ? 0u : 1u;
+                    S.big[slot] = it;
+                } else {
+                    atomicOr(c->err_flag, 2u);
+                }
             } else {
-                atomicOr(c->err_flag, 2u);
+                const u32 slot = atomicAdd(&S.nitems, 1u);
+                if (slot < ITEM_CAP) S.items[slot] = s | (h << 13) | ((kind == CK_RECURSE ? 0u : 1u) << 24);
+                else atomicOr(c->err_flag, 2u);
             }
         }
     }
-    // Bs are relative to the partitioned range; make them absolute buffer positions
-    for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) S.Bs[u] += base_pos;
-    if (threadIdx.x == 0) {
-        u32 cs = max(64u, (m + 2 * K7_WARPS - 1) / (2 * K7_WARPS));
-        S.chunk_sz = cs;
-        S.nchunks = (m + cs - 1) / cs;
-        S.chunk_next = 0;
-    }
     __syncthreads();
+    // key-parallel rank sort of the small Standard-Sort buckets
+    for (u32 i = p + threadIdx.x; i < p + m; i += K7_THREADS) {
+        const u32 u = S.U[i];
+        if (u < nb && S.kindc[u] == CK_RANK) {
+            const u32 st = S.Bs[u], en = st + S.Hc[u];
+            if (i >= st && i < en) rank_place<K>(Y, i, st, en, gout);
+        }
+    }
+    // warp items: recursing buckets (warp_node) and mid-size sorted buckets
+    const u32 nitems = min(S.nitems, (u32)ITEM_CAP);
     const u32 lane = lane_id();
     for (;;) {
-        u32 ch = 0;
-        if (lane == 0) ch = atomicAdd(&S.chunk_next, 1u);
-        ch = __shfl_sync(0xffffffffu, ch, 0);
-        if (ch >= S.nchunks) break;
-        // buckets whose start lies in [ch*cs, (ch+1)*cs) (relative): lower bounds over Bs
-        u32 lo_key = base_pos + ch * S.chunk_sz, hi_key = base_pos + (ch + 1) * S.chunk_sz;
-        u32 a = 0, b = nb;
-        while (a < b) { u32 mid = (a + b) >> 1; if (S.Bs[mid] < lo_key) a = mid + 1; else b = mid; }
-        u32 u0 = a;
-        b = nb;
-        while (a < b) { u32 mid = (a + b) >> 1; if (S.Bs[mid] < hi_key) a = mid + 1; else b = mid; }
-        u32 u1 = a;
-        if (u0 < u1) warp_range<K>(c, S, ybuf, u0, u1, delta, Lc, gbase, gout);
+        u32 idx = 0;
+        if (lane == 0) idx = atomicAdd(&S.item_next, 1u);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= nitems) break;
+        const u32 it = S.items[idx];
+        const u32 pos = it & 0x1fffu, size = (it >> 13) & 0x7ffu;
+        if (it >> 24) warp_sort_write<K>(Y + pos, size, gout + pos);
+        else warp_node<K>(c, S, ybuf, pos, size, Lc, gbase, gout);
     }
     __syncthreads();
 }
 
 // CTA-level Alg. 1 on X[p, p+m) (WMAX < m <= S_CAP), level L, global offset
-// gbase + p.  Leaves sorted or partitions into the other buffer and dispatches.
+// gbase + p.  Leaves sorted or partitions into the other buffer and recurses.
 template <class K>
 __device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32 L, u64 gbase, u64 *gout) {
     u64 *X = xbuf ? S.B : S.A;
@@ -590,7 +557,7 @@ __device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32
     mn = cta_reduce_min(S, mn);
     mx = cta_reduce_max(S, mx);
     Model md;
-    u32 P = (u32)iroot34(m);
+    const u32 P = iroot34_small(m);
     if (!make_model<K>(mn, mx, P, md)) { cta_sort_write<K>(X + p, m, gout + p); return; }
     const u32 alpha = sample_all ? m : P, beta = P, gamma = P, delta = P;
     u32 *cnt = S.u.fit.cnt, *T = S.u.fit.T;
@@ -602,7 +569,6 @@ __device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32
         atomicAdd(&cnt[interval_index<K>(X[p + pos], md)], 1u);
     }
     __syncthreads();
-    // inclusive prefix over cnt[1..beta+1]: exclusive scan of cnt[1..] then add own
     for (u32 i = threadIdx.x; i <= beta; i += K7_THREADS) T[i] = cnt[i + 1];
     __syncthreads();
     cta_excl_scan(S, T, beta + 1);
@@ -619,10 +585,9 @@ __device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32
     }
     __syncthreads();
     if (logging) db = cta_reduce_sum64(S, db);
-    for (u32 k = threadIdx.x; k < m; k += K7_THREADS) S.U[k] = (u16)(T[interval_index<K>(X[p + k], md)] - 1u);
+    for (u32 k = threadIdx.x; k < m; k += K7_THREADS) S.U[p + k] = (u16)(T[interval_index<K>(X[p + k], md)] - 1u);
     __syncthreads();
-    // partition X[p..] -> Y[p..]: cta_partition works on positions 0..m of U, so shift U
-    cta_partition(S, X + p, Y + p, m, gamma + 1);
+    cta_partition(S, X, Y, p, m, gamma + 1);
     if (logging) {
         u64 dh = 0;
         u32 nf = 0, ns = 0, nr = 0;
@@ -639,10 +604,42 @@ __device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32
         if (L == 1 && c->l1_h)
             for (u32 u = threadIdx.x; u <= gamma && u < c->l1_cap; u += K7_THREADS) c->l1_h[u] = S.Hc[u];
     }
-    cta_dispatch<K>(c, S, xbuf ^ 1u, p, m, gamma + 1, delta, L + 1, gbase, gout);
+    cta_children<K>(c, S, xbuf ^ 1u, p, m, gamma + 1, delta, L + 1, gbase, gout);
 }
 
 // ------------------------------------------------------------------ the kernel
+__device__ __forceinline__ ulonglong2 ld_stream2(const ulonglong2 *p) {
+    ulonglong2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p));
+    return r;
+}
+
+// Load src[0, m) into A as ordered keys; returns true if a NaN was seen (f64).
+template <class K>
+__device__ __forceinline__ bool load_task(K7Smem &S, const u64 *src, u32 m) {
+    bool nan = false;
+    auto put = [&](u32 k, u64 raw) {
+        if (K::is_f64) nan |= (raw & 0x7fffffffffffffffull) > 0x7ff0000000000000ull;
+        S.A[k] = K::to_okey(raw);
+    };
+    const u32 head = ((uintptr_t)src & 15) ? 1u : 0u;
+    if (head && m && threadIdx.x == 0) put(0, src[0]);
+    const u32 nv = (m - min(head, m)) / 2;
+    const ulonglong2 *v = reinterpret_cast<const ulonglong2 *>(src + head);
+    constexpr u32 U4 = 4;
+    u32 i = threadIdx.x;
+    for (; i + (U4 - 1) * K7_THREADS < nv; i += U4 * K7_THREADS) {
+        ulonglong2 r[U4];
+#pragma unroll
+        for (u32 q = 0; q < U4; ++q) r[q] = ld_stream2(v + i + q * K7_THREADS);
+#pragma unroll
+        for (u32 q = 0; q < U4; ++q) { put(head + 2 * (i + q * K7_THREADS), r[q].x); put(head + 2 * (i + q * K7_THREADS) + 1, r[q].y); }
+    }
+    for (; i < nv; i += K7_THREADS) { ulonglong2 r = ld_stream2(v + i); put(head + 2 * i, r.x); put(head + 2 * i + 1, r.y); }
+    if (m > head && ((m - head) & 1) && threadIdx.x == 0) put(m - 1, src[m - 1]);
+    return nan;
+}
+
 template <class K>
 __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restrict__ c) {
     extern __shared__ __align__(16) unsigned char k7_smem_raw[];
@@ -661,12 +658,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
         const u64 *src = c->buf[task.src] + task.off;
         u64 *gout = c->buf[2] + task.off;
         const u32 m = task.size;
-        bool nan_here = false;
-        for (u32 k = threadIdx.x; k < m; k += K7_THREADS) {
-            u64 raw = src[k];
-            if (K::is_f64 && (raw & 0x7fffffffffffffffull) > 0x7ff0000000000000ull) nan_here = true;
-            S.A[k] = K::to_okey(raw);
-        }
+        const bool nan_here = load_task<K>(S, src, m);
         if (K::is_f64 && task.level == 1 && __syncthreads_or(nan_here)) {
             if (threadIdx.x == 0) atomicOr(c->nan_flag, 1u);
             return;
@@ -694,20 +686,30 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
             __syncthreads();
             const Model md = S.gmd;
             const u32 *gT = S.gT;
-            for (u32 k = threadIdx.x; k < m; k += K7_THREADS)
-                S.U[k] = (u16)(__ldg(&gT[interval_index<K>(S.A[k], md)]) - task.jlo);
+            constexpr u32 G4 = 4;
+            u32 k = threadIdx.x;
+            for (; k + (G4 - 1) * K7_THREADS < m; k += G4 * K7_THREADS) {
+                u32 ix[G4], j[G4];
+#pragma unroll
+                for (u32 q = 0; q < G4; ++q) ix[q] = interval_index<K>(S.A[k + q * K7_THREADS], md);
+#pragma unroll
+                for (u32 q = 0; q < G4; ++q) j[q] = __ldg(&gT[ix[q]]);
+#pragma unroll
+                for (u32 q = 0; q < G4; ++q) S.U[k + q * K7_THREADS] = (u16)(j[q] - task.jlo);
+            }
+            for (; k < m; k += K7_THREADS) S.U[k] = (u16)(__ldg(&gT[interval_index<K>(S.A[k], md)]) - task.jlo);
             __syncthreads();
             const u32 nb = task.jhi - task.jlo;
-            cta_partition(S, S.A, S.B, m, nb);
+            cta_partition(S, S.A, S.B, 0u, m, nb);
             for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) S.gH[task.jlo + u] = S.Hc[u];
-            cta_dispatch<K>(c, S, 1u, 0u, m, nb, S.gnode_delta, S.gnode_level + 1, task.off, gout);
+            cta_children<K>(c, S, 1u, 0u, m, nb, S.gnode_delta, S.gnode_level + 1, task.off, gout);
         }
         // big items (> WMAX): processed by the whole CTA, LIFO
         for (;;) {
             __syncthreads();
-            u32 nb_ = S.nbig;
+            const u32 nb_ = S.nbig;
             if (nb_ == 0 || nb_ > BIG_CAP) break;
-            BigItem it = S.big[nb_ - 1];
+            const BigItem it = S.big[nb_ - 1];
             __syncthreads();
             if (threadIdx.x == 0) S.nbig = nb_ - 1;
             __syncthreads();
