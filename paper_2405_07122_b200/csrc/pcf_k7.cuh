@@ -41,6 +41,7 @@ struct BigItem {
 
 constexpr int BIG_CAP = 48;
 constexpr int ITEM_CAP = NB_CAP + 64;
+constexpr u32 RANK_MAX = 16;   // buckets up to this size are rank-sorted key-parallel
 enum : u32 { CK_EMPTY = 0, CK_RANK = 1, CK_RECURSE = 2, CK_BITONIC = 3 };
 
 struct K7Smem {
@@ -156,17 +157,47 @@ __device__ void warp_bitonic_smem(u64 *a, u32 n) {
     }
 }
 
+// Register bitonic for 16 < n <= 64: lane l holds elements l and l+32 (+inf padded).
+template <class K>
+__device__ void warp_sort64_write(const u64 *a, u32 n, u64 *gout_raw) {
+    const u32 lane = lane_id();
+    u64 v0 = lane < n ? a[lane] : ~0ull;
+    u64 v1 = lane + 32 < n ? a[lane + 32] : ~0ull;
+    const u32 kmax = n > 32 ? 64 : 32;
+    for (u32 k = 2; k <= kmax; k <<= 1) {
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {   // partner of element lane is lane+32 (same lane); k == 64 -> ascending
+                const u64 lo = v0 < v1 ? v0 : v1, hi = v0 < v1 ? v1 : v0;
+                v0 = lo; v1 = hi;
+            } else {
+                const u64 p0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                const bool low = (lane & j) == 0;
+                const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
+                v0 = (low == up0) ? (v0 < p0 ? v0 : p0) : (v0 > p0 ? v0 : p0);
+                if (kmax == 64) {
+                    const u64 p1 = __shfl_xor_sync(0xffffffffu, v1, j);
+                    v1 = (low == up1) ? (v1 < p1 ? v1 : p1) : (v1 > p1 ? v1 : p1);
+                }
+            }
+        }
+    }
+    if (lane < n) gout_raw[lane] = K::from_okey(v0);
+    if (lane + 32 < n) gout_raw[lane + 32] = K::from_okey(v1);
+}
+
 // Whole segment a[0, n) sorted by one warp and written (raw keys) to gout[0, n).
 template <class K>
 __device__ void warp_sort_write(u64 *a, u32 n, u64 *gout_raw) {
     const u32 lane = lane_id();
-    if (n <= 64) {   // rank sort: each key counts the keys before it in sorted order
+    if (n <= RANK_MAX) {   // rank sort: each key counts the keys before it in sorted order
         for (u32 i = lane; i < n; i += 32) {
             u64 v = a[i];
             u32 r = 0;
             for (u32 j = 0; j < n; ++j) { u64 w = a[j]; r += (w < v) | ((w == v) & (j < i)); }
             gout_raw[r] = K::from_okey(v);
         }
+    } else if (n <= 64) {
+        warp_sort64_write<K>(a, n, gout_raw);
     } else {
         warp_bitonic_smem(a, n);
         for (u32 k = lane; k < n; k += 32) gout_raw[k] = K::from_okey(a[k]);
@@ -335,7 +366,7 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
             if (u < ng) {
                 h = ws.H[u];
                 s = ws.C[u] - h;
-                if (h) kind = (h >= delta || h < tau) ? (h <= 64 ? CK_RANK : CK_BITONIC) : CK_RECURSE;
+                if (h) kind = (h >= delta || h < tau) ? (h <= RANK_MAX ? CK_RANK : CK_BITONIC) : CK_RECURSE;
                 ws.T[u] = (u16)kind;
                 if (kind == CK_RANK)
                     for (u32 i = s; i < s + h; ++i) S.U[p + i] = (u16)u;
@@ -496,7 +527,7 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
     for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
         const u32 h = S.Hc[u], s = S.Bs[u];
         u32 kind = CK_EMPTY;
-        if (h) kind = (h >= delta || h < tau) ? (h <= 64 ? CK_RANK : CK_BITONIC) : CK_RECURSE;
+        if (h) kind = (h >= delta || h < tau) ? (h <= RANK_MAX ? CK_RANK : CK_BITONIC) : CK_RECURSE;
         S.kindc[u] = (u8)kind;
         if (kind == CK_RANK) {
             for (u32 i = s; i < s + h; ++i) S.U[i] = (u16)u;
