@@ -41,7 +41,7 @@ struct BigItem {
 
 constexpr int BIG_CAP = 48;
 constexpr int ITEM_CAP = NB_CAP + 64;
-constexpr u32 RANK_MAX = 16;   // buckets up to this size are rank-sorted key-parallel
+constexpr u32 RANK_MAX = 64;   // Standard-Sort buckets up to this size are rank-sorted key-parallel
 enum : u32 { CK_EMPTY = 0, CK_RANK = 1, CK_RECURSE = 2, CK_BITONIC = 3 };
 
 struct K7Smem {
