@@ -390,7 +390,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
                 k_scan_final<<<nblk, SCAN_THREADS, 0, st>>>(d_C, ctot, d_bsum, d_P);
                 tm.end();
                 tm.begin(PH_SCATTER);
-                k_split_scatter<K><<<tiles, SPLIT_THREADS, split_smem_bytes(), st>>>(d_ctx, d_list, ns, d_P);
+                k_split_scatter<K><<<tiles, SC_THREADS, split_smem_bytes(), st>>>(d_ctx, d_list, ns, d_P);
                 tm.end();
                 tm.begin(PH_OTHER);
                 k_split_taskgen<<<ns, 256, 0, st>>>(d_ctx, d_list, d_P);

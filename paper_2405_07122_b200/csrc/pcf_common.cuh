@@ -25,8 +25,12 @@ constexpr int WMAX = 1024;               // largest segment a single warp runs A
 constexpr int WNB = 184;                 // >= iroot34(WMAX) + 2 (warp scratch bins)
 constexpr int WSTACK = 320;              // warp DFS stack entries (bound: DESIGN.md §5.3)
 constexpr int GMAX = 1024;               // digits per global split pass
-constexpr int SPLIT_THREADS = 512;
-constexpr int SPLIT_TILE = 16384;        // keys per split tile (per-tile counts fit u16? no: u32)
+constexpr int SPLIT_THREADS = 512;       // split count kernel block
+constexpr int SC_WARPS = 12;             // split scatter: warps per CTA
+constexpr int SC_THREADS = SC_WARPS * 32;
+constexpr int SC_KPL = 16;               // keys per lane held in registers
+constexpr int SC_PER_WARP = SC_KPL * 32; // 512 consecutive keys per warp
+constexpr int SPLIT_TILE = SC_WARPS * SC_PER_WARP;   // 6144 keys per split tile
 constexpr u64 GOLDEN = 0x9E3779B97F4A7C15ull;
 
 // ---------------------------------------------------------------- key transforms

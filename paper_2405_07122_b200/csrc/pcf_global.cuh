@@ -271,13 +271,22 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_fit_final(const DevCtx *__rest
 }
 
 // --- stable scatter by digit
+// One CTA per tile of SPLIT_TILE keys; warp w owns keys [w*SC_PER_WARP, ...)
+// of the tile and holds them in registers (SC_KPL per lane).  Pass 1 ranks the
+// keys stably inside the warp (__match_any_sync per 32-key chunk, per-warp
+// counters); the tile is then staged in shared memory in digit order (stable)
+// and written out run by run, so global writes are coalesced per digit run.
 struct SplitScatterSmem {
-    u32 wc[SPLIT_THREADS / 32][GMAX];
-    u16 dig[SPLIT_TILE];
+    u64 stage[SPLIT_TILE];
+    u16 sdig[SPLIT_TILE];
+    u16 wc[SC_WARPS][GMAX];     // per-warp counts -> warp-exclusive offsets within (tile, digit)
+    u32 tstart[GMAX + 1];       // tile-local start of each digit's run
+    u32 gbase[GMAX];            // segment-relative destination of each digit's run
+    u32 scan_tmp[SC_WARPS + 1];
 };
 
 template <class K>
-__global__ void __launch_bounds__(SPLIT_THREADS) k_split_scatter(const DevCtx *__restrict__ c, const SplitTask *__restrict__ L,
+__global__ void __launch_bounds__(SC_THREADS, 2) k_split_scatter(const DevCtx *__restrict__ c, const SplitTask *__restrict__ L,
                                                                  u32 ns, const u32 *__restrict__ P) {
     extern __shared__ __align__(16) unsigned char sc_smem_raw[];
     SplitScatterSmem &S = *reinterpret_cast<SplitScatterSmem *>(sc_smem_raw);
@@ -292,63 +301,88 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_scatter(const DevCtx *_
     const u64 *x = c->buf[st.src] + st.off;
     u64 *y = c->buf[st.dst] + st.off;
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr u32 NW = SPLIT_THREADS / 32;
+    const u32 G = st.G;
     const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
-    const u32 R = (k1 - k0 + NW - 1) / NW;
-    const u32 r0 = min(k0 + w * R, k1), r1 = min(r0 + R, k1);
-    for (u32 d = lane; d < st.G; d += 32) S.wc[w][d] = 0;
+    const u32 ntile = k1 - k0;
+    const u32 r0 = k0 + w * SC_PER_WARP;
+    for (u32 d = lane; d < G; d += 32) S.wc[w][d] = 0;
+    // load this lane's keys (coalesced per chunk) and compute their digits
+    u64 key[SC_KPL];
+    u32 dig[SC_KPL];
+#pragma unroll
+    for (u32 q = 0; q < SC_KPL; ++q) { u32 k = r0 + q * 32 + lane; key[q] = k < k1 ? x[k] : 0; }
+#pragma unroll
+    for (u32 q = 0; q < SC_KPL; ++q) {
+        u32 k = r0 + q * 32 + lane;
+        dig[q] = k < k1 ? interval_index<K>(K::to_okey(key[q]), md) : 0u;
+    }
+#pragma unroll
+    for (u32 q = 0; q < SC_KPL; ++q) {
+        u32 k = r0 + q * 32 + lane;
+        dig[q] = k < k1 ? (__ldg(&T[dig[q]]) - st.jlo) >> st.shift : 0xffffffffu;
+    }
     __syncwarp();
-    constexpr u32 UB = 4;
-    for (u32 kb = r0; kb < r1; kb += 32 * UB) {
-        u64 raw[UB];
-        u32 d[UB];
+    // pass 1: stable rank within the warp, chunk by chunk
+    u32 rk[SC_KPL];
 #pragma unroll
-        for (u32 q = 0; q < UB; ++q) { u32 k = kb + q * 32 + lane; raw[q] = k < r1 ? x[k] : 0; }
+    for (u32 q = 0; q < SC_KPL; ++q) {
+        const u32 d = dig[q];
+        const u32 peers = __match_any_sync(0xffffffffu, d);
+        const u32 leader = __ffs(peers) - 1;
+        u32 old = 0;
+        if (d != 0xffffffffu && lane == leader) { old = S.wc[w][d]; S.wc[w][d] = (u16)(old + __popc(peers)); }
+        old = __shfl_sync(0xffffffffu, old, leader);
+        rk[q] = old + __popc(peers & ((1u << lane) - 1));
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: warp-exclusive offsets, tile totals
+    for (u32 d = threadIdx.x; d < G; d += SC_THREADS) {
+        u32 run = 0;
 #pragma unroll
-        for (u32 q = 0; q < UB; ++q) {
-            u32 k = kb + q * 32 + lane;
-            d[q] = k < r1 ? interval_index<K>(K::to_okey(raw[q]), md) : 0u;
+        for (u32 ww = 0; ww < SC_WARPS; ++ww) { u32 cc = S.wc[ww][d]; S.wc[ww][d] = (u16)run; run += cc; }
+        S.tstart[d] = run;
+        S.gbase[d] = P[st.cbase + (u64)d * st.ntiles + lt] - (u32)st.mbase;
+    }
+    __syncthreads();
+    // exclusive scan of the tile totals over the digits (G <= GMAX)
+    {
+        constexpr u32 PER = (GMAX + SC_THREADS - 1) / SC_THREADS;
+        const u32 b0 = threadIdx.x * PER;
+        u32 v[PER], loc = 0;
+#pragma unroll
+        for (u32 i = 0; i < PER; ++i) { v[i] = b0 + i < G ? S.tstart[b0 + i] : 0; loc += v[i]; }
+        u32 incl = loc;
+        for (int o = 1; o < 32; o <<= 1) { u32 y2 = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= (u32)o) incl += y2; }
+        if (lane == 31) S.scan_tmp[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            u32 t = lane < SC_WARPS ? S.scan_tmp[lane] : 0;
+            u32 ti = t;
+            for (int o = 1; o < 32; o <<= 1) { u32 y2 = __shfl_up_sync(0xffffffffu, ti, o); if (lane >= (u32)o) ti += y2; }
+            if (lane < SC_WARPS) S.scan_tmp[lane] = ti - t;
         }
+        __syncthreads();
+        u32 run = S.scan_tmp[w] + incl - loc;
 #pragma unroll
-        for (u32 q = 0; q < UB; ++q) {
-            u32 k = kb + q * 32 + lane;
-            d[q] = k < r1 ? (__ldg(&T[d[q]]) - st.jlo) >> st.shift : 0xffffffffu;
-        }
+        for (u32 i = 0; i < PER; ++i) if (b0 + i < G) { S.tstart[b0 + i] = run; run += v[i]; }
+    }
+    __syncthreads();
+    // stage in digit order (stable: digit run, then warp, then in-warp rank)
 #pragma unroll
-        for (u32 q = 0; q < UB; ++q) {
-            u32 k = kb + q * 32 + lane;
-            bool act = k < r1;
-            if (act) S.dig[k - k0] = (u16)d[q];
-            u32 peers = __match_any_sync(0xffffffffu, d[q]);
-            if (act && (peers & ((1u << lane) - 1)) == 0) S.wc[w][d[q]] += __popc(peers);
-            __syncwarp();
+    for (u32 q = 0; q < SC_KPL; ++q) {
+        const u32 d = dig[q];
+        if (d != 0xffffffffu) {
+            const u32 lp = S.tstart[d] + S.wc[w][d] + rk[q];
+            S.stage[lp] = key[q];
+            S.sdig[lp] = (u16)d;
         }
     }
     __syncthreads();
-    for (u32 dd = threadIdx.x; dd < st.G; dd += SPLIT_THREADS) {
-        u32 run = P[st.cbase + (u64)dd * st.ntiles + lt] - (u32)st.mbase;
-        for (u32 ww = 0; ww < NW; ++ww) { u32 cc = S.wc[ww][dd]; S.wc[ww][dd] = run; run += cc; }
-    }
-    __syncthreads();
-    for (u32 kb = r0; kb < r1; kb += 32 * UB) {
-        u64 raw[UB];
-#pragma unroll
-        for (u32 q = 0; q < UB; ++q) { u32 k = kb + q * 32 + lane; raw[q] = k < r1 ? x[k] : 0; }
-#pragma unroll
-        for (u32 q = 0; q < UB; ++q) {
-            u32 k = kb + q * 32 + lane;
-            bool act = k < r1;
-            u32 d = act ? (u32)S.dig[k - k0] : 0xffffffffu;
-            u32 peers = __match_any_sync(0xffffffffu, d);
-            u32 base = act ? S.wc[w][d] : 0;
-            __syncwarp();
-            if (act) {
-                u32 rank = __popc(peers & ((1u << lane) - 1));
-                y[base + rank] = raw[q];
-                if (rank == 0) S.wc[w][d] = base + __popc(peers);
-            }
-            __syncwarp();
-        }
+    // coalesced write-out, run by run
+    for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) {
+        const u32 d = S.sdig[i];
+        y[S.gbase[d] + (i - S.tstart[d])] = S.stage[i];
     }
 }
 

@@ -42,7 +42,8 @@ struct BigItem {
 constexpr int BIG_CAP = 48;
 constexpr int ITEM_CAP = NB_CAP + 64;
 constexpr u32 RANK_MAX = 64;   // Standard-Sort buckets up to this size are rank-sorted key-parallel
-enum : u32 { CK_EMPTY = 0, CK_RANK = 1, CK_RECURSE = 2, CK_BITONIC = 3 };
+enum : u32 { CK_EMPTY = 0, CK_RANK = 1, CK_RECURSE = 2, CK_BITONIC = 3, CK_NET = 4 };
+constexpr u32 NET_MAX = 16;    // Standard-Sort buckets up to this size: one thread, register network
 
 struct K7Smem {
     u64 A[S_CAP];
@@ -232,6 +233,46 @@ __device__ void cta_sort_write(u64 *a, u32 n, u64 *gout_raw) {
     __syncthreads();
 }
 
+// One thread sorts a whole bucket of h <= N keys (Y[s, s+h)) in registers with
+// a fully unrolled bitonic network (+inf padded) and writes it to gout[s, s+h).
+// Predicated on `act`; the warp executes the network once for up to 32 buckets.
+template <class K, int N>
+__device__ __forceinline__ void net_sort_write(bool act, const u64 *Y, u32 s, u32 h, u64 *gout) {
+    u64 v[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = (act && (u32)i < h) ? Y[s + i] : ~0ull;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    const u64 a = v[i], b = v[l];
+                    const bool sw = up ? (a > b) : (a < b);
+                    v[i] = sw ? b : a;
+                    v[l] = sw ? a : b;
+                }
+            }
+        }
+    }
+    if (act) {
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+            if ((u32)i < h) gout[s + i] = K::from_okey(v[i]);
+    }
+}
+
+// Sort every bucket of kind CK_NET held by this thread (h <= 16): 8- or 16-wide network.
+template <class K>
+__device__ __forceinline__ void net_sort_bucket(bool is_net, const u64 *Y, u32 s, u32 h, u64 *gout) {
+    const bool n8 = is_net && h <= 8, n16 = is_net && h > 8;
+    if (__any_sync(0xffffffffu, n8)) net_sort_write<K, 8>(n8, Y, s, h, gout);
+    if (__any_sync(0xffffffffu, n16)) net_sort_write<K, 16>(n16, Y, s, h, gout);
+}
+
 // Rank-sort the key at buffer position i of a small bucket [s, e) and write it.
 template <class K>
 __device__ __forceinline__ void rank_place(const u64 *Y, u32 i, u32 s, u32 e, u64 *gout) {
@@ -366,11 +407,13 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
             if (u < ng) {
                 h = ws.H[u];
                 s = ws.C[u] - h;
-                if (h) kind = (h >= delta || h < tau) ? (h <= RANK_MAX ? CK_RANK : CK_BITONIC) : CK_RECURSE;
+                if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_NET : h <= RANK_MAX ? CK_RANK : CK_BITONIC)
+                                                      : CK_RECURSE;
                 ws.T[u] = (u16)kind;
                 if (kind == CK_RANK)
                     for (u32 i = s; i < s + h; ++i) S.U[p + i] = (u16)u;
             }
+            net_sort_bucket<K>(kind == CK_NET, Y + p, s, h, gout + p);
             const u32 rmask = __ballot_sync(0xffffffffu, kind == CK_RECURSE);
             if (kind == CK_RECURSE) {
                 const u32 slot = sp + __popc(rmask & lanemask_lt());
@@ -524,14 +567,18 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
     u64 *Y = ybuf ? S.B : S.A;
     if (threadIdx.x == 0) { S.nitems = 0; S.item_next = 0; }
     __syncthreads();
-    for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
-        const u32 h = S.Hc[u], s = S.Bs[u];
+    for (u32 u0 = 0; u0 < nb; u0 += K7_THREADS) {   // warp-uniform trip count (net sort uses __any_sync)
+        const u32 u = u0 + threadIdx.x;
+        const bool valid = u < nb;
+        const u32 h = valid ? S.Hc[u] : 0, s = valid ? S.Bs[u] : 0;
         u32 kind = CK_EMPTY;
-        if (h) kind = (h >= delta || h < tau) ? (h <= RANK_MAX ? CK_RANK : CK_BITONIC) : CK_RECURSE;
-        S.kindc[u] = (u8)kind;
+        if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_NET : h <= RANK_MAX ? CK_RANK : CK_BITONIC)
+                                              : CK_RECURSE;
+        if (valid) S.kindc[u] = (u8)kind;
+        net_sort_bucket<K>(kind == CK_NET, Y, s, h, gout);
         if (kind == CK_RANK) {
             for (u32 i = s; i < s + h; ++i) S.U[i] = (u16)u;
-        } else if (kind != CK_EMPTY) {
+        } else if (kind == CK_RECURSE || kind == CK_BITONIC) {
             if (h > WMAX) {
                 const u32 slot = atomicAdd(&S.nbig, 1u);
                 if (slot < BIG_CAP) {
