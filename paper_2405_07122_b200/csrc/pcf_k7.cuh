@@ -53,6 +53,8 @@ struct K7Smem {
     u32 Bs[NB_CAP + 1];      // CTA-level bucket starts (absolute buffer positions)
     u8 kindc[NB_CAP + 4];
     u32 items[ITEM_CAP];     // warp items: pos(13) | size(11) << 13 | kind(1) << 24 (0 node, 1 sort)
+    u32 leaf[3][NB_CAP];     // CTA-level network-sorted leaf buckets by class (<=4, <=8, <=16): pos | h << 16
+    u32 nleaf[3];
     union {
         u16 wcnt[K7_WARPS][NB_CAP];               // CTA partition per-warp counters
         struct { u32 cnt[S_CAP / 8 + 8]; u32 T[S_CAP / 8 + 8]; } fit;   // CTA fit (beta+2 <= 863)
@@ -265,12 +267,14 @@ __device__ __forceinline__ void net_sort_write(bool act, const u64 *Y, u32 s, u3
     }
 }
 
-// Sort every bucket of kind CK_NET held by this thread (h <= 16): 8- or 16-wide network.
+// Size class of a network-sorted leaf bucket: 0 (<= 4 keys), 1 (<= 8), 2 (<= 16).
+__device__ __forceinline__ u32 net_class(u32 h) { return h <= 4 ? 0u : h <= 8 ? 1u : 2u; }
+
 template <class K>
-__device__ __forceinline__ void net_sort_bucket(bool is_net, const u64 *Y, u32 s, u32 h, u64 *gout) {
-    const bool n8 = is_net && h <= 8, n16 = is_net && h > 8;
-    if (__any_sync(0xffffffffu, n8)) net_sort_write<K, 8>(n8, Y, s, h, gout);
-    if (__any_sync(0xffffffffu, n16)) net_sort_write<K, 16>(n16, Y, s, h, gout);
+__device__ __forceinline__ void net_sort_class(u32 cls, bool act, const u64 *Y, u32 s, u32 h, u64 *gout) {
+    if (cls == 0) net_sort_write<K, 4>(act, Y, s, h, gout);
+    else if (cls == 1) net_sort_write<K, 8>(act, Y, s, h, gout);
+    else net_sort_write<K, 16>(act, Y, s, h, gout);
 }
 
 // Rank-sort the key at buffer position i of a small bucket [s, e) and write it.
@@ -413,7 +417,6 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
                 if (kind == CK_RANK)
                     for (u32 i = s; i < s + h; ++i) S.U[p + i] = (u16)u;
             }
-            net_sort_bucket<K>(kind == CK_NET, Y + p, s, h, gout + p);
             const u32 rmask = __ballot_sync(0xffffffffu, kind == CK_RECURSE);
             if (kind == CK_RECURSE) {
                 const u32 slot = sp + __popc(rmask & lanemask_lt());
@@ -430,6 +433,25 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
             }
         }
         __syncwarp();
+        // leaf buckets of <= 16 keys: compacted per size class (list in ws.cnt),
+        // one lane per bucket, register network
+#pragma unroll 1
+        for (u32 cls = 0; cls < 3; ++cls) {
+            u32 nl = 0;
+            for (u32 u0 = 0; u0 < ng; u0 += 32) {
+                const u32 u = u0 + lane;
+                const bool in = u < ng && ws.T[u] == CK_NET && net_class(ws.H[u]) == cls;
+                const u32 mk = __ballot_sync(0xffffffffu, in);
+                if (in) ws.cnt[nl + __popc(mk & lanemask_lt())] = (u16)u;
+                nl += __popc(mk);
+            }
+            __syncwarp();
+            for (u32 i = lane; i < nl; i += 32) {
+                const u32 u = ws.cnt[i], h = ws.H[u];
+                net_sort_class<K>(cls, true, Y + p, ws.C[u] - h, h, gout + p);
+            }
+            __syncwarp();
+        }
         // key-parallel rank sort of the small Standard-Sort buckets
         for (u32 i = lane; i < m; i += 32) {
             const u32 u = S.U[p + i];
@@ -565,7 +587,7 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
                              u64 gbase, u64 *gout) {
     const u32 tau = c->tau;
     u64 *Y = ybuf ? S.B : S.A;
-    if (threadIdx.x == 0) { S.nitems = 0; S.item_next = 0; }
+    if (threadIdx.x == 0) { S.nitems = 0; S.item_next = 0; S.nleaf[0] = S.nleaf[1] = S.nleaf[2] = 0; }
     __syncthreads();
     for (u32 u0 = 0; u0 < nb; u0 += K7_THREADS) {   // warp-uniform trip count (net sort uses __any_sync)
         const u32 u = u0 + threadIdx.x;
@@ -575,7 +597,17 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
         if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_NET : h <= RANK_MAX ? CK_RANK : CK_BITONIC)
                                               : CK_RECURSE;
         if (valid) S.kindc[u] = (u8)kind;
-        net_sort_bucket<K>(kind == CK_NET, Y, s, h, gout);
+#pragma unroll
+        for (u32 cls = 0; cls < 3; ++cls) {   // warp-aggregated append to the class list
+            const bool in = kind == CK_NET && net_class(h) == cls;
+            const u32 mk = __ballot_sync(0xffffffffu, in);
+            if (mk) {
+                u32 base = 0;
+                if (lane_id() == (u32)(__ffs(mk) - 1)) base = atomicAdd(&S.nleaf[cls], (u32)__popc(mk));
+                base = __shfl_sync(0xffffffffu, base, __ffs(mk) - 1);
+                if (in) S.leaf[cls][base + __popc(mk & lanemask_lt())] = s | (h << 16);
+            }
+        }
         if (kind == CK_RANK) {
             for (u32 i = s; i < s + h; ++i) S.U[i] = (u16)u;
         } else if (kind == CK_RECURSE || kind == CK_BITONIC) {
@@ -596,6 +628,15 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
         }
     }
     __syncthreads();
+    // leaf buckets of <= 16 keys: one thread per bucket, register network, by size class
+#pragma unroll 1
+    for (u32 cls = 0; cls < 3; ++cls) {
+        const u32 nl = S.nleaf[cls];
+        for (u32 i = threadIdx.x; i < nl; i += K7_THREADS) {
+            const u32 e = S.leaf[cls][i];
+            net_sort_class<K>(cls, true, Y, e & 0xffffu, e >> 16, gout);
+        }
+    }
     // key-parallel rank sort of the small Standard-Sort buckets
     for (u32 i = p + threadIdx.x; i < p + m; i += K7_THREADS) {
         const u32 u = S.U[i];
