@@ -65,15 +65,18 @@ static Caps caps_for(u64 n) {
     c.k7_cap = (u32)std::min<u64>(n / 32 + 65536, 0xffffffffull);
     c.split_cap = (u32)(n / 1024 + 4096);
     c.items_cap = (u32)(n / S_CAP + 64);
-    c.cmat_cap = (n / SPLIT_TILE + 64) * (u64)GMAX;
+    // every split of a round has <= GMAX digits and ceil(m/SPLIT_TILE) tiles; a round's
+    // splits are disjoint segments of > S_CAP keys (or of wider-than-NB_CAP bucket ranges)
+    c.cmat_cap = (n / SPLIT_TILE + n / S_CAP + 64) * (u64)GMAX;
     c.bsum_cap = c.cmat_cap / SCAN_CHUNK + 2;
     return c;
 }
 
 struct Counters {             // zeroed at the start of every call
     u32 nan_flag, err_flag, k7_count, k7_next;
-    u32 nsplits_out, nitems, pad0, pad1;
-    unsigned long long rec_count, k7_keys;
+    u32 nsplits[2], nitems, k7_begin;
+    unsigned long long rec_count, k7_keys, split_keys, pad;
+    RoundPlan plan;
 };
 
 struct Layout {
@@ -257,18 +260,26 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.nodes = (GNode *)(ws + L.nodes);
         hc.k7 = (K7Task *)(ws + L.k7);
         hc.k7_cap = caps.k7_cap;
-        hc.splits_out = (SplitTask *)(ws + L.splits_b);
+        hc.splits[0] = (SplitTask *)(ws + L.splits_a);
+        hc.splits[1] = (SplitTask *)(ws + L.splits_b);
         hc.splits_cap = caps.split_cap;
         hc.items = (SegItem *)(ws + L.items);
         hc.items_cap = caps.items_cap;
+        hc.cmat = (u32 *)(ws + L.cmat);
+        hc.pmat = (u32 *)(ws + L.pmat);
+        hc.bsum = (u32 *)(ws + L.bsum);
+        hc.cmat_cap = caps.cmat_cap;
     }
     hc.nan_flag = &d_cnt->nan_flag;
     hc.err_flag = &d_cnt->err_flag;
     hc.k7_count = &d_cnt->k7_count;
     hc.k7_next = &d_cnt->k7_next;
-    hc.nsplits_out = &d_cnt->nsplits_out;
+    hc.nsplits = d_cnt->nsplits;
     hc.nitems = &d_cnt->nitems;
     hc.k7_keys = &d_cnt->k7_keys;
+    hc.k7_begin = &d_cnt->k7_begin;
+    hc.split_keys = &d_cnt->split_keys;
+    hc.plan = &d_cnt->plan;
     if (!logging) hc.rec_count = &d_cnt->rec_count;
     CK(cudaMemcpyAsync(d_ctx, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_cnt, 0, sizeof(Counters), st));
@@ -353,95 +364,87 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             list.push_back(s);
             return PCF_OK;
         };
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        // host-side list of splits to append to the device list of the next round
         rc = add_node(0, (u32)n, 1, 0);
         if (rc) return rc;
-
-        SplitTask *d_list = (SplitTask *)(ws + L.splits_a);
-        u32 *d_C = (u32 *)(ws + L.cmat), *d_P = (u32 *)(ws + L.pmat), *d_bsum = (u32 *)(ws + L.bsum);
         u32 round = 0;
-        while (!list.empty()) {
+        u32 pending = 0;   // splits already in the device list splits[round & 1]
+        auto flush_list = [&]() -> int {
+            if (list.empty()) return PCF_OK;
+            const u32 cur = round & 1u;
+            if (pending + list.size() > caps.split_cap) return fail(PCF_ERR_INTERNAL, "split list capacity exceeded");
+            CK(cudaMemcpyAsync(hc.splits[cur] + pending, list.data(), list.size() * sizeof(SplitTask),
+                               cudaMemcpyHostToDevice, st));
+            pending += (u32)list.size();
+            CK(cudaMemcpyAsync(&d_cnt->nsplits[cur], &pending, 4, cudaMemcpyHostToDevice, st));
+            list.clear();
+            return PCF_OK;
+        };
+        auto enqueue_round = [&]() {
+            const u32 cur = round & 1u;
+            tm.begin(PH_OTHER);
+            k_round_plan<<<1, 1024, 0, st>>>(d_ctx, cur);
+            tm.end();
+            tm.begin(PH_COUNT);
+            k_split_count<K><<<nsm * 4, SPLIT_THREADS, 0, st>>>(d_ctx, cur);
+            tm.end();
+            tm.begin(PH_OTHER);
+            k_scanp_partials<<<nsm * 2, SCAN_THREADS, 0, st>>>(d_ctx);
+            k_scanp_bsums<<<1, SCAN_THREADS, 0, st>>>(d_ctx);
+            k_scanp_final<<<nsm * 2, SCAN_THREADS, 0, st>>>(d_ctx);
+            tm.end();
+            tm.begin(PH_SCATTER);
+            k_split_scatter<K><<<nsm * 2, SC_THREADS, split_smem_bytes(), st>>>(d_ctx, cur);
+            tm.end();
+            tm.begin(PH_OTHER);
+            k_split_taskgen<<<nsm * 2, 256, 0, st>>>(d_ctx, cur);
+            tm.end();
+            launches += 7;
             round++;
-            // launch the list in batches whose count matrices fit
-            size_t i0 = 0;
-            while (i0 < list.size()) {
-                u64 ctot = 0, mtot = 0;
-                u32 tiles = 0;
-                size_t i1 = i0;
-                while (i1 < list.size()) {
-                    SplitTask &s = list[i1];
-                    u32 nt = (s.m + SPLIT_TILE - 1) / SPLIT_TILE;
-                    u64 need_c = (u64)nt * s.G;
-                    if (i1 > i0 && ctot + need_c > caps.cmat_cap) break;
-                    if (need_c > caps.cmat_cap) return fail(PCF_ERR_INTERNAL, "split count matrix too large");
-                    s.tile_begin = tiles; s.ntiles = nt; s.cbase = ctot; s.mbase = mtot;
-                    tiles += nt; ctot += need_c; mtot += s.m;
-                    if (i1 - i0 + 1 >= caps.split_cap) { i1++; break; }
-                    i1++;
-                }
-                u32 ns = (u32)(i1 - i0);
-                CK(cudaMemcpyAsync(d_list, list.data() + i0, ns * sizeof(SplitTask), cudaMemcpyHostToDevice, st));
-                tm.begin(PH_COUNT);
-                k_split_count<K><<<tiles, SPLIT_THREADS, 0, st>>>(d_ctx, d_list, ns, d_C);
-                tm.end();
-                tm.begin(PH_OTHER);
-                u32 nblk = (u32)((ctot + SCAN_CHUNK - 1) / SCAN_CHUNK);
-                k_scan_partials<<<nblk, SCAN_THREADS, 0, st>>>(d_C, ctot, d_bsum);
-                k_scan_bsums<<<1, SCAN_THREADS, 0, st>>>(d_bsum, nblk);
-                k_scan_final<<<nblk, SCAN_THREADS, 0, st>>>(d_C, ctot, d_bsum, d_P);
-                tm.end();
-                tm.begin(PH_SCATTER);
-                k_split_scatter<K><<<tiles, SC_THREADS, split_smem_bytes(), st>>>(d_ctx, d_list, ns, d_P);
-                tm.end();
-                tm.begin(PH_OTHER);
-                k_split_taskgen<<<ns, 256, 0, st>>>(d_ctx, d_list, d_P);
-                tm.end();
-                CK(cudaGetLastError());
-                launches += 6;
-                bytes[PH_COUNT] += 8ull * mtot;
-                bytes[PH_SCATTER] += 16ull * mtot;
-                stats.split_tasks += ns;
-                i0 = i1;
-            }
-            // read back what the round produced
+        };
+        u32 rounds_per_batch = 3;   // enough for n <= 2^32 on well-modelled data
+        for (;;) {
+            rc = flush_list();
+            if (rc) return rc;
+            for (u32 k = 0; k < rounds_per_batch; ++k) enqueue_round();
+            CK(cudaGetLastError());
+            // K7 over every group produced so far (persistent grid; reads the task count on the device)
+            tm.begin(PH_K7);
+            k7_kernel<K><<<nsm, K7_THREADS, k7_smem_bytes(), st>>>(d_ctx);
+            k_k7_advance<<<1, 1, 0, st>>>(d_ctx);
+            tm.end();
+            CK(cudaGetLastError());
+            launches += 2;
             Counters hcnt;
             CK(cudaMemcpyAsync(&hcnt, d_cnt, sizeof hcnt, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             stats.host_syncs++;
             if (hcnt.nan_flag) { status = PCF_ERR_NAN; break; }
             if (hcnt.err_flag) return fail(PCF_ERR_INTERNAL, "device work-queue capacity exceeded (err_flag=" + std::to_string(hcnt.err_flag) + ")");
-            std::vector<SplitTask> next(hcnt.nsplits_out);
-            if (hcnt.nsplits_out)
-                CK(cudaMemcpyAsync(next.data(), hc.splits_out, hcnt.nsplits_out * sizeof(SplitTask), cudaMemcpyDeviceToHost, st));
+            k7_tasks = hcnt.k7_count;
+            pending = hcnt.nsplits[round & 1u];
             std::vector<SegItem> items(hcnt.nitems);
-            if (hcnt.nitems)
+            if (hcnt.nitems) {
                 CK(cudaMemcpyAsync(items.data(), hc.items, hcnt.nitems * sizeof(SegItem), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            CK(cudaMemsetAsync(&d_cnt->nsplits_out, 0, 8, st));   // nsplits_out and nitems
-            list.swap(next);
+                CK(cudaStreamSynchronize(st));
+                CK(cudaMemsetAsync(&d_cnt->nitems, 0, 4, st));
+            }
             for (const SegItem &it : items) {
                 if (it.kind == 0) { rc = add_node(it.off, it.m, it.level, it.src); if (rc) return rc; }
                 else fallbacks.push_back(it);
             }
+            bytes[PH_COUNT] = 8ull * hcnt.split_keys;
+            bytes[PH_SCATTER] = 16ull * hcnt.split_keys;
+            bytes[PH_K7] = 16ull * hcnt.k7_keys;
+            if (pending == 0 && list.empty()) break;
+            rounds_per_batch = 2;
         }
         stats.rounds = round;
+        stats.split_tasks = 0;
         if (status == PCF_OK) {
-            Counters hcnt;
-            CK(cudaMemcpyAsync(&hcnt, d_cnt, sizeof hcnt, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            stats.host_syncs++;
-            k7_tasks = hcnt.k7_count;
-            bytes[PH_K7] += 16ull * hcnt.k7_keys;
-            if (k7_tasks) {
-                int dev = 0, nsm = 148;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-                u32 grid = (u32)std::min<u64>(k7_tasks, (u64)nsm);
-                tm.begin(PH_K7);
-                k7_kernel<K><<<grid, K7_THREADS, k7_smem_bytes(), st>>>(d_ctx);
-                tm.end();
-                CK(cudaGetLastError());
-                launches++;
-            }
             // K8: global Standard-Sort of large buckets
             for (const SegItem &it : fallbacks) {
                 const u64 m = it.m;

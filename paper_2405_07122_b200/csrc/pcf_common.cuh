@@ -193,6 +193,16 @@ struct SegItem {
     u32 kind;       // 0 = recurse (new global node), 1 = fallback sort
 };
 
+// Sizes of one split round, computed on the device by k_round_plan.
+struct RoundPlan {
+    u32 ns;        // splits processed this round
+    u32 tiles;     // total tiles
+    u32 nblk;      // scan blocks over the count matrix
+    u32 pad;
+    u64 ctot;      // count-matrix entries
+    u64 mtot;      // keys moved
+};
+
 struct DevCtx {
     u64 *buf[3];            // in (const, never written unless in==out), tmp, out
     u64 n;
@@ -205,10 +215,16 @@ struct DevCtx {
     u32 *k7_count;
     u32 k7_cap;
     u32 *k7_next;
-    // next-round splits / segments
-    SplitTask *splits_out;
-    u32 *nsplits_out;
+    u32 *k7_begin;          // first task of the current K7 launch
+    // split rounds, planned on the device: round r consumes splits[r & 1] and
+    // appends the next round's splits to splits[(r + 1) & 1]
+    SplitTask *splits[2];
+    u32 *nsplits;           // [2]
     u32 splits_cap;
+    struct RoundPlan *plan;
+    u32 *cmat, *pmat, *bsum;
+    u64 cmat_cap;
+    unsigned long long *split_keys;   // keys moved by split passes (byte accounting)
     SegItem *items;
     u32 *nitems;
     u32 items_cap;

@@ -131,39 +131,44 @@ __device__ __forceinline__ u32 digit_of(u64 okey, const Model &md, const u32 *__
 }
 
 template <class K>
-__global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__restrict__ c, const SplitTask *__restrict__ L,
-                                                               u32 ns, u32 *__restrict__ C) {
+__global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__restrict__ c, u32 cur) {
     __shared__ u32 hist[GMAX];
     if (*c->nan_flag) return;
-    const u32 s = find_split(L, ns, blockIdx.x);
-    const SplitTask st = L[s];
-    const u32 lt = blockIdx.x - st.tile_begin;
-    const GNode &g = c->nodes[st.node];
-    for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) hist[d] = 0;
-    __syncthreads();
-    const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
-    if (g.degenerate) {
-        if (threadIdx.x == 0) hist[0] = k1 - k0;
-    } else {
-        const Model md = g.md;
-        const u64 *x = c->buf[st.src] + st.off;
-        const u32 *T = g.T;
-        constexpr u32 UB = 4;
-        u32 k = k0 + threadIdx.x;
-        for (; k + (UB - 1) * SPLIT_THREADS < k1; k += UB * SPLIT_THREADS) {
-            u64 raw[UB];
-            u32 ix[UB];
+    const RoundPlan pl = *c->plan;
+    const SplitTask *__restrict__ L = c->splits[cur];
+    u32 *__restrict__ C = c->cmat;
+    for (u32 tile = blockIdx.x; tile < pl.tiles; tile += gridDim.x) {
+        const u32 s = find_split(L, pl.ns, tile);
+        const SplitTask st = L[s];
+        const u32 lt = tile - st.tile_begin;
+        const GNode &g = c->nodes[st.node];
+        for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) hist[d] = 0;
+        __syncthreads();
+        const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
+        if (g.degenerate) {
+            if (threadIdx.x == 0) hist[0] = k1 - k0;
+        } else {
+            const Model md = g.md;
+            const u64 *x = c->buf[st.src] + st.off;
+            const u32 *T = g.T;
+            constexpr u32 UB = 4;
+            u32 k = k0 + threadIdx.x;
+            for (; k + (UB - 1) * SPLIT_THREADS < k1; k += UB * SPLIT_THREADS) {
+                u64 raw[UB];
+                u32 ix[UB];
 #pragma unroll
-            for (u32 q = 0; q < UB; ++q) raw[q] = x[k + q * SPLIT_THREADS];
+                for (u32 q = 0; q < UB; ++q) raw[q] = x[k + q * SPLIT_THREADS];
 #pragma unroll
-            for (u32 q = 0; q < UB; ++q) ix[q] = __ldg(&T[interval_index<K>(K::to_okey(raw[q]), md)]);
+                for (u32 q = 0; q < UB; ++q) ix[q] = __ldg(&T[interval_index<K>(K::to_okey(raw[q]), md)]);
 #pragma unroll
-            for (u32 q = 0; q < UB; ++q) atomicAdd(&hist[(ix[q] - st.jlo) >> st.shift], 1u);
+                for (u32 q = 0; q < UB; ++q) atomicAdd(&hist[(ix[q] - st.jlo) >> st.shift], 1u);
+            }
+            for (; k < k1; k += SPLIT_THREADS) atomicAdd(&hist[digit_of<K>(K::to_okey(x[k]), md, T, st.jlo, st.shift)], 1u);
         }
-        for (; k < k1; k += SPLIT_THREADS) atomicAdd(&hist[digit_of<K>(K::to_okey(x[k]), md, T, st.jlo, st.shift)], 1u);
+        __syncthreads();
+        for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
+        __syncthreads();
     }
-    __syncthreads();
-    for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
 }
 
 // --- exclusive scan of a u32 array (3 phases)
@@ -229,6 +234,129 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const u32 *__restri
     for (int k = 0; k < SCAN_ITEMS; ++k) { if (base + k < n) out[base + k] = e; e += v[k]; }
 }
 
+// Same three phases over the count matrix of a split round, sizes from the plan.
+__global__ void __launch_bounds__(SCAN_THREADS) k_scanp_partials(const DevCtx *__restrict__ c) {
+    __shared__ u32 wsum[33];
+    const RoundPlan pl = *c->plan;
+    for (u32 b = blockIdx.x; b < pl.nblk; b += gridDim.x) {
+        const u64 base = (u64)b * SCAN_CHUNK + (u64)threadIdx.x * SCAN_ITEMS;
+        u32 sum = 0;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) if (base + k < pl.ctot) sum += c->cmat[base + k];
+        u32 total;
+        block_excl_scan_1024(sum, wsum, total);
+        if (threadIdx.x == 0) c->bsum[b] = total;
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scanp_bsums(const DevCtx *__restrict__ c) {
+    __shared__ u32 wsum[33];
+    const u32 nb = c->plan->nblk;
+    u32 carry = 0;
+    for (u32 base = 0; base < nb; base += SCAN_THREADS) {
+        const u32 i = base + threadIdx.x;
+        const u32 v = i < nb ? c->bsum[i] : 0;
+        u32 total;
+        const u32 e = block_excl_scan_1024(v, wsum, total);
+        if (i < nb) c->bsum[i] = carry + e;
+        carry += total;
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scanp_final(const DevCtx *__restrict__ c) {
+    __shared__ u32 wsum[33];
+    const RoundPlan pl = *c->plan;
+    for (u32 b = blockIdx.x; b < pl.nblk; b += gridDim.x) {
+        const u64 base = (u64)b * SCAN_CHUNK + (u64)threadIdx.x * SCAN_ITEMS;
+        u32 v[SCAN_ITEMS];
+        u32 sum = 0;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) { v[k] = base + k < pl.ctot ? c->cmat[base + k] : 0; sum += v[k]; }
+        u32 total;
+        u32 e = block_excl_scan_1024(sum, wsum, total) + c->bsum[b];
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) { if (base + k < pl.ctot) c->pmat[base + k] = e; e += v[k]; }
+    }
+}
+
+// Plan split round `cur`: tiles, count-matrix offsets and key offsets of every
+// split (one CTA).  Splits that do not fit the count matrix are carried over to
+// the next round's list; the next list's counter is reset here.
+__global__ void __launch_bounds__(1024) k_round_plan(const DevCtx *__restrict__ c, u32 cur) {
+    __shared__ u32 wsum[33];
+    __shared__ unsigned long long wsum64[33];
+    __shared__ u32 cut_s;
+    SplitTask *L = c->splits[cur];
+    const u32 nxt = cur ^ 1u;
+    u32 ns = *c->nan_flag ? 0u : min(c->nsplits[cur], c->splits_cap);
+    if (threadIdx.x == 0) { c->nsplits[nxt] = 0; cut_s = ns; }
+    const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u32 carry_t = 0;
+    u64 carry_c = 0, carry_m = 0;
+    for (u32 base = 0; base < ns; base += 1024) {
+        const u32 s = base + threadIdx.x;
+        u32 nt = 0;
+        u64 cc = 0, mm = 0;
+        if (s < ns) {
+            const SplitTask &t = L[s];
+            nt = (t.m + SPLIT_TILE - 1) / SPLIT_TILE;
+            cc = (u64)nt * t.G;
+            mm = t.m;
+        }
+        u32 tot_t;
+        const u32 ex_t = block_excl_scan_1024(nt, wsum, tot_t);
+        // u64 exclusive scans of cc and mm (two passes through the same helper)
+        u64 vals[2] = {cc, mm}, ex[2], tot[2];
+        for (int q = 0; q < 2; ++q) {
+            u64 x = vals[q];
+            for (int o = 1; o < 32; o <<= 1) { u64 y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= (u32)o) x += y; }
+            if (lane == 31) wsum64[w] = x;
+            __syncthreads();
+            if (w == 0) {
+                u64 sv = wsum64[lane], t2 = sv;
+                for (int o = 1; o < 32; o <<= 1) { u64 y = __shfl_up_sync(0xffffffffu, t2, o); if (lane >= (u32)o) t2 += y; }
+                wsum64[lane] = t2 - sv;
+                if (lane == 31) wsum64[32] = t2;
+            }
+            __syncthreads();
+            ex[q] = wsum64[w] + x - vals[q];
+            tot[q] = wsum64[32];
+            __syncthreads();
+        }
+        if (s < ns) {
+            const u64 cb = carry_c + ex[0];
+            L[s].tile_begin = carry_t + ex_t;
+            L[s].ntiles = nt;
+            L[s].cbase = cb;
+            L[s].mbase = carry_m + ex[1];
+            if (cb + cc > c->cmat_cap) atomicMin(&cut_s, s);   // does not fit this round
+        }
+        carry_t += tot_t; carry_c += tot[0]; carry_m += tot[1];
+    }
+    __syncthreads();
+    const u32 cut = cut_s;
+    // carry splits [cut, ns) over to the next round
+    for (u32 s = cut + threadIdx.x; s < ns; s += 1024) c->splits[nxt][s - cut] = L[s];
+    if (threadIdx.x == 0) {
+        if (cut < ns) c->nsplits[nxt] = ns - cut;
+        RoundPlan pl;
+        if (cut == ns) {
+            pl.ns = ns; pl.tiles = carry_t; pl.ctot = carry_c; pl.mtot = carry_m;
+        } else if (cut == 0) {
+            pl.ns = 0; pl.tiles = 0; pl.ctot = 0; pl.mtot = 0;
+            if (ns) atomicOr(c->err_flag, 4u);   // a single split larger than the matrix
+        } else {
+            const SplitTask &lst = L[cut - 1];
+            pl.ns = cut; pl.tiles = lst.tile_begin + lst.ntiles;
+            pl.ctot = lst.cbase + (u64)lst.ntiles * lst.G; pl.mtot = lst.mbase + lst.m;
+        }
+        pl.nblk = (u32)((pl.ctot + SCAN_CHUNK - 1) / SCAN_CHUNK);
+        pl.pad = 0;
+        *c->plan = pl;
+        atomicAdd(c->split_keys, (unsigned long long)pl.mtot);
+    }
+}
+
 // b[i] = inclusive prefix of cnt[1..beta+1] (exclusive block offsets from the
 // k_scan_partials/k_scan_bsums pass over cnt+1), T[i] = floor(b_i*gamma/alpha)+1
 // (R7), digest of b and the level-1 dump for the pass log.
@@ -286,14 +414,8 @@ struct SplitScatterSmem {
 };
 
 template <class K>
-__global__ void __launch_bounds__(SC_THREADS, 2) k_split_scatter(const DevCtx *__restrict__ c, const SplitTask *__restrict__ L,
-                                                                 u32 ns, const u32 *__restrict__ P) {
-    extern __shared__ __align__(16) unsigned char sc_smem_raw[];
-    SplitScatterSmem &S = *reinterpret_cast<SplitScatterSmem *>(sc_smem_raw);
-    if (*c->nan_flag) return;
-    const u32 s = find_split(L, ns, blockIdx.x);
-    const SplitTask st = L[s];
-    const u32 lt = blockIdx.x - st.tile_begin;
+__device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c, SplitScatterSmem &S, const SplitTask &st,
+                                                   u32 lt, const u32 *__restrict__ P) {
     const GNode &g = c->nodes[st.node];
     if (g.degenerate) return;
     const Model md = g.md;
@@ -386,6 +508,20 @@ __global__ void __launch_bounds__(SC_THREADS, 2) k_split_scatter(const DevCtx *_
     }
 }
 
+template <class K>
+__global__ void __launch_bounds__(SC_THREADS, 2) k_split_scatter(const DevCtx *__restrict__ c, u32 cur) {
+    extern __shared__ __align__(16) unsigned char sc_smem_raw[];
+    SplitScatterSmem &S = *reinterpret_cast<SplitScatterSmem *>(sc_smem_raw);
+    if (*c->nan_flag) return;
+    const RoundPlan pl = *c->plan;
+    const SplitTask *__restrict__ L = c->splits[cur];
+    for (u32 tile = blockIdx.x; tile < pl.tiles; tile += gridDim.x) {
+        const SplitTask st = L[find_split(L, pl.ns, tile)];
+        split_scatter_tile<K>(c, S, st, tile - st.tile_begin, c->pmat);
+        __syncthreads();
+    }
+}
+
 __host__ __device__ inline u32 ceil_log2_u32(u32 v) {   // v >= 1
     u32 r = 0;
     while ((1ull << r) < v) ++r;
@@ -416,11 +552,15 @@ __device__ __forceinline__ void push_k7(const DevCtx *c, const K7Task &t) {
     else atomicOr(c->err_flag, 1u);
 }
 
-__global__ void k_split_taskgen(const DevCtx *__restrict__ c, const SplitTask *__restrict__ L, const u32 *__restrict__ P) {
+__global__ void k_split_taskgen(const DevCtx *__restrict__ c, u32 cur) {
     if (*c->nan_flag) return;
-    const SplitTask st = L[blockIdx.x];
+    const RoundPlan pl = *c->plan;
+    const u32 nxt = cur ^ 1u;
+    const u32 *__restrict__ P = c->pmat;
+    for (u32 si = blockIdx.x; si < pl.ns; si += gridDim.x) {
+    const SplitTask st = c->splits[cur][si];
     GNode &g = c->nodes[st.node];
-    if (g.degenerate) return;
+    if (g.degenerate) continue;
     const u32 tau = c->tau;
     for (u32 d = threadIdx.x; d < st.G; d += blockDim.x) {
         u32 start = P[st.cbase + (u64)d * st.ntiles] - (u32)st.mbase;
@@ -452,11 +592,17 @@ __global__ void k_split_taskgen(const DevCtx *__restrict__ c, const SplitTask *_
             nt.G = (W + (1u << nt.shift) - 1) >> nt.shift;
             nt.src = st.dst; nt.dst = st.dst == 1 ? 2 : 1;
             nt.tile_begin = 0; nt.ntiles = 0; nt.cbase = 0; nt.mbase = 0;
-            u32 slot = atomicAdd(c->nsplits_out, 1u);
-            if (slot < c->splits_cap) c->splits_out[slot] = nt;
+            u32 slot = atomicAdd(&c->nsplits[nxt], 1u);
+            if (slot < c->splits_cap) c->splits[nxt][slot] = nt;
             else atomicOr(c->err_flag, 1u);
         }
     }
+    }
+}
+
+__global__ void k_k7_advance(const DevCtx *__restrict__ c) {
+    *c->k7_begin = *c->k7_count;
+    *c->k7_next = 0;
 }
 
 // ------------------------------------------------------------------ pass-log finalisation of a global node

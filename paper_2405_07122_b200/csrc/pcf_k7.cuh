@@ -765,9 +765,10 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
     K7Smem &S = *reinterpret_cast<K7Smem *>(k7_smem_raw);
     if (*c->nan_flag) return;
     const u32 ntasks = *c->k7_count;
+    const u32 begin = *c->k7_begin;
     for (;;) {
         if (threadIdx.x == 0) {
-            S.task_idx = atomicAdd(c->k7_next, 1u);
+            S.task_idx = begin + atomicAdd(c->k7_next, 1u);
             if (S.task_idx < ntasks) S.task = c->k7[S.task_idx];
             S.nbig = 0;
         }
