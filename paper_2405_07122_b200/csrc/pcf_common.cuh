@@ -198,6 +198,8 @@ struct RoundPlan {
     u32 ns;        // splits processed this round
     u32 tiles;     // total tiles
     u32 nblk;      // scan blocks over the count matrix
+    u32 next_count;   // dynamic tile claims of k_split_count
+    u32 next_scatter; // dynamic tile claims of k_split_scatter
     u32 pad;
     u64 ctot;      // count-matrix entries
     u64 mtot;      // keys moved

@@ -137,7 +137,12 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__r
     const RoundPlan pl = *c->plan;
     const SplitTask *__restrict__ L = c->splits[cur];
     u32 *__restrict__ C = c->cmat;
-    for (u32 tile = blockIdx.x; tile < pl.tiles; tile += gridDim.x) {
+    __shared__ u32 tile_s;
+    for (;;) {
+        if (threadIdx.x == 0) tile_s = atomicAdd(&c->plan->next_count, 1u);
+        __syncthreads();
+        const u32 tile = tile_s;
+        if (tile >= pl.tiles) break;
         const u32 s = find_split(L, pl.ns, tile);
         const SplitTask st = L[s];
         const u32 lt = tile - st.tile_begin;
@@ -351,6 +356,7 @@ __global__ void __launch_bounds__(1024) k_round_plan(const DevCtx *__restrict__ 
             pl.ctot = lst.cbase + (u64)lst.ntiles * lst.G; pl.mtot = lst.mbase + lst.m;
         }
         pl.nblk = (u32)((pl.ctot + SCAN_CHUNK - 1) / SCAN_CHUNK);
+        pl.next_count = 0; pl.next_scatter = 0;
         pl.pad = 0;
         *c->plan = pl;
         atomicAdd(c->split_keys, (unsigned long long)pl.mtot);
@@ -445,16 +451,15 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
     }
     __syncwarp();
     // pass 1: stable rank within the warp, chunk by chunk
-    u32 rk[SC_KPL];
 #pragma unroll
-    for (u32 q = 0; q < SC_KPL; ++q) {
+    for (u32 q = 0; q < SC_KPL; ++q) {   // dig[q] becomes digit | in-warp rank << 16 (digit 0xffff: none)
         const u32 d = dig[q];
         const u32 peers = __match_any_sync(0xffffffffu, d);
         const u32 leader = __ffs(peers) - 1;
         u32 old = 0;
         if (d != 0xffffffffu && lane == leader) { old = S.wc[w][d]; S.wc[w][d] = (u16)(old + __popc(peers)); }
         old = __shfl_sync(0xffffffffu, old, leader);
-        rk[q] = old + __popc(peers & ((1u << lane) - 1));
+        dig[q] = (d & 0xffffu) | ((old + __popc(peers & ((1u << lane) - 1))) << 16);
         __syncwarp();
     }
     __syncthreads();
@@ -493,9 +498,9 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
     // stage in digit order (stable: digit run, then warp, then in-warp rank)
 #pragma unroll
     for (u32 q = 0; q < SC_KPL; ++q) {
-        const u32 d = dig[q];
-        if (d != 0xffffffffu) {
-            const u32 lp = S.tstart[d] + S.wc[w][d] + rk[q];
+        const u32 d = dig[q] & 0xffffu;
+        if (d != 0xffffu) {
+            const u32 lp = S.tstart[d] + S.wc[w][d] + (dig[q] >> 16);
             S.stage[lp] = key[q];
             S.sdig[lp] = (u16)d;
         }
@@ -515,7 +520,12 @@ __global__ void __launch_bounds__(SC_THREADS, 2) k_split_scatter(const DevCtx *_
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
     const SplitTask *__restrict__ L = c->splits[cur];
-    for (u32 tile = blockIdx.x; tile < pl.tiles; tile += gridDim.x) {
+    __shared__ u32 tile_s;
+    for (;;) {
+        if (threadIdx.x == 0) tile_s = atomicAdd(&c->plan->next_scatter, 1u);
+        __syncthreads();
+        const u32 tile = tile_s;
+        if (tile >= pl.tiles) break;
         const SplitTask st = L[find_split(L, pl.ns, tile)];
         split_scatter_tile<K>(c, S, st, tile - st.tile_begin, c->pmat);
         __syncthreads();
