@@ -383,13 +383,19 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             list.clear();
             return PCF_OK;
         };
+        // upper bound on the tiles of the next round: its keys are <= n and it has at most
+        // (splits in it) partial tiles; the first round has 1 split, the second <= GMAX
+        u64 splits_bound = 0;   // upper bound on the splits of the round being enqueued
         auto enqueue_round = [&]() {
             const u32 cur = round & 1u;
+            const u32 tile_grid = (u32)std::min<u64>(n / SPLIT_TILE + 1 + splits_bound, 0x7fffffffull);
+            // each split yields <= GMAX next splits; overflow carry-over adds <= the current ones
+            splits_bound = std::min<u64>(splits_bound * (GMAX + 1), caps.split_cap);
             tm.begin(PH_OTHER);
             k_round_plan<<<1, 1024, 0, st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_COUNT);
-            k_split_count<K><<<nsm * 4, SPLIT_THREADS, 0, st>>>(d_ctx, cur);
+            k_split_count<K><<<tile_grid, SPLIT_THREADS, 0, st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_OTHER);
             k_scanp_partials<<<nsm * 2, SCAN_THREADS, 0, st>>>(d_ctx);
@@ -397,7 +403,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             k_scanp_final<<<nsm * 2, SCAN_THREADS, 0, st>>>(d_ctx);
             tm.end();
             tm.begin(PH_SCATTER);
-            k_split_scatter<K><<<nsm * 2, SC_THREADS, split_smem_bytes(), st>>>(d_ctx, cur);
+            k_split_scatter<K><<<tile_grid, SC_THREADS, split_smem_bytes(), st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_OTHER);
             k_split_taskgen<<<nsm * 2, 256, 0, st>>>(d_ctx, cur);
@@ -409,6 +415,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         for (;;) {
             rc = flush_list();
             if (rc) return rc;
+            splits_bound = pending;
             for (u32 k = 0; k < rounds_per_batch; ++k) enqueue_round();
             CK(cudaGetLastError());
             // K7 over every group produced so far (persistent grid; reads the task count on the device)

@@ -137,12 +137,9 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__r
     const RoundPlan pl = *c->plan;
     const SplitTask *__restrict__ L = c->splits[cur];
     u32 *__restrict__ C = c->cmat;
-    __shared__ u32 tile_s;
-    for (;;) {
-        if (threadIdx.x == 0) tile_s = atomicAdd(&c->plan->next_count, 1u);
-        __syncthreads();
-        const u32 tile = tile_s;
-        if (tile >= pl.tiles) break;
+    {
+        const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
+        if (tile >= pl.tiles) return;
         const u32 s = find_split(L, pl.ns, tile);
         const SplitTask st = L[s];
         const u32 lt = tile - st.tile_begin;
@@ -172,7 +169,6 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__r
         }
         __syncthreads();
         for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
-        __syncthreads();
     }
 }
 
@@ -520,16 +516,10 @@ __global__ void __launch_bounds__(SC_THREADS, 2) k_split_scatter(const DevCtx *_
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
     const SplitTask *__restrict__ L = c->splits[cur];
-    __shared__ u32 tile_s;
-    for (;;) {
-        if (threadIdx.x == 0) tile_s = atomicAdd(&c->plan->next_scatter, 1u);
-        __syncthreads();
-        const u32 tile = tile_s;
-        if (tile >= pl.tiles) break;
-        const SplitTask st = L[find_split(L, pl.ns, tile)];
-        split_scatter_tile<K>(c, S, st, tile - st.tile_begin, c->pmat);
-        __syncthreads();
-    }
+    const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
+    if (tile >= pl.tiles) return;
+    const SplitTask st = L[find_split(L, pl.ns, tile)];
+    split_scatter_tile<K>(c, S, st, tile - st.tile_begin, c->pmat);
 }
 
 __host__ __device__ inline u32 ceil_log2_u32(u32 v) {   // v >= 1
