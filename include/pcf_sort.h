@@ -133,7 +133,9 @@ int pcf_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const pcf_params *
 
 /* End-to-end entry: HOST pointers (pinned memory recommended).  Copies the n
  * keys to the device, sorts them with pcf_sort_*, copies the result back and
- * synchronises `stream`.  Device buffers are stream-ordered allocations freed
+ * synchronises `stream`.  If p->workspace holds at least
+ * round_up(8n, 256) + pcf_workspace_bytes(n) bytes it is used as [device keys |
+ * sort workspace]; otherwise device buffers are stream-ordered allocations freed
  * before return.  in_host == out_host is allowed. */
 int pcf_sort_f64_host(const double *in_host, double *out_host, size_t n, const pcf_params *p, void *stream);
 int pcf_sort_u64_host(const uint64_t *in_host, uint64_t *out_host, size_t n, const pcf_params *p, void *stream);

@@ -12,7 +12,7 @@ import os
 
 from ._build import LIB_PATH, build  # noqa: F401
 
-__all__ = ["build", "lib", "sort", "sort_host", "workspace_bytes", "PCFError", "KEY_F64", "KEY_U64",
+__all__ = ["build", "lib", "sort", "sort_host", "workspace_bytes", "host_workspace_bytes", "PCFError", "KEY_F64", "KEY_U64",
            "FLAG_SYNC", "FLAG_SAMPLE_ALL", "FLAG_TIMING", "PHASES"]
 
 KEY_F64, KEY_U64 = 0, 1
@@ -195,9 +195,16 @@ def NODE_DTYPE():
                      ("n_recurse", "<u4"), ("reserved", "<u4")])
 
 
-def sort_host(x, out=None, *, tau: int = 64, seed: int = 0, stream=None):
+def host_workspace_bytes(n: int) -> int:
+    """Device workspace that lets ``sort_host`` run without allocating: the n keys
+    (rounded to 256 B) followed by ``workspace_bytes(n)``."""
+    return ((8 * n + 255) // 256) * 256 + workspace_bytes(n)
+
+
+def sort_host(x, out=None, *, tau: int = 64, seed: int = 0, workspace=None, stream=None):
     """End-to-end sort of HOST keys (numpy array or CPU tensor; pinned recommended)
-    through ``pcf_sort_*_host``: H2D copy, device sort, D2H copy, synchronise."""
+    through ``pcf_sort_*_host``: H2D copy, device sort, D2H copy, synchronise.
+    ``workspace`` (a CUDA tensor of >= host_workspace_bytes(n) bytes) avoids allocations."""
     import numpy as np
     import torch
 
@@ -218,6 +225,8 @@ def sort_host(x, out=None, *, tau: int = 64, seed: int = 0, stream=None):
         optr = out.ctypes.data
     fn = lib().pcf_sort_f64_host if is_f64 else lib().pcf_sort_u64_host
     p = make_params(tau, seed, FLAG_SYNC)
+    if workspace is not None:
+        p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
     s = stream if stream is not None else torch.cuda.current_stream()
     rc = fn(ctypes.c_void_p(ptr), ctypes.c_void_p(optr), n, ctypes.byref(p), ctypes.c_void_p(s.cuda_stream))
     _check(rc)

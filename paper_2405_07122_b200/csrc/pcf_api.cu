@@ -411,7 +411,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             launches += 7;
             round++;
         };
-        u32 rounds_per_batch = 3;   // enough for n <= 2^32 on well-modelled data
+        u32 rounds_per_batch = 2;   // enough for 10^6..10^9 keys of well-modelled data
         for (;;) {
             rc = flush_list();
             if (rc) return rc;
@@ -525,17 +525,35 @@ static int sort_host(const u64 *in_h, u64 *out_h, size_t n, const pcf_params *pp
     if (n == 0) return PCF_OK;
     if (!in_h || !out_h) return fail(PCF_ERR_INVALID_ARG, "NULL host pointer with n > 0");
     u64 *d = nullptr;
-    cudaError_t e = cudaMallocAsync((void **)&d, n * 8, st);
-    if (e != cudaSuccess) { cudaGetLastError(); return fail(PCF_ERR_OOM, "cudaMallocAsync keys failed"); }
+    cudaError_t e = cudaSuccess;
+    const size_t key_bytes = align_up(n * 8, 256);
+    const size_t sort_ws = workspace_bytes_impl(n);
+    pcf_params p;
+    pcf_params_init(&p);
+    if (pp) {
+        if (pp->struct_size < sizeof(pcf_params)) return fail(PCF_ERR_INVALID_ARG, "pcf_params.struct_size too small");
+        p = *pp;
+    }
+    const bool own_keys = !(p.workspace && p.workspace_bytes >= key_bytes + sort_ws);
+    if (own_keys) {
+        p.workspace = nullptr;
+        p.workspace_bytes = 0;
+        e = cudaMallocAsync((void **)&d, n * 8, st);
+        if (e != cudaSuccess) { cudaGetLastError(); return fail(PCF_ERR_OOM, "cudaMallocAsync keys failed"); }
+    } else {   // caller workspace: [keys | sort workspace]
+        d = (u64 *)p.workspace;
+        p.workspace = (char *)p.workspace + key_bytes;
+        p.workspace_bytes -= key_bytes;
+    }
     int rc = PCF_OK;
     e = cudaMemcpyAsync(d, in_h, n * 8, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
-    if (!rc) rc = sort_device<K>(d, d, n, pp, st);
+    if (!rc) rc = sort_device<K>(d, d, n, &p, st);
     if (!rc) {
         e = cudaMemcpyAsync(out_h, d, n * 8, cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
     }
-    cudaFreeAsync(d, st);
+    if (own_keys) cudaFreeAsync(d, st);
     e = cudaStreamSynchronize(st);
     if (!rc && e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
     return rc;
