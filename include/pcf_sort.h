@@ -31,7 +31,7 @@ extern "C" {
 
 /* ---- status codes (every entry point returns one) ---------------------- */
 #define PCF_OK 0
-#define PCF_ERR_INVALID_ARG 1          /* NULL with n>0, tau<2, bad overlap, n > 2^40, bad struct_size */
+#define PCF_ERR_INVALID_ARG 1          /* NULL with n>0, tau<2, bad overlap, n >= 2^32, bad struct_size */
 #define PCF_ERR_NAN 2                  /* f64 input contains a NaN (domain error)         */
 #define PCF_ERR_WORKSPACE_TOO_SMALL 3  /* caller workspace smaller than pcf_workspace_bytes()          */
 #define PCF_ERR_OOM 4                  /* device allocation failed                                     */
@@ -47,6 +47,7 @@ extern "C" {
 #define PCF_FLAG_SYNC       1u  /* synchronise the stream before returning and report NaN/overflow */
 #define PCF_FLAG_SAMPLE_ALL 2u  /* test mode (reading R14): sample = whole segment, alpha = m      */
 #define PCF_FLAG_TIMING     4u  /* record CUDA events per phase into stats->phase_ms (implies SYNC) */
+#define PCF_FLAG_PROFILE    8u  /* K7 per-phase SM cycle counters into stats->k7_cycles (with SYNC) */
 
 /* One record per bucketing node, i.e. per call of Alg. 1 that reaches its
  * model-based bucketing step.  Identical layout to the
@@ -94,6 +95,8 @@ typedef struct pcf_stats {
      * [4] smem subtree (K7)  [5] global fallback sort  [6] other  [7] total */
     float phase_ms[PCF_PHASES];
     uint64_t phase_bytes[PCF_PHASES];  /* algorithmic bytes per phase */
+    /* PCF_FLAG_PROFILE: clock64 cycles summed over K7 CTAs per phase (see pcf_k7.cuh prof_mark) */
+    uint64_t k7_cycles[16];
 } pcf_stats;
 
 typedef struct pcf_params {

@@ -16,7 +16,7 @@ __all__ = ["build", "lib", "sort", "sort_host", "workspace_bytes", "host_workspa
            "FLAG_SYNC", "FLAG_SAMPLE_ALL", "FLAG_TIMING", "PHASES"]
 
 KEY_F64, KEY_U64 = 0, 1
-FLAG_SYNC, FLAG_SAMPLE_ALL, FLAG_TIMING = 1, 2, 4
+FLAG_SYNC, FLAG_SAMPLE_ALL, FLAG_TIMING, FLAG_PROFILE = 1, 2, 4, 8
 PHASES = ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "total"]
 STATUS = {0: "PCF_OK", 1: "PCF_ERR_INVALID_ARG", 2: "PCF_ERR_NAN", 3: "PCF_ERR_WORKSPACE_TOO_SMALL",
           4: "PCF_ERR_OOM", 5: "PCF_ERR_CUDA", 6: "PCF_ERR_LOG_OVERFLOW", 7: "PCF_ERR_INTERNAL"}
@@ -42,7 +42,8 @@ class Stats(ctypes.Structure):
                 ("host_syncs", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
                 ("groups_smem", ctypes.c_uint64), ("split_tasks", ctypes.c_uint64),
                 ("global_nodes", ctypes.c_uint64), ("fallback_keys_global", ctypes.c_uint64),
-                ("phase_ms", ctypes.c_float * 8), ("phase_bytes", ctypes.c_uint64 * 8)]
+                ("phase_ms", ctypes.c_float * 8), ("phase_bytes", ctypes.c_uint64 * 8),
+                ("k7_cycles", ctypes.c_uint64 * 16)]
 
     def as_dict(self):
         return {"kernel_launches": self.kernel_launches, "rounds": self.rounds,
@@ -50,7 +51,8 @@ class Stats(ctypes.Structure):
                 "split_tasks": self.split_tasks, "global_nodes": self.global_nodes,
                 "fallback_keys_global": self.fallback_keys_global,
                 "phase_ms": {PHASES[i]: float(self.phase_ms[i]) for i in range(8)},
-                "phase_bytes": {PHASES[i]: int(self.phase_bytes[i]) for i in range(8)}}
+                "phase_bytes": {PHASES[i]: int(self.phase_bytes[i]) for i in range(8)},
+                "k7_cycles": [int(v) for v in self.k7_cycles]}
 
 
 class Params(ctypes.Structure):
@@ -125,7 +127,7 @@ class SortInfo:
 
 def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False, log: bool = False,
          timing: bool = False, stats: bool = False, sync: bool = True, workspace=None, node_capacity=None,
-         stream=None):
+         profile: bool = False, stream=None):
     """Sort a 1-D CUDA tensor of float64 or uint64 keys ascending (totalOrder for f64).
 
     Returns ``out`` (a new tensor unless given; ``out is x`` sorts in place), or
@@ -146,11 +148,12 @@ def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False,
     n = x.numel()
     if out is None:
         out = torch.empty_like(x)
-    flags = (FLAG_SYNC if sync else 0) | (FLAG_SAMPLE_ALL if sample_all else 0) | (FLAG_TIMING if timing else 0)
+    flags = (FLAG_SYNC if sync else 0) | (FLAG_SAMPLE_ALL if sample_all else 0) | (FLAG_TIMING if timing else 0) \
+        | (FLAG_PROFILE if profile else 0)
     p = make_params(tau, seed, flags)
     if workspace is not None:
         p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
-    info = SortInfo() if (log or timing or stats) else None
+    info = SortInfo() if (log or timing or stats or profile) else None
     keep = []
     if log:
         cap = node_capacity if node_capacity is not None else min(n, 12 * (n // max(tau, 1))) + 64

@@ -77,6 +77,7 @@ struct Counters {             // zeroed at the start of every call
     u32 nsplits[2], nitems, k7_begin;
     unsigned long long rec_count, k7_keys, split_keys, pad;
     RoundPlan plan;
+    unsigned long long k7_prof[K7_PROF_SLOTS];
 };
 
 struct Layout {
@@ -280,6 +281,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     hc.k7_begin = &d_cnt->k7_begin;
     hc.split_keys = &d_cnt->split_keys;
     hc.plan = &d_cnt->plan;
+    hc.k7_prof = (p.flags & PCF_FLAG_PROFILE) ? d_cnt->k7_prof : nullptr;
     if (!logging) hc.rec_count = &d_cnt->rec_count;
     CK(cudaMemcpyAsync(d_ctx, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_cnt, 0, sizeof(Counters), st));
@@ -505,6 +507,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             if (cnt > p.log->capacity) status = fail(PCF_ERR_LOG_OVERFLOW, "pass log capacity exceeded");
         }
         if (status == PCF_ERR_NAN) fail(PCF_ERR_NAN, "input contains NaN");
+        for (int i = 0; i < K7_PROF_SLOTS; ++i) stats.k7_cycles[i] = hcnt.k7_prof[i];
     }
     stats.kernel_launches = launches;
     if (timing) {

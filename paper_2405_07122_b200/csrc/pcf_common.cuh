@@ -227,6 +227,7 @@ struct DevCtx {
     u32 *cmat, *pmat, *bsum;
     u64 cmat_cap;
     unsigned long long *split_keys;   // keys moved by split passes (byte accounting)
+    unsigned long long *k7_prof;      // PCF_FLAG_PROFILE: K7 cycles per phase (NULL = off)
     SegItem *items;
     u32 *nitems;
     u32 items_cap;
@@ -243,5 +244,6 @@ struct DevCtx {
 };
 
 constexpr u32 FLAG_SAMPLE_ALL = 2u;
+constexpr int K7_PROF_SLOTS = 16;
 
 }  // namespace pcf

@@ -71,7 +71,22 @@ struct K7Smem {
     Model gmd;
     const u32 *gT;
     u32 *gH;
+    long long prof_t;                       // PCF_FLAG_PROFILE bookkeeping (thread 0)
+    unsigned long long prof[K7_PROF_SLOTS];
 };
+
+// K7 phase profiling (PCF_FLAG_PROFILE): thread 0 charges the cycles since the
+// previous mark to slot `id`.  Slots: 0 claim, 1 load, 2 group classify,
+// 3 group partition, 4 children: classify+lists, 5 children: networks,
+// 6 children: rank, 7 children: warp items (incl. barrier wait), 8 cta_node
+// fit+classify, 9 cta_node partition, 10 sort/node tasks, 11 tasks, 12 keys.
+__device__ __forceinline__ void prof_mark(const DevCtx *c, K7Smem &S, int id) {
+    if (c->k7_prof && threadIdx.x == 0) {
+        long long t = clock64();
+        S.prof[id] += (unsigned long long)(t - S.prof_t);
+        S.prof_t = t;
+    }
+}
 
 // ------------------------------------------------------------------ small helpers
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }
@@ -628,6 +643,7 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
         }
     }
     __syncthreads();
+    prof_mark(c, S, 4);
     // leaf buckets of <= 16 keys: one thread per bucket, register network, by size class
 #pragma unroll 1
     for (u32 cls = 0; cls < 3; ++cls) {
@@ -637,6 +653,7 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
             net_sort_class<K>(cls, true, Y, e & 0xffffu, e >> 16, gout);
         }
     }
+    prof_mark(c, S, 5);
     // key-parallel rank sort of the small Standard-Sort buckets
     for (u32 i = p + threadIdx.x; i < p + m; i += K7_THREADS) {
         const u32 u = S.U[i];
@@ -645,6 +662,7 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
             if (i >= st && i < en) rank_place<K>(Y, i, st, en, gout);
         }
     }
+    prof_mark(c, S, 6);
     // warp items: recursing buckets (warp_node) and mid-size sorted buckets
     const u32 nitems = min(S.nitems, (u32)ITEM_CAP);
     const u32 lane = lane_id();
@@ -659,6 +677,7 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
         else warp_node<K>(c, S, ybuf, pos, size, Lc, gbase, gout);
     }
     __syncthreads();
+    prof_mark(c, S, 7);
 }
 
 // CTA-level Alg. 1 on X[p, p+m) (WMAX < m <= S_CAP), level L, global offset
@@ -706,7 +725,9 @@ __device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32
     if (logging) db = cta_reduce_sum64(S, db);
     for (u32 k = threadIdx.x; k < m; k += K7_THREADS) S.U[p + k] = (u16)(T[interval_index<K>(X[p + k], md)] - 1u);
     __syncthreads();
+    prof_mark(c, S, 8);
     cta_partition(S, X, Y, p, m, gamma + 1);
+    prof_mark(c, S, 9);
     if (logging) {
         u64 dh = 0;
         u32 nf = 0, ns = 0, nr = 0;
@@ -766,6 +787,10 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
     if (*c->nan_flag) return;
     const u32 ntasks = *c->k7_count;
     const u32 begin = *c->k7_begin;
+    if (c->k7_prof && threadIdx.x == 0) {
+        for (int i = 0; i < K7_PROF_SLOTS; ++i) S.prof[i] = 0;
+        S.prof_t = clock64();
+    }
     for (;;) {
         if (threadIdx.x == 0) {
             S.task_idx = begin + atomicAdd(c->k7_next, 1u);
@@ -774,6 +799,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
         }
         __syncthreads();
         if (S.task_idx >= ntasks) break;
+        prof_mark(c, S, 0);
         const K7Task task = S.task;
         const u64 *src = c->buf[task.src] + task.off;
         u64 *gout = c->buf[2] + task.off;
@@ -784,8 +810,11 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
             return;
         }
         __syncthreads();
+        prof_mark(c, S, 1);
+        if (threadIdx.x == 0 && c->k7_prof) { S.prof[11] += 1; S.prof[12] += m; }
         if (task.kind == K7_SORT) {
             cta_sort_write<K>(S.A, m, gout);
+            prof_mark(c, S, 10);
         } else if (task.kind == K7_NODE) {
             if (m <= WMAX) {
                 if (warp_id() == 0) warp_node<K>(c, S, 0u, 0u, m, task.level, task.off, gout);
@@ -819,8 +848,10 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
             }
             for (; k < m; k += K7_THREADS) S.U[k] = (u16)(__ldg(&gT[interval_index<K>(S.A[k], md)]) - task.jlo);
             __syncthreads();
+            prof_mark(c, S, 2);
             const u32 nb = task.jhi - task.jlo;
             cta_partition(S, S.A, S.B, 0u, m, nb);
+            prof_mark(c, S, 3);
             for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) S.gH[task.jlo + u] = S.Hc[u];
             cta_children<K>(c, S, 1u, 0u, m, nb, S.gnode_delta, S.gnode_level + 1, task.off, gout);
         }
@@ -839,6 +870,8 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
         }
         __syncthreads();
     }
+    if (c->k7_prof && threadIdx.x == 0)
+        for (int i = 0; i < K7_PROF_SLOTS; ++i) atomicAdd(&c->k7_prof[i], S.prof[i]);
 }
 
 }  // namespace pcf

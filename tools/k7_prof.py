@@ -1,0 +1,21 @@
+"""Print K7's per-phase cycle breakdown (PCF_FLAG_PROFILE) for a workload.
+python tools/k7_prof.py --config c2"""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2405_07122_b200 as pcf
+import synth
+NAMES = ["claim", "load", "group classify", "group partition", "children: kinds+lists", "children: networks",
+         "children: rank", "children: warp items+wait", "cta_node fit+classify", "cta_node partition",
+         "sort/node tasks", "tasks", "keys", "-", "-", "-"]
+ap = argparse.ArgumentParser(); ap.add_argument("--config", default="c2"); ap.add_argument("--n", type=int, default=None)
+a = ap.parse_args()
+x = torch.from_numpy(synth.config(a.config, n=a.n)).cuda()
+out = torch.empty_like(x)
+pcf.sort(x, out)
+_, info = pcf.sort(x, out, profile=True)
+cy = info.stats["k7_cycles"]
+tot = sum(cy[:11])
+print(f"{a.config}: tasks {cy[11]} keys {cy[12]}  total CTA-cycles {tot:.3e}  cycles/key {tot / max(cy[12], 1):.1f}")
+for i in range(11):
+    print(f"  {NAMES[i]:28s} {cy[i]:.3e}  {100 * cy[i] / max(tot, 1):5.1f}%  {cy[i] / max(cy[12], 1):6.2f} cyc/key")
