@@ -66,7 +66,7 @@ struct K7Smem {
     K7Task task;
     u32 task_idx;
     u32 nbig;
-    u32 nitems, item_next;
+    u32 nitems, nitems_lo, item_next;
     u32 gnode_delta, gnode_level;
     Model gmd;
     const u32 *gT;
@@ -253,24 +253,31 @@ __device__ void cta_sort_write(u64 *a, u32 n, u64 *gout_raw) {
 // One thread sorts a whole bucket of h <= N keys (Y[s, s+h)) in registers with
 // a fully unrolled bitonic network (+inf padded) and writes it to gout[s, s+h).
 // Predicated on `act`; the warp executes the network once for up to 32 buckets.
+template <int N>
+struct CeilLog2 { static constexpr int v = N <= 1 ? 0 : 1 + CeilLog2<(N + 1) / 2>::v; };
+template <>
+struct CeilLog2<1> { static constexpr int v = 0; };
+
 template <class K, int N>
 __device__ __forceinline__ void net_sort_write(bool act, const u64 *Y, u32 s, u32 h, u64 *gout) {
     u64 v[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = (act && (u32)i < h) ? Y[s + i] : ~0ull;
+    // Batcher's merge exchange (Knuth, TAOCP 5.2.2 Algorithm M); every step ascending
+    constexpr int T = CeilLog2<N>::v;
 #pragma unroll
-    for (int k = 2; k <= N; k <<= 1) {
+    for (int pe = T - 1; pe >= 0; --pe) {
+        const int p = 1 << pe;
 #pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int k = 0; k <= T - 1 - pe; ++k) {
+            const int d = k == 0 ? p : (1 << (T - k)) - p;
+            const int r = k == 0 ? 0 : p;
 #pragma unroll
             for (int i = 0; i < N; ++i) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const bool up = (i & k) == 0;
-                    const u64 a = v[i], b = v[l];
-                    const bool sw = up ? (a > b) : (a < b);
-                    v[i] = sw ? b : a;
-                    v[l] = sw ? a : b;
+                if (i + d < N && (i & p) == r) {
+                    const u64 a = v[i], b = v[i + d];
+                    v[i] = a < b ? a : b;
+                    v[i + d] = a < b ? b : a;
                 }
             }
         }
@@ -426,11 +433,8 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
             if (u < ng) {
                 h = ws.H[u];
                 s = ws.C[u] - h;
-                if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_NET : h <= RANK_MAX ? CK_RANK : CK_BITONIC)
-                                                      : CK_RECURSE;
+                if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_NET : CK_BITONIC) : CK_RECURSE;
                 ws.T[u] = (u16)kind;
-                if (kind == CK_RANK)
-                    for (u32 i = s; i < s + h; ++i) S.U[p + i] = (u16)u;
             }
             const u32 rmask = __ballot_sync(0xffffffffu, kind == CK_RECURSE);
             if (kind == CK_RECURSE) {
@@ -467,15 +471,6 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
             }
             __syncwarp();
         }
-        // key-parallel rank sort of the small Standard-Sort buckets
-        for (u32 i = lane; i < m; i += 32) {
-            const u32 u = S.U[p + i];
-            if (u < ng && ws.T[u] == CK_RANK) {
-                const u32 en = ws.C[u], st = en - ws.H[u];
-                if (i >= st && i < en) rank_place<K>(Y + p, i, st, en, gout + p);
-            }
-        }
-        __syncwarp();
     }
 }
 
@@ -547,21 +542,35 @@ __device__ u32 cta_excl_scan(K7Smem &S, u32 *a, u32 n) {
     return total;
 }
 
-// Stable partition X[p..p+m) -> Y[p..p+m) by U[p+k] in [0, nb): per-warp
-// contiguous ranges, per-warp counters.  Hc = bucket sizes, Bs = absolute starts.
+// Stable partition X[p..p+m) -> Y[p..p+m) by U[p+k] in [0, nb): warp w owns a
+// contiguous range of <= 512 keys; pass 1 ranks each key inside its warp
+// (__match_any_sync per 32-key chunk, per-warp counters) and keeps bucket and
+// rank in a register; after the cross-warp prefix every key is placed directly.
+// Hc = bucket sizes, Bs = absolute bucket starts.
+constexpr int PART_CH = S_CAP / K7_WARPS / 32;   // <= 16 chunks per warp
 __device__ void cta_partition(K7Smem &S, const u64 *X, u64 *Y, u32 p, u32 m, u32 nb) {
     const u32 w = warp_id(), lane = lane_id();
     const u32 R = (m + K7_WARPS - 1) / K7_WARPS;
     const u32 r0 = p + min(w * R, m), r1 = p + min(w * R + R, m);
+    const u32 nch = (r1 - r0 + 31) / 32;
     for (u32 u = lane; u < nb; u += 32) S.u.wcnt[w][u] = 0;
     __syncwarp();
-    for (u32 k0 = r0; k0 < r1; k0 += 32) {
-        const u32 k = k0 + lane;
-        const bool act = k < r1;
-        const u32 u = act ? (u32)S.U[k] : 0xffffffffu;
-        const u32 peers = __match_any_sync(0xffffffffu, u);
-        if (act && (peers & lanemask_lt()) == 0) S.u.wcnt[w][u] += (u16)__popc(peers);
-        __syncwarp();
+    u32 pk[PART_CH];
+#pragma unroll
+    for (int q = 0; q < PART_CH; ++q) {
+        pk[q] = 0xffffffffu;
+        if ((u32)q < nch) {   // warp-uniform
+            const u32 k = r0 + q * 32 + lane;
+            const bool act = k < r1;
+            const u32 u = act ? (u32)S.U[k] : 0xffffffffu;
+            const u32 peers = __match_any_sync(0xffffffffu, u);
+            const u32 leader = __ffs(peers) - 1;
+            u32 old = 0;
+            if (act && lane == leader) { old = S.u.wcnt[w][u]; S.u.wcnt[w][u] = (u16)(old + __popc(peers)); }
+            old = __shfl_sync(0xffffffffu, old, leader);
+            if (act) pk[q] = u | ((old + __popc(peers & lanemask_lt())) << 16);
+            __syncwarp();
+        }
     }
     __syncthreads();
     for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
@@ -578,19 +587,12 @@ __device__ void cta_partition(K7Smem &S, const u64 *X, u64 *Y, u32 p, u32 m, u32
         for (u32 ww = 0; ww < K7_WARPS; ++ww) { u32 cc = S.u.wcnt[ww][u]; S.u.wcnt[ww][u] = (u16)run; run += cc; }
     }
     __syncthreads();
-    for (u32 k0 = r0; k0 < r1; k0 += 32) {
-        const u32 k = k0 + lane;
-        const bool act = k < r1;
-        const u32 u = act ? (u32)S.U[k] : 0xffffffffu;
-        const u32 peers = __match_any_sync(0xffffffffu, u);
-        const u32 base = act ? S.u.wcnt[w][u] : 0;
-        __syncwarp();
-        if (act) {
-            const u32 rank = __popc(peers & lanemask_lt());
-            Y[base + rank] = X[k];
-            if (rank == 0) S.u.wcnt[w][u] = (u16)(base + __popc(peers));
+#pragma unroll
+    for (int q = 0; q < PART_CH; ++q) {
+        if (pk[q] != 0xffffffffu) {
+            const u32 k = r0 + q * 32 + lane;
+            Y[S.u.wcnt[w][pk[q] & 0xffffu] + (pk[q] >> 16)] = X[k];
         }
-        __syncwarp();
     }
     __syncthreads();
 }
@@ -602,15 +604,14 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
                              u64 gbase, u64 *gout) {
     const u32 tau = c->tau;
     u64 *Y = ybuf ? S.B : S.A;
-    if (threadIdx.x == 0) { S.nitems = 0; S.item_next = 0; S.nleaf[0] = S.nleaf[1] = S.nleaf[2] = 0; }
+    if (threadIdx.x == 0) { S.nitems = 0; S.nitems_lo = 0; S.item_next = 0; S.nleaf[0] = S.nleaf[1] = S.nleaf[2] = 0; }
     __syncthreads();
     for (u32 u0 = 0; u0 < nb; u0 += K7_THREADS) {   // warp-uniform trip count (net sort uses __any_sync)
         const u32 u = u0 + threadIdx.x;
         const bool valid = u < nb;
         const u32 h = valid ? S.Hc[u] : 0, s = valid ? S.Bs[u] : 0;
         u32 kind = CK_EMPTY;
-        if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_NET : h <= RANK_MAX ? CK_RANK : CK_BITONIC)
-                                              : CK_RECURSE;
+        if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_NET : CK_BITONIC) : CK_RECURSE;
         if (valid) S.kindc[u] = (u8)kind;
 #pragma unroll
         for (u32 cls = 0; cls < 3; ++cls) {   // warp-aggregated append to the class list
@@ -623,9 +624,7 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
                 if (in) S.leaf[cls][base + __popc(mk & lanemask_lt())] = s | (h << 16);
             }
         }
-        if (kind == CK_RANK) {
-            for (u32 i = s; i < s + h; ++i) S.U[i] = (u16)u;
-        } else if (kind == CK_RECURSE || kind == CK_BITONIC) {
+        if (kind == CK_RECURSE || kind == CK_BITONIC) {
             if (h > WMAX) {
                 const u32 slot = atomicAdd(&S.nbig, 1u);
                 if (slot < BIG_CAP) {
@@ -636,8 +635,11 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
                     atomicOr(c->err_flag, 2u);
                 }
             } else {
-                const u32 slot = atomicAdd(&S.nitems, 1u);
-                if (slot < ITEM_CAP) S.items[slot] = s | (h << 13) | ((kind == CK_RECURSE ? 0u : 1u) << 24);
+                // large items from the front, small ones from the back: processed largest-first
+                const bool large = h >= 256;
+                const u32 slot = atomicAdd(large ? &S.nitems : &S.nitems_lo, 1u);
+                if (slot + (large ? S.nitems_lo : S.nitems) < ITEM_CAP)
+                    S.items[large ? slot : ITEM_CAP - 1 - slot] = s | (h << 13) | ((kind == CK_RECURSE ? 0u : 1u) << 24);
                 else atomicOr(c->err_flag, 2u);
             }
         }
@@ -654,24 +656,17 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
         }
     }
     prof_mark(c, S, 5);
-    // key-parallel rank sort of the small Standard-Sort buckets
-    for (u32 i = p + threadIdx.x; i < p + m; i += K7_THREADS) {
-        const u32 u = S.U[i];
-        if (u < nb && S.kindc[u] == CK_RANK) {
-            const u32 st = S.Bs[u], en = st + S.Hc[u];
-            if (i >= st && i < en) rank_place<K>(Y, i, st, en, gout);
-        }
-    }
     prof_mark(c, S, 6);
     // warp items: recursing buckets (warp_node) and mid-size sorted buckets
-    const u32 nitems = min(S.nitems, (u32)ITEM_CAP);
+    const u32 nhi = S.nitems, nlo = S.nitems_lo;
+    const u32 nitems = min(nhi + nlo, (u32)ITEM_CAP);
     const u32 lane = lane_id();
     for (;;) {
         u32 idx = 0;
         if (lane == 0) idx = atomicAdd(&S.item_next, 1u);
         idx = __shfl_sync(0xffffffffu, idx, 0);
         if (idx >= nitems) break;
-        const u32 it = S.items[idx];
+        const u32 it = S.items[idx < nhi ? idx : ITEM_CAP - 1 - (idx - nhi)];
         const u32 pos = it & 0x1fffu, size = (it >> 13) & 0x7ffu;
         if (it >> 24) warp_sort_write<K>(Y + pos, size, gout + pos);
         else warp_node<K>(c, S, ybuf, pos, size, Lc, gbase, gout);
