@@ -433,7 +433,9 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
             if (u < ng) {
                 h = ws.H[u];
                 s = ws.C[u] - h;
-                if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_RANK : CK_BITONIC) : CK_RECURSE;
+                // small leaves: rank pass for nodes with few buckets, class networks otherwise
+                if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? (ng < 64 ? CK_RANK : CK_NET) : CK_BITONIC)
+                                                      : CK_RECURSE;
                 ws.T[u] = (u16)kind;
                 if (kind == CK_RANK)
                     for (u32 i = s; i < s + h; ++i) S.U[p + i] = (u16)u;
@@ -454,12 +456,34 @@ __device__ void warp_node(const DevCtx *c, K7Smem &S, u32 buf0, u32 p0, u32 m0, 
             }
         }
         __syncwarp();
-        // leaf buckets of <= 16 keys: key-parallel rank sort (each key scans its own bucket)
-        for (u32 i = lane; i < m; i += 32) {
-            const u32 u = S.U[p + i];
-            if (u < ng && ws.T[u] == CK_RANK) {
-                const u32 en = ws.C[u], st = en - ws.H[u];
-                if (i >= st && i < en) rank_place<K>(Y + p, i, st, en, gout + p);
+        if (ng < 64) {
+            // leaf buckets of <= 16 keys: key-parallel rank sort (each key scans its own bucket)
+            for (u32 i = lane; i < m; i += 32) {
+                const u32 u = S.U[p + i];
+                if (u < ng && ws.T[u] == CK_RANK) {
+                    const u32 en = ws.C[u], st = en - ws.H[u];
+                    if (i >= st && i < en) rank_place<K>(Y + p, i, st, en, gout + p);
+                }
+            }
+        } else {
+            // leaf buckets of <= 16 keys: compacted per size class (list in ws.cnt),
+            // one lane per bucket, register network
+#pragma unroll 1
+            for (u32 cls = 0; cls < 3; ++cls) {
+                u32 nl = 0;
+                for (u32 u0 = 0; u0 < ng; u0 += 32) {
+                    const u32 u = u0 + lane;
+                    const bool in = u < ng && ws.T[u] == CK_NET && net_class(ws.H[u]) == cls;
+                    const u32 mk = __ballot_sync(0xffffffffu, in);
+                    if (in) ws.cnt[nl + __popc(mk & lanemask_lt())] = (u16)u;
+                    nl += __popc(mk);
+                }
+                __syncwarp();
+                for (u32 i = lane; i < nl; i += 32) {
+                    const u32 u = ws.cnt[i], h = ws.H[u];
+                    net_sort_class<K>(cls, true, Y + p, ws.C[u] - h, h, gout + p);
+                }
+                __syncwarp();
             }
         }
         __syncwarp();
