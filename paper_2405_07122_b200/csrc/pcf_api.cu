@@ -81,7 +81,7 @@ struct Counters {             // zeroed at the start of every call
 };
 
 struct Layout {
-    size_t ctx, counters, tmp, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
+    size_t ctx, counters, tmp, digs, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
 };
 
 static Layout layout_for(const Caps &c) {
@@ -91,6 +91,7 @@ static Layout layout_for(const Caps &c) {
     L.ctx = take(sizeof(DevCtx));
     L.counters = take(sizeof(Counters));
     L.tmp = take(c.n * 8);
+    L.digs = take(c.n * 2);
     L.nodes = take((size_t)c.node_cap * sizeof(GNode));
     L.acc = take((size_t)c.node_cap * sizeof(NodeAcc));
     L.arena = take(c.arena_u32 * 4);
@@ -270,6 +271,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.pmat = (u32 *)(ws + L.pmat);
         hc.bsum = (u32 *)(ws + L.bsum);
         hc.cmat_cap = caps.cmat_cap;
+        hc.digs = (u16 *)(ws + L.digs);
     }
     hc.nan_flag = &d_cnt->nan_flag;
     hc.err_flag = &d_cnt->err_flag;

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__r
             const Model md = g.md;
             const u64 *x = c->buf[st.src] + st.off;
             const u32 *T = g.T;
+            u16 *dg = c->digs + st.off;
             constexpr u32 UB = 4;
             u32 k = k0 + threadIdx.x;
             for (; k + (UB - 1) * SPLIT_THREADS < k1; k += UB * SPLIT_THREADS) {
@@ -163,9 +164,17 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__r
 #pragma unroll
                 for (u32 q = 0; q < UB; ++q) ix[q] = __ldg(&T[interval_index<K>(K::to_okey(raw[q]), md)]);
 #pragma unroll
-                for (u32 q = 0; q < UB; ++q) atomicAdd(&hist[(ix[q] - st.jlo) >> st.shift], 1u);
+                for (u32 q = 0; q < UB; ++q) {
+                    const u32 d = (ix[q] - st.jlo) >> st.shift;
+                    dg[k + q * SPLIT_THREADS] = (u16)d;
+                    atomicAdd(&hist[d], 1u);
+                }
             }
-            for (; k < k1; k += SPLIT_THREADS) atomicAdd(&hist[digit_of<K>(K::to_okey(x[k]), md, T, st.jlo, st.shift)], 1u);
+            for (; k < k1; k += SPLIT_THREADS) {
+                const u32 d = digit_of<K>(K::to_okey(x[k]), md, T, st.jlo, st.shift);
+                dg[k] = (u16)d;
+                atomicAdd(&hist[d], 1u);
+            }
         }
         __syncthreads();
         for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
@@ -435,15 +444,11 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
     u32 dig[SC_KPL];
 #pragma unroll
     for (u32 q = 0; q < SC_KPL; ++q) { u32 k = r0 + q * 32 + lane; key[q] = k < k1 ? x[k] : 0; }
+    const u16 *dg = c->digs + st.off;   // digits cached by k_split_count
 #pragma unroll
     for (u32 q = 0; q < SC_KPL; ++q) {
         u32 k = r0 + q * 32 + lane;
-        dig[q] = k < k1 ? interval_index<K>(K::to_okey(key[q]), md) : 0u;
-    }
-#pragma unroll
-    for (u32 q = 0; q < SC_KPL; ++q) {
-        u32 k = r0 + q * 32 + lane;
-        dig[q] = k < k1 ? (__ldg(&T[dig[q]]) - st.jlo) >> st.shift : 0xffffffffu;
+        dig[q] = k < k1 ? (u32)dg[k] : 0xffffffffu;
     }
     __syncwarp();
     // pass 1: stable rank within the warp, chunk by chunk
