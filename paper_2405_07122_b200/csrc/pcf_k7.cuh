@@ -66,7 +66,7 @@ struct K7Smem {
     K7Task task;
     u32 task_idx;
     u32 nbig;
-    u32 nitems, nitems_lo, item_next, item_keys;
+    u32 nitems, nitems_lo, item_next;
     u32 gnode_delta, gnode_level;
     Model gmd;
     const u32 *gT;
@@ -620,10 +620,7 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
                              u64 gbase, u64 *gout) {
     const u32 tau = c->tau;
     u64 *Y = ybuf ? S.B : S.A;
-    if (threadIdx.x == 0) {
-        S.nitems = 0; S.nitems_lo = 0; S.item_next = 0; S.item_keys = 0;
-        S.nleaf[0] = S.nleaf[1] = S.nleaf[2] = 0;
-    }
+    if (threadIdx.x == 0) { S.nitems = 0; S.nitems_lo = 0; S.item_next = 0; S.nleaf[0] = S.nleaf[1] = S.nleaf[2] = 0; }
     __syncthreads();
     for (u32 u0 = 0; u0 < nb; u0 += K7_THREADS) {   // warp-uniform trip count (net sort uses __any_sync)
         const u32 u = u0 + threadIdx.x;
@@ -643,19 +640,8 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
                 if (in) S.leaf[cls][base + __popc(mk & lanemask_lt())] = s | (h << 16);
             }
         }
-        u32 ik = (kind == CK_RECURSE || kind == CK_BITONIC) && h <= WMAX ? h : 0u;
-        ik = warp_sum_u32(ik);
-        if (lane_id() == 0 && ik) atomicAdd(&S.item_keys, ik);
-    }
-    __syncthreads();
-    // Items larger than an eighth of all item keys would leave most warps idle behind
-    // one long warp_node: the whole CTA runs them instead (cta_node / cta_sort).
-    const u32 promote = max(256u, S.item_keys / 8);
-    for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
-        const u32 kind = S.kindc[u];
         if (kind == CK_RECURSE || kind == CK_BITONIC) {
-            const u32 h = S.Hc[u], s = S.Bs[u];
-            if (h > WMAX || h > promote) {
+            if (h > WMAX) {
                 const u32 slot = atomicAdd(&S.nbig, 1u);
                 if (slot < BIG_CAP) {
                     BigItem it;
