@@ -429,8 +429,6 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
                                                    u32 lt, const u32 *__restrict__ P) {
     const GNode &g = c->nodes[st.node];
     if (g.degenerate) return;
-    const Model md = g.md;
-    const u32 *T = g.T;
     const u64 *x = c->buf[st.src] + st.off;
     u64 *y = c->buf[st.dst] + st.off;
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -589,18 +589,28 @@ __device__ void cta_partition(K7Smem &S, const u64 *X, u64 *Y, u32 p, u32 m, u32
         }
     }
     __syncthreads();
-    for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
-        u32 tot = 0;
-        for (u32 ww = 0; ww < K7_WARPS; ++ww) tot += S.u.wcnt[ww][u];
-        S.Hc[u] = tot;
-        S.Bs[u] = tot;
-    }
-    __syncthreads();
-    cta_excl_scan(S, S.Bs, nb);
-    for (u32 u = threadIdx.x; u < nb; u += K7_THREADS) {
-        u32 run = p + S.Bs[u];
-        S.Bs[u] = run;
-        for (u32 ww = 0; ww < K7_WARPS; ++ww) { u32 cc = S.u.wcnt[ww][u]; S.u.wcnt[ww][u] = (u16)run; run += cc; }
+    // bucket totals, their exclusive scan and the per-warp offsets in one step
+    // (thread t owns buckets 2t and 2t+1; nb <= NB_CAP = 2 * K7_THREADS)
+    {
+        const u32 u0 = 2 * threadIdx.x, u1 = u0 + 1;
+        u32 t0 = 0, t1 = 0;
+        if (u0 < nb) for (u32 ww = 0; ww < K7_WARPS; ++ww) t0 += S.u.wcnt[ww][u0];
+        if (u1 < nb) for (u32 ww = 0; ww < K7_WARPS; ++ww) t1 += S.u.wcnt[ww][u1];
+        const u32 loc = t0 + t1;
+        const u32 incl = warp_incl_scan(loc);
+        if (lane == 31) S.scan_tmp[w] = incl;
+        __syncthreads();
+        u32 wbase = 0;
+        for (u32 ww = 0; ww < w; ++ww) wbase += S.scan_tmp[ww];
+        u32 run = p + wbase + incl - loc;
+        if (u0 < nb) {
+            S.Hc[u0] = t0; S.Bs[u0] = run;
+            for (u32 ww = 0; ww < K7_WARPS; ++ww) { u32 cc = S.u.wcnt[ww][u0]; S.u.wcnt[ww][u0] = (u16)run; run += cc; }
+        }
+        if (u1 < nb) {
+            S.Hc[u1] = t1; S.Bs[u1] = run;
+            for (u32 ww = 0; ww < K7_WARPS; ++ww) { u32 cc = S.u.wcnt[ww][u1]; S.u.wcnt[ww][u1] = (u16)run; run += cc; }
+        }
     }
     __syncthreads();
 #pragma unroll
@@ -662,12 +672,13 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
     }
     __syncthreads();
     prof_mark(c, S, 4);
-    // leaf buckets of <= 16 keys: one thread per bucket, register network, by size class
-#pragma unroll 1
-    for (u32 cls = 0; cls < 3; ++cls) {
-        const u32 nl = S.nleaf[cls];
-        for (u32 i = threadIdx.x; i < nl; i += K7_THREADS) {
-            const u32 e = S.leaf[cls][i];
+    // leaf buckets of <= 16 keys: one thread per bucket, register network; the three
+    // size-class lists form one index space so every warp gets work
+    {
+        const u32 n0 = S.nleaf[0], n1 = S.nleaf[1], n2 = S.nleaf[2];
+        for (u32 i = threadIdx.x; i < n0 + n1 + n2; i += K7_THREADS) {
+            const u32 cls = i < n0 ? 0u : i < n0 + n1 ? 1u : 2u;
+            const u32 e = S.leaf[cls][i - (cls == 0 ? 0u : cls == 1 ? n0 : n0 + n1)];
             net_sort_class<K>(cls, true, Y, e & 0xffffu, e >> 16, gout);
         }
     }
@@ -701,36 +712,49 @@ __device__ void cta_node(const DevCtx *c, K7Smem &S, u32 xbuf, u32 p, u32 m, u32
     const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
     const bool logging = c->rec != nullptr;
     if (m < tau) { cta_sort_write<K>(X + p, m, gout + p); return; }
-    u64 mn = ~0ull, mx = 0;
-    for (u32 k = threadIdx.x; k < m; k += K7_THREADS) { u64 v = X[p + k]; mn = v < mn ? v : mn; mx = v > mx ? v : mx; }
-    mn = cta_reduce_min(S, mn);
-    mx = cta_reduce_max(S, mx);
-    Model md;
     const u32 P = iroot34_small(m);
-    if (!make_model<K>(mn, mx, P, md)) { cta_sort_write<K>(X + p, m, gout + p); return; }
     const u32 alpha = sample_all ? m : P, beta = P, gamma = P, delta = P;
     u32 *cnt = S.u.fit.cnt, *T = S.u.fit.T;
     for (u32 i = threadIdx.x; i <= beta + 1; i += K7_THREADS) cnt[i] = 0;
+    // x_min, x_max: one fused min/max reduction
+    u64 mn = ~0ull, mx = 0;
+    for (u32 k = threadIdx.x; k < m; k += K7_THREADS) { u64 v = X[p + k]; mn = v < mn ? v : mn; mx = v > mx ? v : mx; }
+    mn = warp_min_u64(mn);
+    mx = warp_max_u64(mx);
+    if (lane_id() == 0) { S.red[warp_id()] = mn; S.red[K7_WARPS + warp_id()] = mx; }
     __syncthreads();
+    mn = S.red[0]; mx = S.red[K7_WARPS];
+    for (u32 w = 1; w < K7_WARPS; ++w) { mn = S.red[w] < mn ? S.red[w] : mn; mx = S.red[K7_WARPS + w] > mx ? S.red[K7_WARPS + w] : mx; }
+    Model md;
+    if (!make_model<K>(mn, mx, P, md)) { __syncthreads(); cta_sort_write<K>(X + p, m, gout + p); return; }
     const u64 nkey = node_key(c->seed, L, gbase + p);
     for (u32 k = threadIdx.x; k < alpha; k += K7_THREADS) {
         u32 pos = sample_all ? k : (u32)sample_pos(nkey, k, m);
         atomicAdd(&cnt[interval_index<K>(X[p + pos], md)], 1u);
     }
     __syncthreads();
-    for (u32 i = threadIdx.x; i <= beta; i += K7_THREADS) T[i] = cnt[i + 1];
-    __syncthreads();
-    cta_excl_scan(S, T, beta + 1);
+    // b = inclusive prefix of cnt[1..beta+1] and T, in one CTA scan
     u64 db = 0;
-    for (u32 i = threadIdx.x; i <= beta; i += K7_THREADS) {
-        u32 b = T[i] + cnt[i + 1];
-        if (logging) db += digest_term(i + 1, b);
-        cnt[i + 1] = b;
-    }
-    __syncthreads();
-    for (u32 i = threadIdx.x; i <= beta; i += K7_THREADS) {
-        T[i + 1] = bucket_of(cnt[i + 1], alpha, gamma);
-        if (logging && L == 1 && c->l1_b && i < c->l1_cap) c->l1_b[i] = cnt[i + 1];
+    {
+        const u32 i0 = 2 * threadIdx.x + 1, i1 = i0 + 1;
+        const u32 v0 = i0 <= beta + 1 ? cnt[i0] : 0, v1 = i1 <= beta + 1 ? cnt[i1] : 0;
+        const u32 loc = v0 + v1;
+        const u32 incl = warp_incl_scan(loc);
+        if (lane_id() == 31) S.scan_tmp[warp_id()] = incl;
+        __syncthreads();
+        u32 wbase = 0;
+        for (u32 w = 0; w < warp_id(); ++w) wbase += S.scan_tmp[w];
+        const u32 b0 = wbase + incl - loc + v0, b1 = b0 + v1;
+        if (i0 <= beta + 1) {
+            cnt[i0] = b0; T[i0] = bucket_of(b0, alpha, gamma);
+            if (logging) db += digest_term(i0, b0);
+            if (logging && L == 1 && c->l1_b && i0 - 1 < c->l1_cap) c->l1_b[i0 - 1] = b0;
+        }
+        if (i1 <= beta + 1) {
+            cnt[i1] = b1; T[i1] = bucket_of(b1, alpha, gamma);
+            if (logging) db += digest_term(i1, b1);
+            if (logging && L == 1 && c->l1_b && i1 - 1 < c->l1_cap) c->l1_b[i1 - 1] = b1;
+        }
     }
     __syncthreads();
     if (logging) db = cta_reduce_sum64(S, db);
