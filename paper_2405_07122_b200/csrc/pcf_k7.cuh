@@ -35,6 +35,32 @@ struct WarpScratch {
     u32 stack[WSTACK];
 };
 
+// Batched processing of all small recursing nodes of one level (<= BATCH_MAX_M
+// keys each): flat key-, sample-, bin- and bucket-parallel steps for every node
+// at once, one warp per group of whole nodes for the stable placement.
+constexpr int BN_MAX = 128;          // nodes per batch
+constexpr int BBINS = 3072;          // sum of (beta+2) (and of gamma+1) per batch
+constexpr int BLIST_CAP = 1024;      // nodes per level list
+constexpr u32 BATCH_MAX_M = 1024;
+constexpr u32 BATCH_MIN_TAU = 16;    // batching needs nodes of >= 16 keys (bounds BBINS)
+constexpr int LEAF_CAP = BBINS;
+
+struct BatchSmem {
+    u32 cnt[BBINS];          // per-bin sample counts; after the fit: u16 bucket cursors
+    u16 T[BBINS];            // bucket table per node segment (1-based bins)
+    u32 H[BBINS];            // bucket sizes per node segment
+    u16 npos[BN_MAX], nm[BN_MAX], nP[BN_MAX], nal[BN_MAX];
+    u32 nbin[BN_MAX + 1], nbkt[BN_MAX + 1], nsmp[BN_MAX + 1], nkey[BN_MAX + 1];
+    unsigned long long nmin[BN_MAX], nmax[BN_MAX];
+    double nxm[BN_MAX], nrr[BN_MAX];
+    unsigned long long ndb[BN_MAX], ndh[BN_MAX];
+    u32 ncnt[BN_MAX];        // pass log: nf | ns << 10 | nr << 20
+    u8 ndeg[BN_MAX], nwarp[BN_MAX];
+    u32 list[2][BLIST_CAP];  // level node lists: pos | m << 13
+    u32 nlist[2];
+    u32 nsub;                // nodes in the current sub-batch
+};
+
 struct BigItem {
     u32 pos, size, level, buf, kind;   // kind: 0 node, 1 sort
 };
@@ -53,12 +79,13 @@ struct K7Smem {
     u32 Bs[NB_CAP + 1];      // CTA-level bucket starts (absolute buffer positions)
     u8 kindc[NB_CAP + 4];
     u32 items[ITEM_CAP];     // warp items: pos(13) | size(11) << 13 | kind(1) << 24 (0 node, 1 sort)
-    u32 leaf[3][NB_CAP];     // CTA-level network-sorted leaf buckets by class (<=4, <=8, <=16): pos | h << 16
-    u32 nleaf[3];
+    u32 leaf[LEAF_CAP];      // network-sorted leaf buckets, class segments (<=4, <=8, <=16): pos | h << 16
+    u32 nleaf[3], leafbase[3], leafcur[3];
     union {
         u16 wcnt[K7_WARPS][NB_CAP];               // CTA partition per-warp counters
         struct { u32 cnt[S_CAP / 8 + 8]; u32 T[S_CAP / 8 + 8]; } fit;   // CTA fit (beta+2 <= 863)
         WarpScratch w[K7_WARPS];
+        BatchSmem b;
     } u;
     BigItem big[BIG_CAP];
     u64 red[2 * K7_WARPS];
@@ -623,68 +650,52 @@ __device__ void cta_partition(K7Smem &S, const u64 *X, u64 *Y, u32 p, u32 m, u32
     __syncthreads();
 }
 
-// Children of a CTA-level partition into Y (Hc/Bs valid for nb buckets of the
-// range [p, p+m)): rank-sort small Standard-Sort buckets, queue the rest.
-template <class K>
-__device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m, u32 nb, u32 delta, u32 Lc,
-                             u64 gbase, u64 *gout) {
-    const u32 tau = c->tau;
-    u64 *Y = ybuf ? S.B : S.A;
-    if (threadIdx.x == 0) { S.nitems = 0; S.nitems_lo = 0; S.item_next = 0; S.nleaf[0] = S.nleaf[1] = S.nleaf[2] = 0; }
-    __syncthreads();
-    for (u32 u0 = 0; u0 < nb; u0 += K7_THREADS) {   // warp-uniform trip count (net sort uses __any_sync)
-        const u32 u = u0 + threadIdx.x;
-        const bool valid = u < nb;
-        const u32 h = valid ? S.Hc[u] : 0, s = valid ? S.Bs[u] : 0;
-        u32 kind = CK_EMPTY;
-        if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_NET : CK_BITONIC) : CK_RECURSE;
-        if (valid) S.kindc[u] = (u8)kind;
+// ------------------------------------------------------------------ leaf lists (class segments)
+// Pass 1 counts network-sorted leaf buckets per size class, leaf_segments() lays
+// the classes out in S.leaf, pass 2 appends.  Called with warp-uniform trip counts.
+__device__ __forceinline__ void leaf_count(K7Smem &S, bool is_net, u32 h) {
 #pragma unroll
-        for (u32 cls = 0; cls < 3; ++cls) {   // warp-aggregated append to the class list
-            const bool in = kind == CK_NET && net_class(h) == cls;
-            const u32 mk = __ballot_sync(0xffffffffu, in);
-            if (mk) {
-                u32 base = 0;
-                if (lane_id() == (u32)(__ffs(mk) - 1)) base = atomicAdd(&S.nleaf[cls], (u32)__popc(mk));
-                base = __shfl_sync(0xffffffffu, base, __ffs(mk) - 1);
-                if (in) S.leaf[cls][base + __popc(mk & lanemask_lt())] = s | (h << 16);
-            }
-        }
-        if (kind == CK_RECURSE || kind == CK_BITONIC) {
-            if (h > WMAX) {
-                const u32 slot = atomicAdd(&S.nbig, 1u);
-                if (slot < BIG_CAP) {
-                    BigItem it;
-                    it.pos = s; it.size = h; it.level = Lc; it.buf = ybuf; it.kind = kind == CK_RECURSE ? 0u : 1u;
-                    S.big[slot] = it;
-                } else {
-                    atomicOr(c->err_flag, 2u);
-                }
-            } else {
-                // large items from the front, small ones from the back: processed largest-first
-                const bool large = h >= 256;
-                const u32 slot = atomicAdd(large ? &S.nitems : &S.nitems_lo, 1u);
-                if (slot + (large ? S.nitems_lo : S.nitems) < ITEM_CAP)
-                    S.items[large ? slot : ITEM_CAP - 1 - slot] = s | (h << 13) | ((kind == CK_RECURSE ? 0u : 1u) << 24);
-                else atomicOr(c->err_flag, 2u);
-            }
+    for (u32 cls = 0; cls < 3; ++cls) {
+        const u32 mk = __ballot_sync(0xffffffffu, is_net && net_class(h) == cls);
+        if (mk && lane_id() == (u32)(__ffs(mk) - 1)) atomicAdd(&S.nleaf[cls], (u32)__popc(mk));
+    }
+}
+__device__ __forceinline__ void leaf_segments(const DevCtx *c, K7Smem &S) {
+    if (threadIdx.x == 0) {
+        S.leafbase[0] = 0; S.leafbase[1] = S.nleaf[0]; S.leafbase[2] = S.nleaf[0] + S.nleaf[1];
+        S.leafcur[0] = S.leafcur[1] = S.leafcur[2] = 0;
+        if (S.nleaf[0] + S.nleaf[1] + S.nleaf[2] > (u32)LEAF_CAP) atomicOr(c->err_flag, 2u);
+    }
+}
+__device__ __forceinline__ void leaf_append(K7Smem &S, bool is_net, u32 s, u32 h) {
+#pragma unroll
+    for (u32 cls = 0; cls < 3; ++cls) {
+        const bool in = is_net && net_class(h) == cls;
+        const u32 mk = __ballot_sync(0xffffffffu, in);
+        if (mk) {
+            u32 base = 0;
+            if (lane_id() == (u32)(__ffs(mk) - 1)) base = atomicAdd(&S.leafcur[cls], (u32)__popc(mk));
+            base = __shfl_sync(0xffffffffu, base, __ffs(mk) - 1);
+            const u32 slot = S.leafbase[cls] + base + __popc(mk & lanemask_lt());
+            if (in && slot < (u32)LEAF_CAP) S.leaf[slot] = s | (h << 16);
         }
     }
-    __syncthreads();
-    prof_mark(c, S, 4);
-    // leaf buckets of <= 16 keys: one thread per bucket, register network; the three
-    // size-class lists form one index space so every warp gets work
+}
+// Networks over the leaf list (one thread per bucket), then the warp items
+// (sorted buckets of 17..WMAX keys, and -- outside batch mode -- recursing ones).
+template <class K>
+__device__ void run_leaves_and_items(const DevCtx *c, K7Smem &S, u32 ybuf, u32 Lc, u64 gbase, u64 *gout) {
+    u64 *Y = ybuf ? S.B : S.A;
     {
         const u32 n0 = S.nleaf[0], n1 = S.nleaf[1], n2 = S.nleaf[2];
-        for (u32 i = threadIdx.x; i < n0 + n1 + n2; i += K7_THREADS) {
+        const u32 nt = min(n0 + n1 + n2, (u32)LEAF_CAP);
+        for (u32 i = threadIdx.x; i < nt; i += K7_THREADS) {
             const u32 cls = i < n0 ? 0u : i < n0 + n1 ? 1u : 2u;
-            const u32 e = S.leaf[cls][i - (cls == 0 ? 0u : cls == 1 ? n0 : n0 + n1)];
+            const u32 e = S.leaf[i];
             net_sort_class<K>(cls, true, Y, e & 0xffffu, e >> 16, gout);
         }
     }
     prof_mark(c, S, 5);
-    prof_mark(c, S, 6);
-    // warp items: recursing buckets (warp_node) and mid-size sorted buckets
     const u32 nhi = S.nitems, nlo = S.nitems_lo;
     const u32 nitems = min(nhi + nlo, (u32)ITEM_CAP);
     const u32 lane = lane_id();
@@ -699,6 +710,375 @@ __device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m,
         else warp_node<K>(c, S, ybuf, pos, size, Lc, gbase, gout);
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ void push_item(const DevCtx *c, K7Smem &S, u32 s, u32 h, bool sort) {
+    // large items from the front, small ones from the back: processed largest-first
+    const bool large = h >= 256;
+    const u32 slot = atomicAdd(large ? &S.nitems : &S.nitems_lo, 1u);
+    if (slot + (large ? S.nitems_lo : S.nitems) < ITEM_CAP)
+        S.items[large ? slot : ITEM_CAP - 1 - slot] = s | (h << 13) | ((sort ? 1u : 0u) << 24);
+    else atomicOr(c->err_flag, 2u);
+}
+
+__device__ __forceinline__ void reset_child_lists(K7Smem &S) {
+    if (threadIdx.x == 0) {
+        S.nitems = 0; S.nitems_lo = 0; S.item_next = 0;
+        S.nleaf[0] = S.nleaf[1] = S.nleaf[2] = 0;
+    }
+}
+
+// largest i in [0, n) with a[i] <= x (a non-decreasing, a[0] <= x)
+template <class T>
+__device__ __forceinline__ u32 seg_of(const T *a, u32 n, u32 x) {
+    u32 lo = 0, hi = n - 1;
+    while (lo < hi) { const u32 mid = (lo + hi + 1) >> 1; if (a[mid] <= x) lo = mid; else hi = mid - 1; }
+    return lo;
+}
+
+template <class K>
+__device__ __forceinline__ Model batch_model(const BatchSmem &B, u32 i) {
+    Model md;
+    md.xmin = B.nxm[i]; md.r = B.nrr[i]; md.betad = (double)B.nP[i]; md.umin = B.nmin[i];
+    md.beta = B.nP[i]; md.pad = 0;
+    return md;
+}
+
+// One batch: nodes list[cur][first, first+N), all at level L in buffer xbuf.
+// Alg. 1 lines 152-167 for every node at once; recursing children go to list[cur^1].
+template <class K>
+__device__ void batch_one(const DevCtx *c, K7Smem &S, u32 xbuf, u32 cur, u32 first, u32 N, u32 L, u64 gbase,
+                          u64 *gout) {
+    BatchSmem &B = S.u.b;
+    u64 *X = xbuf ? S.B : S.A;
+    u64 *Y = xbuf ? S.A : S.B;
+    const u32 tau = c->tau;
+    const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
+    const bool logging = c->rec != nullptr;
+    const u32 tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    // S1: per-node parameters and four exclusive scans (bins, buckets, samples, keys)
+    {
+        u32 v[4] = {0, 0, 0, 0};
+        u32 pos = 0, m = 0, P = 0, al = 0;
+        if (tid < N) {
+            const u32 e = B.list[cur][first + tid];
+            pos = e & 0x1fffu; m = e >> 13;
+            P = iroot34_small(m); al = sample_all ? m : P;
+            v[0] = P + 2; v[1] = P + 1; v[2] = al; v[3] = m;
+        }
+        u32 incl[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) incl[q] = warp_incl_scan(v[q]);
+        if (lane == 31 && w < BN_MAX / 32) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) S.red[w * 4 + q] = incl[q];   // red has 2*K7_WARPS u64 slots
+        }
+        __syncthreads();
+        if (tid < BN_MAX) {
+            u32 base[4] = {0, 0, 0, 0};
+            for (u32 ww = 0; ww < w; ++ww)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) base[q] += (u32)S.red[ww * 4 + q];
+            if (tid < N) {
+                B.npos[tid] = (u16)pos; B.nm[tid] = (u16)m; B.nP[tid] = (u16)P; B.nal[tid] = (u16)al;
+                B.nbin[tid] = base[0] + incl[0] - v[0]; B.nbkt[tid] = base[1] + incl[1] - v[1];
+                B.nsmp[tid] = base[2] + incl[2] - v[2]; B.nkey[tid] = base[3] + incl[3] - v[3];
+                B.nmin[tid] = ~0ull; B.nmax[tid] = 0; B.ndb[tid] = 0; B.ndh[tid] = 0; B.ncnt[tid] = 0; B.ndeg[tid] = 0;
+            }
+            if (tid == N - 1) {
+                B.nbin[N] = base[0] + incl[0]; B.nbkt[N] = base[1] + incl[1];
+                B.nsmp[N] = base[2] + incl[2]; B.nkey[N] = base[3] + incl[3];
+            }
+        }
+        __syncthreads();
+    }
+    const u32 M = B.nkey[N], Btot = B.nbin[N], Ktot = B.nbkt[N], Stot = B.nsmp[N];
+    for (u32 i = tid; i < N; i += K7_THREADS) B.nwarp[i] = (u8)min((u32)(K7_WARPS - 1), B.nkey[i] * K7_WARPS / M);
+    for (u32 i = tid; i < Btot; i += K7_THREADS) B.cnt[i] = 0;
+    for (u32 i = tid; i < Ktot; i += K7_THREADS) B.H[i] = 0;
+    // S2: node id of every key (into U) and per-node x_min / x_max
+    const u32 fw0 = w * (S_CAP / K7_WARPS);
+    {
+        u32 node = fw0 + lane < M ? seg_of(B.nkey, N, fw0 + lane) : 0;
+        u64 mn = ~0ull, mx = 0;
+        for (u32 j = 0; j < S_CAP / K7_WARPS / 32; ++j) {
+            const u32 f = fw0 + j * 32 + lane;
+            if (f >= M) break;
+            while (node + 1 < N && f >= B.nkey[node + 1]) {
+                if (mn != ~0ull) { atomicMin(&B.nmin[node], mn); atomicMax(&B.nmax[node], mx); }
+                mn = ~0ull; mx = 0; ++node;
+            }
+            const u32 pos = B.npos[node] + (f - B.nkey[node]);
+            const u64 v = X[pos];
+            S.U[pos] = (u16)node;
+            mn = v < mn ? v : mn; mx = v > mx ? v : mx;
+        }
+        if (mn != ~0ull) { atomicMin(&B.nmin[node], mn); atomicMax(&B.nmax[node], mx); }
+    }
+    __syncthreads();
+    // S3: models (R9/R10: degenerate nodes are sorted as a whole)
+    for (u32 i = tid; i < N; i += K7_THREADS) {
+        Model md;
+        const bool ok = make_model<K>(B.nmin[i], B.nmax[i], B.nP[i], md);
+        B.nxm[i] = md.xmin; B.nrr[i] = md.r; B.ndeg[i] = ok ? 0 : 1;
+    }
+    __syncthreads();
+    // S4: samples (R3, R4) -> per-bin counts
+    for (u32 sidx = tid; sidx < Stot; sidx += K7_THREADS) {
+        const u32 i = seg_of(B.nsmp, N, sidx);
+        const u32 k = sidx - B.nsmp[i], m = B.nm[i], p0 = B.npos[i];
+        if (B.ndeg[i]) {   // keep the segment totals consistent for the scan
+            if (k == 0) atomicAdd(&B.cnt[B.nbin[i] + 1], (u32)B.nal[i]);
+            continue;
+        }
+        const Model md = batch_model<K>(B, i);
+        const u32 pos = sample_all ? k : (u32)sample_pos(node_key(c->seed, L, gbase + p0), k, m);
+        atomicAdd(&B.cnt[B.nbin[i] + interval_index<K>(X[p0 + pos], md)], 1u);
+    }
+    __syncthreads();
+    // S5: b = prefix of the counts per node, T = floor(b*gamma/alpha)+1
+    {
+        constexpr u32 PER = (BBINS + K7_THREADS - 1) / K7_THREADS;
+        const u32 e0 = tid * PER;
+        u32 val[PER], loc = 0;
+#pragma unroll
+        for (u32 q = 0; q < PER; ++q) { val[q] = e0 + q < Btot ? B.cnt[e0 + q] : 0; loc += val[q]; }
+        const u32 incl = warp_incl_scan(loc);
+        if (lane == 31) S.scan_tmp[w] = incl;
+        __syncthreads();
+        u32 run = incl - loc;
+        for (u32 ww = 0; ww < w; ++ww) run += S.scan_tmp[ww];
+        u32 i = e0 < Btot ? seg_of(B.nbin, N, e0) : 0;
+#pragma unroll
+        for (u32 q = 0; q < PER; ++q) {
+            const u32 e = e0 + q;
+            run += val[q];
+            if (e < Btot) {
+                while (i + 1 < N && e >= B.nbin[i + 1]) ++i;
+                const u32 bi = e - B.nbin[i];   // 1-based interval index within the node
+                if (bi >= 1 && bi <= (u32)B.nP[i] + 1 && !B.ndeg[i]) {
+                    const u32 b = run - B.nsmp[i];
+                    B.T[e] = (u16)bucket_of(b, B.nal[i], B.nP[i]);
+                    if (logging) atomicAdd(&B.ndb[i], digest_term(bi, b));
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // S6: classify every key: flat bucket id (node's bucket base + T[i(x)] - 1) into U; sizes H
+    {
+        u32 node = fw0 + lane < M ? seg_of(B.nkey, N, fw0 + lane) : 0;
+        for (u32 j = 0; j < S_CAP / K7_WARPS / 32; ++j) {
+            const u32 f = fw0 + j * 32 + lane;
+            if (f >= M) break;
+            while (node + 1 < N && f >= B.nkey[node + 1]) ++node;
+            const u32 pos = B.npos[node] + (f - B.nkey[node]);
+            u32 u = 0;
+            if (!B.ndeg[node]) u = B.T[B.nbin[node] + interval_index<K>(X[pos], batch_model<K>(B, node))] - 1u;
+            const u32 fb = B.nbkt[node] + u;
+            S.U[pos] = (u16)fb;
+            atomicAdd(&B.H[fb], 1u);
+        }
+    }
+    __syncthreads();
+    // S7: bucket starts (node-local exclusive prefix of H) -> cursors; pass-log sums
+    u16 *CUR = reinterpret_cast<u16 *>(B.cnt);
+    {
+        constexpr u32 PER = (BBINS + K7_THREADS - 1) / K7_THREADS;
+        const u32 e0 = tid * PER;
+        u32 val[PER], loc = 0;
+#pragma unroll
+        for (u32 q = 0; q < PER; ++q) { val[q] = e0 + q < Ktot ? B.H[e0 + q] : 0; loc += val[q]; }
+        const u32 incl = warp_incl_scan(loc);
+        if (lane == 31) S.scan_tmp[w] = incl;
+        __syncthreads();
+        u32 run = incl - loc;
+        for (u32 ww = 0; ww < w; ++ww) run += S.scan_tmp[ww];
+        u32 i = e0 < Ktot ? seg_of(B.nbkt, N, e0) : 0;
+#pragma unroll
+        for (u32 q = 0; q < PER; ++q) {
+            const u32 e = e0 + q;
+            if (e < Ktot) {
+                while (i + 1 < N && e >= B.nbkt[i + 1]) ++i;
+                CUR[e] = (u16)(B.npos[i] + (run - B.nkey[i]));
+                if (logging && !B.ndeg[i]) {
+                    const u32 h = val[q], P = B.nP[i];
+                    atomicAdd(&B.ndh[i], digest_term(e - B.nbkt[i] + 1, h));
+                    if (h) atomicAdd(&B.ncnt[i], h >= P ? 1u : h < tau ? (1u << 10) : (1u << 20));
+                }
+            }
+            run += val[q];
+        }
+    }
+    __syncthreads();
+    // S8: stable placement (Append order); warp w places its whole nodes
+    {
+        const u32 wa = (w == 0) ? 0u : (B.nwarp[N - 1] < w ? N : seg_of(B.nwarp, N, w - 1) + 1);
+        u32 wb = wa;
+        while (wb < N && B.nwarp[wb] == w) ++wb;
+        for (u32 i = wa; i < wb; ++i) {
+            const u32 p0 = B.npos[i], m = B.nm[i];
+            for (u32 k0 = 0; k0 < m; k0 += 32) {
+                const u32 k = k0 + lane;
+                const bool act = k < m;
+                const u32 fb = act ? (u32)S.U[p0 + k] : 0xffffffffu;
+                const u32 peers = __match_any_sync(0xffffffffu, fb);
+                const u32 base = act ? CUR[fb] : 0;
+                __syncwarp();
+                if (act) {
+                    const u32 rank = __popc(peers & lanemask_lt());
+                    Y[base + rank] = X[p0 + k];
+                    if (rank == 0) CUR[fb] = (u16)(base + __popc(peers));
+                }
+                __syncwarp();
+            }
+        }
+    }
+    __syncthreads();
+    // S9: children: leaves to the networks / warp sorts, recursions to the next list
+    reset_child_lists(S);
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+        for (u32 u0 = 0; u0 < Ktot; u0 += K7_THREADS) {   // warp-uniform trip count
+            const u32 fb = u0 + tid;
+            const bool valid = fb < Ktot;
+            const u32 h = valid ? B.H[fb] : 0;
+            u32 kind = CK_EMPTY, s = 0;
+            if (h) {
+                const u32 i = seg_of(B.nbkt, N, fb);
+                s = CUR[fb] - h;
+                const bool leaf = B.ndeg[i] || h >= B.nP[i] || h < tau;
+                kind = leaf ? (h <= NET_MAX ? CK_NET : CK_BITONIC) : CK_RECURSE;
+            }
+            if (pass == 0) {
+                leaf_count(S, kind == CK_NET, h);
+                if (kind == CK_BITONIC) push_item(c, S, s, h, true);
+                const u32 rm = __ballot_sync(0xffffffffu, kind == CK_RECURSE);
+                if (rm) {
+                    u32 base = 0;
+                    if (lane == (u32)(__ffs(rm) - 1)) base = atomicAdd(&B.nlist[cur ^ 1u], (u32)__popc(rm));
+                    base = __shfl_sync(0xffffffffu, base, __ffs(rm) - 1);
+                    const u32 slot = base + __popc(rm & lanemask_lt());
+                    if (kind == CK_RECURSE) {
+                        if (slot < BLIST_CAP) B.list[cur ^ 1u][slot] = s | (h << 13);
+                        else atomicOr(c->err_flag, 2u);
+                    }
+                }
+            } else {
+                leaf_append(S, kind == CK_NET, s, h);
+            }
+        }
+        __syncthreads();
+        if (pass == 0) leaf_segments(c, S);
+        __syncthreads();
+    }
+    // S10: sort the leaves; S11: node records
+    run_leaves_and_items<K>(c, S, xbuf ^ 1u, L + 1, gbase, gout);
+    if (logging) {
+        for (u32 i = tid; i < N; i += K7_THREADS) {
+            if (B.ndeg[i]) continue;
+            const u32 cc = B.ncnt[i];
+            write_record(c, L, B.nal[i], gbase + B.npos[i], B.nm[i], K::from_okey(B.nmin[i]), K::from_okey(B.nmax[i]),
+                         B.ndb[i], B.ndh[i], cc & 1023u, (cc >> 10) & 1023u, cc >> 20);
+        }
+    }
+    __syncthreads();
+}
+
+// All levels of batched nodes starting from list[0] (level L, buffer xbuf).
+template <class K>
+__device__ void batch_levels(const DevCtx *c, K7Smem &S, u32 xbuf, u32 L, u64 gbase, u64 *gout) {
+    BatchSmem &B = S.u.b;
+    u32 cur = 0;
+    for (;;) {
+        __syncthreads();
+        const u32 ntot = min(B.nlist[cur], (u32)BLIST_CAP);
+        if (ntot == 0) break;
+        __syncthreads();
+        if (threadIdx.x == 0) B.nlist[cur ^ 1u] = 0;
+        __syncthreads();
+        for (u32 first = 0; first < ntot;) {
+            // sub-batch: <= BN_MAX nodes with sum(beta+2) <= BBINS
+            if (threadIdx.x < BN_MAX) {
+                const u32 i = first + threadIdx.x;
+                const u32 v = i < ntot ? iroot34_small(B.list[cur][i] >> 13) + 2 : (u32)BBINS + 1;
+                const u32 incl = warp_incl_scan(v);
+                if (lane_id() == 31) S.scan_tmp[warp_id()] = incl;
+                // count of prefixes that fit (per warp, combined below)
+            }
+            __syncthreads();
+            if (threadIdx.x < BN_MAX) {
+                const u32 i = first + threadIdx.x;
+                const u32 v = i < ntot ? iroot34_small(B.list[cur][i] >> 13) + 2 : (u32)BBINS + 1;
+                u32 incl = warp_incl_scan(v);
+                for (u32 ww = 0; ww < warp_id(); ++ww) incl += S.scan_tmp[ww];
+                const u32 fits = __ballot_sync(0xffffffffu, i < ntot && incl <= (u32)BBINS);
+                if (lane_id() == 0) S.red[warp_id()] = __popc(fits);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                u32 nsub = 0;
+                for (u32 ww = 0; ww < BN_MAX / 32; ++ww) nsub += (u32)S.red[ww];
+                B.nsub = max(nsub, 1u);
+            }
+            __syncthreads();
+            const u32 N = B.nsub;
+            batch_one<K>(c, S, xbuf, cur, first, N, L, gbase, gout);
+            first += N;
+        }
+        cur ^= 1u;
+        xbuf ^= 1u;
+        L += 1;
+    }
+}
+
+// Children of a CTA-level partition into Y (Hc/Bs valid for nb buckets of the
+// range [p, p+m)): leaves sorted (networks, warp sorts), recursing buckets as
+// CTA items (> WMAX), batched nodes (tau >= BATCH_MIN_TAU) or warp items.
+template <class K>
+__device__ void cta_children(const DevCtx *c, K7Smem &S, u32 ybuf, u32 p, u32 m, u32 nb, u32 delta, u32 Lc,
+                             u64 gbase, u64 *gout) {
+    const u32 tau = c->tau;
+    const bool batch = tau >= BATCH_MIN_TAU;
+    reset_child_lists(S);
+    if (threadIdx.x == 0) S.u.b.nlist[0] = 0;
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+        for (u32 u0 = 0; u0 < nb; u0 += K7_THREADS) {   // warp-uniform trip count
+            const u32 u = u0 + threadIdx.x;
+            const bool valid = u < nb;
+            const u32 h = valid ? S.Hc[u] : 0, s = valid ? S.Bs[u] : 0;
+            u32 kind = CK_EMPTY;
+            if (h) kind = (h >= delta || h < tau) ? (h <= NET_MAX ? CK_NET : CK_BITONIC) : CK_RECURSE;
+            if (pass == 1) { leaf_append(S, kind == CK_NET, s, h); continue; }
+            leaf_count(S, kind == CK_NET, h);
+            if (kind == CK_RECURSE || kind == CK_BITONIC) {
+                if (h > WMAX) {
+                    const u32 slot = atomicAdd(&S.nbig, 1u);
+                    if (slot < BIG_CAP) {
+                        BigItem it;
+                        it.pos = s; it.size = h; it.level = Lc; it.buf = ybuf; it.kind = kind == CK_RECURSE ? 0u : 1u;
+                        S.big[slot] = it;
+                    } else {
+                        atomicOr(c->err_flag, 2u);
+                    }
+                } else if (kind == CK_RECURSE && batch && h <= BATCH_MAX_M) {
+                    const u32 slot = atomicAdd(&S.u.b.nlist[0], 1u);
+                    if (slot < BLIST_CAP) S.u.b.list[0][slot] = s | (h << 13);
+                    else atomicOr(c->err_flag, 2u);
+                } else {
+                    push_item(c, S, s, h, kind == CK_BITONIC);
+                }
+            }
+        }
+        __syncthreads();
+        if (pass == 0) leaf_segments(c, S);
+        __syncthreads();
+    }
+    prof_mark(c, S, 4);
+    run_leaves_and_items<K>(c, S, ybuf, Lc, gbase, gout);
+    prof_mark(c, S, 6);
+    if (batch) batch_levels<K>(c, S, ybuf, Lc, gbase, gout);
     prof_mark(c, S, 7);
 }
 
