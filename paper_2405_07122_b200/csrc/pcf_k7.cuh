@@ -796,14 +796,16 @@ __device__ void batch_one(const DevCtx *c, K7Smem &S, u32 xbuf, u32 cur, u32 fir
     for (u32 i = tid; i < N; i += K7_THREADS) B.nwarp[i] = (u8)min((u32)(K7_WARPS - 1), B.nkey[i] * K7_WARPS / M);
     for (u32 i = tid; i < Btot; i += K7_THREADS) B.cnt[i] = 0;
     for (u32 i = tid; i < Ktot; i += K7_THREADS) B.H[i] = 0;
-    // S2: node id of every key (into U) and per-node x_min / x_max
-    const u32 fw0 = w * (S_CAP / K7_WARPS);
+    // S2: node id of every key (into U) and per-node x_min / x_max;
+    // warp w takes the flat keys [w*R, (w+1)*R), R a multiple of 32
+    const u32 Rw = ((M + K7_WARPS * 32 - 1) / (K7_WARPS * 32)) * 32;
+    const u32 fw0 = w * Rw, fw1 = min(M, fw0 + Rw);
     {
-        u32 node = fw0 + lane < M ? seg_of(B.nkey, N, fw0 + lane) : 0;
+        u32 node = fw0 + lane < fw1 ? seg_of(B.nkey, N, fw0 + lane) : 0;
         u64 mn = ~0ull, mx = 0;
-        for (u32 j = 0; j < S_CAP / K7_WARPS / 32; ++j) {
+        for (u32 j = 0; j < Rw / 32; ++j) {
             const u32 f = fw0 + j * 32 + lane;
-            if (f >= M) break;
+            if (f >= fw1) break;
             while (node + 1 < N && f >= B.nkey[node + 1]) {
                 if (mn != ~0ull) { atomicMin(&B.nmin[node], mn); atomicMax(&B.nmax[node], mx); }
                 mn = ~0ull; mx = 0; ++node;
@@ -867,10 +869,10 @@ __device__ void batch_one(const DevCtx *c, K7Smem &S, u32 xbuf, u32 cur, u32 fir
     __syncthreads();
     // S6: classify every key: flat bucket id (node's bucket base + T[i(x)] - 1) into U; sizes H
     {
-        u32 node = fw0 + lane < M ? seg_of(B.nkey, N, fw0 + lane) : 0;
-        for (u32 j = 0; j < S_CAP / K7_WARPS / 32; ++j) {
+        u32 node = fw0 + lane < fw1 ? seg_of(B.nkey, N, fw0 + lane) : 0;
+        for (u32 j = 0; j < Rw / 32; ++j) {
             const u32 f = fw0 + j * 32 + lane;
-            if (f >= M) break;
+            if (f >= fw1) break;
             while (node + 1 < N && f >= B.nkey[node + 1]) ++node;
             const u32 pos = B.npos[node] + (f - B.nkey[node]);
             u32 u = 0;
