@@ -57,11 +57,32 @@ struct Model {
     double xmin;    // f64: x_min as a double
     double r;       // fl(x_max - x_min)  (f64)  or  RN(x_max - x_min) (u64, R15)
     double betad;   // (double)beta, exact
+    double s;       // fl(beta / r): fast-path scale (NaN disables the fast path)
+    double eps;     // beta * 2^-48: fast-path guard band
     u64 umin;       // u64: x_min
     u32 beta;
     u32 pad;
 };
 
+// Reading R6 evaluated exactly as written: d = x - x_min, q = d / r, t = q * beta,
+// every op binary64 round-to-nearest-even, i = floor(t) + 1.
+__device__ __noinline__ u32 interval_index_exact(double d, double r, double betad) {
+    const double q = __ddiv_rn(d, r);
+    const double t = __dmul_rn(q, betad);
+    return __double2uint_rz(t) + 1u;   // t in [0, beta]  (R6: no clamp needed)
+}
+
+// Certified fast path for the same value.  With u = 2^-53 and
+// every intermediate normal, the exact t = fl(fl(d/r)*beta) and the estimate
+// t' = fl(d*s), s = fl(beta/r), satisfy t/t' = (1+e1)(1+e2)/((1+e3)(1+e4)),
+// |e_k| <= u, so |t - t'| <= 4.0001 u t' <= 4.0001 u beta (1 + 4u) < eps =
+// 2^-48 beta = 32 u beta.  Hence if frac(t') lies in [eps, 1 - eps], t lies in
+// the same open unit interval (floor(t'), floor(t') + 1) and floor(t) =
+// floor(t').  frac(t') >= eps also forces t' >= eps >= 32u, i.e. q and d*s
+// normal, so the relative bounds apply; a subnormal or huge s is replaced by
+// NaN in make_model (every comparison with NaN fails -> exact path), as is any
+// t' that is NaN or infinite.  Keys inside the band (x_max itself, keys within
+// a few ulps of a bin edge) take the exact path.
 template <class K>
 __device__ __forceinline__ u32 interval_index(u64 okey, const Model &md) {
     double d;
@@ -71,9 +92,11 @@ __device__ __forceinline__ u32 interval_index(u64 okey, const Model &md) {
     } else {
         d = __ull2double_rn(okey - md.umin);
     }
-    double q = __ddiv_rn(d, md.r);
-    double t = __dmul_rn(q, md.betad);
-    return __double2uint_rz(t) + 1u;   // t in [0, beta]  (R6: no clamp needed)
+    const double t = __dmul_rn(d, md.s);
+    const double fl = floor(t);
+    const double fr = __dsub_rn(t, fl);
+    if (fr >= md.eps && fr <= 1.0 - md.eps) return (u32)fl + 1u;
+    return interval_index_exact(d, md.r, md.betad);
 }
 
 // Build the model from the node's ordered min/max keys.  Returns false when
@@ -83,19 +106,24 @@ __device__ inline bool make_model(u64 kmin, u64 kmax, u32 beta, Model &md) {
     md.beta = beta;
     md.betad = (double)beta;
     md.pad = 0;
+    bool ok;
     if (K::is_f64) {
         double xa = __longlong_as_double((long long)K::from_okey(kmin));
         double xb = __longlong_as_double((long long)K::from_okey(kmax));
         md.xmin = xa;
         md.umin = 0;
         md.r = __dsub_rn(xb, xa);
-        return (md.r > 0.0) && (md.r <= 1.7976931348623157e308);
+        ok = (md.r > 0.0) && (md.r <= 1.7976931348623157e308);
     } else {
         md.xmin = 0.0;
         md.umin = kmin;
         md.r = __ull2double_rn(kmax - kmin);
-        return kmax > kmin;
+        ok = kmax > kmin;
     }
+    const double s = ok ? __ddiv_rn(md.betad, md.r) : 0.0;
+    md.s = (s >= 0x1p-1000 && s <= 0x1p1000) ? s : __longlong_as_double(0x7ff8000000000000ll);
+    md.eps = __dmul_rn(md.betad, 0x1p-48);
+    return ok;
 }
 
 // ---------------------------------------------------------------- floor(m^{3/4})  (R5)

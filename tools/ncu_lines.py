@@ -1,12 +1,14 @@
 """Summarise an ncu report's source page by CUDA source line:
-python tools/ncu_lines.py report.ncu-rep [top]  -> lines sorted by stall samples."""
+python tools/ncu_lines.py report.ncu-rep [top] [--by-instr]  -> lines sorted by stall samples
+(or by executed warp instructions)."""
 import csv
 import io
 import subprocess
 import sys
 
 rep = sys.argv[1]
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+top = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 40
+by_instr = "--by-instr" in sys.argv
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
@@ -34,7 +36,7 @@ for r in rows:
     out.append((s, ins, f"{cur_file}:{r[0]}", r[1][:70], topst))
     tot_s += s
     tot_i += ins
-out.sort(key=lambda t: -t[0])
+out.sort(key=lambda t: -(t[1] if by_instr else t[0]))
 print(f"total samples {tot_s}  total warp-instructions {tot_i}")
 for s, ins, loc, src, st in out[:top]:
     sts = " ".join(f"{k[6:]}={v}" for k, v in st if v)
