@@ -227,14 +227,16 @@ def run_gpu(args):
         return
     peak, peak_src = load_peaks()
     passes = {}
-    for k in ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort"]:
+    for k in ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other"]:
         ms = phase_ms.get(k, 0.0)
         by = phase_bytes.get(k, 0)
-        if ms > 0 and by > 0:
+        if ms > 0 and by == 0:
+            passes[k] = {"ms_per_step": ms / args.steps, "note": "round plans, count-matrix scans, task generation"}
+        elif ms > 0 and by > 0:
             gbs = by / (ms * 1e-3) / 1e9
             passes[k] = {"ms_per_step": ms / args.steps, "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
                          "bytes_per_step": by // args.steps, "bytes_rule": PASS_NOTE.get(k)}
-    dom = max(passes, key=lambda k: passes[k]["ms_per_step"]) if passes else None
+    dom = max((k for k in passes if "gbs" in passes[k]), key=lambda k: passes[k]["ms_per_step"], default=None)
     roof = None
     if dom:
         tr = traffic_from_profiles(dom)

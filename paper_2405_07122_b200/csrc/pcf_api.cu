@@ -410,7 +410,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             k_split_scatter<K><<<tile_grid, SC_THREADS, split_smem_bytes(), st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_OTHER);
-            k_split_taskgen<<<nsm * 2, 256, 0, st>>>(d_ctx, cur);
+            k_split_taskgen<<<nsm * 2, TG_THREADS, 0, st>>>(d_ctx, cur);
             tm.end();
             launches += 7;
             round++;

@@ -555,51 +555,104 @@ __device__ __forceinline__ void push_k7(const DevCtx *c, const K7Task &t) {
     else atomicOr(c->err_flag, 1u);
 }
 
-__global__ void k_split_taskgen(const DevCtx *__restrict__ c, u32 cur) {
+// Tasks of the digit groups of every split of round `cur`.  Groups larger than
+// a K7 CTA (keys > S_CAP or buckets > NB_CAP) become the next round's splits
+// (or, for a single bucket, host items: a new global node / fallback sort).
+// Runs of consecutive smaller groups are packed greedily into one K7 task of
+// <= S_CAP keys and <= NB_CAP buckets: a K7_GROUP over the run's bucket range,
+// or, for a run of one bucket, a K7_NODE / K7_SORT task (Alg. 1).
+__device__ __forceinline__ void emit_run(const DevCtx *c, const SplitTask &st, GNode &g, u32 d0, u32 d1, u32 keys,
+                                         const u32 *__restrict__ P) {
+    if (keys == 0) return;
+    const u32 start = P[st.cbase + (u64)d0 * st.ntiles] - (u32)st.mbase;
+    const u32 jlo = st.jlo + (d0 << st.shift);
+    const u32 jhi = min(st.jlo + ((d1 + 1) << st.shift), st.jhi);
+    K7Task t;
+    t.off = st.off + start; t.size = keys; t.src = st.dst; t.node = st.node; t.jlo = jlo; t.jhi = jhi; t.pad = 0;
+    if (jhi - jlo == 1) {
+        g.H[jlo] = keys;
+        const bool sort = keys >= g.delta || keys < c->tau;
+        t.kind = sort ? K7_SORT : K7_NODE;
+        t.level = g.level + 1;
+    } else {
+        t.kind = K7_GROUP;
+        t.level = g.level;
+    }
+    push_k7(c, t);
+}
+
+constexpr int TG_THREADS = 256;
+__global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__restrict__ c, u32 cur) {
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
     const u32 nxt = cur ^ 1u;
     const u32 *__restrict__ P = c->pmat;
-    for (u32 si = blockIdx.x; si < pl.ns; si += gridDim.x) {
-    const SplitTask st = c->splits[cur][si];
-    GNode &g = c->nodes[st.node];
-    if (g.degenerate) continue;
-    const u32 tau = c->tau;
-    for (u32 d = threadIdx.x; d < st.G; d += blockDim.x) {
-        u32 start = P[st.cbase + (u64)d * st.ntiles] - (u32)st.mbase;
-        u32 end = d + 1 < st.G ? P[st.cbase + (u64)(d + 1) * st.ntiles] - (u32)st.mbase : st.m;
-        u32 cnt = end - start;
-        if (cnt == 0) continue;
-        u32 jlo = st.jlo + (d << st.shift);
-        u32 jhi = min(jlo + (1u << st.shift), st.jhi);
-        u32 W = jhi - jlo;
-        u64 goff = st.off + start;
-        if (W == 1) {
-            g.H[jlo] = cnt;
-            bool sort = cnt >= g.delta || cnt < tau;   // Alg. 1
-            if (cnt <= (u32)S_CAP) {
-                K7Task t; t.off = goff; t.size = cnt; t.kind = sort ? K7_SORT : K7_NODE; t.src = st.dst;
-                t.level = g.level + 1; t.node = st.node; t.jlo = jlo; t.jhi = jhi; t.pad = 0;
-                push_k7(c, t);
-            } else {
-                push_item(c, goff, cnt, g.level + 1, st.dst, sort ? 1u : 0u);
+    const u32 lane = threadIdx.x & 31;
+    const u32 gw = blockIdx.x * (TG_THREADS / 32) + (threadIdx.x >> 5), nw = gridDim.x * (TG_THREADS / 32);
+    for (u32 si = gw; si < pl.ns; si += nw) {   // one warp per split
+        const SplitTask st = c->splits[cur][si];
+        GNode &g = c->nodes[st.node];
+        if (g.degenerate) continue;
+        u32 run_d0 = 0, run_keys = 0;
+        for (u32 base = 0; base < st.G; base += 32) {
+            // this lane's digit: count, bucket range, packable into a K7 task?
+            const u32 d = base + lane;
+            const bool valid = d < st.G;
+            u32 cn = 0, dhi = 0;
+            bool pk = true;
+            if (valid) {
+                const u32 start = P[st.cbase + (u64)d * st.ntiles] - (u32)st.mbase;
+                const u32 end = d + 1 < st.G ? P[st.cbase + (u64)(d + 1) * st.ntiles] - (u32)st.mbase : st.m;
+                cn = end - start;
+                const u32 jlo = st.jlo + (d << st.shift);
+                dhi = min(jlo + (1u << st.shift), st.jhi);
+                const u32 W = dhi - jlo;
+                pk = cn <= (u32)S_CAP && W <= (u32)NB_CAP;
+                if (!pk && cn > 0) {   // too large for a K7 CTA
+                    const u64 goff = st.off + start;
+                    if (W == 1) {
+                        g.H[jlo] = cn;
+                        const bool sort = cn >= g.delta || cn < c->tau;   // Alg. 1
+                        push_item(c, goff, cn, g.level + 1, st.dst, sort ? 1u : 0u);
+                    } else {
+                        SplitTask nt;
+                        nt.off = goff; nt.m = cn; nt.node = st.node; nt.jlo = jlo; nt.jhi = dhi;
+                        nt.shift = choose_shift(W, cn);
+                        nt.G = (W + (1u << nt.shift) - 1) >> nt.shift;
+                        nt.src = st.dst; nt.dst = st.dst == 1 ? 2 : 1;
+                        nt.tile_begin = 0; nt.ntiles = 0; nt.cbase = 0; nt.mbase = 0;
+                        u32 slot = atomicAdd(&c->nsplits[nxt], 1u);
+                        if (slot < c->splits_cap) c->splits[nxt][slot] = nt;
+                        else atomicOr(c->err_flag, 1u);
+                    }
+                }
             }
-        } else if (cnt <= (u32)S_CAP && W <= (u32)NB_CAP) {
-            K7Task t; t.off = goff; t.size = cnt; t.kind = K7_GROUP; t.src = st.dst;
-            t.level = g.level; t.node = st.node; t.jlo = jlo; t.jhi = jhi; t.pad = 0;
-            push_k7(c, t);
-        } else {
-            SplitTask nt;
-            nt.off = goff; nt.m = cnt; nt.node = st.node; nt.jlo = jlo; nt.jhi = jhi;
-            nt.shift = choose_shift(W, cnt);
-            nt.G = (W + (1u << nt.shift) - 1) >> nt.shift;
-            nt.src = st.dst; nt.dst = st.dst == 1 ? 2 : 1;
-            nt.tile_begin = 0; nt.ntiles = 0; nt.cbase = 0; nt.mbase = 0;
-            u32 slot = atomicAdd(&c->nsplits[nxt], 1u);
-            if (slot < c->splits_cap) c->splits[nxt][slot] = nt;
-            else atomicOr(c->err_flag, 1u);
+            // greedy next-fit packing of the packable digits
+            const u32 npm = __ballot_sync(0xffffffffu, !pk);
+            u32 s = 0;   // first lane of the chunk not yet assigned to a run
+            for (u32 guard = 0; s < 32 && guard < 64; ++guard) {   // each step retires >= 1 lane
+                u32 incl = lane >= s ? cn : 0;
+                for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= (u32)o) incl += y; }
+                const u32 run_jlo = st.jlo + (run_d0 << st.shift);
+                const bool bad = valid && lane >= s && (!pk || run_keys + incl > (u32)S_CAP || dhi - run_jlo > (u32)NB_CAP);
+                const u32 bm = __ballot_sync(0xffffffffu, bad);
+                if (bm == 0) { run_keys += __shfl_sync(0xffffffffu, incl, 31); s = 32; break; }
+                const u32 b = __ffs(bm) - 1;
+                const u32 before = __shfl_sync(0xffffffffu, incl, (b + 31) & 31);
+                const u32 keys = run_keys + (b > s ? before : 0);
+                if (lane == 0 && base + b > run_d0) emit_run(c, st, g, run_d0, base + b - 1, keys, P);
+                run_keys = 0;
+                if ((npm >> b) & 1u) {   // skip the non-packable digits at b, b+1, ...
+                    const u32 rest = ~npm & (b == 31 ? 0u : (0xffffffffu << (b + 1)));
+                    s = rest ? (u32)(__ffs(rest) - 1) : 32u;
+                } else {
+                    s = b;
+                }
+                run_d0 = base + s;
+            }
+            if (s < 32 && lane == 0) atomicOr(c->err_flag, 2u);   // unreachable: the loop retires a lane per step
         }
-    }
+        if (lane == 0 && run_d0 < st.G) emit_run(c, st, g, run_d0, st.G - 1, run_keys, P);
     }
 }
 
