@@ -412,13 +412,16 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_fit_final(const DevCtx *__rest
 // --- stable scatter by digit
 // One CTA per tile of SPLIT_TILE keys; warp w owns keys [w*SC_PER_WARP, ...)
 // of the tile and holds them in registers (SC_KPL per lane).  Pass 1 ranks the
-// keys stably inside the warp (__match_any_sync per 32-key chunk, per-warp
-// counters); the tile is then staged in shared memory in digit order (stable)
-// and written out run by run, so global writes are coalesced per digit run.
+// keys stably inside the warp (per-warp counters; half a chunk at a time each
+// lane ORs its bit into the high half of its digit's counter word, so after a
+// __syncwarp the word holds count | peers -- the CUB "atomic-or match", much
+// cheaper on B200 than __match_any_sync over ~30 distinct digits); the tile is
+// then staged in shared memory in digit order (stable) and written out run by
+// run, so global writes are coalesced per digit run.
 struct SplitScatterSmem {
     u64 stage[SPLIT_TILE];
     u16 sdig[SPLIT_TILE];
-    u16 wc[SC_WARPS][GMAX];     // per-warp counts -> warp-exclusive offsets within (tile, digit)
+    u32 wc[SC_WARPS][GMAX];     // per-warp count | mask -> warp-exclusive offsets within (tile, digit)
     u32 tstart[GMAX + 1];       // tile-local start of each digit's run
     u32 gbase[GMAX];            // segment-relative destination of each digit's run
     u32 scan_tmp[SC_WARPS + 1];
@@ -453,20 +456,29 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
 #pragma unroll
     for (u32 q = 0; q < SC_KPL; ++q) {   // dig[q] becomes digit | in-warp rank << 16 (digit 0xffff: none)
         const u32 d = dig[q];
-        const u32 peers = __match_any_sync(0xffffffffu, d);
-        const u32 leader = __ffs(peers) - 1;
-        u32 old = 0;
-        if (d != 0xffffffffu && lane == leader) { old = S.wc[w][d]; S.wc[w][d] = (u16)(old + __popc(peers)); }
-        old = __shfl_sync(0xffffffffu, old, leader);
-        dig[q] = (d & 0xffffu) | ((old + __popc(peers & ((1u << lane) - 1))) << 16);
-        __syncwarp();
+        u32 rank = 0;
+#pragma unroll
+        for (u32 half = 0; half < 2; ++half) {
+            const bool mine = (lane >> 4) == half && d != 0xffffffffu;
+            if (mine) atomicOr(&S.wc[w][d], 1u << (16 + (lane & 15)));
+            __syncwarp();
+            const u32 e = mine ? S.wc[w][d] : 0u;
+            __syncwarp();
+            if (mine) {
+                const u32 msk = e >> 16, lt = (1u << (lane & 15)) - 1u;
+                rank = (e & 0xffffu) + __popc(msk & lt);
+                if ((msk & lt) == 0) S.wc[w][d] = (e & 0xffffu) + __popc(msk);
+            }
+            __syncwarp();
+        }
+        dig[q] = (d & 0xffffu) | (rank << 16);
     }
     __syncthreads();
     // per digit: warp-exclusive offsets, tile totals
     for (u32 d = threadIdx.x; d < G; d += SC_THREADS) {
         u32 run = 0;
 #pragma unroll
-        for (u32 ww = 0; ww < SC_WARPS; ++ww) { u32 cc = S.wc[ww][d]; S.wc[ww][d] = (u16)run; run += cc; }
+        for (u32 ww = 0; ww < SC_WARPS; ++ww) { u32 cc = S.wc[ww][d]; S.wc[ww][d] = run; run += cc; }
         S.tstart[d] = run;
         S.gbase[d] = P[st.cbase + (u64)d * st.ntiles + lt] - (u32)st.mbase;
     }
