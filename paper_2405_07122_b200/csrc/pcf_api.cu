@@ -81,7 +81,7 @@ struct Counters {             // zeroed at the start of every call
 };
 
 struct Layout {
-    size_t ctx, counters, tmp, digs, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
+    size_t ctx, counters, tmp, digs, tmap, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
 };
 
 static Layout layout_for(const Caps &c) {
@@ -92,6 +92,7 @@ static Layout layout_for(const Caps &c) {
     L.counters = take(sizeof(Counters));
     L.tmp = take(c.n * 8);
     L.digs = take(c.n * 2);
+    L.tmap = take((c.n / SPLIT_TILE + c.split_cap + 64) * 4);
     L.nodes = take((size_t)c.node_cap * sizeof(GNode));
     L.acc = take((size_t)c.node_cap * sizeof(NodeAcc));
     L.arena = take(c.arena_u32 * 4);
@@ -272,6 +273,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.bsum = (u32 *)(ws + L.bsum);
         hc.cmat_cap = caps.cmat_cap;
         hc.digs = (u16 *)(ws + L.digs);
+        hc.tmap = (u32 *)(ws + L.tmap);
     }
     hc.nan_flag = &d_cnt->nan_flag;
     hc.err_flag = &d_cnt->err_flag;
@@ -397,6 +399,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             splits_bound = std::min<u64>(splits_bound * (GMAX + 1), caps.split_cap);
             tm.begin(PH_OTHER);
             k_round_plan<<<1, 1024, 0, st>>>(d_ctx, cur);
+            k_tile_map<<<(tile_grid + 255) / 256, 256, 0, st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_COUNT);
             k_split_count<K><<<tile_grid, SPLIT_THREADS, 0, st>>>(d_ctx, cur);
@@ -412,7 +415,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             tm.begin(PH_OTHER);
             k_split_taskgen<<<nsm * 2, TG_THREADS, 0, st>>>(d_ctx, cur);
             tm.end();
-            launches += 7;
+            launches += 8;
             round++;
         };
         u32 rounds_per_batch = 2;   // enough for 10^6..10^9 keys of well-modelled data

@@ -257,6 +257,7 @@ struct DevCtx {
     unsigned long long *split_keys;   // keys moved by split passes (byte accounting)
     unsigned long long *k7_prof;      // PCF_FLAG_PROFILE: K7 cycles per phase (NULL = off)
     u16 *digs;              // split digit of the key at each array position (count -> scatter)
+    u32 *tmap;              // split of each tile of the current round (k_tile_map)
     SegItem *items;
     u32 *nitems;
     u32 items_cap;

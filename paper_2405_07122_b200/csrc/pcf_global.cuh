@@ -124,6 +124,14 @@ __device__ __forceinline__ u32 find_split(const SplitTask *L, u32 ns, u32 tile) 
     return lo;
 }
 
+// Split of every tile of round `cur` (one thread per tile): the count and
+// scatter CTAs read it instead of each searching the split list.
+__global__ void k_tile_map(const DevCtx *__restrict__ c, u32 cur) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    const RoundPlan pl = *c->plan;
+    if (t < pl.tiles) c->tmap[t] = find_split(c->splits[cur], pl.ns, t);
+}
+
 template <class K>
 __device__ __forceinline__ u32 digit_of(u64 okey, const Model &md, const u32 *__restrict__ T, u32 jlo, u32 shift) {
     u32 j = __ldg(&T[interval_index<K>(okey, md)]);
@@ -140,7 +148,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__r
     {
         const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
         if (tile >= pl.tiles) return;
-        const u32 s = find_split(L, pl.ns, tile);
+        const u32 s = c->tmap[tile];
         const SplitTask st = L[s];
         const u32 lt = tile - st.tile_begin;
         const GNode &g = c->nodes[st.node];
@@ -533,7 +541,7 @@ __global__ void __launch_bounds__(SC_THREADS, 2) k_split_scatter(const DevCtx *_
     const SplitTask *__restrict__ L = c->splits[cur];
     const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
     if (tile >= pl.tiles) return;
-    const SplitTask st = L[find_split(L, pl.ns, tile)];
+    const SplitTask st = L[c->tmap[tile]];
     split_scatter_tile<K>(c, S, st, tile - st.tile_begin, c->pmat);
 }
 
