@@ -399,7 +399,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             splits_bound = std::min<u64>(splits_bound * (GMAX + 1), caps.split_cap);
             tm.begin(PH_OTHER);
             k_round_plan<<<1, 1024, 0, st>>>(d_ctx, cur);
-            k_tile_map<<<(tile_grid + 255) / 256, 256, 0, st>>>(d_ctx, cur);
+            k_tile_map<<<nsm * 2, 256, 0, st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_COUNT);
             k_split_count<K><<<tile_grid, SPLIT_THREADS, 0, st>>>(d_ctx, cur);

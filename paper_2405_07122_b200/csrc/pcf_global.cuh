@@ -127,9 +127,12 @@ __device__ __forceinline__ u32 find_split(const SplitTask *L, u32 ns, u32 tile) 
 // Split of every tile of round `cur` (one thread per tile): the count and
 // scatter CTAs read it instead of each searching the split list.
 __global__ void k_tile_map(const DevCtx *__restrict__ c, u32 cur) {
-    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     const RoundPlan pl = *c->plan;
-    if (t < pl.tiles) c->tmap[t] = find_split(c->splits[cur], pl.ns, t);
+    const SplitTask *__restrict__ L = c->splits[cur];
+    for (u32 si = blockIdx.x; si < pl.ns; si += gridDim.x) {   // one CTA per split
+        const u32 tb = L[si].tile_begin, nt = L[si].ntiles;
+        for (u32 t = threadIdx.x; t < nt; t += blockDim.x) c->tmap[tb + t] = si;
+    }
 }
 
 template <class K>
@@ -603,51 +606,59 @@ __device__ __forceinline__ void emit_run(const DevCtx *c, const SplitTask &st, G
 
 constexpr int TG_THREADS = 256;
 __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__restrict__ c, u32 cur) {
+    __shared__ u32 dcnt[GMAX];
+    __shared__ u8 dpack[GMAX];
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
     const u32 nxt = cur ^ 1u;
     const u32 *__restrict__ P = c->pmat;
     const u32 lane = threadIdx.x & 31;
-    const u32 gw = blockIdx.x * (TG_THREADS / 32) + (threadIdx.x >> 5), nw = gridDim.x * (TG_THREADS / 32);
-    for (u32 si = gw; si < pl.ns; si += nw) {   // one warp per split
+    for (u32 si = blockIdx.x; si < pl.ns; si += gridDim.x) {   // one CTA per split
         const SplitTask st = c->splits[cur][si];
         GNode &g = c->nodes[st.node];
         if (g.degenerate) continue;
-        u32 run_d0 = 0, run_keys = 0;
-        for (u32 base = 0; base < st.G; base += 32) {
-            // this lane's digit: count, bucket range, packable into a K7 task?
-            const u32 d = base + lane;
-            const bool valid = d < st.G;
-            u32 cn = 0, dhi = 0;
-            bool pk = true;
-            if (valid) {
-                const u32 start = P[st.cbase + (u64)d * st.ntiles] - (u32)st.mbase;
-                const u32 end = d + 1 < st.G ? P[st.cbase + (u64)(d + 1) * st.ntiles] - (u32)st.mbase : st.m;
-                cn = end - start;
-                const u32 jlo = st.jlo + (d << st.shift);
-                dhi = min(jlo + (1u << st.shift), st.jhi);
-                const u32 W = dhi - jlo;
-                pk = cn <= (u32)S_CAP && W <= (u32)NB_CAP;
-                if (!pk && cn > 0) {   // too large for a K7 CTA
-                    const u64 goff = st.off + start;
-                    if (W == 1) {
-                        g.H[jlo] = cn;
-                        const bool sort = cn >= g.delta || cn < c->tau;   // Alg. 1
-                        push_item(c, goff, cn, g.level + 1, st.dst, sort ? 1u : 0u);
-                    } else {
-                        SplitTask nt;
-                        nt.off = goff; nt.m = cn; nt.node = st.node; nt.jlo = jlo; nt.jhi = dhi;
-                        nt.shift = choose_shift(W, cn);
-                        nt.G = (W + (1u << nt.shift) - 1) >> nt.shift;
-                        nt.src = st.dst; nt.dst = st.dst == 1 ? 2 : 1;
-                        nt.tile_begin = 0; nt.ntiles = 0; nt.cbase = 0; nt.mbase = 0;
-                        u32 slot = atomicAdd(&c->nsplits[nxt], 1u);
-                        if (slot < c->splits_cap) c->splits[nxt][slot] = nt;
-                        else atomicOr(c->err_flag, 1u);
-                    }
+        __syncthreads();
+        // every digit in parallel: count, packable into a K7 task?  Groups too large
+        // for a K7 CTA become the next round's splits or host items.
+        for (u32 d = threadIdx.x; d < st.G; d += TG_THREADS) {
+            const u32 start = P[st.cbase + (u64)d * st.ntiles] - (u32)st.mbase;
+            const u32 end = d + 1 < st.G ? P[st.cbase + (u64)(d + 1) * st.ntiles] - (u32)st.mbase : st.m;
+            const u32 cn = end - start;
+            const u32 jlo = st.jlo + (d << st.shift);
+            const u32 dhi = min(jlo + (1u << st.shift), st.jhi);
+            const u32 W = dhi - jlo;
+            const bool pk = cn <= (u32)S_CAP && W <= (u32)NB_CAP;
+            dcnt[d] = cn;
+            dpack[d] = pk ? 1 : 0;
+            if (!pk && cn > 0) {
+                const u64 goff = st.off + start;
+                if (W == 1) {
+                    g.H[jlo] = cn;
+                    const bool sort = cn >= g.delta || cn < c->tau;   // Alg. 1
+                    push_item(c, goff, cn, g.level + 1, st.dst, sort ? 1u : 0u);
+                } else {
+                    SplitTask nt;
+                    nt.off = goff; nt.m = cn; nt.node = st.node; nt.jlo = jlo; nt.jhi = dhi;
+                    nt.shift = choose_shift(W, cn);
+                    nt.G = (W + (1u << nt.shift) - 1) >> nt.shift;
+                    nt.src = st.dst; nt.dst = st.dst == 1 ? 2 : 1;
+                    nt.tile_begin = 0; nt.ntiles = 0; nt.cbase = 0; nt.mbase = 0;
+                    u32 slot = atomicAdd(&c->nsplits[nxt], 1u);
+                    if (slot < c->splits_cap) c->splits[nxt][slot] = nt;
+                    else atomicOr(c->err_flag, 1u);
                 }
             }
-            // greedy next-fit packing of the packable digits
+        }
+        __syncthreads();
+        if (threadIdx.x >= 32) continue;
+        // warp 0: greedy next-fit packing of the packable digits, 32 digits per step
+        u32 run_d0 = 0, run_keys = 0;
+        for (u32 base = 0; base < st.G; base += 32) {
+            const u32 d = base + lane;
+            const bool valid = d < st.G;
+            const u32 cn = valid ? dcnt[d] : 0;
+            const bool pk = valid ? dpack[d] != 0 : true;
+            const u32 dhi = valid ? min(st.jlo + ((d + 1) << st.shift), st.jhi) : 0;
             const u32 npm = __ballot_sync(0xffffffffu, !pk);
             u32 s = 0;   // first lane of the chunk not yet assigned to a run
             for (u32 guard = 0; s < 32 && guard < 64; ++guard) {   // each step retires >= 1 lane
