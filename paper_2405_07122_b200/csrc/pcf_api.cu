@@ -165,6 +165,7 @@ static int configure_kernels() {
     if (done) return PCF_OK;
     CK(cudaFuncSetAttribute(k7_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
+    CK(cudaFuncSetAttribute(k8_merge<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
     done = true;
     return PCF_OK;
 }
@@ -459,30 +460,47 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         stats.rounds = round;
         stats.split_tasks = 0;
         if (status == PCF_OK) {
-            // K8: global Standard-Sort of large buckets
-            for (const SegItem &it : fallbacks) {
+            // K8: global Standard-Sort of large buckets (flags in pmat, merge splits in cmat:
+            // both are free once the split rounds are done)
+            u32 *k8_flags = hc.pmat, *k8_sp = hc.cmat;
+            if (!fallbacks.empty()) CK(cudaMemsetAsync(k8_flags, 0, 4 * fallbacks.size(), st));
+            for (size_t fi = 0; fi < fallbacks.size(); ++fi) {
+                const SegItem &it = fallbacks[fi];
                 const u64 m = it.m;
                 u64 *src = (it.src == 0 ? const_cast<u64 *>(in) : it.src == 1 ? hc.buf[1] : out) + it.off;
                 u64 *bo = out + it.off, *bt = hc.buf[1] + it.off;
+                u32 *flag = k8_flags + fi;
                 u32 npass = 1;
                 for (u64 w = K8_TILE; w < m; w *= 2) npass++;
                 // pass k writes `out` iff (npass - 1 - k) is even, so the last pass lands in out
                 u64 *dst0 = ((npass - 1) % 2 == 0) ? bo : bt;
-                u32 nblk = (u32)((m + K8_TILE - 1) / K8_TILE);
+                const u32 nblk = (u32)((m + K8_TILE - 1) / K8_TILE);
                 tm.begin(PH_K8);
-                k8_blocksort<K><<<nblk, K8_THREADS, 0, st>>>(src, dst0, m);
+                k8_check<<<(u32)std::min<u64>(4ull * nsm, (m + 255) / 256), 256, 0, st>>>(src, m, flag);
+                k8_blocksort<K><<<nblk, K8_THREADS, 0, st>>>(src, dst0, bo, m, flag);
                 u64 *cur = dst0;
                 for (u64 w = K8_TILE; w < m; w *= 2) {
                     u64 *nxt = cur == bo ? bt : bo;
-                    k8_merge<K><<<nblk, K8_THREADS, 0, st>>>(cur, nxt, m, w);
+                    k8_partition<K><<<(nblk + 255) / 256, 256, 0, st>>>(cur, m, w, nblk, k8_sp, flag);
+                    k8_merge<K><<<nblk, K8_THREADS, K8_MERGE_SMEM, st>>>(cur, nxt, m, w, k8_sp, flag);
                     cur = nxt;
-                    launches++;
+                    launches += 2;
                 }
                 tm.end();
-                launches++;
+                launches += 2;
                 CK(cudaGetLastError());
-                bytes[PH_K8] += 16ull * m * npass;
+                bytes[PH_K8] += 24ull * m;   // check + block sort; the merge passes are added below (timing)
                 stats.fallback_keys_global += m;
+            }
+            if (timing && !fallbacks.empty()) {   // merge passes run only for buckets with two distinct keys
+                std::vector<u32> fl(fallbacks.size());
+                CK(cudaMemcpyAsync(fl.data(), k8_flags, 4 * fl.size(), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                for (size_t fi = 0; fi < fl.size(); ++fi) {
+                    u32 npass = 1;
+                    for (u64 w = K8_TILE; w < fallbacks[fi].m; w *= 2) npass++;
+                    if (fl[fi]) bytes[PH_K8] += 16ull * fallbacks[fi].m * (npass - 1);
+                }
             }
             // pass log: records of the global nodes (need the complete H)
             if (logging) {
