@@ -252,12 +252,22 @@ __device__ __noinline__ void leaf_phase(K7Smem &S) {
             const u32 e = S.leaf[my], st = e & 0xffffu, h = e >> 16;
             const u32 p = st + (k - S.lkp[my]);
             const u64 v = S.B[p];
+            // rank = #{j : (B[j], j) < (v, p)} (keys below v, and equal keys before p):
+            // one 96-bit subtract chain per key; PTX's carry flag after it is set iff
+            // (B[j], j) >= (v, p) (carry = no borrow), so r counts the others and
+            // rank = h - r
             u32 r = 0;
-            for (u32 j = st; j < st + h; ++j) {   // keys below v, and equal keys before p
+            const u32 vlo = (u32)v, vhi = (u32)(v >> 32);
+            for (u32 j = st; j < st + h; ++j) {
                 const u64 x = S.B[j];
-                r += (x < v || (x == v && j < p)) ? 1u : 0u;
+                asm("{\n\t.reg .u32 t;\n\t"
+                    "sub.cc.u32 t, %1, %2;\n\t"
+                    "subc.cc.u32 t, %3, %4;\n\t"
+                    "subc.cc.u32 t, %5, %6;\n\t"
+                    "addc.u32 %0, %0, 0;\n\t}"
+                    : "+r"(r) : "r"(j), "r"(p), "r"((u32)x), "r"(vlo), "r"((u32)(x >> 32)), "r"(vhi));
             }
-            S.A[st + r] = v;
+            S.A[st + (h - r)] = v;
         }
         // leaf of key k0 + 32
         a += __popc(mask);
