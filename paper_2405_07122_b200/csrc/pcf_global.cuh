@@ -584,13 +584,11 @@ __device__ __forceinline__ void push_k7(const DevCtx *c, const K7Task &t) {
 // Runs of consecutive smaller groups are packed greedily into one K7 task of
 // <= S_CAP keys and <= NB_CAP buckets: a K7_GROUP over the run's bucket range,
 // or, for a run of one bucket, a K7_NODE / K7_SORT task (Alg. 1).
-__device__ __forceinline__ void emit_run(const DevCtx *c, const SplitTask &st, GNode &g, u32 d0, u32 d1, u32 keys,
-                                         const u32 *__restrict__ P) {
-    if (keys == 0) return;
+__device__ __forceinline__ void make_run_task(const DevCtx *c, const SplitTask &st, GNode &g, u32 d0, u32 d1, u32 keys,
+                                              const u32 *__restrict__ P, K7Task &t) {
     const u32 start = P[st.cbase + (u64)d0 * st.ntiles] - (u32)st.mbase;
     const u32 jlo = st.jlo + (d0 << st.shift);
     const u32 jhi = min(st.jlo + ((d1 + 1) << st.shift), st.jhi);
-    K7Task t;
     t.off = st.off + start; t.size = keys; t.src = st.dst; t.node = st.node; t.jlo = jlo; t.jhi = jhi; t.pad = 0;
     if (jhi - jlo == 1) {
         g.H[jlo] = keys;
@@ -601,13 +599,14 @@ __device__ __forceinline__ void emit_run(const DevCtx *c, const SplitTask &st, G
         t.kind = K7_GROUP;
         t.level = g.level;
     }
-    push_k7(c, t);
 }
 
 constexpr int TG_THREADS = 256;
 __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__restrict__ c, u32 cur) {
     __shared__ u32 dcnt[GMAX];
     __shared__ u8 dpack[GMAX];
+    __shared__ u32 rd0[GMAX], rd1[GMAX], rk[GMAX];   // packed runs of the split (warp 0)
+    __shared__ u32 nrun, rbase;
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
     const u32 nxt = cur ^ 1u;
@@ -649,10 +648,16 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
                 }
             }
         }
+        if (threadIdx.x == 0) nrun = 0;
         __syncthreads();
-        if (threadIdx.x >= 32) continue;
+        if (threadIdx.x < 32) {
         // warp 0: greedy next-fit packing of the packable digits, 32 digits per step
         u32 run_d0 = 0, run_keys = 0;
+        auto emit = [&](u32 d0, u32 d1, u32 keys) {   // lane 0
+            if (keys == 0) return;
+            const u32 r = nrun++;
+            rd0[r] = d0; rd1[r] = d1; rk[r] = keys;
+        };
         for (u32 base = 0; base < st.G; base += 32) {
             const u32 d = base + lane;
             const bool valid = d < st.G;
@@ -671,7 +676,7 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
                 const u32 b = __ffs(bm) - 1;
                 const u32 before = __shfl_sync(0xffffffffu, incl, (b + 31) & 31);
                 const u32 keys = run_keys + (b > s ? before : 0);
-                if (lane == 0 && base + b > run_d0) emit_run(c, st, g, run_d0, base + b - 1, keys, P);
+                if (lane == 0 && base + b > run_d0) emit(run_d0, base + b - 1, keys);
                 run_keys = 0;
                 if ((npm >> b) & 1u) {   // skip the non-packable digits at b, b+1, ...
                     const u32 rest = ~npm & (b == 31 ? 0u : (0xffffffffu << (b + 1)));
@@ -683,7 +688,24 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
             }
             if (s < 32 && lane == 0) atomicOr(c->err_flag, 2u);   // unreachable: the loop retires a lane per step
         }
-        if (lane == 0 && run_d0 < st.G) emit_run(c, st, g, run_d0, st.G - 1, run_keys, P);
+        if (lane == 0 && run_d0 < st.G) emit(run_d0, st.G - 1, run_keys);
+        }
+        __syncthreads();
+        // all threads: reserve the K7 slots of the split's runs at once, write the tasks
+        const u32 nr = nrun;
+        if (threadIdx.x == 0 && nr) {
+            u32 tk = 0;
+            for (u32 r = 0; r < nr; ++r) tk += rk[r];
+            rbase = atomicAdd(c->k7_count, nr);
+            atomicAdd(c->k7_keys, (unsigned long long)tk);
+        }
+        __syncthreads();
+        for (u32 r = threadIdx.x; r < nr; r += TG_THREADS) {
+            K7Task t;
+            make_run_task(c, st, g, rd0[r], rd1[r], rk[r], P, t);
+            if (rbase + r < c->k7_cap) c->k7[rbase + r] = t;
+            else atomicOr(c->err_flag, 1u);
+        }
     }
 }
 
