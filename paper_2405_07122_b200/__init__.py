@@ -77,10 +77,11 @@ def lib():
     """Load libpcfsort.so (built in-tree by ``build()``); raise if it is missing."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} not built: run __graft_entry__.build() "
+        path = os.environ.get("PCF_LIB", LIB_PATH)   # PCF_LIB: an alternative build (tuning experiments)
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} not built: run __graft_entry__.build() "
                                "(there is no CPU fallback)")
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         vp, sz, i32, u32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32
         PP = ctypes.POINTER(Params)
         L.pcf_params_init.argtypes = [PP]; L.pcf_params_init.restype = None

@@ -18,6 +18,16 @@ def _sources():
                   + [os.path.join(ROOT, "include", "pcf_sort.h")])
 
 
+def build_variant(out: str, defines: dict) -> str:
+    """Build a tuning variant (-D defines) to `out` (load it with PCF_LIB=out)."""
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", out,
+           *[f"-D{k}={v}" for k, v in defines.items()], os.path.join(CSRC, "pcf_api.cu")]
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    subprocess.check_call(cmd)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = _sources()
     if not force and os.path.exists(LIB_PATH):

@@ -41,8 +41,8 @@ struct KeyF64 {
     __host__ __device__ static inline u64 to_okey(u64 raw) {
         return raw ^ ((u64)((long long)raw >> 63) | 0x8000000000000000ull);
     }
-    __host__ __device__ static inline u64 from_okey(u64 k) {
-        return (k >> 63) ? (k ^ 0x8000000000000000ull) : ~k;
+    __host__ __device__ static inline u64 from_okey(u64 k) {   // (k >> 63) ? k ^ sign : ~k
+        return k ^ (~(u64)((long long)k >> 63) | 0x8000000000000000ull);
     }
 };
 struct KeyU64 {
@@ -83,6 +83,21 @@ __device__ __noinline__ u32 interval_index_exact(double d, double r, double beta
 // NaN in make_model (every comparison with NaN fails -> exact path), as is any
 // t' that is NaN or infinite.  Keys inside the band (x_max itself, keys within
 // a few ulps of a bin edge) take the exact path.
+template <class K>
+__device__ __forceinline__ double key_offset(u64 okey, const Model &md) {   // d = x - x_min (R6, R15)
+    if (K::is_f64) return __dsub_rn(__longlong_as_double((long long)K::from_okey(okey)), md.xmin);
+    return __ull2double_rn(okey - md.umin);
+}
+// Branch-free fast path: floor(t') + 1 and whether it is certified (ok); the
+// caller takes interval_index_exact for the rare uncertified keys.
+template <class K>
+__device__ __forceinline__ u32 interval_index_fast(u64 okey, const Model &md, bool &ok) {
+    const double t = __dmul_rn(key_offset<K>(okey, md), md.s);
+    const double fl = floor(t);
+    const double fr = __dsub_rn(t, fl);
+    ok = fr >= md.eps && fr <= 1.0 - md.eps;
+    return (u32)fl + 1u;
+}
 template <class K>
 __device__ __forceinline__ u32 interval_index(u64 okey, const Model &md) {
     double d;

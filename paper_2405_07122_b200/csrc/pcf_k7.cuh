@@ -13,79 +13,89 @@
 // The task's keys are read once from HBM, every deeper level runs in shared
 // memory, and the finished (sorted) task is written back once, coalesced.
 //
-// Level-synchronous, key-parallel design:
-//  * The nodes of one recursion level form an ordered list (a ring of
-//    (position, size) entries).  They are processed in sub-batches whose
-//    bucket columns fit the counter matrix (MC columns): every step of
-//    Alg. 1 lines 152-158 runs flat over all keys / samples / bins /
-//    buckets of the sub-batch at once, so every lane has work regardless of
-//    the node sizes.
+// Work split inside the CTA:
+//  * CTA-wide (16 warps): the K7_GROUP placement by the global model, and any
+//    node of more than GCAP keys (its children are < delta <= 861 keys).
+//  * Node groups (4 groups of 4 warps, named barriers 1..4): every other node
+//    is run, start to finish, by one group, with its keys held in registers
+//    (<= 16 per thread): min/max, alpha seeded samples (R3) ->
+//    per-bin counts, b = prefix, T, classify + per-warp
+//    counts, one column pass (bucket sizes, destinations, Alg. 1
+//    dispatch), placement, and Standard-Sort of the leaf buckets.  Recursing
+//    buckets go onto the group's stack; groups take the task's level-1 nodes
+//    from a shared list.  Groups never wait for each other inside a task.
+//  * Buffers: a node at relative depth r lives in A (r even) or B (r odd);
+//    recursing buckets are placed into the other buffer, leaf buckets of
+//    >= 2 keys into B (scratch) and then sorted into A, single keys straight
+//    into A.  Every position ends in A, sorted.
 //  * Stable placement (Append order; readings R4, R16): warp
-//    w owns a contiguous range of the sub-batch's keys; one pass computes each
-//    key's bucket, then ranks it inside its warp with __match_any_sync and a
-//    per-warp counter row (no shared-memory atomics on the per-key path); a
-//    column pass turns the [warp x bucket] counts into destinations.
-//  * Each node's columns are preceded by a "gap" column holding the number of
-//    buffer positions between it and the previous node, so one exclusive scan
-//    over the columns yields absolute buffer positions, and a max-scan over
-//    the gap markers tells every column its node.
-//  * Buckets Alg. 1 sends to Standard-Sort (|c_j| >= delta or |c_j| < tau) are
-//    placed directly into buffer A and sorted there in place (per-thread
-//    register networks for <= 32 keys, compacted by size class; warp sorts up
-//    to 1024; a CTA sort above); recursing buckets go to the other buffer and
-//    to the next level's node list.  Every position ends in A, sorted; one
-//    coalesced copy writes the task out.
+//    w of a group owns a contiguous range of the node's keys.  Leaf keys take an
+//    unstable rank from a shared-memory atomic (their bucket is sorted next);
+//    keys of recursing buckets are re-ranked stably (chunk order, MATCH) when
+//    they are placed.  The K7_GROUP placement ranks every key stably.
 #pragma once
 #include "pcf_common.cuh"
 
 namespace pcf {
 
-constexpr int MC = 1280;                          // bucket columns (and bins) of one sub-batch
-constexpr int NCAP = 256;                         // nodes of one sub-batch
-constexpr int RING = S_CAP / 2;                   // level node lists: nodes hold >= 2 keys (tau >= 2)
-constexpr int CH = S_CAP / (K7_WARPS * 32);       // 32-key chunks per warp (16)
-constexpr int BIGM = 1024;                        // nodes above this size: CTA-wide min/max
-constexpr int BIGCAP = S_CAP / BIGM;
-constexpr u32 SMALL_MAX = 64;                     // leaves up to this size: key-parallel rank sort
-constexpr int BLCAP = S_CAP / (SMALL_MAX + 1) + 1;  // larger leaves of one sub-batch
+#ifndef PCF_GW
+#define PCF_GW 4
+#endif
+constexpr int GW = PCF_GW;                         // warps per team
+constexpr int NGRP = K7_WARPS / GW;                // teams per CTA
+constexpr int GT = GW * 32;                        // threads per team
+constexpr int KPT = S_CAP / K7_THREADS;            // keys per thread held in registers (16)
+constexpr int GCAP = GT * KPT;                     // largest node a team runs (2048)
+constexpr int WCAP = 32 * KPT;                     // largest node a single warp runs (512)
+constexpr int CCOLS = NB_CAP + 2;                  // counter columns (CTA view): >= iroot34(S_CAP) + 2 = 863
+constexpr int WCOLS = 128;                         // T / size columns per warp slice: >= iroot34(WCAP) + 2 = 109;
+                                                   // a team's slices give 512 >= iroot34(GCAP) + 2 = 306
+constexpr u32 SMALL_MAX = 64;                      // leaves up to this size: key-parallel rank sort
+constexpr int LIST_CAP = S_CAP / 2;                // nodes hold >= tau >= 2 keys
+constexpr int LSM_CAP = LIST_CAP + K7_WARPS + 16;  // small-node list: + one over-claimed ticket per warp
+constexpr int LBIG_CAP = 32;                       // nodes > WCAP keys of one task (<= 16)
+constexpr int STK_CAP = WCAP / 2;                  // per-warp DFS stack
+constexpr int BL_CAP = 128;                        // leaves > SMALL_MAX keys of one node: <= S_CAP / 65
+constexpr int BL_W = BL_CAP / K7_WARPS;            // per-warp slice (a warp's node has <= 7)
 constexpr u32 NONE = 0xffffffffu;
-// destination row entries: buffer position | target (Y: recursing bucket, A: leaf of
-// one key -- final, B: larger leaf -- sorted into A by the leaf phase)
+// destination entries: node-relative position | target (Y: recursing bucket,
+// A: leaf of one key -- final, B: larger leaf -- sorted into A next)
 constexpr u32 DEST_A = 0x4000u, DEST_B = 0x8000u, POS_MASK = 0x3fffu;
+static_assert(K7_WARPS * WCOLS >= CCOLS, "CTA view of the column arrays");
+static_assert((CCOLS * 2) % 4 == 0, "counter rows must stay 4-byte aligned");
+
+// node entry: pos (13 bits) | m << 13 (14 bits) | relative depth << 27
+__device__ __forceinline__ u32 ent_make(u32 pos, u32 m, u32 rel) { return pos | (m << 13) | (rel << 27); }
+__device__ __forceinline__ u32 ent_pos(u32 e) { return e & 0x1fffu; }
+__device__ __forceinline__ u32 ent_m(u32 e) { return (e >> 13) & 0x3fffu; }
+__device__ __forceinline__ u32 ent_rel(u32 e) { return e >> 27; }
 
 struct K7Smem {
     u64 A[S_CAP];
     u64 B[S_CAP];
-    union {
-        u16 wcnt[K7_WARPS][MC];   // per-warp bucket counters -> per-warp destinations
-        u32 cnt[MC];              // fit: per-bin sample counts (dead before the rank pass)
-    } m;
-    u16 T[MC];                    // bucket table of every node's bins (1-based within the node)
-    u16 GM[MC];                   // column marker: node index + 1 at the node's gap column
-    u32 leaf[MC];                 // leaves of 2..SMALL_MAX keys, in position order: pos | h << 16
-    u16 lkp[MC + 1];              // exclusive key prefix over leaf[]
-    u32 bleaf[BLCAP];             // leaves of > SMALL_MAX keys: pos | h << 16
-    u32 ring[RING];               // node lists: pos | m << 13
-    // node table of the current sub-batch
-    u32 nkey[NCAP + 1];           // flat key offsets
-    u16 nb0[NCAP + 1];            // first column / bin (the gap column; bins are 1-based)
-    u16 nsmp[NCAP + 1];           // flat sample offsets
-    u16 npos[NCAP], nm[NCAP], nP[NCAP], nal[NCAP], ngap[NCAP];
-    u8 ndeg[NCAP];
-    u64 nmin[NCAP], nmax[NCAP];
-    u64 ndb[NCAP], ndh[NCAP];
-    u32 ncnt[NCAP];               // pass log: nf | ns << 10 | nr << 20
-    u16 big[BIGCAP];
-    u32 nbig;
-    u32 nleaf, lkeys, nbleaf;
-    u32 scan_a[K7_WARPS][4], scan_b[K7_WARPS][2], scan_c[K7_WARPS][3];
-    u32 N, head, tail, level_end, item_next, new_tail;
+    u16 W[K7_WARPS * CCOLS];      // per-warp column counters -> destinations (rows of CCOLS);
+                                  // a group's rows double as its u32 per-bin sample counts
+    u16 T16[K7_WARPS * WCOLS];    // bucket table of the current node (slices of the node's warps)
+    u16 hcol[K7_WARPS * WCOLS];   // bucket sizes of the current node (same slices)
+    u16 LC[S_CAP];                // per position: bucket column of a B-leaf key, 0 otherwise
+    u32 lsm[LSM_CAP];             // nodes <= WCAP keys (tickets; 0 = not yet pushed)
+    u32 lbig[LBIG_CAP];           // nodes > WCAP keys
+    u32 stk[K7_WARPS][STK_CAP];   // per-warp DFS stacks (a team's first stack: its children before publication)
+    u32 bl[BL_CAP];               // leaves > SMALL_MAX keys of the current node (slices of the node's warps)
+    u64 wmn[K7_WARPS], wmx[K7_WARPS];
+    u32 wsum[K7_WARPS];
+    // per node, indexed by the node's first warp
+    unsigned long long db[K7_WARPS], dh[K7_WARPS];
+    u32 ncnt[K7_WARPS];           // pass log: nf | ns << 10 | nr << 20
+    u32 nbl[K7_WARPS];
+    u32 top[K7_WARPS], cur[K7_WARPS];
+    u32 stot, snext, btot, bnext, big_active;
     u32 task_idx;
     K7Task task;
     Model gmd;
     const u32 *gT;
     u32 *gH;
-    u32 gdelta, glevel, gjlo;
+    u32 gdelta, glevel, gjlo, gjhi;
     long long prof_t;                       // PCF_FLAG_PROFILE bookkeeping (thread 0)
     unsigned long long prof[K7_PROF_SLOTS];
 };
@@ -94,8 +104,8 @@ static_assert(sizeof(K7Smem) <= 232448, "K7 shared memory exceeds 227 KB");
 
 // K7 phase profiling (PCF_FLAG_PROFILE): thread 0 charges the cycles since the
 // previous mark to slot `id` (barrier waits included).  Slots: 0 claim, 1 load,
-// 2 group rank, 3 group columns+place, 4 leaves, 5 setup, 6 min/max,
-// 7 sample, 8 fit, 9 rank, 10 columns+place, 11 tasks, 12 keys, 13 store.
+// 2 group placement (CTA), 4 CTA-run nodes, 5 node groups, 6 sort tasks,
+// 11 tasks, 12 keys, 13 store.
 __device__ __forceinline__ void prof_mark(const DevCtx *c, K7Smem &S, int id) {
     if (c->k7_prof && threadIdx.x == 0) {
         long long t = clock64();
@@ -130,12 +140,8 @@ __device__ __forceinline__ u32 warp_incl_scan(u32 v) {
     }
     return v;
 }
-__device__ __forceinline__ u32 warp_incl_max(u32 v) {
-    const u32 lane = lane_id();
-    for (int o = 1; o < 32; o <<= 1) {
-        u32 w = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= (u32)o) v = w > v ? w : v;
-    }
+__device__ __forceinline__ u64 warp_sum_u64(u64 v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
@@ -149,13 +155,20 @@ __device__ __forceinline__ u32 iroot34_small(u32 m) {
     return c;
 }
 
-// largest i in [0, n) with a[i] <= x (a non-decreasing, a[0] <= x)
-template <class T>
-__device__ __forceinline__ u32 seg_of(const T *a, u32 n, u32 x) {
-    u32 lo = 0, hi = n - 1;
-    while (lo < hi) { const u32 mid = (lo + hi + 1) >> 1; if ((u32)a[mid] <= x) lo = mid; else hi = mid - 1; }
-    return lo;
-}
+// A set of NW warps that runs one node: the whole CTA (barrier 0) or a node
+// group (named barrier g + 1).
+template <int NW>
+struct Grp {
+    static constexpr int NT = NW * 32;
+    u32 g;    // group index (0 for the CTA)
+    u32 t;    // thread index inside the set
+    u32 w0;   // first CTA warp of the set
+    __device__ __forceinline__ void bar() const {
+        if (NW == K7_WARPS) __syncthreads();
+        else if (NW == 1) __syncwarp();
+        else asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(NT) : "memory");
+    }
+};
 
 // ------------------------------------------------------------------ node record (pass log)
 __device__ __forceinline__ void write_record(const DevCtx *c, u32 level, u32 alpha, u64 off, u64 m,
@@ -173,486 +186,388 @@ __device__ __forceinline__ void write_record(const DevCtx *c, u32 level, u32 alp
 }
 
 // ------------------------------------------------------------------ Standard-Sort (R2) on ordered keys
-// Bitonic network over a[0, n) by one warp in shared memory; all merges
-// ascending (first step of each stage compares i with its mirror), so the
-// virtual +inf padding never moves.
-__device__ void warp_bitonic_smem(u64 *a, u32 n) {
+// Rank of (v, p) among (B[j], j), j in [st, st + h): keys below v, and equal
+// keys before p.  One 96-bit subtract chain per comparison; PTX's carry after
+// it is set iff (B[j], j) >= (v, p), so r counts the others and rank = h - r.
+__device__ __forceinline__ u32 rank_in_leaf(const u64 *B, u32 st, u32 h, u64 v, u32 p) {
+    u32 r = 0;
+    const u32 vlo = (u32)v, vhi = (u32)(v >> 32);
+    for (u32 j = st; j < st + h; ++j) {
+        const u64 x = B[j];
+        asm("{\n\t.reg .u32 t;\n\t"
+            "sub.cc.u32 t, %1, %2;\n\t"
+            "subc.cc.u32 t, %3, %4;\n\t"
+            "subc.cc.u32 t, %5, %6;\n\t"
+            "addc.u32 %0, %0, 0;\n\t}"
+            : "+r"(r) : "r"(j), "r"(p), "r"((u32)x), "r"(vlo), "r"((u32)(x >> 32)), "r"(vhi));
+    }
+    return h - r;
+}
+
+// Bitonic network over a[0, n) by a thread set; all merges ascending (the
+// first step of each stage compares i with its mirror), so the virtual +inf
+// padding never moves.
+template <int NW>
+__device__ void set_bitonic(u64 *a, u32 n, const Grp<NW> &G) {
+    constexpr u32 NT = NW * 32;
     if (n <= 1) return;
     const u32 P = next_pow2(n);
-    const u32 lane = lane_id();
     const u32 lgP = 31 - __clz(P);
     for (u32 lk = 1; lk <= lgP; ++lk) {
         const u32 k = 1u << lk, lh = lk - 1;
-        for (u32 t = lane; t < (P >> 1); t += 32) {
+        for (u32 t = G.t; t < (P >> 1); t += NT) {
             const u32 blk = t >> lh, w = t & ((1u << lh) - 1);
             const u32 lo = (blk << lk) + w, hi = (blk << lk) + k - 1 - w;
             if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
         }
-        __syncwarp();
+        G.bar();
         for (int lj = (int)lh - 1; lj >= 0; --lj) {
             const u32 j = 1u << lj;
-            for (u32 t = lane; t < (P >> 1); t += 32) {
+            for (u32 t = G.t; t < (P >> 1); t += NT) {
                 const u32 lo = ((t >> lj) << (lj + 1)) + (t & (j - 1)), hi = lo + j;
                 if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
             }
-            __syncwarp();
+            G.bar();
         }
     }
 }
 
-// Same network by the whole CTA (leaves > 1024 keys: rare fallback buckets).
-__device__ void cta_bitonic_smem(u64 *a, u32 n) {
-    if (n > 1) {
-        const u32 P = next_pow2(n);
-        const u32 lgP = 31 - __clz(P);
-        for (u32 lk = 1; lk <= lgP; ++lk) {
-            const u32 k = 1u << lk, lh = lk - 1;
-            for (u32 t = threadIdx.x; t < (P >> 1); t += K7_THREADS) {
-                const u32 blk = t >> lh, w = t & ((1u << lh) - 1);
-                const u32 lo = (blk << lk) + w, hi = (blk << lk) + k - 1 - w;
-                if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
-            }
-            __syncthreads();
-            for (int lj = (int)lh - 1; lj >= 0; --lj) {
-                const u32 j = 1u << lj;
-                for (u32 t = threadIdx.x; t < (P >> 1); t += K7_THREADS) {
-                    const u32 lo = ((t >> lj) << (lj + 1)) + (t & (j - 1)), hi = lo + j;
-                    if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
-                }
-                __syncthreads();
-            }
-        }
+// Standard-Sort of the leaf B[st, st + h) into A[st, st + h) by a thread set.
+// Ends with a barrier of the set.
+template <int NW>
+__device__ void sort_range(K7Smem &S, u32 st, u32 h, const Grp<NW> &G) {
+    constexpr u32 NT = NW * 32;
+    if (h <= SMALL_MAX) {
+        for (u32 p = st + G.t; p < st + h; p += NT) S.A[st + rank_in_leaf(S.B, st, h, S.B[p], p)] = S.B[p];
+    } else {
+        set_bitonic<NW>(S.B + st, h, G);
+        for (u32 p = st + G.t; p < st + h; p += NT) S.A[p] = S.B[p];
     }
-    __syncthreads();
+    G.bar();
 }
 
-// Standard-Sort of every leaf of the sub-batch (keys in B) into A.
-// Leaves of <= SMALL_MAX keys: one thread per key, flat over all their keys
-// (every lane busy, one compact loop): the key's rank inside its leaf counts
-// the smaller keys and the equal keys before it, and the key is written to
-// A[leaf start + rank].  A warp handles 32 consecutive keys; it finds their
-// leaves with one binary search and a bit mask of the leaf boundaries.
-// Larger leaves (fallback buckets, rare): bitonic networks by a warp (<= 1024
-// keys) or by the CTA, in B, then copied to A.
-__device__ __noinline__ void leaf_phase(K7Smem &S) {
-    const u32 lane = lane_id(), w = warp_id();
-    const u32 NL = S.nleaf, K = S.lkeys;
-    // warp w: keys [w*RW, (w+1)*RW); the leaf of the first key is carried from chunk to chunk
-    const u32 RW = ((K + K7_THREADS - 1) / K7_THREADS) * 32;
-    const u32 kw0 = w * RW, kw1 = min(kw0 + RW, K);
-    u32 a = kw0 < kw1 ? seg_of(S.lkp, NL, kw0) : 0;
-    for (u32 k0 = kw0; k0 < kw1; k0 += 32) {
-        const u32 bi = a + 1 + lane;
-        const u32 b = bi <= NL ? (u32)S.lkp[bi] : 0xffffffffu;
-        const u32 bit = (b - k0 < 32u) ? (1u << (b - k0)) : 0u;      // boundaries in (k0, k0 + 31]
-        const u32 mask = __reduce_or_sync(0xffffffffu, bit);
-        const u32 my = a + __popc(mask & ((2u << lane) - 1u));
-        const u32 k = k0 + lane;
-        if (k < kw1) {
-            const u32 e = S.leaf[my], st = e & 0xffffu, h = e >> 16;
-            const u32 p = st + (k - S.lkp[my]);
-            const u64 v = S.B[p];
-            // rank = #{j : (B[j], j) < (v, p)} (keys below v, and equal keys before p):
-            // one 96-bit subtract chain per key; PTX's carry flag after it is set iff
-            // (B[j], j) >= (v, p) (carry = no borrow), so r counts the others and
-            // rank = h - r
-            u32 r = 0;
-            const u32 vlo = (u32)v, vhi = (u32)(v >> 32);
-            for (u32 j = st; j < st + h; ++j) {
-                const u64 x = S.B[j];
-                asm("{\n\t.reg .u32 t;\n\t"
-                    "sub.cc.u32 t, %1, %2;\n\t"
-                    "subc.cc.u32 t, %3, %4;\n\t"
-                    "subc.cc.u32 t, %5, %6;\n\t"
-                    "addc.u32 %0, %0, 0;\n\t}"
-                    : "+r"(r) : "r"(j), "r"(p), "r"((u32)x), "r"(vlo), "r"((u32)(x >> 32)), "r"(vhi));
-            }
-            S.A[st + (h - r)] = v;
-        }
-        // leaf of key k0 + 32
-        a += __popc(mask);
-        if (a + 1 <= NL && (u32)S.lkp[a + 1] <= k0 + 32) ++a;
-    }
-    const u32 NB = S.nbleaf;
-    for (;;) {
-        u32 idx = 0;
-        if (lane == 0) idx = atomicAdd(&S.item_next, 1u);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= NB) break;
-        const u32 e = S.bleaf[idx], st = e & 0xffffu, h = e >> 16;
-        if (h > 1024) continue;
-        warp_bitonic_smem(S.B + st, h);
-        for (u32 i = lane; i < h; i += 32) S.A[st + i] = S.B[st + i];
-        __syncwarp();
-    }
-    __syncthreads();
-    for (u32 idx = 0; idx < NB; ++idx) {
-        const u32 e = S.bleaf[idx], st = e & 0xffffu, h = e >> 16;
-        if (h <= 1024) continue;
-        cta_bitonic_smem(S.B + st, h);
-        for (u32 i = threadIdx.x; i < h; i += K7_THREADS) S.A[st + i] = S.B[st + i];
-        __syncthreads();
-    }
-}
+// ------------------------------------------------------------------ one bucketing node
+// MODE_NODE:   a Learned-Sort call on keys X[pos, pos + m) (Alg. 1 lines
+//              148-167; m >= tau): min/max, model, samples, fit, bucketing,
+//              dispatch of every bucket, Standard-Sort of the leaves, record.
+// MODE_GLOBAL: the K7_GROUP placement: model and T of the global node,
+//              columns = buckets [jlo, jhi); keys in A[0, m).
+// Recursing buckets become node entries: a single warp keeps them on its own
+// stack; a team publishes them to the small-node list after placement; the CTA
+// appends them to the task's lists by size.  Ends with a barrier of the set.
+enum { MODE_NODE = 0, MODE_GLOBAL = 1 };
 
-// ------------------------------------------------------------------ one sub-batch of a level
-// Setup: take nodes ring[head ..) while their columns (P+2 each: gap + P+1
-// buckets) fit MC and they fit NCAP; node table, flat offsets, markers.
-__device__ void sub_setup(const DevCtx *c, K7Smem &S) {
-    const u32 tid = threadIdx.x, lane = lane_id(), w = warp_id();
-    const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
-    const u32 head = S.head, navail = S.level_end - S.head;
-    for (u32 i = tid; i < MC; i += K7_THREADS) { S.m.cnt[i] = 0; S.GM[i] = 0; }
-    if (tid == 0) S.nbig = 0;
-    u32 pos = 0, m = 0, P = 0, al = 0, sz = 0;
-    const bool valid = tid < NCAP && tid < navail;
-    if (valid) {
-        const u32 e = S.ring[(head + tid) & (RING - 1)];
-        pos = e & 0x1fffu; m = e >> 13;
-        P = iroot34_small(m); al = sample_all ? m : P; sz = P + 2;
-    }
-    u32 isz = 0, im = 0, ial = 0;
-    if (tid < NCAP) {
-        isz = warp_incl_scan(sz); im = warp_incl_scan(m); ial = warp_incl_scan(al);
-        if (lane == 31) { S.scan_a[w][0] = isz; S.scan_a[w][1] = im; S.scan_a[w][2] = ial; }
-    }
-    __syncthreads();
-    if (tid < NCAP) {
-        for (u32 ww = 0; ww < w; ++ww) { isz += S.scan_a[ww][0]; im += S.scan_a[ww][1]; ial += S.scan_a[ww][2]; }
-        const bool fits = valid && isz <= (u32)MC;
-        if (fits) {
-            const u32 i = tid;
-            u32 prev_end = 0;
-            if (i > 0) { const u32 pe = S.ring[(head + i - 1) & (RING - 1)]; prev_end = (pe & 0x1fffu) + (pe >> 13); }
-            S.npos[i] = (u16)pos; S.nm[i] = (u16)m; S.nP[i] = (u16)P; S.nal[i] = (u16)al;
-            S.ngap[i] = (u16)(pos - prev_end);
-            S.nkey[i] = im - m; S.nb0[i] = (u16)(isz - sz); S.nsmp[i] = (u16)(ial - al);
-            S.nmin[i] = ~0ull; S.nmax[i] = 0; S.ndb[i] = 0; S.ndh[i] = 0; S.ncnt[i] = 0;
-            S.GM[isz - sz] = (u16)(i + 1);
-            if (m > (u32)BIGM) { const u32 b = atomicAdd(&S.nbig, 1u); if (b < (u32)BIGCAP) S.big[b] = (u16)i; }
-            // last fitting node: totals
-            bool last = i + 1 >= navail || i + 1 >= (u32)NCAP;
-            if (!last) {
-                const u32 e2 = S.ring[(head + i + 1) & (RING - 1)];
-                last = isz + iroot34_small(e2 >> 13) + 2 > (u32)MC;
-            }
-            if (last) { S.N = i + 1; S.nkey[i + 1] = im; S.nb0[i + 1] = (u16)isz; S.nsmp[i + 1] = (u16)ial; }
-        }
-    }
-    __syncthreads();
-}
-
-// x_min, x_max of every node: one warp per node <= BIGM keys,
-// the whole CTA for the few larger ones.
-__device__ void sub_minmax(K7Smem &S, const u64 *X) {
-    const u32 N = S.N, w = warp_id(), lane = lane_id();
-    for (u32 i = w; i < N; i += K7_WARPS) {
-        const u32 m = S.nm[i];
-        if (m > (u32)BIGM) continue;
-        const u64 *x = X + S.npos[i];
-        u64 mn = ~0ull, mx = 0;
-        for (u32 k = lane; k < m; k += 32) { const u64 v = x[k]; mn = v < mn ? v : mn; mx = v > mx ? v : mx; }
-        mn = warp_min_u64(mn);
-        mx = warp_max_u64(mx);
-        if (lane == 0) { S.nmin[i] = mn; S.nmax[i] = mx; }
-    }
-    const u32 nb = min(S.nbig, (u32)BIGCAP);
-    for (u32 b = 0; b < nb; ++b) {
-        const u32 i = S.big[b], m = S.nm[i];
-        const u64 *x = X + S.npos[i];
-        u64 mn = ~0ull, mx = 0;
-        for (u32 k = threadIdx.x; k < m; k += K7_THREADS) { const u64 v = x[k]; mn = v < mn ? v : mn; mx = v > mx ? v : mx; }
-        mn = warp_min_u64(mn);
-        mx = warp_max_u64(mx);
-        if (lane == 0) { atomicMin(&S.nmin[i], mn); atomicMax(&S.nmax[i], mx); }
-    }
-    __syncthreads();
-}
-
-// alpha samples per node (R3, R4) -> per-bin counts.
+// i(x) of every valid slot (pk != NONE) into pk: certified fast path for all
+// slots, the exact sub/div/mul evaluation (R6) only for the rare keys in the
+// guard band, behind one warp-uniform branch.
 template <class K>
-__device__ void sub_sample(const DevCtx *c, K7Smem &S, const u64 *X, u32 L, u64 gbase) {
-    const u32 N = S.N, Stot = S.nsmp[N];
-    const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
-    for (u32 i = threadIdx.x; i < N; i += K7_THREADS) {
-        Model md;
-        S.ndeg[i] = make_model<K>(S.nmin[i], S.nmax[i], S.nP[i], md) ? 0 : 1;
+__device__ __forceinline__ void classify_slots(const u64 (&key)[KPT], u32 (&pk)[KPT], const Model &md) {
+    u32 bad = 0;
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+        bool ok;
+        const u32 i = interval_index_fast<K>(key[q], md, ok);
+        const bool v = pk[q] != NONE;
+        bad |= (v && !ok) ? (1u << q) : 0u;
+        pk[q] = v ? i : NONE;
     }
-    for (u32 s = threadIdx.x; s < Stot; s += K7_THREADS) {
-        const u32 i = seg_of(S.nsmp, N, s);
-        const u32 k = s - S.nsmp[i];
-        Model md;
-        if (!make_model<K>(S.nmin[i], S.nmax[i], S.nP[i], md)) {   // R9/R10: whole node to Standard-Sort
-            if (k == 0) atomicAdd(&S.m.cnt[S.nb0[i]], (u32)S.nal[i]);   // keeps the flat prefix per node
-            continue;
-        }
-        const u32 p0 = S.npos[i];
-        const u32 pos = sample_all ? k : (u32)sample_pos(node_key(c->seed, L, gbase + p0), k, S.nm[i]);
-        atomicAdd(&S.m.cnt[S.nb0[i] + interval_index<K>(X[p0 + pos], md)], 1u);
+    if (__any_sync(0xffffffffu, bad != 0)) {
+#pragma unroll
+        for (int q = 0; q < KPT; ++q)
+            if (bad & (1u << q)) pk[q] = interval_index_exact(key_offset<K>(key[q], md), md.r, md.betad);
     }
-    __syncthreads();
 }
 
-// b = inclusive prefix of the counts per node, T = floor(b*gamma/alpha)+1 (R7).
-__device__ void sub_fit(const DevCtx *c, K7Smem &S, u32 L) {
-    constexpr u32 PER = (MC + K7_THREADS - 1) / K7_THREADS;
-    const u32 N = S.N, nbins = S.nb0[N];
-    const u32 tid = threadIdx.x, lane = lane_id(), w = warp_id();
+template <class K, int NW, int MODE>
+__device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos, u32 m, u32 L, u32 rel, u64 gbase) {
+    constexpr u32 NT = NW * 32;
+    constexpr bool CTA = NW == K7_WARPS;
+    // bins / columns per thread: node <= S_CAP (CTA, 862 bins; 1024 group columns) or <= GCAP (group, 305)
+    constexpr u32 BPT = CTA ? 2 : NW == 1 ? 4 : 3;   // warp: node <= WCAP, 108 bins
+    const u32 t = G.t, g = G.g, w = warp_id(), wg = w - G.w0, lane = lane_id();
+    u64 *X = (rel & 1) ? S.B : S.A;
+    u64 *Y = (rel & 1) ? S.A : S.B;
+    u16 *Wg = S.W + G.w0 * CCOLS;
+    u16 *Wrow = Wg + wg * CCOLS;
+    u32 *row32 = reinterpret_cast<u32 *>(Wrow);
+    u32 *cnt = reinterpret_cast<u32 *>(Wg);
+    const u32 w0 = G.w0;
+    u16 *T16 = S.T16 + w0 * WCOLS;
+    u16 *hc = S.hcol + w0 * WCOLS;
+    u32 *bl = S.bl + w0 * BL_W;
     const bool logging = c->rec != nullptr;
-    const u32 e0 = tid * PER;
-    u32 v[PER], loc = 0;
+    const u32 tau = c->tau;
+
+    // ---- this thread's keys: warp wg owns [f0, f1), chunk q = 32 consecutive keys
+    const u32 R = ((m + NT - 1) / NT) * 32;
+    const u32 f0 = wg * R, f1 = min(f0 + R, m);
+    const u32 nch = f1 > f0 ? (f1 - f0 + 31) / 32 : 0;   // uniform per warp
+    // All KPT slots are processed branch-free (slots past the warp's range load
+    // the node's first key and are marked NONE), so the unrolled loops compile
+    // to straight-line code with the keys in registers.
+    u64 key[KPT];
+    u32 pk[KPT];
+    u64 mn = ~0ull, mx = 0;
 #pragma unroll
-    for (u32 q = 0; q < PER; ++q) { v[q] = e0 + q < nbins ? S.m.cnt[e0 + q] : 0; loc += v[q]; }
-    const u32 incl = warp_incl_scan(loc);
-    if (lane == 31) S.scan_b[w][0] = incl;
-    __syncthreads();
-    u32 run = incl - loc;
-    for (u32 ww = 0; ww < w; ++ww) run += S.scan_b[ww][0];
-    if (e0 < nbins) {
-        u32 i = seg_of(S.nb0, N, e0);
+    for (int q = 0; q < KPT; ++q) {
+        const u32 f = f0 + q * 32 + lane;
+        const bool v = f < f1;
+        key[q] = X[pos + (v ? f : 0u)];
+        pk[q] = v ? 0u : NONE;
+        mn = v && key[q] < mn ? key[q] : mn;
+        mx = v && key[q] > mx ? key[q] : mx;
+    }
+
+    if (c->k7_prof && t == 0) {   // node statistics: slots 7/8 group nodes / keys, 9/10 CTA nodes / keys
+        atomicAdd(&S.prof[CTA ? 9 : 7], 1ull);
+        atomicAdd(&S.prof[CTA ? 10 : 8], (unsigned long long)m);
+    }
+    u32 P = 0, alpha = 0, ncol, delta;
+    Model md;
+    if (MODE == MODE_NODE) {
+        P = iroot34_small(m);
+        alpha = (c->flags & FLAG_SAMPLE_ALL) ? m : P;
+        ncol = P + 1;
+        delta = P;
+        for (u32 i = t; i < P + 2; i += NT) cnt[i] = 0;
+        mn = warp_min_u64(mn);
+        mx = warp_max_u64(mx);
+        if (lane == 0) { S.wmn[w] = mn; S.wmx[w] = mx; }
+        if (t == 0) { S.db[w0] = 0; S.dh[w0] = 0; S.ncnt[w0] = 0; S.nbl[w0] = 0; if (NW > 1 && !CTA) S.top[w0] = 0; }
+        G.bar();
+        mn = S.wmn[G.w0];
+        mx = S.wmx[G.w0];
 #pragma unroll
-        for (u32 q = 0; q < PER; ++q) {
-            const u32 e = e0 + q;
-            run += v[q];
-            if (e < nbins) {
-                while (e >= S.nb0[i + 1]) ++i;
-                const u32 ix = e - S.nb0[i];   // 1-based interval index within the node
-                if (ix >= 1 && !S.ndeg[i]) {
-                    const u32 b = run - S.nsmp[i];
-                    S.T[e] = (u16)bucket_of(b, S.nal[i], S.nP[i]);
+        for (int i = 1; i < NW; ++i) {
+            const u64 a = S.wmn[G.w0 + i], b = S.wmx[G.w0 + i];
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+        if (!make_model<K>(mn, mx, P, md)) {
+            // R9/R10: the whole node goes to Standard-Sort (no bucketing, no record)
+            if (!(rel & 1)) {
+#pragma unroll
+                for (int q = 0; q < KPT; ++q) if (pk[q] != NONE) S.B[pos + f0 + q * 32 + lane] = key[q];
+            }
+            G.bar();
+            sort_range<NW>(S, pos, m, G);
+            return;
+        }
+        // ---- alpha samples (R3, R4) -> per-bin counts
+        {
+            const bool all = (c->flags & FLAG_SAMPLE_ALL) != 0;
+            const u64 nk = node_key(c->seed, L, gbase + pos);
+            for (u32 s = t; s < alpha; s += NT) {
+                const u32 p = all ? s : (u32)sample_pos(nk, s, m);
+                atomicAdd(&cnt[interval_index<K>(X[pos + p], md)], 1u);
+            }
+        }
+        G.bar();
+        // ---- fit: b = inclusive prefix over bins 1..P+1, T = floor(b*gamma/alpha)+1 (R7)
+        {
+            const u32 e0 = 1 + t * BPT;
+            u32 v[BPT], loc = 0;
+#pragma unroll
+            for (u32 k = 0; k < BPT; ++k) { v[k] = e0 + k <= P + 1 ? cnt[e0 + k] : 0; loc += v[k]; }
+            const u32 incl = warp_incl_scan(loc);
+            if (lane == 31) S.wsum[w] = incl;
+            G.bar();
+            u32 run = incl - loc;
+            for (u32 i = 0; i < wg; ++i) run += S.wsum[G.w0 + i];
+            for (u32 i = lane; i < (P + 3) / 2; i += 32) row32[i] = 0;   // counts are dead: zero this warp's row
+            u64 db = 0;
+#pragma unroll
+            for (u32 k = 0; k < BPT; ++k) {
+                const u32 e = e0 + k;
+                run += v[k];
+                if (e <= P + 1) {
+                    T16[e] = (u16)bucket_of(run, alpha, P);
                     if (logging) {
-                        atomicAdd((unsigned long long *)&S.ndb[i], (unsigned long long)digest_term(ix, b));
-                        if (L == 1 && c->l1_b && ix - 1 < c->l1_cap) c->l1_b[ix - 1] = b;
+                        db += digest_term(e, run);
+                        if (L == 1 && c->l1_b && e - 1 < c->l1_cap) c->l1_b[e - 1] = run;
                     }
                 }
             }
-        }
-    }
-    __syncthreads();
-}
-
-// Classify + rank + columns + placement of one sub-batch (or of a K7 group).
-// X -> Y for recursing buckets, X -> A for leaves.  Appends the children.
-template <class K, bool GROUP>
-__device__ void sub_place(const DevCtx *c, K7Smem &S, const u64 *X, u64 *Y, u32 L) {
-    const u32 tid = threadIdx.x, w = warp_id(), lane = lane_id();
-    const u32 N = S.N, Mtot = S.nkey[N], ncols = S.nb0[N];
-    const u32 tau = c->tau;
-    const bool logging = c->rec != nullptr;
-    // ---- pass 1: bucket column of every key (flat index f over the sub-batch's keys)
-    {
-        u32 *row32 = reinterpret_cast<u32 *>(S.m.wcnt[w]);
-        for (u32 i = lane; i < (ncols + 1) / 2; i += 32) row32[i] = 0;
-    }
-    const u32 R = ((Mtot + K7_WARPS * 32 - 1) / (K7_WARPS * 32)) * 32;
-    const u32 f0 = w * R, f1 = min(f0 + R, Mtot);
-    const u32 nch = f1 > f0 ? (f1 - f0 + 31) / 32 : 0;
-    u64 key[CH];
-    u32 pk[CH];
-    if (GROUP) {
-        const Model md = S.gmd;
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-            pk[q] = NONE;
-            key[q] = 0;
-            const u32 f = f0 + q * 32 + lane;
-            if ((u32)q < nch && f < f1) { key[q] = X[f]; pk[q] = interval_index<K>(key[q], md); }
-        }
-        const u32 *gT = S.gT;
-        const u32 jb = S.gjlo - 1u;
-#pragma unroll
-        for (int q = 0; q < CH; ++q)
-            if (pk[q] != NONE) pk[q] = __ldg(gT + pk[q]) - jb;   // column 1 + (j - jlo)
-    } else {
-        u32 node = 0, cn = NONE, base = 0;
-        int pdelta = 0;
-        bool deg = false;
-        Model md;
-        if (f0 + lane < f1) node = seg_of(S.nkey, N, f0 + lane);
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-            pk[q] = NONE;
-            key[q] = 0;
-            const u32 f = f0 + q * 32 + lane;
-            if ((u32)q < nch && f < f1) {
-                while (f >= S.nkey[node + 1]) ++node;
-                if (node != cn) {
-                    cn = node;
-                    base = S.nb0[node];
-                    pdelta = (int)S.npos[node] - (int)S.nkey[node];
-                    deg = S.ndeg[node] != 0;
-                    if (!deg) make_model<K>(S.nmin[node], S.nmax[node], S.nP[node], md);
-                }
-                const u64 x = X[(int)f + pdelta];
-                key[q] = x;
-                pk[q] = deg ? base + 1 : base + S.T[base + interval_index<K>(x, md)];
+            if (logging) {
+                db = warp_sum_u64(db);
+                if (lane == 0) atomicAdd(&S.db[w0], (unsigned long long)db);
             }
         }
-    }
-    __syncwarp();
-    // ---- pass 2: counts per (warp, column) and a rank inside the warp.
-    // Group level: stable ranks (Append order; almost every key recurses) with
-    // __match_any_sync.  Deeper levels: almost every key goes to a leaf, whose
-    // order is irrelevant (it is sorted next), so each key takes an unstable rank
-    // from a shared-memory atomic (8 cycles/chunk on B200 vs ~60 for MATCH over
-    // ~30 distinct columns); keys of recursing buckets are re-ranked stably at
-    // placement time.
-    if (GROUP) {
+        G.bar();
+        // ---- classify (i(x) -> T) and count per (warp, column); unstable rank
+        classify_slots<K>(key, pk, md);
 #pragma unroll
-        for (int q = 0; q < CH; ++q) {
+        for (int q = 0; q < KPT; ++q) {
+            const bool v = pk[q] != NONE;
+            const u32 u = T16[v ? pk[q] : 1u];
+            u32 old = 0;
+            if (v) old = atomicAdd(&row32[u >> 1], (u & 1) ? 0x10000u : 1u);
+            pk[q] = v ? u | ((((u & 1) ? old >> 16 : old) & 0xffffu) << 16) : NONE;
+        }
+    } else {
+        md = S.gmd;
+        ncol = S.gjhi - S.gjlo;
+        delta = S.gdelta;
+        for (u32 i = lane; i < (ncol + 2) / 2; i += 32) row32[i] = 0;
+        if (t == 0) S.nbl[w0] = 0;
+        const u32 *gT = S.gT;
+        const u32 jb = S.gjlo - 1u;
+        classify_slots<K>(key, pk, md);
+#pragma unroll
+        for (int q = 0; q < KPT; ++q) {
+            const bool v = pk[q] != NONE;
+            u32 j = 0;
+            if (v) j = __ldg(gT + pk[q]);
+            pk[q] = v ? j - jb : NONE;   // column 1 + (j - jlo)
+        }
+        __syncwarp();
+        // stable ranks (Append order): chunk by chunk, MATCH per chunk
+#pragma unroll
+        for (int q = 0; q < KPT; ++q) {
             if ((u32)q < nch) {
                 const u32 u = pk[q];
                 const u32 peers = __match_any_sync(0xffffffffu, u);
                 const u32 leader = __ffs(peers) - 1;
                 u32 old = 0;
-                if (u != NONE && lane == leader) { old = S.m.wcnt[w][u]; S.m.wcnt[w][u] = (u16)(old + __popc(peers)); }
+                if (u != NONE && lane == leader) { old = Wrow[u]; Wrow[u] = (u16)(old + __popc(peers)); }
                 old = __shfl_sync(0xffffffffu, old, leader);
                 if (u != NONE) pk[q] = u | ((old + __popc(peers & lanemask_lt())) << 16);
                 __syncwarp();
             }
         }
-    } else {
-        u32 *row32 = reinterpret_cast<u32 *>(S.m.wcnt[w]);
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-            if ((u32)q < nch && pk[q] != NONE) {
-                const u32 u = pk[q];
-                const u32 old = atomicAdd(&row32[u >> 1], (u & 1) ? 0x10000u : 1u);
-                pk[q] = u | (((u & 1) ? old >> 16 : old & 0xffffu) << 16);
-            }
-        }
     }
-    __syncthreads();
-    if (GROUP) prof_mark(c, S, 2); else prof_mark(c, S, 9);
-    // ---- columns: totals, positions (exclusive scan incl. gaps), node of each column (max-scan)
-    constexpr u32 CPT = (MC + K7_THREADS - 1) / K7_THREADS;   // columns per thread
-    const u32 c0 = tid * CPT;
-    u32 h[CPT], mk[CPT];
-    u32 sum = 0, mxk = 0;
-#pragma unroll
-    for (u32 k = 0; k < CPT; ++k) {
-        const u32 col = c0 + k;
-        h[k] = 0; mk[k] = 0;
-        if (col < ncols) {
-            mk[k] = S.GM[col];
-            if (mk[k]) h[k] = S.ngap[mk[k] - 1];
-            else {
-                u32 t = 0;
-#pragma unroll
-                for (u32 ww = 0; ww < (u32)K7_WARPS; ++ww) t += S.m.wcnt[ww][col];
-                h[k] = t;
-            }
-        }
-        sum += h[k];
-        mxk = mk[k] > mxk ? mk[k] : mxk;
-    }
-    const u32 isum = warp_incl_scan(sum), imx = warp_incl_max(mxk);
-    if (lane == 31) { S.scan_b[w][0] = isum; S.scan_b[w][1] = imx; }
-    __syncthreads();
-    u32 run = isum - sum;
-    u32 rmx = __shfl_up_sync(0xffffffffu, imx, 1);
-    if (lane == 0) rmx = 0;
-    for (u32 ww = 0; ww < w; ++ww) { run += S.scan_b[ww][0]; rmx = S.scan_b[ww][1] > rmx ? S.scan_b[ww][1] : rmx; }
-    // kinds: 0 none/gap/empty, 1 leaf of 2..SMALL_MAX keys, 2 leaf of one key, 3 node, 4 larger leaf
-    u32 st[CPT], kd[CPT];
-    u32 nl = 0, kl = 0, nn = 0;
-#pragma unroll
-    for (u32 k = 0; k < CPT; ++k) {
-        const u32 col = c0 + k;
-        rmx = mk[k] > rmx ? mk[k] : rmx;
-        st[k] = run;
-        kd[k] = 0;
-        if (col < ncols && !mk[k] && rmx) {
-            const u32 i = rmx - 1;
-            const u32 j = col - S.nb0[i];     // 1-based bucket index of the node
-            const u32 hh = h[k];
-            const bool deg = GROUP ? false : S.ndeg[i] != 0;
-            const u32 delta = GROUP ? S.gdelta : (u32)S.nP[i];
-            if (hh) {
-                const bool leaf = deg || hh >= delta || hh < tau;   // Alg. 1
-                kd[k] = !leaf ? 3u : hh == 1 ? 2u : hh <= SMALL_MAX ? 1u : 4u;
-                nn += kd[k] == 3u ? 1u : 0u;
-                nl += kd[k] == 1u ? 1u : 0u;
-                kl += kd[k] == 1u ? hh : 0u;
-                // per-warp destinations of this column
-                u32 d = run | (kd[k] == 3u ? 0u : kd[k] == 2u ? DEST_A : DEST_B);
-#pragma unroll
-                for (u32 ww = 0; ww < (u32)K7_WARPS; ++ww) { const u32 o = S.m.wcnt[ww][col]; S.m.wcnt[ww][col] = (u16)d; d += o; }
-                if (kd[k] == 4u) {
-                    const u32 sl = atomicAdd(&S.nbleaf, 1u);
-                    if (sl < (u32)BLCAP) S.bleaf[sl] = run | (hh << 16);
-                    else atomicOr(c->err_flag, 2u);
-                }
-            }
-            if (GROUP) {
-                S.gH[S.gjlo + j - 1] = hh;
-            } else if (logging && !deg) {
-                atomicAdd((unsigned long long *)&S.ndh[i], (unsigned long long)digest_term(j, hh));
-                if (hh) atomicAdd(&S.ncnt[i], hh >= delta ? 1u : hh < tau ? (1u << 10) : (1u << 20));
-                if (L == 1 && c->l1_h && j - 1 < c->l1_cap) c->l1_h[j - 1] = hh;
-            }
-        }
-        run += h[k];
-    }
-    // ordered appends: counts of small leaves, their keys, nodes per warp
-    const u32 inl = warp_incl_scan(nl), ikl = warp_incl_scan(kl), inn = warp_incl_scan(nn);
-    if (lane == 31) { S.scan_c[w][0] = inl; S.scan_c[w][1] = ikl; S.scan_c[w][2] = inn; }
-    __syncthreads();
+    G.bar();
+
+    // ---- column pass: sizes, positions, Alg. 1 lines 160-167 dispatch, destinations per warp
     {
-        u32 sl = inl - nl, sk = ikl - kl, sn = S.tail + inn - nn;
-        for (u32 ww = 0; ww < w; ++ww) { sl += S.scan_c[ww][0]; sk += S.scan_c[ww][1]; sn += S.scan_c[ww][2]; }
+        const u32 c0 = 1 + t * BPT;
+        u32 h[BPT], sum = 0;
 #pragma unroll
-        for (u32 k = 0; k < CPT; ++k) {
-            if (kd[k] == 1u) { S.leaf[sl] = st[k] | (h[k] << 16); S.lkp[sl] = (u16)sk; ++sl; sk += h[k]; }
-            else if (kd[k] == 3u) { S.ring[sn & (RING - 1)] = st[k] | (h[k] << 13); ++sn; }
-        }
-        if (tid == K7_THREADS - 1) {
-            u32 tl = 0, tk = 0, tn = 0;
-            for (u32 ww = 0; ww < (u32)K7_WARPS; ++ww) { tl += S.scan_c[ww][0]; tk += S.scan_c[ww][1]; tn += S.scan_c[ww][2]; }
-            S.nleaf = tl; S.lkeys = tk; S.lkp[tl] = (u16)tk;
-            S.new_tail = S.tail + tn;
-        }
+        for (u32 k = 0; k < BPT; ++k) {
+            const u32 col = c0 + k;
+            h[k] = 0;
+            if (col <= ncol) {
 #pragma unroll
-        for (int q = 0; q < CH; ++q) {
-            if ((u32)q < nch) {
-                const u32 u = pk[q] & 0xffffu;
-                u32 d = 0;
-                if (pk[q] != NONE) d = (u32)S.m.wcnt[w][u] + (pk[q] >> 16);
-                if (!GROUP) {   // recursing bucket: stable rank (Append order), running per-warp cursor
-                    const bool nd = pk[q] != NONE && (d & (DEST_A | DEST_B)) == 0;
-                    if (__any_sync(0xffffffffu, nd)) {
-                        const u32 peers = __match_any_sync(0xffffffffu, nd ? u : NONE);
-                        const u32 leader = __ffs(peers) - 1;
-                        u32 base = 0;
-                        if (nd && lane == leader) { base = S.m.wcnt[w][u]; S.m.wcnt[w][u] = (u16)(base + __popc(peers)); }
-                        base = __shfl_sync(0xffffffffu, base, leader);
-                        if (nd) d = base + __popc(peers & lanemask_lt());
-                        __syncwarp();
+                for (int ww = 0; ww < NW; ++ww) h[k] += Wg[ww * CCOLS + col];
+            }
+            sum += h[k];
+        }
+        const u32 isum = warp_incl_scan(sum);
+        if (lane == 31) S.wsum[w] = isum;
+        G.bar();
+        u32 run = isum - sum;
+        for (u32 i = 0; i < wg; ++i) run += S.wsum[G.w0 + i];
+        u32 ncc = 0;
+        unsigned long long dh = 0;
+#pragma unroll
+        for (u32 k = 0; k < BPT; ++k) {
+            const u32 col = c0 + k;
+            if (col <= ncol) {
+                const u32 hh = h[k];
+                hc[col] = (u16)hh;
+                if (hh) {
+                    const bool leaf = hh >= delta || hh < tau;   // Alg. 1
+                    u32 d = run | (!leaf ? 0u : hh == 1 ? DEST_A : DEST_B);
+#pragma unroll
+                    for (int ww = 0; ww < NW; ++ww) { const u32 o = Wg[ww * CCOLS + col]; Wg[ww * CCOLS + col] = (u16)d; d += o; }
+                    if (!leaf) {
+                        const u32 e = ent_make(pos + run, hh, rel + 1);
+                        if (CTA && hh > (u32)WCAP) {
+                            const u32 sl = atomicAdd(&S.btot, 1u);
+                            if (sl < (u32)LBIG_CAP) S.lbig[sl] = e; else atomicOr(c->err_flag, 2u);
+                        } else if (CTA) {
+                            const u32 sl = atomicAdd(&S.stot, 1u);
+                            if (sl < (u32)LIST_CAP) S.lsm[sl] = e; else atomicOr(c->err_flag, 2u);
+                        } else {   // warp: own stack; team: staged in its warps' stacks (contiguous rows)
+                            const u32 sl = atomicAdd(&S.top[w0], 1u);
+                            if (sl < (u32)(STK_CAP * NW)) (&S.stk[w0][0])[sl] = e; else atomicOr(c->err_flag, 2u);
+                        }
+                    } else if (hh > SMALL_MAX) {
+                        const u32 sl = atomicAdd(&S.nbl[w0], 1u);
+                        if (sl < (u32)(BL_W * NW)) bl[sl] = run | (hh << 13);
+                        else atomicOr(c->err_flag, 2u);
                     }
+                    ncc += hh >= delta ? 1u : hh < tau ? (1u << 10) : (1u << 20);
                 }
-                if (pk[q] != NONE) {
-                    u64 *dst = (d & DEST_A) ? S.A : (d & DEST_B) ? S.B : Y;
-                    dst[d & POS_MASK] = key[q];
+                if (MODE == MODE_GLOBAL) {
+                    S.gH[S.gjlo + col - 1] = hh;
+                } else if (logging) {
+                    dh += digest_term(col, hh);
+                    if (L == 1 && c->l1_h && col - 1 < c->l1_cap) c->l1_h[col - 1] = hh;
                 }
+                run += hh;
+            }
+        }
+        if (MODE == MODE_NODE && logging) {
+            dh = warp_sum_u64(dh);
+            for (int o = 16; o > 0; o >>= 1) ncc += __shfl_xor_sync(0xffffffffu, ncc, o);
+            if (lane == 0) { atomicAdd(&S.dh[w0], dh); atomicAdd(&S.ncnt[w0], ncc); }
+        }
+    }
+    G.bar();
+
+    // ---- placement (chunk order: stable re-rank of recursing keys)
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+        {
+            const u32 u = pk[q] & 0xffffu;
+            const bool valid = pk[q] != NONE;
+            u32 d = valid ? (u32)Wrow[u] + (pk[q] >> 16) : 0u;
+            if (MODE == MODE_NODE) {
+                const bool nd = valid && (d & (DEST_A | DEST_B)) == 0;
+                if (__any_sync(0xffffffffu, nd)) {
+                    const u32 peers = __match_any_sync(0xffffffffu, nd ? u : NONE);
+                    const u32 leader = __ffs(peers) - 1;
+                    u32 base = 0;
+                    if (nd && lane == leader) { base = Wrow[u]; Wrow[u] = (u16)(base + __popc(peers)); }
+                    base = __shfl_sync(0xffffffffu, base, leader);
+                    if (nd) d = base + __popc(peers & lanemask_lt());
+                    __syncwarp();
+                }
+            }
+            const u32 p = pos + (d & POS_MASK);
+            u64 *dst = (d & DEST_A) ? S.A : (d & DEST_B) ? S.B : Y;
+            if (valid) {
+                dst[p] = key[q];
+                S.LC[p] = (d & DEST_B) ? (u16)u : (u16)0;
             }
         }
     }
-    __syncthreads();
-}
-
-// Node records of the sub-batch (pass log).
-template <class K>
-__device__ void sub_records(const DevCtx *c, K7Smem &S, u32 L, u64 gbase) {
-    for (u32 i = threadIdx.x; i < S.N; i += K7_THREADS) {
-        if (S.ndeg[i]) continue;
-        const u32 cc = S.ncnt[i];
-        write_record(c, L, S.nal[i], gbase + S.npos[i], S.nm[i], K::from_okey(S.nmin[i]), K::from_okey(S.nmax[i]),
-                     S.ndb[i], S.ndh[i], cc & 1023u, (cc >> 10) & 1023u, cc >> 20);
+    G.bar();
+    if (NW > 1 && !CTA) {   // team: publish the children (their keys are placed) to the small-node list
+        const u32 nc = S.top[w0];
+        if (nc) {
+            __threadfence_block();
+            for (u32 i = t; i < nc; i += NT) {
+                const u32 sl = atomicAdd(&S.stot, 1u);
+                if (sl < (u32)LIST_CAP) *(volatile u32 *)&S.lsm[sl] = (&S.stk[w0][0])[i]; else atomicOr(c->err_flag, 2u);
+            }
+        }
     }
-}
 
-__device__ __forceinline__ void reset_leaf_lists(K7Smem &S) {
-    if (threadIdx.x == 0) { S.item_next = 0; S.nbleaf = 0; S.nleaf = 0; S.lkeys = 0; }
+    // ---- Standard-Sort of the leaves: <= SMALL_MAX keys key-parallel, larger ones by bitonic networks
+    for (u32 p = t; p < m; p += NT) {
+        const u32 cc = S.LC[pos + p];
+        if (!cc) continue;
+        const u32 hh = hc[cc];
+        if (hh > SMALL_MAX) continue;
+        const u32 st = pos + ((u32)Wg[cc] & POS_MASK);
+        const u64 v = S.B[pos + p];
+        S.A[st + rank_in_leaf(S.B, st, hh, v, pos + p)] = v;
+    }
+    const u32 nb = S.nbl[w0];
+    for (u32 i = 0; i < nb; ++i) {
+        const u32 e = bl[i];
+        const u32 st = pos + (e & 0x1fffu), hh = e >> 13;
+        set_bitonic<NW>(S.B + st, hh, G);
+        for (u32 p = st + t; p < st + hh; p += NT) S.A[p] = S.B[p];
+    }
+    if (MODE == MODE_NODE && logging && t == 0) {
+        const u32 cc = S.ncnt[w0];
+        write_record(c, L, alpha, gbase + pos, m, K::from_okey(mn), K::from_okey(mx), S.db[w0], S.dh[w0],
+                     cc & 1023u, (cc >> 10) & 1023u, cc >> 20);
+    }
+    G.bar();
 }
 
 // ------------------------------------------------------------------ global I/O
@@ -705,6 +620,17 @@ __device__ __forceinline__ void store_task(const K7Smem &S, u64 *dst, u32 m) {
 }
 
 // ------------------------------------------------------------------ the kernel
+// Node entry of size m from the CTA phases: big list (> WCAP keys) or small list.
+__device__ __forceinline__ void push_root(const DevCtx *c, K7Smem &S, u32 e) {
+    if (ent_m(e) > (u32)WCAP) {
+        const u32 sl = atomicAdd(&S.btot, 1u);
+        if (sl < (u32)LBIG_CAP) S.lbig[sl] = e; else atomicOr(c->err_flag, 2u);
+    } else {
+        const u32 sl = atomicAdd(&S.stot, 1u);
+        if (sl < (u32)LIST_CAP) S.lsm[sl] = e; else atomicOr(c->err_flag, 2u);
+    }
+}
+
 template <class K>
 __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restrict__ c) {
     extern __shared__ __align__(16) unsigned char k7_smem_raw[];
@@ -712,6 +638,11 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
     if (*c->nan_flag) return;
     const u32 ntasks = *c->k7_count;
     const u32 begin = *c->k7_begin;
+    const u32 w = warp_id(), lane = lane_id();
+    const Grp<K7_WARPS> CT{0u, threadIdx.x, 0u};
+    const Grp<GW> GG{w / GW, threadIdx.x % GT, (w / GW) * GW};
+    const Grp<1> GS{w, lane, w};
+    for (u32 i = threadIdx.x; i < (u32)LSM_CAP; i += K7_THREADS) S.lsm[i] = 0;   // tickets read 0 until pushed
     if (c->k7_prof && threadIdx.x == 0) {
         for (int i = 0; i < K7_PROF_SLOTS; ++i) S.prof[i] = 0;
         S.prof_t = clock64();
@@ -720,9 +651,8 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
         if (threadIdx.x == 0) {
             S.task_idx = begin + atomicAdd(c->k7_next, 1u);
             if (S.task_idx < ntasks) S.task = c->k7[S.task_idx];
-            S.head = 0; S.tail = 0; S.level_end = 0;
+            S.stot = 0; S.snext = 0; S.btot = 0; S.bnext = 0; S.big_active = NGRP;
         }
-        reset_leaf_lists(S);
         __syncthreads();
         if (S.task_idx >= ntasks) break;
         prof_mark(c, S, 0);
@@ -739,71 +669,86 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
         __syncthreads();
         prof_mark(c, S, 1);
         if (threadIdx.x == 0 && c->k7_prof) { S.prof[11] += 1; S.prof[12] += M; }
-        u32 L = task.level;
-        u32 xbuf = 0;   // buffer holding the current level's nodes (0: A, 1: B)
-        if (sort_task) {   // the task is one leaf (keys in B)
-            if (threadIdx.x == 0) {
-                if (M <= SMALL_MAX) { S.leaf[0] = 0u | (M << 16); S.lkp[0] = 0; S.lkp[1] = (u16)M; S.nleaf = 1; S.lkeys = M; }
-                else { S.bleaf[0] = 0u | (M << 16); S.nbleaf = 1; }
-            }
-            __syncthreads();
-            leaf_phase(S);
-            __syncthreads();
-        } else if (task.kind == K7_NODE) {
-            if (threadIdx.x == 0) { S.ring[0] = 0u | (M << 13); S.tail = 1; S.level_end = 1; }
-            __syncthreads();
-        } else {   // K7_GROUP: finish the global node's placement for buckets [jlo, jhi)
-            if (threadIdx.x == 0) {
-                const GNode &g = c->nodes[task.node];
-                S.gmd = g.md; S.gT = g.T; S.gH = g.H;
-                S.gdelta = g.delta; S.glevel = g.level; S.gjlo = task.jlo;
-                S.N = 1; S.nkey[0] = 0; S.nkey[1] = M; S.nb0[0] = 0; S.nb0[1] = (u16)(task.jhi - task.jlo + 1);
-                S.npos[0] = 0; S.nm[0] = (u16)M; S.ngap[0] = 0; S.ndeg[0] = 0;
-            }
-            for (u32 i = threadIdx.x; i < MC; i += K7_THREADS) S.GM[i] = i == 0 ? 1 : 0;
-            __syncthreads();
-            sub_place<K, true>(c, S, S.A, S.B, S.glevel);
-            prof_mark(c, S, 3);
-            leaf_phase(S);
-            if (threadIdx.x == 0) { S.tail = S.new_tail; S.level_end = S.tail; }
-            reset_leaf_lists(S);
-            __syncthreads();
-            prof_mark(c, S, 4);
-            L = S.glevel + 1;
-            xbuf = 1;
-        }
-        // ---- recursion levels (Alg. 1 on every recursing bucket, level by level)
-        for (;;) {
-            if (S.head == S.tail) break;
-            if (S.head == S.level_end) {   // uniform: shared values read after a barrier
-                __syncthreads();
-                if (threadIdx.x == 0) S.level_end = S.tail;
-                __syncthreads();
-                L += 1;
-                xbuf ^= 1u;
-            }
-            u64 *X = xbuf ? S.B : S.A;
-            u64 *Y = xbuf ? S.A : S.B;
-            sub_setup(c, S);
-            prof_mark(c, S, 5);
-            sub_minmax(S, X);
+        if (sort_task) {
+            sort_range<K7_WARPS>(S, 0, M, CT);
             prof_mark(c, S, 6);
-            sub_sample<K>(c, S, X, L, task.off);
-            prof_mark(c, S, 7);
-            sub_fit(c, S, L);
-            prof_mark(c, S, 8);
-            sub_place<K, false>(c, S, X, Y, L);
-            prof_mark(c, S, 10);
-            leaf_phase(S);
-            if (c->rec) sub_records<K>(c, S, L, task.off);
-            if (threadIdx.x == 0) {
-                S.head += S.N;
-                S.tail = S.new_tail;
-                if (S.tail - S.head > (u32)RING) atomicOr(c->err_flag, 2u);
+        } else {
+            u32 Lb;
+            if (task.kind == K7_GROUP) {   // finish the global node's placement for buckets [jlo, jhi)
+                if (threadIdx.x == 0) {
+                    const GNode &gn = c->nodes[task.node];
+                    S.gmd = gn.md; S.gT = gn.T; S.gH = gn.H;
+                    S.gdelta = gn.delta; S.glevel = gn.level; S.gjlo = task.jlo; S.gjhi = task.jhi;
+                }
+                __syncthreads();
+                Lb = S.glevel;
+                node_step<K, K7_WARPS, MODE_GLOBAL>(c, S, CT, 0, M, Lb, 0, task.off);
+                prof_mark(c, S, 2);
+            } else {   // K7_NODE: a fresh Learned-Sort call on the whole task
+                Lb = task.level;
+                if (threadIdx.x == 0) push_root(c, S, ent_make(0, M, 0));
+                __syncthreads();
             }
-            reset_leaf_lists(S);
-            __syncthreads();
+            // nodes larger than a team's register capacity: the whole CTA, one level
+            for (u32 i = 0; i < S.btot; ++i) {
+                const u32 e = S.lbig[i];
+                if (ent_m(e) > (u32)GCAP) {
+                    __syncthreads();
+                    if (threadIdx.x == 0) S.lbig[i] = 0;
+                    node_step<K, K7_WARPS, MODE_NODE>(c, S, CT, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                }
+            }
             prof_mark(c, S, 4);
+            // teams of GW warps take the nodes of (WCAP, GCAP] keys (their children go to the small
+            // list); then every warp runs small nodes and their whole subtrees on its own
+            for (;;) {
+                if (GG.t == 0) {
+                    u32 e = 0;
+                    for (;;) {
+                        const u32 i = atomicAdd(&S.bnext, 1u);
+                        if (i >= S.btot) break;
+                        e = S.lbig[i];
+                        if (e) break;
+                    }
+                    S.cur[GG.w0] = e;
+                }
+                GG.bar();
+                const u32 e = S.cur[GG.w0];
+                if (!e) break;
+                node_step<K, GW, MODE_NODE>(c, S, GG, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+            }
+            if (GG.t == 0) { __threadfence_block(); atomicSub(&S.big_active, 1u); }
+            if (lane == 0) S.top[w] = 0;
+            __syncwarp();
+            for (;;) {
+                u32 e = 0;
+                if (lane == 0) {
+                    if (S.top[w] > 0) {
+                        e = S.stk[w][--S.top[w]];
+                    } else {
+                        const u32 tk = atomicAdd(&S.snext, 1u);
+                        volatile u32 *slot = &S.lsm[tk < (u32)LSM_CAP ? tk : LSM_CAP - 1];
+                        u32 ns = 32;
+                        for (;;) {   // wait (backing off, so the working teams keep the issue slots)
+                            e = *slot;
+                            if (e) { *slot = 0; break; }
+                            if (*(volatile u32 *)&S.big_active == 0) {   // no more pushes
+                                __threadfence_block();
+                                e = *slot;
+                                if (e) *slot = 0;
+                                break;
+                            }
+                            __nanosleep(ns);
+                            ns = ns < 2048 ? ns * 2 : ns;
+                        }
+                    }
+                }
+                e = __shfl_sync(0xffffffffu, e, 0);
+                if (!e) break;
+                node_step<K, 1, MODE_NODE>(c, S, GS, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+            }
+            __syncthreads();
+            prof_mark(c, S, 5);
         }
         store_task<K>(S, gout, M);
         prof_mark(c, S, 13);

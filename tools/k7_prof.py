@@ -5,9 +5,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2405_07122_b200 as pcf
 import synth
-NAMES = ["claim", "load", "group rank", "group columns+place", "leaves", "setup", "min/max", "sample", "fit",
-         "rank", "columns+place", "tasks", "keys", "store", "-", "-"]
-SLOTS = [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 13]
+NAMES = ["claim", "load", "group placement (CTA)", "-", "CTA-run nodes", "node groups", "sort tasks", "#group nodes",
+         "group node keys", "#CTA nodes", "CTA node keys", "tasks", "keys", "store", "-", "-"]
+SLOTS = [0, 1, 2, 4, 5, 6, 13]
 ap = argparse.ArgumentParser(); ap.add_argument("--config", default="c2"); ap.add_argument("--n", type=int, default=None)
 a = ap.parse_args()
 x = torch.from_numpy(synth.config(a.config, n=a.n)).cuda()
@@ -19,3 +19,6 @@ tot = sum(cy[i] for i in SLOTS)
 print(f"{a.config}: tasks {cy[11]} keys {cy[12]}  total CTA-cycles {tot:.3e}  cycles/key {tot / max(cy[12], 1):.1f}")
 for i in SLOTS:
     print(f"  {NAMES[i]:28s} {cy[i]:.3e}  {100 * cy[i] / max(tot, 1):5.1f}%  {cy[i] / max(cy[12], 1):6.2f} cyc/key")
+for i in (7, 8, 9, 10):
+    print(f"  {NAMES[i]:28s} {cy[i]:.0f}")
+print(f"  mean group node {cy[8] / max(cy[7], 1):.1f} keys, mean CTA node {cy[10] / max(cy[9], 1):.1f} keys")
