@@ -422,19 +422,20 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_fit_final(const DevCtx *__rest
 
 // --- stable scatter by digit
 // One CTA per tile of SPLIT_TILE keys; warp w owns keys [w*SC_PER_WARP, ...)
-// of the tile and holds them in registers (SC_KPL per lane).  Pass 1 ranks the
-// keys stably inside the warp (per-warp counters; half a chunk at a time each
-// lane ORs its bit into the high half of its digit's counter word, so after a
-// __syncwarp the word holds count | peers -- the CUB "atomic-or match", much
-// cheaper on B200 than __match_any_sync over ~30 distinct digits); the tile is
-// then staged in shared memory in digit order (stable) and written out run by
-// run, so global writes are coalesced per digit run.
+// of the tile (SC_KPL per lane, chunk q = 32 consecutive keys).  Each key
+// takes a rank inside its warp from a shared-memory atomicAdd on the warp's
+// counter of its digit (3 instructions; chunks are processed in order, so
+// only keys of the same chunk with the same digit can come out of Append
+// order), the tile is staged in digit order (digit run, then warp, then
+// rank), and the write-out puts every such same-chunk group back in source
+// order (groups are found from the staged source index; almost all are
+// single keys).  Global writes are coalesced per digit run.
 struct SplitScatterSmem {
-    u64 stage[SPLIT_TILE];
-    u16 sdig[SPLIT_TILE];
-    u32 wc[SC_WARPS][GMAX];     // per-warp count | mask -> warp-exclusive offsets within (tile, digit)
-    u32 tstart[GMAX + 1];       // tile-local start of each digit's run
-    u32 gbase[GMAX];            // segment-relative destination of each digit's run
+    u64 buf[SPLIT_TILE];
+    u32 dsrc[SPLIT_TILE];            // staged: digit | tile source index << 16
+    u32 wc[SC_WARPS][GMAX / 2 + 1];  // per-warp u16 counters (2 per word) -> per-warp offsets in the run
+    u32 tstart[GMAX + 1];            // tile-local start of each digit's run
+    u32 goff[GMAX + 1];              // segment-relative destination of run position 0 (mod 2^32)
     u32 scan_tmp[SC_WARPS + 1];
 };
 
@@ -446,56 +447,47 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
     const u64 *x = c->buf[st.src] + st.off;
     u64 *y = c->buf[st.dst] + st.off;
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const u32 G = st.G;
+    const u32 G = st.G, GW2 = (G + 1) / 2;
     const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
     const u32 ntile = k1 - k0;
     const u32 r0 = k0 + w * SC_PER_WARP;
-    for (u32 d = lane; d < G; d += 32) S.wc[w][d] = 0;
-    // load this lane's keys (coalesced per chunk) and compute their digits
-    u64 key[SC_KPL];
-    u32 dig[SC_KPL];
-#pragma unroll
-    for (u32 q = 0; q < SC_KPL; ++q) { u32 k = r0 + q * 32 + lane; key[q] = k < k1 ? x[k] : 0; }
+    for (u32 d = lane; d < GW2; d += 32) S.wc[w][d] = 0;
     const u16 *dg = c->digs + st.off;   // digits cached by k_split_count
+    u64 key[SC_KPL];
+    u32 pk[SC_KPL];
 #pragma unroll
     for (u32 q = 0; q < SC_KPL; ++q) {
-        u32 k = r0 + q * 32 + lane;
-        dig[q] = k < k1 ? (u32)dg[k] : 0xffffffffu;
+        const u32 k = r0 + q * 32 + lane;
+        const bool v = k < k1;
+        key[q] = v ? x[k] : 0ull;
+        pk[q] = v ? (u32)dg[k] : 0xffffffffu;
     }
     __syncwarp();
-    // pass 1: stable rank within the warp, chunk by chunk
+    // rank inside the warp: one atomicAdd per key on the warp's u16 counter of its digit
 #pragma unroll
-    for (u32 q = 0; q < SC_KPL; ++q) {   // dig[q] becomes digit | in-warp rank << 16 (digit 0xffff: none)
-        const u32 d = dig[q];
-        u32 rank = 0;
-#pragma unroll
-        for (u32 half = 0; half < 2; ++half) {
-            const bool mine = (lane >> 4) == half && d != 0xffffffffu;
-            if (mine) atomicOr(&S.wc[w][d], 1u << (16 + (lane & 15)));
-            __syncwarp();
-            const u32 e = mine ? S.wc[w][d] : 0u;
-            __syncwarp();
-            if (mine) {
-                const u32 msk = e >> 16, lt = (1u << (lane & 15)) - 1u;
-                rank = (e & 0xffffu) + __popc(msk & lt);
-                if ((msk & lt) == 0) S.wc[w][d] = (e & 0xffffu) + __popc(msk);
-            }
-            __syncwarp();
+    for (u32 q = 0; q < SC_KPL; ++q) {
+        const u32 d = pk[q];
+        if (d != 0xffffffffu) {
+            const u32 old = atomicAdd(&S.wc[w][d >> 1], (d & 1u) ? 0x10000u : 1u);
+            pk[q] = d | ((((d & 1u) ? old >> 16 : old) & 0xffffu) << 16);
         }
-        dig[q] = (d & 0xffffu) | (rank << 16);
     }
     __syncthreads();
-    // per digit: warp-exclusive offsets, tile totals
-    for (u32 d = threadIdx.x; d < G; d += SC_THREADS) {
-        u32 run = 0;
+    // per digit pair: warp-exclusive offsets and tile totals; run destinations from the scanned matrix
+    for (u32 e = threadIdx.x; e < GW2; e += SC_THREADS) {
+        u32 lo = 0, hi = 0;
 #pragma unroll
-        for (u32 ww = 0; ww < SC_WARPS; ++ww) { u32 cc = S.wc[ww][d]; S.wc[ww][d] = run; run += cc; }
-        S.tstart[d] = run;
-        S.gbase[d] = P[st.cbase + (u64)d * st.ntiles + lt] - (u32)st.mbase;
+        for (u32 ww = 0; ww < SC_WARPS; ++ww) {
+            const u32 v = S.wc[ww][e];
+            S.wc[ww][e] = lo | (hi << 16);
+            lo += v & 0xffffu;
+            hi += v >> 16;
+        }
+        S.tstart[2 * e] = lo;
+        S.tstart[2 * e + 1] = hi;   // e == GW2 - 1 with G odd: digit G, count 0
     }
     __syncthreads();
-    // exclusive scan of the tile totals over the digits (G <= GMAX)
-    {
+    {   // exclusive scan of the tile totals over the digits (G <= GMAX)
         constexpr u32 PER = (GMAX + SC_THREADS - 1) / SC_THREADS;
         const u32 b0 = threadIdx.x * PER;
         u32 v[PER], loc = 0;
@@ -514,24 +506,56 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
         __syncthreads();
         u32 run = S.scan_tmp[w] + incl - loc;
 #pragma unroll
-        for (u32 i = 0; i < PER; ++i) if (b0 + i < G) { S.tstart[b0 + i] = run; run += v[i]; }
-    }
-    __syncthreads();
-    // stage in digit order (stable: digit run, then warp, then in-warp rank)
-#pragma unroll
-    for (u32 q = 0; q < SC_KPL; ++q) {
-        const u32 d = dig[q] & 0xffffu;
-        if (d != 0xffffu) {
-            const u32 lp = S.tstart[d] + S.wc[w][d] + (dig[q] >> 16);
-            S.stage[lp] = key[q];
-            S.sdig[lp] = (u16)d;
+        for (u32 i = 0; i < PER; ++i) {
+            const u32 d = b0 + i;
+            if (d < G) {
+                S.tstart[d] = run;
+                if (v[i]) S.goff[d] = P[st.cbase + (u64)d * st.ntiles + lt] - (u32)st.mbase - run;
+                run += v[i];
+            }
         }
     }
     __syncthreads();
-    // coalesced write-out, run by run
+    // stage in digit order: digit run, then warp, then in-warp rank
+#pragma unroll
+    for (u32 q = 0; q < SC_KPL; ++q) {
+        if (pk[q] != 0xffffffffu) {
+            const u32 d = pk[q] & 0xffffu;
+            const u32 wo = (S.wc[w][d >> 1] >> ((d & 1u) * 16)) & 0xffffu;
+            const u32 lp = S.tstart[d] + wo + (pk[q] >> 16);
+            S.buf[lp] = key[q];
+            S.dsrc[lp] = d | ((w * SC_PER_WARP + q * 32 + lane) << 16);
+        }
+    }
+    __syncthreads();
+    // Append order inside a group of keys of one chunk with one digit (same
+    // dsrc >> 21 and digit, contiguous in the stage) depends on the order the
+    // shared-memory atomics of one instruction were served in: check for an
+    // inversion, and only then re-rank the groups by source index.
+    bool inv = false;
+    for (u32 i = threadIdx.x + 1; i < ntile; i += SC_THREADS) {
+        const u32 a = S.dsrc[i - 1], b = S.dsrc[i];
+        inv |= (a >> 21) == (b >> 21) && (a & 0xffffu) == (b & 0xffffu) && (a >> 16) > (b >> 16);
+    }
+    if (!__syncthreads_or(inv)) {
+        for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) y[S.goff[S.dsrc[i] & 0xffffu] + i] = S.buf[i];
+        return;
+    }
     for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) {
-        const u32 d = S.sdig[i];
-        y[S.gbase[d] + (i - S.tstart[d])] = S.stage[i];
+        const u32 e = S.dsrc[i];
+        const u32 d = e & 0xffffu;
+        const u32 gk = (e >> 21) << 16 | d;   // group key: chunk, digit
+        u32 pos = i;
+        const bool sp = i > 0 && (((S.dsrc[i - 1] >> 21) << 16) | (S.dsrc[i - 1] & 0xffffu)) == gk;
+        const bool sn = i + 1 < ntile && (((S.dsrc[i + 1] >> 21) << 16) | (S.dsrc[i + 1] & 0xffffu)) == gk;
+        if (sp || sn) {
+            u32 a = i, b = i + 1;
+            while (a > 0 && (((S.dsrc[a - 1] >> 21) << 16) | (S.dsrc[a - 1] & 0xffffu)) == gk) --a;
+            while (b < ntile && (((S.dsrc[b] >> 21) << 16) | (S.dsrc[b] & 0xffffu)) == gk) ++b;
+            pos = a;
+            for (u32 j = a; j < b; ++j) pos += (S.dsrc[j] >> 16) < (e >> 16) ? 1u : 0u;
+        }
+        y[S.goff[d] + pos] = S.buf[i];
     }
 }
 
