@@ -403,7 +403,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             k_tile_map<<<nsm * 2, 256, 0, st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_COUNT);
-            k_split_count<K><<<tile_grid, SPLIT_THREADS, 0, st>>>(d_ctx, cur);
+            k_split_count<K><<<tile_grid, SC_THREADS, 0, st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_OTHER);
             k_scanp_partials<<<nsm * 2, SCAN_THREADS, 0, st>>>(d_ctx);

@@ -141,55 +141,67 @@ __device__ __forceinline__ u32 digit_of(u64 okey, const Model &md, const u32 *__
     return (j - jlo) >> shift;
 }
 
+// Counts of the digit (T[i(x)] - jlo) >> shift per tile (one CTA per tile of
+// SPLIT_TILE keys, the same warp-strided layout as the scatter), written to the
+// digit-major count matrix; every key's digit is cached (u16) for the scatter.
+// All SC_KPL key loads of a thread are issued before any use, then all T
+// gathers (memory-level parallelism: the pass is latency-bound otherwise).
 template <class K>
-__global__ void __launch_bounds__(SPLIT_THREADS) k_split_count(const DevCtx *__restrict__ c, u32 cur) {
+__global__ void __launch_bounds__(SC_THREADS, 2) k_split_count(const DevCtx *__restrict__ c, u32 cur) {
     __shared__ u32 hist[GMAX];
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
     const SplitTask *__restrict__ L = c->splits[cur];
     u32 *__restrict__ C = c->cmat;
-    {
-        const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
-        if (tile >= pl.tiles) return;
-        const u32 s = c->tmap[tile];
-        const SplitTask st = L[s];
-        const u32 lt = tile - st.tile_begin;
-        const GNode &g = c->nodes[st.node];
-        for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) hist[d] = 0;
-        __syncthreads();
-        const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
-        if (g.degenerate) {
-            if (threadIdx.x == 0) hist[0] = k1 - k0;
-        } else {
-            const Model md = g.md;
-            const u64 *x = c->buf[st.src] + st.off;
-            const u32 *T = g.T;
-            u16 *dg = c->digs + st.off;
-            constexpr u32 UB = 4;
-            u32 k = k0 + threadIdx.x;
-            for (; k + (UB - 1) * SPLIT_THREADS < k1; k += UB * SPLIT_THREADS) {
-                u64 raw[UB];
-                u32 ix[UB];
+    const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
+    if (tile >= pl.tiles) return;
+    const u32 s = c->tmap[tile];
+    const SplitTask st = L[s];
+    const u32 lt = tile - st.tile_begin;
+    const GNode &g = c->nodes[st.node];
+    for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) hist[d] = 0;
+    const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
+    const bool deg = g.degenerate != 0;
+    __syncthreads();
+    if (deg) {
+        if (threadIdx.x == 0) hist[0] = k1 - k0;
+    } else {
+        const Model md = g.md;
+        const u64 *x = c->buf[st.src] + st.off;
+        const u32 *T = g.T;
+        u16 *dg = c->digs + st.off;
+        const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const u32 r0 = k0 + w * SC_PER_WARP + lane;
+        u64 raw[SC_KPL];
+        u32 ix[SC_KPL];
 #pragma unroll
-                for (u32 q = 0; q < UB; ++q) raw[q] = x[k + q * SPLIT_THREADS];
+        for (u32 q = 0; q < SC_KPL; ++q) { const u32 k = r0 + q * 32; raw[q] = k < k1 ? x[k] : x[k0]; }
+        u32 bad = 0;
 #pragma unroll
-                for (u32 q = 0; q < UB; ++q) ix[q] = __ldg(&T[interval_index<K>(K::to_okey(raw[q]), md)]);
+        for (u32 q = 0; q < SC_KPL; ++q) {
+            bool ok;
+            ix[q] = interval_index_fast<K>(K::to_okey(raw[q]), md, ok);
+            bad |= ok ? 0u : (1u << q);
+        }
+        if (bad) {   // rare: keys in the fast path's guard band
 #pragma unroll
-                for (u32 q = 0; q < UB; ++q) {
-                    const u32 d = (ix[q] - st.jlo) >> st.shift;
-                    dg[k + q * SPLIT_THREADS] = (u16)d;
-                    atomicAdd(&hist[d], 1u);
-                }
-            }
-            for (; k < k1; k += SPLIT_THREADS) {
-                const u32 d = digit_of<K>(K::to_okey(x[k]), md, T, st.jlo, st.shift);
+            for (u32 q = 0; q < SC_KPL; ++q)
+                if (bad & (1u << q)) ix[q] = interval_index_exact(key_offset<K>(K::to_okey(raw[q]), md), md.r, md.betad);
+        }
+#pragma unroll
+        for (u32 q = 0; q < SC_KPL; ++q) ix[q] = __ldg(&T[ix[q]]);
+#pragma unroll
+        for (u32 q = 0; q < SC_KPL; ++q) {
+            const u32 k = r0 + q * 32;
+            if (k < k1) {
+                const u32 d = (ix[q] - st.jlo) >> st.shift;
                 dg[k] = (u16)d;
                 atomicAdd(&hist[d], 1u);
             }
         }
-        __syncthreads();
-        for (u32 d = threadIdx.x; d < st.G; d += SPLIT_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
     }
+    __syncthreads();
+    for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
 }
 
 // --- exclusive scan of a u32 array (3 phases)

@@ -89,7 +89,7 @@ struct K7Smem {
     u32 ncnt[K7_WARPS];           // pass log: nf | ns << 10 | nr << 20
     u32 nbl[K7_WARPS];
     u32 top[K7_WARPS], cur[K7_WARPS];
-    u32 stot, snext, btot, bnext, big_active;
+    u32 stot, snext, btot, bnext, bnext2, big_active;
     u32 task_idx;
     K7Task task;
     Model gmd;
@@ -160,13 +160,13 @@ __device__ __forceinline__ u32 iroot34_small(u32 m) {
 template <int NW>
 struct Grp {
     static constexpr int NT = NW * 32;
-    u32 g;    // group index (0 for the CTA)
+    u32 g;    // named barrier of the set (0: the CTA)
     u32 t;    // thread index inside the set
     u32 w0;   // first CTA warp of the set
     __device__ __forceinline__ void bar() const {
         if (NW == K7_WARPS) __syncthreads();
         else if (NW == 1) __syncwarp();
-        else asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(NT) : "memory");
+        else asm volatile("bar.sync %0, %1;" ::"r"(g), "r"(NT) : "memory");
     }
 };
 
@@ -283,7 +283,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
     constexpr u32 NT = NW * 32;
     constexpr bool CTA = NW == K7_WARPS;
     // bins / columns per thread: node <= S_CAP (CTA, 862 bins; 1024 group columns) or <= GCAP (group, 305)
-    constexpr u32 BPT = CTA ? 2 : NW == 1 ? 4 : 3;   // warp: node <= WCAP, 108 bins
+    constexpr u32 BPT = CTA ? 2 : NW == 1 ? 4 : 3;   // warp: node <= WCAP, 108 bins; double team: <= 2 GCAP, 513
     const u32 t = G.t, g = G.g, w = warp_id(), wg = w - G.w0, lane = lane_id();
     u64 *X = (rel & 1) ? S.B : S.A;
     u64 *Y = (rel & 1) ? S.A : S.B;
@@ -640,7 +640,8 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
     const u32 begin = *c->k7_begin;
     const u32 w = warp_id(), lane = lane_id();
     const Grp<K7_WARPS> CT{0u, threadIdx.x, 0u};
-    const Grp<GW> GG{w / GW, threadIdx.x % GT, (w / GW) * GW};
+    const Grp<GW> GG{1 + w / GW, threadIdx.x % GT, (w / GW) * GW};            // barriers 1..4
+    const Grp<2 * GW> GH{1 + NGRP + w / (2 * GW), threadIdx.x % (2 * GT), (w / (2 * GW)) * (2 * GW)};   // 5..6
     const Grp<1> GS{w, lane, w};
     for (u32 i = threadIdx.x; i < (u32)LSM_CAP; i += K7_THREADS) S.lsm[i] = 0;   // tickets read 0 until pushed
     if (c->k7_prof && threadIdx.x == 0) {
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
         if (threadIdx.x == 0) {
             S.task_idx = begin + atomicAdd(c->k7_next, 1u);
             if (S.task_idx < ntasks) S.task = c->k7[S.task_idx];
-            S.stot = 0; S.snext = 0; S.btot = 0; S.bnext = 0; S.big_active = NGRP;
+            S.stot = 0; S.snext = 0; S.btot = 0; S.bnext = 0; S.bnext2 = 0; S.big_active = NGRP;
         }
         __syncthreads();
         if (S.task_idx >= ntasks) break;
@@ -689,14 +690,32 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
                 if (threadIdx.x == 0) push_root(c, S, ent_make(0, M, 0));
                 __syncthreads();
             }
-            // nodes larger than a team's register capacity: the whole CTA, one level
+            // nodes larger than two teams' register capacity: the whole CTA, one level
             for (u32 i = 0; i < S.btot; ++i) {
                 const u32 e = S.lbig[i];
-                if (ent_m(e) > (u32)GCAP) {
+                if (ent_m(e) > (u32)(2 * GCAP)) {
                     __syncthreads();
                     if (threadIdx.x == 0) S.lbig[i] = 0;
                     node_step<K, K7_WARPS, MODE_NODE>(c, S, CT, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
                 }
+            }
+            // double teams (2 x GW warps) take the nodes of (GCAP, 2 GCAP] keys
+            for (;;) {
+                if (GH.t == 0) {
+                    u32 e = 0;
+                    for (;;) {
+                        const u32 i = atomicAdd(&S.bnext2, 1u);
+                        if (i >= S.btot) break;
+                        e = S.lbig[i];
+                        if (ent_m(e) > (u32)GCAP) break;
+                        e = 0;
+                    }
+                    S.cur[GH.w0] = e;
+                }
+                GH.bar();
+                const u32 e = S.cur[GH.w0];
+                if (!e) break;
+                node_step<K, 2 * GW, MODE_NODE>(c, S, GH, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
             }
             prof_mark(c, S, 4);
             // teams of GW warps take the nodes of (WCAP, GCAP] keys (their children go to the small
@@ -708,7 +727,8 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restr
                         const u32 i = atomicAdd(&S.bnext, 1u);
                         if (i >= S.btot) break;
                         e = S.lbig[i];
-                        if (e) break;
+                        if (e && ent_m(e) <= (u32)GCAP) break;
+                        e = 0;
                     }
                     S.cur[GG.w0] = e;
                 }
