@@ -160,6 +160,17 @@ static int k7_smem_bytes() { return (int)sizeof(K7Smem); }
 static int split_smem_bytes() { return (int)sizeof(SplitScatterSmem); }
 
 template <class K>
+static int k7_ctas_per_sm() {   // resident K7 CTAs per SM (persistent grid size)
+    static thread_local int v = 0;
+    if (!v) {
+        int b = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k7_kernel<K>, K7_THREADS, k7_smem_bytes()) != cudaSuccess || b < 1) b = 1;
+        v = b;
+    }
+    return v;
+}
+
+template <class K>
 static int configure_kernels() {
     static thread_local bool done = false;
     if (done) return PCF_OK;
@@ -428,7 +439,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             CK(cudaGetLastError());
             // K7 over every group produced so far (persistent grid; reads the task count on the device)
             tm.begin(PH_K7);
-            k7_kernel<K><<<nsm, K7_THREADS, k7_smem_bytes(), st>>>(d_ctx);
+            k7_kernel<K><<<nsm * k7_ctas_per_sm<K>(), K7_THREADS, k7_smem_bytes(), st>>>(d_ctx);
             k_k7_advance<<<1, 1, 0, st>>>(d_ctx);
             tm.end();
             CK(cudaGetLastError());

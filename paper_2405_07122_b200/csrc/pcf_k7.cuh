@@ -61,7 +61,7 @@ constexpr u32 NONE = 0xffffffffu;
 // destination entries: node-relative position | target (Y: recursing bucket,
 // A: leaf of one key -- final, B: larger leaf -- sorted into A next)
 constexpr u32 DEST_A = 0x4000u, DEST_B = 0x8000u, POS_MASK = 0x3fffu;
-static_assert(K7_WARPS * WCOLS >= CCOLS, "CTA view of the column arrays");
+constexpr int TCOLS = K7_WARPS * WCOLS > CCOLS ? K7_WARPS * WCOLS : CCOLS;   // CTA view of the column arrays
 static_assert((CCOLS * 2) % 4 == 0, "counter rows must stay 4-byte aligned");
 
 // node entry: pos (13 bits) | m << 13 (14 bits) | relative depth << 27
@@ -75,8 +75,8 @@ struct K7Smem {
     u64 B[S_CAP];
     u16 W[K7_WARPS * CCOLS];      // per-warp column counters -> destinations (rows of CCOLS);
                                   // a group's rows double as its u32 per-bin sample counts
-    u16 T16[K7_WARPS * WCOLS];    // bucket table of the current node (slices of the node's warps)
-    u16 hcol[K7_WARPS * WCOLS];   // bucket sizes of the current node (same slices)
+    u16 T16[TCOLS];    // bucket table of the current node (slices of the node's warps)
+    u16 hcol[TCOLS];   // bucket sizes of the current node (same slices)
     u16 LC[S_CAP];                // per position: bucket column of a B-leaf key, 0 otherwise
     u32 lsm[LSM_CAP];             // nodes <= WCAP keys (tickets; 0 = not yet pushed)
     u32 lbig[LBIG_CAP];           // nodes > WCAP keys
@@ -632,7 +632,7 @@ __device__ __forceinline__ void push_root(const DevCtx *c, K7Smem &S, u32 e) {
 }
 
 template <class K>
-__global__ void __launch_bounds__(K7_THREADS, 1) k7_kernel(const DevCtx *__restrict__ c) {
+__global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kernel(const DevCtx *__restrict__ c) {
     extern __shared__ __align__(16) unsigned char k7_smem_raw[];
     K7Smem &S = *reinterpret_cast<K7Smem *>(k7_smem_raw);
     if (*c->nan_flag) return;
