@@ -54,6 +54,8 @@ struct Caps {
     u64 bsum_cap;
 };
 
+constexpr u32 BND_MIN_LOG2 = 24;   // nodes of >= 2^20 keys get the gather-free digit table
+
 static Caps caps_for(u64 n) {
     Caps c;
     c.n = n;
@@ -61,7 +63,8 @@ static Caps caps_for(u64 n) {
     c.node_cap = (u32)(n / S_CAP + 2);
     // root tables + every oversized node: sum of 3*(m^{3/4}+2) over disjoint m > S_CAP
     // is <= 3*(n^{3/4} + n / S_CAP^{1/4} + 2*node_cap)  (S_CAP^{1/4} > 9.5)
-    c.arena_u32 = 3ull * ((u64)c.P + 2) + 3ull * (n * 2 / 19 + 2ull * c.node_cap) + 64;
+    c.arena_u32 = 3ull * ((u64)c.P + 2) + 3ull * (n * 2 / 19 + 2ull * c.node_cap) + 64
+                  + (u64)GMAX * ((n >> BND_MIN_LOG2) + 1);   // digit boundaries of large nodes
     c.k7_cap = (u32)std::min<u64>(n / 32 + 65536, 0xffffffffull);
     c.split_cap = (u32)(n / 1024 + 4096);
     c.items_cap = (u32)(n / S_CAP + 64);
@@ -171,11 +174,23 @@ static int k7_ctas_per_sm() {   // resident K7 CTAs per SM (persistent grid size
 }
 
 template <class K>
+static int count_ctas_per_sm() {
+    static thread_local int v = 0;
+    if (!v) {
+        int b = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_split_count<K>, CNT_THREADS, (int)sizeof(CountSmem)) != cudaSuccess || b < 1) b = 1;
+        v = b;
+    }
+    return v;
+}
+
+template <class K>
 static int configure_kernels() {
     static thread_local bool done = false;
     if (done) return PCF_OK;
     CK(cudaFuncSetAttribute(k7_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
+    CK(cudaFuncSetAttribute(k_split_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
     CK(cudaFuncSetAttribute(k8_merge<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
     done = true;
     return PCF_OK;
@@ -345,6 +360,13 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             g.T = g.cnt + (P + 2);
             g.H = g.T + (P + 2);
             arena_used += need_u32;
+            const u32 sh0 = choose_shift(P + 1, m);
+            if (m >= (1u << BND_MIN_LOG2) && arena_used + GMAX <= caps.arena_u32) {
+                g.bnd = arena + arena_used;
+                arena_used += GMAX;
+                g.bshift = sh0;
+                g.bG = (P + 1 + (1u << sh0) - 1) >> sh0;
+            }
             u32 idx = node_count++;
             CK(cudaMemcpyAsync(hc.nodes + idx, &g, sizeof g, cudaMemcpyHostToDevice, st));
             CK(cudaMemsetAsync(g.cnt, 0, need_u32 * 4, st));
@@ -376,7 +398,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             SplitTask s;
             memset(&s, 0, sizeof s);
             s.off = off; s.m = m; s.node = idx; s.jlo = 1; s.jhi = P + 2;
-            s.shift = choose_shift(P + 1, m);
+            s.shift = sh0;
             s.G = (P + 1 + (1u << s.shift) - 1) >> s.shift;
             s.src = src; s.dst = src == 1 ? 2 : 1;
             list.push_back(s);
@@ -414,7 +436,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             k_tile_map<<<nsm * 2, 256, 0, st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_COUNT);
-            k_split_count<K><<<tile_grid, SC_THREADS, 0, st>>>(d_ctx, cur);
+            k_split_count<K><<<nsm * count_ctas_per_sm<K>(), CNT_THREADS, (int)sizeof(CountSmem), st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_OTHER);
             k_scanp_partials<<<nsm * 2, SCAN_THREADS, 0, st>>>(d_ctx);

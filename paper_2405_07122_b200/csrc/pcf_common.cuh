@@ -205,6 +205,10 @@ struct GNode {
     u32 *T;         // [beta+2]  bucket table, 1-based
     u32 *H;         // [gamma+2] bucket sizes, 1-based (written by the split/K7 leaves)
     u64 digest_b;
+    // digit boundaries of the node's first split (large nodes; NULL otherwise):
+    // bnd[d] = first bin i whose digit (T[i] - 1) >> bshift is >= d, d in [1, bG)
+    u32 *bnd;
+    u32 bshift, bG;
 };
 
 // Work item of the smem-subtree kernel (K7).
@@ -293,6 +297,35 @@ struct DevCtx {
     u32 *l1_b, *l1_h;
     u64 l1_cap;
 };
+
+// ---------------------------------------------------------------- bulk copies (TMA, 1D) + mbarriers
+__device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64 *b, u32 n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// one arrival that also announces `tx` bytes of bulk copies completing on the barrier
+__device__ __forceinline__ void mbar_arrive_tx(u64 *b, u32 tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64 *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void named_bar(u32 id, u32 nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64 *b, u32 parity) {
+    asm volatile("{\n\t.reg .pred p;\n\tW%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra W%=;\n\t}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+// global -> shared bulk copy; dst, src 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, u32 bytes, u64 *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+// generic-proxy accesses of a shared buffer before it is refilled by the async proxy
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 constexpr u32 FLAG_SAMPLE_ALL = 2u;
 constexpr int K7_PROF_SLOTS = 16;

@@ -141,67 +141,183 @@ __device__ __forceinline__ u32 digit_of(u64 okey, const Model &md, const u32 *__
     return (j - jlo) >> shift;
 }
 
-// Counts of the digit (T[i(x)] - jlo) >> shift per tile (one CTA per tile of
-// SPLIT_TILE keys, the same warp-strided layout as the scatter), written to the
-// digit-major count matrix; every key's digit is cached (u16) for the scatter.
-// All SC_KPL key loads of a thread are issued before any use, then all T
-// gathers (memory-level parallelism: the pass is latency-bound otherwise).
-template <class K>
-__global__ void __launch_bounds__(SC_THREADS, 2) k_split_count(const DevCtx *__restrict__ c, u32 cur) {
-    __shared__ u32 hist[GMAX];
-    if (*c->nan_flag) return;
-    const RoundPlan pl = *c->plan;
-    const SplitTask *__restrict__ L = c->splits[cur];
-    u32 *__restrict__ C = c->cmat;
-    const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
-    if (tile >= pl.tiles) return;
-    const u32 s = c->tmap[tile];
-    const SplitTask st = L[s];
-    const u32 lt = tile - st.tile_begin;
+// Counts of the digit (T[i(x)] - jlo) >> shift per tile of SPLIT_TILE keys,
+// written to the digit-major count matrix; every key's digit is cached (u16)
+// for the scatter.  Persistent CTAs (grid-stride over the round's tiles); the
+// keys of the next tile stream into a second shared buffer by one bulk copy
+// (TMA, mbarrier completion) while the current tile is classified, so the pass
+// keeps HBM busy instead of waiting on each tile's loads.
+struct CountStage {
+    SplitTask st;
+    const u32 *T;
+    const u32 *bnd;                // digit boundaries (first split of a large node) or NULL
+    Model md;
+    u32 tile, head, direct, deg;   // head: index of the tile's first key in `in`; direct: no bulk copy
+    u32 node, beta;
+};
+// Digit lookup without gathers from T (the first split of a large node, where
+// T is large and the keys are random): bins are grouped in NCELL cells of
+// 2^cs bins; ct[c] = digit of the cell's first bin, and the digit of bin i is
+// ct[c] plus the boundaries bnd[] inside its cell at or below i.
+constexpr int NCELL = 8192;
+struct CountSmem {
+    u64 in[2][SPLIT_TILE + 2];
+    u32 hist[GMAX];
+    u32 bnd[GMAX];
+    u16 ct[NCELL + 1];
+    u32 tab_node, tab_cs;
+    CountStage meta[2];
+    u64 full[2], empty[2];
+};
+
+// Producer (one thread): metadata of `tile` and the bulk copy of its keys into stage `sg`.
+__device__ __forceinline__ void count_issue(const DevCtx *__restrict__ c, CountSmem &S, u32 cur, u32 tile, u32 sg) {
+    CountStage &m = S.meta[sg];
+    const SplitTask &st = c->splits[cur][c->tmap[tile]];
+    m.st = st;
     const GNode &g = c->nodes[st.node];
-    for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) hist[d] = 0;
-    const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
-    const bool deg = g.degenerate != 0;
-    __syncthreads();
-    if (deg) {
-        if (threadIdx.x == 0) hist[0] = k1 - k0;
+    m.T = g.T;
+    m.md = g.md;
+    m.deg = g.degenerate;
+    m.tile = tile;
+    m.node = st.node;
+    m.beta = g.beta;
+    m.bnd = (g.bnd && st.jlo == 1u && st.shift == g.bshift && st.G == g.bG) ? g.bnd : nullptr;
+    const u32 lt = tile - st.tile_begin;
+    const u32 k0 = lt * SPLIT_TILE, nt = min(st.m, k0 + SPLIT_TILE) - k0;
+    const u64 *base = c->buf[st.src];
+    const uintptr_t a = (uintptr_t)(base + st.off + k0);
+    const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + 8ull * nt + 15) & ~(uintptr_t)15;
+    m.head = (u32)((a - a0) >> 3);
+    m.direct = 0;
+    if (m.deg) {
+        mbar_arrive_tx(&S.full[sg], 0);
+    } else if (a0 < (uintptr_t)base || a1 > (uintptr_t)(base + c->n)) {   // edge of the buffer: plain loads
+        m.direct = 1;
+        mbar_arrive_tx(&S.full[sg], 0);
     } else {
-        const Model md = g.md;
-        const u64 *x = c->buf[st.src] + st.off;
-        const u32 *T = g.T;
-        u16 *dg = c->digs + st.off;
-        const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        const u32 r0 = k0 + w * SC_PER_WARP + lane;
-        u64 raw[SC_KPL];
-        u32 ix[SC_KPL];
-#pragma unroll
-        for (u32 q = 0; q < SC_KPL; ++q) { const u32 k = r0 + q * 32; raw[q] = k < k1 ? x[k] : x[k0]; }
-        u32 bad = 0;
-#pragma unroll
-        for (u32 q = 0; q < SC_KPL; ++q) {
-            bool ok;
-            ix[q] = interval_index_fast<K>(K::to_okey(raw[q]), md, ok);
-            bad |= ok ? 0u : (1u << q);
-        }
-        if (bad) {   // rare: keys in the fast path's guard band
-#pragma unroll
-            for (u32 q = 0; q < SC_KPL; ++q)
-                if (bad & (1u << q)) ix[q] = interval_index_exact(key_offset<K>(K::to_okey(raw[q]), md), md.r, md.betad);
-        }
-#pragma unroll
-        for (u32 q = 0; q < SC_KPL; ++q) ix[q] = __ldg(&T[ix[q]]);
-#pragma unroll
-        for (u32 q = 0; q < SC_KPL; ++q) {
-            const u32 k = r0 + q * 32;
-            if (k < k1) {
-                const u32 d = (ix[q] - st.jlo) >> st.shift;
-                dg[k] = (u16)d;
-                atomicAdd(&hist[d], 1u);
-            }
-        }
+        fence_proxy_async();
+        mbar_arrive_tx(&S.full[sg], (u32)(a1 - a0));
+        bulk_g2s(S.in[sg], (const void *)a0, (u32)(a1 - a0), &S.full[sg]);
+    }
+}
+
+constexpr int CNT_THREADS = SC_THREADS + 32;   // 12 consumer warps + 1 producer warp
+
+template <class K>
+__global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__restrict__ c, u32 cur) {
+    extern __shared__ __align__(16) unsigned char cnt_smem_raw[];
+    CountSmem &S = *reinterpret_cast<CountSmem *>(cnt_smem_raw);
+    if (*c->nan_flag) return;
+    const u32 ntiles = c->plan->tiles;
+    const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(&S.full[0], 1); mbar_init(&S.full[1], 1);
+        mbar_init(&S.empty[0], 1); mbar_init(&S.empty[1], 1);
+        mbar_init_fence();
+        S.tab_node = 0xffffffffu;
     }
     __syncthreads();
-    for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
+    if (w == SC_WARPS) {   // producer warp: metadata + bulk copy of each tile, two stages ahead of use
+        if (lane == 0) {
+            for (u32 it = 0;; ++it) {
+                const u32 tile = blockIdx.x + it * gridDim.x;
+                if (tile >= ntiles) break;
+                const u32 sg = it & 1u;
+                if (it >= 2) mbar_wait(&S.empty[sg], ((it - 2) >> 1) & 1u);
+                count_issue(c, S, cur, tile, sg);
+            }
+        }
+        return;
+    }
+    u32 *__restrict__ C = c->cmat;
+    for (u32 it = 0;; ++it) {
+        const u32 tile = blockIdx.x + it * gridDim.x;
+        if (tile >= ntiles) break;
+        const u32 sg = it & 1u;
+        mbar_wait(&S.full[sg], (it >> 1) & 1u);
+        const CountStage &m = S.meta[sg];
+        const SplitTask &st = m.st;
+        const u32 G = st.G;
+        for (u32 d = threadIdx.x; d < G; d += SC_THREADS) S.hist[d] = 0;
+        const u32 lt = tile - st.tile_begin;
+        const u32 k0 = lt * SPLIT_TILE, nt = min(st.m, k0 + SPLIT_TILE) - k0;
+        const bool tab = m.bnd != nullptr && !m.deg;
+        if (tab && S.tab_node != m.node) {   // (re)build the cell table of this node's first split
+            named_bar(1, SC_THREADS);
+            for (u32 d = threadIdx.x; d < G; d += SC_THREADS) S.bnd[d] = d ? m.bnd[d] : 0u;
+            u32 cs = 0;
+            while ((m.beta >> cs) >= (u32)NCELL) ++cs;
+            named_bar(1, SC_THREADS);
+            for (u32 cc = threadIdx.x; cc <= (u32)NCELL; cc += SC_THREADS) {
+                const u64 i0 = ((u64)cc << cs) + 1;   // first bin of the cell
+                u32 lo = 0, hi = G - 1;               // largest d in [0, G) with bnd[d] <= i0 (bnd[0] := 0)
+                while (lo < hi) { const u32 mid = (lo + hi + 1) >> 1; if ((u64)S.bnd[mid] <= i0) lo = mid; else hi = mid - 1; }
+                S.ct[cc] = (u16)lo;
+            }
+            if (threadIdx.x == 0) { S.tab_node = m.node; S.tab_cs = cs; }
+        }
+        named_bar(1, SC_THREADS);
+        if (m.deg) {
+            if (threadIdx.x == 0) S.hist[0] = nt;
+        } else {
+            const Model md = m.md;
+            const u32 *T = m.T;
+            const u32 jlo = st.jlo, shift = st.shift;
+            const u64 *in = S.in[sg] + m.head;
+            const u64 *gx = c->buf[st.src] + st.off + k0;
+            const bool direct = m.direct != 0;
+            u16 *dg = c->digs + st.off + k0;
+            const u32 r0 = w * SC_PER_WARP + lane;
+            u64 raw[SC_KPL];
+            u32 ix[SC_KPL];
+#pragma unroll
+            for (u32 q = 0; q < SC_KPL; ++q) {
+                const u32 k = r0 + q * 32;
+                const u32 kk = k < nt ? k : 0u;
+                raw[q] = direct ? gx[kk] : in[kk];
+            }
+            u32 bad = 0;
+#pragma unroll
+            for (u32 q = 0; q < SC_KPL; ++q) {
+                bool ok;
+                ix[q] = interval_index_fast<K>(K::to_okey(raw[q]), md, ok);
+                bad |= ok ? 0u : (1u << q);
+            }
+            if (bad) {   // rare: keys in the fast path's guard band
+#pragma unroll
+                for (u32 q = 0; q < SC_KPL; ++q)
+                    if (bad & (1u << q)) ix[q] = interval_index_exact(key_offset<K>(K::to_okey(raw[q]), md), md.r, md.betad);
+            }
+            if (tab) {
+                const u32 cs = S.tab_cs;
+#pragma unroll
+                for (u32 q = 0; q < SC_KPL; ++q) {
+                    const u32 i = ix[q], cc = (i - 1u) >> cs;
+                    u32 d = S.ct[cc];
+                    const u32 d1 = S.ct[cc + 1];
+                    while (d < d1 && S.bnd[d + 1] <= i) ++d;
+                    ix[q] = d;
+                }
+            } else {
+#pragma unroll
+                for (u32 q = 0; q < SC_KPL; ++q) ix[q] = (__ldg(&T[ix[q]]) - jlo) >> shift;
+            }
+#pragma unroll
+            for (u32 q = 0; q < SC_KPL; ++q) {
+                const u32 k = r0 + q * 32;
+                if (k < nt) {
+                    const u32 d = ix[q];
+                    dg[k] = (u16)d;
+                    atomicAdd(&S.hist[d], 1u);
+                }
+            }
+        }
+        named_bar(1, SC_THREADS);
+        for (u32 d = threadIdx.x; d < G; d += SC_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = S.hist[d];
+        named_bar(1, SC_THREADS);
+        if (threadIdx.x == 0) mbar_arrive(&S.empty[sg]);   // stage sg (keys, metadata) is free
+    }
 }
 
 // --- exclusive scan of a u32 array (3 phases)
@@ -413,13 +529,21 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_fit_final(const DevCtx *__rest
     u32 total;
     u32 e = block_excl_scan_1024(s, wsum, total) + bsum[blockIdx.x];
     u64 db = 0;
+    u32 *bnd = g.bnd;
+    const u32 bsh = g.bshift;
 #pragma unroll
     for (int k = 0; k < SCAN_ITEMS; ++k) {
+        const u32 eprev = e;
         e += v[k];
         if (base + k < n) {
             const u64 i = base + k + 1;   // 1-based interval index
             in[base + k] = e;
-            g.T[i] = bucket_of(e, g.alpha, g.gamma);
+            const u32 Ti = bucket_of(e, g.alpha, g.gamma);
+            g.T[i] = Ti;
+            if (bnd) {   // digit boundaries of the first split: digit (T - 1) >> bshift rises at bin i
+                const u32 d1 = (Ti - 1u) >> bsh, d0 = (bucket_of(eprev, g.alpha, g.gamma) - 1u) >> bsh;
+                for (u32 d = d0 + 1; d <= d1; ++d) bnd[d] = (u32)i;
+            }
             if (logging) db += digest_term(i, e);
             if (copy_l1 && i - 1 < c->l1_cap) c->l1_b[i - 1] = e;
         }
