@@ -294,9 +294,8 @@ __global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__
 #pragma unroll
                 for (u32 q = 0; q < SC_KPL; ++q) {
                     const u32 i = ix[q], cc = (i - 1u) >> cs;
-                    u32 d = S.ct[cc];
-                    const u32 d1 = S.ct[cc + 1];
-                    while (d < d1 && S.bnd[d + 1] <= i) ++d;
+                    u32 d = S.ct[cc], d1 = S.ct[cc + 1];   // largest d in [d, d1] with bnd[d] <= i
+                    while (d < d1) { const u32 mid = (d + d1 + 1) >> 1; if (S.bnd[mid] <= i) d = mid; else d1 = mid - 1; }
                     ix[q] = d;
                 }
             } else {
@@ -853,11 +852,12 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
         __syncthreads();
         // all threads: reserve the K7 slots of the split's runs at once, write the tasks
         const u32 nr = nrun;
-        if (threadIdx.x == 0 && nr) {
+        {   // keys of the runs (block reduction), K7 slots reserved at once
             u32 tk = 0;
-            for (u32 r = 0; r < nr; ++r) tk += rk[r];
-            rbase = atomicAdd(c->k7_count, nr);
-            atomicAdd(c->k7_keys, (unsigned long long)tk);
+            for (u32 r = threadIdx.x; r < nr; r += TG_THREADS) tk += rk[r];
+            for (int o = 16; o > 0; o >>= 1) tk += __shfl_xor_sync(0xffffffffu, tk, o);
+            if (lane == 0 && tk) atomicAdd(c->k7_keys, (unsigned long long)tk);
+            if (threadIdx.x == 0 && nr) rbase = atomicAdd(c->k7_count, nr);
         }
         __syncthreads();
         for (u32 r = threadIdx.x; r < nr; r += TG_THREADS) {
