@@ -72,7 +72,7 @@ __device__ __forceinline__ u32 ent_rel(u32 e) { return e >> 27; }
 
 struct K7Smem {
     u64 A[S_CAP];
-    u64 B[S_CAP];
+    u64 B[S_CAP + 2];             // + 2: the next task's bulk copy may start 8 bytes early
     u16 W[K7_WARPS * CCOLS];      // per-warp column counters -> destinations (rows of CCOLS);
                                   // a group's rows double as its u32 per-bin sample counts
     u16 T16[TCOLS];    // bucket table of the current node (slices of the node's warps)
@@ -90,8 +90,10 @@ struct K7Smem {
     u32 nbl[K7_WARPS];
     u32 top[K7_WARPS], cur[K7_WARPS];
     u32 stot, snext, btot, bnext, bnext2, big_active;
-    u32 task_idx;
-    K7Task task;
+    u32 task_idx, nidx;
+    K7Task task, ntask;
+    u32 lhead, ldirect;           // the loaded task: first key at B[lhead]; ldirect: not bulk-copied
+    u64 tbar;                     // mbarrier of the task bulk copy
     Model gmd;
     const u32 *gT;
     u32 *gH;
@@ -620,6 +622,25 @@ __device__ __forceinline__ void store_task(const K7Smem &S, u64 *dst, u32 m) {
 }
 
 // ------------------------------------------------------------------ the kernel
+// Bulk copy of the raw keys of task t into B (issued while the previous task
+// is stored).  The copy covers the 16-byte aligned superset of the task; a task
+// whose superset leaves the buffer is loaded by plain loads instead.
+__device__ __forceinline__ void k7_issue(const DevCtx *c, K7Smem &S, const K7Task &t) {
+    const u64 *base = c->buf[t.src];
+    const uintptr_t a = (uintptr_t)(base + t.off);
+    const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + 8ull * t.size + 15) & ~(uintptr_t)15;
+    S.lhead = (u32)((a - a0) >> 3);
+    if (a0 < (uintptr_t)base || a1 > (uintptr_t)(base + c->n)) {
+        S.ldirect = 1;
+        mbar_arrive_tx(&S.tbar, 0);
+    } else {
+        S.ldirect = 0;
+        fence_proxy_async();
+        mbar_arrive_tx(&S.tbar, (u32)(a1 - a0));
+        bulk_g2s(S.B, (const void *)a0, (u32)(a1 - a0), &S.tbar);
+    }
+}
+
 // Node entry of size m from the CTA phases: big list (> WCAP keys) or small list.
 __device__ __forceinline__ void push_root(const DevCtx *c, K7Smem &S, u32 e) {
     if (ent_m(e) > (u32)WCAP) {
@@ -648,21 +669,51 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
         for (int i = 0; i < K7_PROF_SLOTS; ++i) S.prof[i] = 0;
         S.prof_t = clock64();
     }
-    for (;;) {
+    if (threadIdx.x == 0) {   // first task: claim + bulk copy
+        mbar_init(&S.tbar, 1);
+        mbar_init_fence();
+        S.nidx = begin + atomicAdd(c->k7_next, 1u);
+        if (S.nidx < ntasks) { S.ntask = c->k7[S.nidx]; k7_issue(c, S, S.ntask); }
+    }
+    __syncthreads();
+    for (u32 it = 0;; ++it) {
         if (threadIdx.x == 0) {
-            S.task_idx = begin + atomicAdd(c->k7_next, 1u);
-            if (S.task_idx < ntasks) S.task = c->k7[S.task_idx];
+            S.task_idx = S.nidx;
+            S.task = S.ntask;
             S.stot = 0; S.snext = 0; S.btot = 0; S.bnext = 0; S.bnext2 = 0; S.big_active = NGRP;
         }
         __syncthreads();
         if (S.task_idx >= ntasks) break;
         prof_mark(c, S, 0);
+        u32 nclaim = 0;
+        if (threadIdx.x == 0) nclaim = begin + atomicAdd(c->k7_next, 1u);   // used when this task is done
         const K7Task task = S.task;
-        const u64 *src = c->buf[task.src] + task.off;
         u64 *gout = c->buf[2] + task.off;
         const u32 M = task.size;
         const bool sort_task = task.kind == K7_SORT || (task.kind == K7_NODE && M < c->tau);
-        const bool nan_here = load_task<K>(sort_task ? S.B : S.A, src, M);
+        u64 *dst = sort_task ? S.B : S.A;
+        bool nan_here = false;
+        mbar_wait(&S.tbar, it & 1u);
+        if (S.ldirect) {
+            nan_here = load_task<K>(dst, c->buf[task.src] + task.off, M);
+        } else {   // raw keys at B[lhead + i] -> ordered keys at dst[i]
+            const u32 hd = S.lhead;
+            u64 r[KPT];
+#pragma unroll
+            for (int q = 0; q < KPT; ++q) {
+                const u32 i = threadIdx.x + q * K7_THREADS;
+                r[q] = i < M ? S.B[hd + i] : 0ull;
+            }
+            if (sort_task && hd) __syncthreads();   // in-place shift
+#pragma unroll
+            for (int q = 0; q < KPT; ++q) {
+                const u32 i = threadIdx.x + q * K7_THREADS;
+                if (i < M) {
+                    if (K::is_f64) nan_here |= (r[q] & 0x7fffffffffffffffull) > 0x7ff0000000000000ull;
+                    dst[i] = K::to_okey(r[q]);
+                }
+            }
+        }
         if (K::is_f64 && task.level == 1 && __syncthreads_or(nan_here)) {
             if (threadIdx.x == 0) atomicOr(c->nan_flag, 1u);
             return;
@@ -769,6 +820,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
             }
             __syncthreads();
             prof_mark(c, S, 5);
+        }
+        if (threadIdx.x == 0) {   // B is free: the next task streams in while this one is stored
+            S.nidx = nclaim;
+            if (nclaim < ntasks) { S.ntask = c->k7[nclaim]; k7_issue(c, S, S.ntask); }
         }
         store_task<K>(S, gout, M);
         prof_mark(c, S, 13);
