@@ -192,6 +192,7 @@ static int configure_kernels() {
     CK(cudaFuncSetAttribute(k_split_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
     CK(cudaFuncSetAttribute(k8_merge<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
+    CK(cudaFuncSetAttribute(k8_blocksort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_SORT_SMEM));
     done = true;
     return PCF_OK;
 }
@@ -510,7 +511,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
                 const u32 nblk = (u32)((m + K8_TILE - 1) / K8_TILE);
                 tm.begin(PH_K8);
                 k8_check<<<(u32)std::min<u64>(4ull * nsm, (m + 255) / 256), 256, 0, st>>>(src, m, flag);
-                k8_blocksort<K><<<nblk, K8_THREADS, 0, st>>>(src, dst0, bo, m, flag);
+                k8_blocksort<K><<<nblk, K8_THREADS, K8_SORT_SMEM, st>>>(src, dst0, bo, m, flag);
                 u64 *cur = dst0;
                 for (u64 w = K8_TILE; w < m; w *= 2) {
                     u64 *nxt = cur == bo ? bt : bo;

@@ -16,7 +16,8 @@ namespace pcf {
 constexpr int K8_THREADS = 512;
 constexpr int K8_TILE = 4096;
 constexpr int K8_IPT = K8_TILE / K8_THREADS;   // 8
-constexpr int K8_MERGE_SMEM = 2 * K8_TILE * 8;
+constexpr int K8_MERGE_SMEM = K8_TILE * 8;
+constexpr int K8_SORT_SMEM = 2 * K8_TILE * 8;
 
 // flag[0] = 1 if the bucket holds two different keys; flag[1] = first key
 __global__ void __launch_bounds__(256) k8_check(const u64 *__restrict__ src, u64 m, u32 *__restrict__ flag) {
@@ -27,32 +28,88 @@ __global__ void __launch_bounds__(256) k8_check(const u64 *__restrict__ src, u64
     if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
+// Compare-exchange of two registers (ascending).
+__device__ __forceinline__ void k8_cx(u64 &a, u64 &b) { const u64 x = a < b ? a : b; b = a < b ? b : a; a = x; }
+
+// Merge-path split inside shared memory: number of keys taken from A (length
+// la) among the first d outputs of merge(A, B) (A first among equal keys).
+__device__ __forceinline__ u32 k8_split(const u64 *A, u32 la, const u64 *B, u32 lb, u32 d) {
+    u32 lo = d > lb ? d - lb : 0, hi = d < la ? d : la;
+    while (lo < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (A[mid] <= B[d - 1 - mid]) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// K8_IPT consecutive outputs of merge(A, B) starting at A[ia], B[ib] into o[].
+__device__ __forceinline__ void k8_merge_seq(const u64 *A, u32 la, const u64 *B, u32 lb, u32 ia, u32 ib, u64 (&o)[K8_IPT]) {
+    u64 xa = ia < la ? A[ia] : ~0ull, xb = ib < lb ? B[ib] : ~0ull;
+#pragma unroll
+    for (int k = 0; k < K8_IPT; ++k) {
+        const bool ta = ib >= lb || (ia < la && xa <= xb);
+        o[k] = ta ? xa : xb;
+        if (ta) { ++ia; xa = ia < la ? A[ia] : ~0ull; }
+        else { ++ib; xb = ib < lb ? B[ib] : ~0ull; }
+    }
+}
+
+// Sorted K8_TILE-key tiles: 8 keys per thread sorted by a register network
+// (Batcher odd-even merge sort, 19 comparators), then log2(K8_TILE / 8) levels
+// of merge-path merges of sorted runs through shared memory (each thread
+// emits 8 consecutive outputs).  Padding with the largest ordered key sorts last.
 template <class K>
 __global__ void __launch_bounds__(K8_THREADS) k8_blocksort(const u64 *__restrict__ src, u64 *__restrict__ dst,
                                                           u64 *__restrict__ out, u64 m, const u32 *__restrict__ flag) {
-    __shared__ u64 a[K8_TILE];
+    extern __shared__ __align__(16) u64 k8_bs[];   // 2 * K8_TILE keys
+    u64 *a = k8_bs, *b = k8_bs + K8_TILE;
     const u64 base = (u64)blockIdx.x * K8_TILE;
     const u32 n = (u32)min((u64)K8_TILE, m - base);
     if (*flag == 0) {   // all keys equal: already sorted, final position
         for (u32 k = threadIdx.x; k < n; k += K8_THREADS) out[base + k] = src[base + k];
         return;
     }
-    for (u32 k = threadIdx.x; k < K8_TILE; k += K8_THREADS) a[k] = k < n ? K::to_okey(src[base + k]) : ~0ull;
-    __syncthreads();
-    // full bitonic sort (padding = max key sorts to the end)
-    for (u32 k = 2; k <= (u32)K8_TILE; k <<= 1) {
-        for (u32 j = k >> 1; j > 0; j >>= 1) {
+    {
+        u64 v[K8_IPT];
 #pragma unroll
-            for (u32 t = threadIdx.x; t < K8_TILE / 2; t += K8_THREADS) {
-                const u32 lo = ((t / j) * 2 * j) + (t % j), hi = lo + j;
-                const bool up = (lo & k) == 0;
-                const u64 x = a[lo], y = a[hi];
-                if ((x > y) == up) { a[lo] = y; a[hi] = x; }
-            }
-            __syncthreads();
+        for (int j = 0; j < K8_IPT; ++j) {
+            const u32 k = threadIdx.x + j * K8_THREADS;
+            v[j] = k < n ? src[base + k] : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < K8_IPT; ++j) {
+            const u32 k = threadIdx.x + j * K8_THREADS;
+            a[k] = k < n ? K::to_okey(v[j]) : ~0ull;
         }
     }
-    for (u32 k = threadIdx.x; k < n; k += K8_THREADS) dst[base + k] = K::from_okey(a[k]);
+    __syncthreads();
+    const u32 t0 = threadIdx.x * K8_IPT;
+    u64 r[K8_IPT];
+#pragma unroll
+    for (int k = 0; k < K8_IPT; ++k) r[k] = a[t0 + ((k + threadIdx.x) & (K8_IPT - 1))];   // rotated: fewer bank conflicts
+    // Batcher odd-even merge sort of 8
+    k8_cx(r[0], r[1]); k8_cx(r[2], r[3]); k8_cx(r[4], r[5]); k8_cx(r[6], r[7]);
+    k8_cx(r[0], r[2]); k8_cx(r[1], r[3]); k8_cx(r[4], r[6]); k8_cx(r[5], r[7]);
+    k8_cx(r[1], r[2]); k8_cx(r[5], r[6]);
+    k8_cx(r[0], r[4]); k8_cx(r[1], r[5]); k8_cx(r[2], r[6]); k8_cx(r[3], r[7]);
+    k8_cx(r[2], r[4]); k8_cx(r[3], r[5]);
+    k8_cx(r[1], r[2]); k8_cx(r[3], r[4]); k8_cx(r[5], r[6]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K8_IPT; ++k) a[t0 + k] = r[k];
+    __syncthreads();
+    u64 *sa = a, *sb = b;
+    for (u32 run = K8_IPT; run < (u32)K8_TILE; run <<= 1) {
+        const u32 p0 = (t0 / (2 * run)) * (2 * run), d = t0 - p0;
+        const u64 *A = sa + p0, *B = sa + p0 + run;
+        const u32 ia = k8_split(A, run, B, run, d);
+        k8_merge_seq(A, run, B, run, ia, d - ia, r);
+#pragma unroll
+        for (int k = 0; k < K8_IPT; ++k) sb[t0 + k] = r[k];
+        __syncthreads();
+        u64 *tmp = sa; sa = sb; sb = tmp;
+    }
+    for (u32 k = threadIdx.x; k < n; k += K8_THREADS) dst[base + k] = K::from_okey(sa[k]);
 }
 
 // Merge-path split of output tile t (diagonal t*K8_TILE inside its run pair):
@@ -78,8 +135,8 @@ __global__ void k8_partition(const u64 *__restrict__ src, u64 m, u64 width, u32 
 template <class K>
 __global__ void __launch_bounds__(K8_THREADS) k8_merge(const u64 *__restrict__ src, u64 *__restrict__ dst, u64 m, u64 width,
                                                       const u32 *__restrict__ sp, const u32 *__restrict__ flag) {
-    extern __shared__ __align__(16) u64 k8_smem[];   // 2 * K8_TILE keys (dynamic: > 48 KB)
-    u64 *sa = k8_smem, *so = k8_smem + K8_TILE;
+    extern __shared__ __align__(16) u64 k8_smem[];   // K8_TILE input keys
+    u64 *sa = k8_smem;
     if (*flag == 0) return;
     const u32 t = blockIdx.x;
     const u64 o0 = (u64)t * K8_TILE;
@@ -92,30 +149,29 @@ __global__ void __launch_bounds__(K8_THREADS) k8_merge(const u64 *__restrict__ s
     const u32 ib0 = (u32)(d0 - ia0), ib1 = (u32)(d1 - ia1);
     const u32 la = ia1 - ia0, lb = ib1 - ib0, tot = la + lb;
     const u64 *A = src + pair0, *B = src + pair0 + na;
-    for (u32 k = threadIdx.x; k < la; k += K8_THREADS) sa[k] = K::to_okey(A[ia0 + k]);
-    for (u32 k = threadIdx.x; k < lb; k += K8_THREADS) sa[la + k] = K::to_okey(B[ib0 + k]);
-    __syncthreads();
-    // per thread: K8_IPT consecutive outputs from its own merge-path split
-    const u32 dd = min(threadIdx.x * K8_IPT, tot);
-    u32 lo = dd > lb ? dd - lb : 0, hi = dd < la ? dd : la;
-    while (lo < hi) {
-        const u32 mid = (lo + hi) >> 1;
-        if (sa[mid] <= sa[la + dd - 1 - mid]) lo = mid + 1; else hi = mid;
-    }
-    u32 ia = lo, ib = dd - lo;
+    {   // all loads of a thread in flight at once, then the stores to shared memory
+        u64 v[K8_IPT];
 #pragma unroll
-    for (int k = 0; k < K8_IPT; ++k) {
-        if (dd + k < tot) {
-            bool takeA;
-            if (ia >= la) takeA = false;
-            else if (ib >= lb) takeA = true;
-            else takeA = sa[ia] <= sa[la + ib];
-            so[dd + k] = takeA ? sa[ia++] : sa[la + ib++];
+        for (int j = 0; j < K8_IPT; ++j) {
+            const u32 k = threadIdx.x + j * K8_THREADS;
+            v[j] = k < la ? A[ia0 + k] : k < tot ? B[ib0 + (k - la)] : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < K8_IPT; ++j) {
+            const u32 k = threadIdx.x + j * K8_THREADS;
+            if (k < tot) sa[k] = K::to_okey(v[j]);
         }
     }
     __syncthreads();
-    u64 *out = dst + o0;
-    for (u32 k = threadIdx.x; k < tot; k += K8_THREADS) out[k] = K::from_okey(so[k]);
+    // per thread: K8_IPT consecutive outputs from its own merge-path split, stored
+    // straight from registers (a warp writes 32 x 64 contiguous bytes)
+    const u32 dd = min(threadIdx.x * K8_IPT, tot);
+    const u32 ia = k8_split(sa, la, sa + la, lb, dd);
+    u64 r[K8_IPT];
+    k8_merge_seq(sa, la, sa + la, lb, ia, dd - ia, r);
+    u64 *outp = dst + o0 + dd;
+#pragma unroll
+    for (int k = 0; k < K8_IPT; ++k) if (dd + k < tot) outp[k] = K::from_okey(r[k]);
 }
 
 }  // namespace pcf
