@@ -516,7 +516,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
                 for (u64 w = K8_TILE; w < m; w *= 2) {
                     u64 *nxt = cur == bo ? bt : bo;
                     k8_partition<K><<<(nblk + 255) / 256, 256, 0, st>>>(cur, m, w, nblk, k8_sp, flag);
-                    k8_merge<K><<<nblk, K8_THREADS, K8_MERGE_SMEM, st>>>(cur, nxt, m, w, k8_sp, flag);
+                    k8_merge<K><<<nblk, K8_THREADS, K8_MERGE_SMEM, st>>>(cur, nxt, m, w, k8_sp, flag, 2 * w >= m ? 1u : 0u);
                     cur = nxt;
                     launches += 2;
                 }

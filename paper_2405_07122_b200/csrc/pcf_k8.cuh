@@ -5,7 +5,8 @@
 // places the merge-path split of each output tile (k8_partition, one thread
 // per tile), then merges tile by tile through shared memory with coalesced
 // loads and stores (k8_merge).  Keys are compared as ordered u64 (IEEE
-// totalOrder for f64, reading R11).  A bucket whose keys are all equal
+// totalOrder for f64, reading R11); the block sort writes ordered keys, the
+// passes keep them, and the last pass writes the raw keys.  A bucket whose keys are all equal
 // (k8_check; e.g. the duplicate-heavy bucket of config c3) is already sorted:
 // its tiles are copied straight to the output and the passes are skipped.
 #pragma once
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(K8_THREADS) k8_blocksort(const u64 *__restrict
         __syncthreads();
         u64 *tmp = sa; sa = sb; sb = tmp;
     }
-    for (u32 k = threadIdx.x; k < n; k += K8_THREADS) dst[base + k] = K::from_okey(sa[k]);
+    for (u32 k = threadIdx.x; k < n; k += K8_THREADS) dst[base + k] = m <= (u64)K8_TILE ? K::from_okey(sa[k]) : sa[k];
 }
 
 // Merge-path split of output tile t (diagonal t*K8_TILE inside its run pair):
@@ -125,16 +126,16 @@ __global__ void k8_partition(const u64 *__restrict__ src, u64 m, u64 width, u32 
     const u64 d = o0 - pair0;
     const u64 *A = src + pair0, *B = src + pair0 + na;
     u64 lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
-    while (lo < hi) {   // first i with A[i] > B[d-1-i]  (A first among equal keys)
+    while (lo < hi) {   // first i with A[i] > B[d-1-i]  (A first among equal keys; ordered keys)
         const u64 mid = (lo + hi) >> 1;
-        if (K::to_okey(A[mid]) <= K::to_okey(B[d - 1 - mid])) lo = mid + 1; else hi = mid;
+        if (A[mid] <= B[d - 1 - mid]) lo = mid + 1; else hi = mid;
     }
     sp[t] = (u32)lo;
 }
 
 template <class K>
 __global__ void __launch_bounds__(K8_THREADS) k8_merge(const u64 *__restrict__ src, u64 *__restrict__ dst, u64 m, u64 width,
-                                                      const u32 *__restrict__ sp, const u32 *__restrict__ flag) {
+                                                      const u32 *__restrict__ sp, const u32 *__restrict__ flag, u32 last) {
     extern __shared__ __align__(16) u64 k8_smem[];   // K8_TILE input keys
     u64 *sa = k8_smem;
     if (*flag == 0) return;
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(K8_THREADS) k8_merge(const u64 *__restrict__ s
 #pragma unroll
         for (int j = 0; j < K8_IPT; ++j) {
             const u32 k = threadIdx.x + j * K8_THREADS;
-            if (k < tot) sa[k] = K::to_okey(v[j]);
+            if (k < tot) sa[k] = v[j];
         }
     }
     __syncthreads();
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(K8_THREADS) k8_merge(const u64 *__restrict__ s
     k8_merge_seq(sa, la, sa + la, lb, ia, dd - ia, r);
     u64 *outp = dst + o0 + dd;
 #pragma unroll
-    for (int k = 0; k < K8_IPT; ++k) if (dd + k < tot) outp[k] = K::from_okey(r[k]);
+    for (int k = 0; k < K8_IPT; ++k) if (dd + k < tot) outp[k] = last ? K::from_okey(r[k]) : r[k];
 }
 
 }  // namespace pcf
