@@ -667,15 +667,18 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
     // dsrc >> 21 and digit, contiguous in the stage) depends on the order the
     // shared-memory atomics of one instruction were served in: check for an
     // inversion, and only then re-rank the groups by source index.
+    // (Fused with the write-out: if an inversion is found, every position of the
+    // tile is written again from the exact ranks below.)
     bool inv = false;
-    for (u32 i = threadIdx.x + 1; i < ntile; i += SC_THREADS) {
-        const u32 a = S.dsrc[i - 1], b = S.dsrc[i];
-        inv |= (a >> 21) == (b >> 21) && (a & 0xffffu) == (b & 0xffffu) && (a >> 16) > (b >> 16);
+    for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) {
+        const u32 b = S.dsrc[i];
+        if (i > 0) {
+            const u32 a = S.dsrc[i - 1];
+            inv |= (a >> 21) == (b >> 21) && (a & 0xffffu) == (b & 0xffffu) && (a >> 16) > (b >> 16);
+        }
+        y[S.goff[b & 0xffffu] + i] = S.buf[i];
     }
-    if (!__syncthreads_or(inv)) {
-        for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) y[S.goff[S.dsrc[i] & 0xffffu] + i] = S.buf[i];
-        return;
-    }
+    if (!__syncthreads_or(inv)) return;
     for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) {
         const u32 e = S.dsrc[i];
         const u32 d = e & 0xffffu;
