@@ -577,8 +577,7 @@ struct SplitScatterSmem {
 template <class K>
 __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c, SplitScatterSmem &S, const SplitTask &st,
                                                    u32 lt, const u32 *__restrict__ P) {
-    const GNode &g = c->nodes[st.node];
-    if (g.degenerate) return;
+    const u32 deg = c->nodes[st.node].degenerate;   // checked after the tile's loads are issued
     const u64 *x = c->buf[st.src] + st.off;
     u64 *y = c->buf[st.dst] + st.off;
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -597,6 +596,15 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
         key[q] = v ? x[k] : 0ull;
         pk[q] = v ? (u32)dg[k] : 0xffffffffu;
     }
+    // destinations of this tile's digit runs (scanned count matrix), needed after the scan
+    constexpr u32 PPER = (GMAX + SC_THREADS - 1) / SC_THREADS;
+    u32 pv[PPER];
+#pragma unroll
+    for (u32 i = 0; i < PPER; ++i) {
+        const u32 d = threadIdx.x * PPER + i;
+        pv[i] = d < G ? P[st.cbase + (u64)d * st.ntiles + lt] : 0u;
+    }
+    if (deg) return;   // uniform: the whole CTA leaves
     __syncwarp();
     // rank inside the warp: one atomicAdd per key on the warp's u16 counter of its digit
 #pragma unroll
@@ -645,7 +653,7 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
             const u32 d = b0 + i;
             if (d < G) {
                 S.tstart[d] = run;
-                if (v[i]) S.goff[d] = P[st.cbase + (u64)d * st.ntiles + lt] - (u32)st.mbase - run;
+                if (v[i]) S.goff[d] = pv[i] - (u32)st.mbase - run;
                 run += v[i];
             }
         }
