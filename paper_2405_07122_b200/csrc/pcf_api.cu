@@ -437,7 +437,8 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             k_tile_map<<<nsm * 2, 256, 0, st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_COUNT);
-            k_split_count<K><<<nsm * count_ctas_per_sm<K>(), CNT_THREADS, (int)sizeof(CountSmem), st>>>(d_ctx, cur);
+            if (n <= (1ull << 25)) k_split_count_tile<K><<<tile_grid, SC_THREADS, 0, st>>>(d_ctx, cur);
+            else k_split_count<K><<<nsm * count_ctas_per_sm<K>(), CNT_THREADS, (int)sizeof(CountSmem), st>>>(d_ctx, cur);
             tm.end();
             tm.begin(PH_OTHER);
             k_scanp_partials<<<nsm * 2, SCAN_THREADS, 0, st>>>(d_ctx);

@@ -319,6 +319,66 @@ __global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__
     }
 }
 
+// One CTA per tile (no pipeline): for rounds of few tiles per SM (n <= 2^25), where
+// the persistent kernel's pipeline never fills.  Same outputs as k_split_count.
+template <class K>
+__global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_tile(const DevCtx *__restrict__ c, u32 cur) {
+    __shared__ u32 hist[GMAX];
+    if (*c->nan_flag) return;
+    const RoundPlan pl = *c->plan;
+    const SplitTask *__restrict__ L = c->splits[cur];
+    u32 *__restrict__ C = c->cmat;
+    const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
+    if (tile >= pl.tiles) return;
+    const u32 s = c->tmap[tile];
+    const SplitTask st = L[s];
+    const u32 lt = tile - st.tile_begin;
+    const GNode &g = c->nodes[st.node];
+    for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) hist[d] = 0;
+    const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
+    const bool deg = g.degenerate != 0;
+    __syncthreads();
+    if (deg) {
+        if (threadIdx.x == 0) hist[0] = k1 - k0;
+    } else {
+        const Model md = g.md;
+        const u64 *x = c->buf[st.src] + st.off;
+        const u32 *T = g.T;
+        u16 *dg = c->digs + st.off;
+        const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const u32 r0 = k0 + w * SC_PER_WARP + lane;
+        u64 raw[SC_KPL];
+        u32 ix[SC_KPL];
+#pragma unroll
+        for (u32 q = 0; q < SC_KPL; ++q) { const u32 k = r0 + q * 32; raw[q] = k < k1 ? x[k] : x[k0]; }
+        u32 bad = 0;
+#pragma unroll
+        for (u32 q = 0; q < SC_KPL; ++q) {
+            bool ok;
+            ix[q] = interval_index_fast<K>(K::to_okey(raw[q]), md, ok);
+            bad |= ok ? 0u : (1u << q);
+        }
+        if (bad) {   // rare: keys in the fast path's guard band
+#pragma unroll
+            for (u32 q = 0; q < SC_KPL; ++q)
+                if (bad & (1u << q)) ix[q] = interval_index_exact(key_offset<K>(K::to_okey(raw[q]), md), md.r, md.betad);
+        }
+#pragma unroll
+        for (u32 q = 0; q < SC_KPL; ++q) ix[q] = __ldg(&T[ix[q]]);
+#pragma unroll
+        for (u32 q = 0; q < SC_KPL; ++q) {
+            const u32 k = r0 + q * 32;
+            if (k < k1) {
+                const u32 d = (ix[q] - st.jlo) >> st.shift;
+                dg[k] = (u16)d;
+                atomicAdd(&hist[d], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
+}
+
 // --- exclusive scan of a u32 array (3 phases)
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_ITEMS = 4;
