@@ -59,6 +59,19 @@ def dist_setup(n_gpus):
     return rank, world, local
 
 
+def max_over_ranks(value, world, device=None):
+    """Max of a per-rank float over all ranks (the step time of a replicated
+    run is the slowest replica's); identity for world == 1.  Works with NCCL
+    (device tensor) and gloo (CPU tensor)."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -196,11 +209,7 @@ def run_gpu(args):
     if world > 1:
         torch.distributed.barrier()
     clocks = sampler.stop() if rank == 0 else None
-    total_ms = sum(times)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(times), world, dev)
 
     # ---- end to end through the public host-buffer API (pinned host in/out)
     pin_in = torch.from_numpy(host).pin_memory()
@@ -216,11 +225,7 @@ def run_gpu(args):
         e1.record(stream)
         e1.synchronize()
         e2e_times.append(e0.elapsed_time(e1))
-    e2e_ms = sum(e2e_times)
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(sum(e2e_times), world, dev)
     e2e_ok = bool(np.array_equal(pin_out.numpy().view(np.uint64), o.view(np.uint64)))
 
     if rank != 0:
