@@ -895,17 +895,18 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
             const bool pk = valid ? dpack[d] != 0 : true;
             const u32 dhi = valid ? min(st.jlo + ((d + 1) << st.shift), st.jhi) : 0;
             const u32 npm = __ballot_sync(0xffffffffu, !pk);
+            u32 incl = cn;   // inclusive prefix of the chunk's counts (once per chunk)
+            for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= (u32)o) incl += y; }
             u32 s = 0;   // first lane of the chunk not yet assigned to a run
             for (u32 guard = 0; s < 32 && guard < 64; ++guard) {   // each step retires >= 1 lane
-                u32 incl = lane >= s ? cn : 0;
-                for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, incl, o); if (lane >= (u32)o) incl += y; }
+                const u32 before_s = s ? __shfl_sync(0xffffffffu, incl, (s + 31) & 31) : 0u;
                 const u32 run_jlo = st.jlo + (run_d0 << st.shift);
-                const bool bad = valid && lane >= s && (!pk || run_keys + incl > (u32)S_CAP || dhi - run_jlo > (u32)NB_CAP);
+                const bool bad = valid && lane >= s && (!pk || run_keys + (incl - before_s) > (u32)S_CAP || dhi - run_jlo > (u32)NB_CAP);
                 const u32 bm = __ballot_sync(0xffffffffu, bad);
-                if (bm == 0) { run_keys += __shfl_sync(0xffffffffu, incl, 31); s = 32; break; }
+                if (bm == 0) { run_keys += __shfl_sync(0xffffffffu, incl, 31) - before_s; s = 32; break; }
                 const u32 b = __ffs(bm) - 1;
-                const u32 before = __shfl_sync(0xffffffffu, incl, (b + 31) & 31);
-                const u32 keys = run_keys + (b > s ? before : 0);
+                const u32 upto = __shfl_sync(0xffffffffu, incl, (b + 31) & 31);
+                const u32 keys = run_keys + (b > s ? upto - before_s : 0);
                 if (lane == 0 && base + b > run_d0) emit(run_d0, base + b - 1, keys);
                 run_keys = 0;
                 if ((npm >> b) & 1u) {   // skip the non-packable digits at b, b+1, ...
