@@ -365,6 +365,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
             }
         }
         G.bar();
+        if (CTA && MODE == MODE_NODE) prof_mark(c, S, 3);
         // ---- fit: b = inclusive prefix over bins 1..P+1, T = floor(b*gamma/alpha)+1 (R7)
         {
             const u32 e0 = 1 + t * BPT;
@@ -439,6 +440,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         }
     }
     G.bar();
+    if (CTA && MODE == MODE_NODE) prof_mark(c, S, 14);
 
     // ---- column pass: sizes, positions, Alg. 1 lines 160-167 dispatch, destinations per warp
     {
@@ -536,6 +538,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         }
     }
     G.bar();
+    if (CTA && MODE == MODE_NODE) prof_mark(c, S, 15);
     if (NW > 1 && !CTA) {   // team: publish the children (their keys are placed) to the small-node list
         const u32 nc = S.top[w0];
         if (nc) {

@@ -5,9 +5,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2405_07122_b200 as pcf
 import synth
-NAMES = ["claim", "load", "group placement (CTA)", "-", "CTA-run nodes", "node groups", "sort tasks", "#group nodes",
-         "group node keys", "#CTA nodes", "CTA node keys", "tasks", "keys", "store", "-", "-"]
-SLOTS = [0, 1, 2, 4, 5, 6, 13]
+NAMES = ["claim", "load", "group placement (CTA)", "CTA node: minmax+samples", "CTA-run nodes", "node groups", "sort tasks", "#group nodes",
+         "group node keys", "#CTA nodes", "CTA node keys", "tasks", "keys", "store", "CTA node: fit+classify", "CTA node: columns+place"]
+SLOTS = [0, 1, 2, 3, 14, 15, 4, 5, 6, 13]
 ap = argparse.ArgumentParser(); ap.add_argument("--config", default="c2"); ap.add_argument("--n", type=int, default=None)
 a = ap.parse_args()
 x = torch.from_numpy(synth.config(a.config, n=a.n)).cuda()
