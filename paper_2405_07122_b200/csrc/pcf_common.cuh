@@ -34,7 +34,10 @@ constexpr int GMAX = 1024;               // digits per global split pass
 constexpr int SPLIT_THREADS = 512;       // split count kernel block
 constexpr int SC_WARPS = 12;             // split scatter: warps per CTA
 constexpr int SC_THREADS = SC_WARPS * 32;
-constexpr int SC_KPL = 14;               // keys per lane held in registers (2 CTAs/SM with the u32 rank counters)
+#ifndef PCF_SC_KPL
+#define PCF_SC_KPL 14
+#endif
+constexpr int SC_KPL = PCF_SC_KPL;             // keys per lane held in registers (2 CTAs/SM with the u32 rank counters)
 constexpr int SC_PER_WARP = SC_KPL * 32; // 512 consecutive keys per warp
 constexpr int SPLIT_TILE = SC_WARPS * SC_PER_WARP;   // 5376 keys per split tile
 constexpr u64 GOLDEN = 0x9E3779B97F4A7C15ull;

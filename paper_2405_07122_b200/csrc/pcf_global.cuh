@@ -766,7 +766,10 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
 }
 
 template <class K>
-__global__ void __launch_bounds__(SC_THREADS, 2) k_split_scatter(const DevCtx *__restrict__ c, u32 cur) {
+#ifndef PCF_SC_MINB
+#define PCF_SC_MINB 2
+#endif
+__global__ void __launch_bounds__(SC_THREADS, PCF_SC_MINB) k_split_scatter(const DevCtx *__restrict__ c, u32 cur) {
     extern __shared__ __align__(16) unsigned char sc_smem_raw[];
     SplitScatterSmem &S = *reinterpret_cast<SplitScatterSmem *>(sc_smem_raw);
     if (*c->nan_flag) return;
