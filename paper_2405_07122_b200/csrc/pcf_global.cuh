@@ -165,7 +165,7 @@ struct CountSmem {
     u32 hist[GMAX];
     u32 bnd[GMAX];
     u16 ct[NCELL + 1];
-    u32 tab_node, tab_cs;
+    u32 tab_node, tab_cs, tab_step;
     CountStage meta[2];
     u64 full[2], empty[2];
 };
@@ -255,7 +255,13 @@ __global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__
                 while (lo < hi) { const u32 mid = (lo + hi + 1) >> 1; if ((u64)S.bnd[mid] <= i0) lo = mid; else hi = mid - 1; }
                 S.ct[cc] = (u16)lo;
             }
-            if (threadIdx.x == 0) { S.tab_node = m.node; S.tab_cs = cs; }
+            named_bar(1, SC_THREADS);
+            u32 mx = 0;   // widest cell (digits it spans) -> largest search step
+            for (u32 cc = threadIdx.x; cc < (u32)NCELL; cc += SC_THREADS) mx = max(mx, (u32)S.ct[cc + 1] - (u32)S.ct[cc]);
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            if (threadIdx.x == 0) { S.tab_node = m.node; S.tab_cs = cs; S.tab_step = 0; }
+            named_bar(1, SC_THREADS);
+            if ((threadIdx.x & 31) == 0) atomicMax(&S.tab_step, mx ? 1u << (31 - __clz(mx)) : 0u);
         }
         named_bar(1, SC_THREADS);
         if (m.deg) {
@@ -294,8 +300,12 @@ __global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__
 #pragma unroll
                 for (u32 q = 0; q < SC_KPL; ++q) {
                     const u32 i = ix[q], cc = (i - 1u) >> cs;
-                    u32 d = S.ct[cc], d1 = S.ct[cc + 1];   // largest d in [d, d1] with bnd[d] <= i
-                    while (d < d1) { const u32 mid = (d + d1 + 1) >> 1; if (S.bnd[mid] <= i) d = mid; else d1 = mid - 1; }
+                    u32 d = S.ct[cc];   // largest d in [ct[cc], ct[cc + 1]] with bnd[d] <= i:
+                    const u32 d1 = S.ct[cc + 1];   // power-of-two steps, the same count for every key
+                    for (u32 step = S.tab_step; step; step >>= 1) {
+                        const u32 nd = d + step;
+                        if (nd <= d1 && S.bnd[nd] <= i) d = nd;
+                    }
                     ix[q] = d;
                 }
             } else {
