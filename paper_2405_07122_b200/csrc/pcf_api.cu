@@ -162,6 +162,22 @@ enum { PH_MINMAX = 0, PH_FIT = 1, PH_COUNT = 2, PH_SCATTER = 3, PH_K7 = 4, PH_K8
 static int k7_smem_bytes() { return (int)sizeof(K7Smem); }
 static int split_smem_bytes() { return (int)sizeof(SplitScatterSmem); }
 
+// Launch with programmatic stream serialization (see pdl_entry()).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+
 template <class K>
 static int k7_ctas_per_sm() {   // resident K7 CTAs per SM (persistent grid size)
     static thread_local int v = 0;
@@ -375,19 +391,19 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             tm.begin(PH_MINMAX);
             u64 nvec = m / 2 + 1;
             u32 grid = (u32)std::min<u64>(148ull * 8, (nvec + MM_THREADS * MM_UNROLL - 1) / (MM_THREADS * MM_UNROLL));
-            k_minmax<K><<<grid, MM_THREADS, 0, st>>>(dc, idx);
+            CK(launch_pdl(k_minmax<K>, grid, MM_THREADS, 0, st, dc, idx));
             tm.end();
             tm.begin(PH_FIT);
-            k_node_model<K><<<1, 1, 0, st>>>(dc, idx);
+            CK(launch_pdl(k_node_model<K>, 1, 1, 0, st, dc, idx));
             u32 alpha = g.alpha;
-            k_fit_sample<K><<<(alpha + 255) / 256, 256, 0, st>>>(dc, idx);
+            CK(launch_pdl(k_fit_sample<K>, (alpha + 255) / 256, 256, 0, st, dc, idx));
             {
                 u64 nbins = (u64)P + 1;
                 u32 nblk = (u32)((nbins + SCAN_CHUNK - 1) / SCAN_CHUNK);
                 u32 *bs = (u32 *)(ws + L.bsum);
-                k_scan_partials<<<nblk, SCAN_THREADS, 0, st>>>(g.cnt + 1, nbins, bs);
-                k_scan_bsums<<<1, SCAN_THREADS, 0, st>>>(bs, nblk);
-                k_fit_final<<<nblk, SCAN_THREADS, 0, st>>>(dc, idx, bs);
+                CK(launch_pdl(k_scan_partials, nblk, SCAN_THREADS, 0, st, (const u32 *)(g.cnt + 1), (u64)nbins, bs));
+                CK(launch_pdl(k_scan_bsums, 1, SCAN_THREADS, 0, st, bs, nblk));
+                CK(launch_pdl(k_fit_final, nblk, SCAN_THREADS, 0, st, dc, idx, (const u32 *)bs));
             }
             tm.end();
             CK(cudaGetLastError());
@@ -427,44 +443,48 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         // upper bound on the tiles of the next round: its keys are <= n and it has at most
         // (splits in it) partial tiles; the first round has 1 split, the second <= GMAX
         u64 splits_bound = 0;   // upper bound on the splits of the round being enqueued
-        auto enqueue_round = [&]() {
+        auto enqueue_round = [&]() -> int {
             const u32 cur = round & 1u;
             const u32 tile_grid = (u32)std::min<u64>(n / SPLIT_TILE + 1 + splits_bound, 0x7fffffffull);
             // each split yields <= GMAX next splits; overflow carry-over adds <= the current ones
             splits_bound = std::min<u64>(splits_bound * (GMAX + 1), caps.split_cap);
             tm.begin(PH_OTHER);
-            k_round_plan<<<1, 1024, 0, st>>>(d_ctx, cur);
-            k_tile_map<<<nsm * 2, 256, 0, st>>>(d_ctx, cur);
+            CK(launch_pdl(k_round_plan, 1, 1024, 0, st, (const DevCtx *)d_ctx, cur));
+            CK(launch_pdl(k_tile_map, nsm * 2, 256, 0, st, (const DevCtx *)d_ctx, cur));
             tm.end();
             tm.begin(PH_COUNT);
-            if (n <= (1ull << 25)) k_split_count_tile<K><<<tile_grid, SC_THREADS, 0, st>>>(d_ctx, cur);
-            else k_split_count<K><<<nsm * count_ctas_per_sm<K>(), CNT_THREADS, (int)sizeof(CountSmem), st>>>(d_ctx, cur);
+            if (n <= (1ull << 25)) CK(launch_pdl(k_split_count_tile<K>, tile_grid, SC_THREADS, 0, st, (const DevCtx *)d_ctx, cur));
+            else CK(launch_pdl(k_split_count<K>, nsm * count_ctas_per_sm<K>(), CNT_THREADS, sizeof(CountSmem), st, (const DevCtx *)d_ctx, cur));
             tm.end();
             tm.begin(PH_OTHER);
-            k_scanp_partials<<<nsm * 2, SCAN_THREADS, 0, st>>>(d_ctx);
-            k_scanp_bsums<<<1, SCAN_THREADS, 0, st>>>(d_ctx);
-            k_scanp_final<<<nsm * 2, SCAN_THREADS, 0, st>>>(d_ctx);
+            CK(launch_pdl(k_scanp_partials, nsm * 2, SCAN_THREADS, 0, st, (const DevCtx *)d_ctx));
+            CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, st, (const DevCtx *)d_ctx));
+            CK(launch_pdl(k_scanp_final, nsm * 2, SCAN_THREADS, 0, st, (const DevCtx *)d_ctx));
             tm.end();
             tm.begin(PH_SCATTER);
-            k_split_scatter<K><<<tile_grid, SC_THREADS, split_smem_bytes(), st>>>(d_ctx, cur);
+            CK(launch_pdl(k_split_scatter<K>, tile_grid, SC_THREADS, split_smem_bytes(), st, (const DevCtx *)d_ctx, cur));
             tm.end();
             tm.begin(PH_OTHER);
-            k_split_taskgen<<<nsm * 2, TG_THREADS, 0, st>>>(d_ctx, cur);
+            CK(launch_pdl(k_split_taskgen, nsm * 2, TG_THREADS, 0, st, (const DevCtx *)d_ctx, cur));
             tm.end();
             launches += 8;
             round++;
+            return PCF_OK;
         };
         u32 rounds_per_batch = 2;   // enough for 10^6..10^9 keys of well-modelled data
         for (;;) {
             rc = flush_list();
             if (rc) return rc;
             splits_bound = pending;
-            for (u32 k = 0; k < rounds_per_batch; ++k) enqueue_round();
+            for (u32 k = 0; k < rounds_per_batch; ++k) {
+                rc = enqueue_round();
+                if (rc) return rc;
+            }
             CK(cudaGetLastError());
             // K7 over every group produced so far (persistent grid; reads the task count on the device)
             tm.begin(PH_K7);
-            k7_kernel<K><<<nsm * k7_ctas_per_sm<K>(), K7_THREADS, k7_smem_bytes(), st>>>(d_ctx);
-            k_k7_advance<<<1, 1, 0, st>>>(d_ctx);
+            CK(launch_pdl(k7_kernel<K>, nsm * k7_ctas_per_sm<K>(), K7_THREADS, k7_smem_bytes(), st, (const DevCtx *)d_ctx));
+            CK(launch_pdl(k_k7_advance, 1, 1, 0, st, (const DevCtx *)d_ctx));
             tm.end();
             CK(cudaGetLastError());
             launches += 2;

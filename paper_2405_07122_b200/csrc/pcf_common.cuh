@@ -330,6 +330,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, u32 bytes, 
 // generic-proxy accesses of a shared buffer before it is refilled by the async proxy
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Programmatic dependent launch: every kernel of the sort's chain first waits
+// for its predecessor grid (complete, memory visible) and then lets its own
+// successor start launching, so launch latency overlaps the tail of the
+// previous kernel.  (No-ops for a kernel launched without the attribute.)
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 constexpr u32 FLAG_SAMPLE_ALL = 2u;
 constexpr int K7_PROF_SLOTS = 16;
 

@@ -37,6 +37,7 @@ __device__ __forceinline__ void mm_acc(u64 raw, u64 &mn, u64 &mx, bool &nan) {
 
 template <class K>
 __global__ void __launch_bounds__(MM_THREADS) k_minmax(const DevCtx *__restrict__ c, u32 node) {
+    pdl_entry();
     GNode &g = c->nodes[node];
     const u64 *x = c->buf[g.src] + g.off;
     const u64 m = g.m;
@@ -91,6 +92,7 @@ __device__ __forceinline__ void push_item(const DevCtx *c, u64 off, u32 m, u32 l
 
 template <class K>
 __global__ void k_node_model(const DevCtx *__restrict__ c, u32 node) {
+    pdl_entry();
     if (*c->nan_flag) return;
     GNode &g = c->nodes[node];
     Model md;
@@ -102,6 +104,7 @@ __global__ void k_node_model(const DevCtx *__restrict__ c, u32 node) {
 
 template <class K>
 __global__ void k_fit_sample(const DevCtx *__restrict__ c, u32 node) {
+    pdl_entry();
     if (*c->nan_flag) return;
     const GNode &g = c->nodes[node];
     if (g.degenerate) return;
@@ -127,6 +130,7 @@ __device__ __forceinline__ u32 find_split(const SplitTask *L, u32 ns, u32 tile) 
 // Split of every tile of round `cur` (one thread per tile): the count and
 // scatter CTAs read it instead of each searching the split list.
 __global__ void k_tile_map(const DevCtx *__restrict__ c, u32 cur) {
+    pdl_entry();
     const RoundPlan pl = *c->plan;
     const SplitTask *__restrict__ L = c->splits[cur];
     for (u32 si = blockIdx.x; si < pl.ns; si += gridDim.x) {   // one CTA per split
@@ -206,6 +210,7 @@ constexpr int CNT_THREADS = SC_THREADS + 32;   // 12 consumer warps + 1 producer
 
 template <class K>
 __global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__restrict__ c, u32 cur) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char cnt_smem_raw[];
     CountSmem &S = *reinterpret_cast<CountSmem *>(cnt_smem_raw);
     if (*c->nan_flag) return;
@@ -333,6 +338,7 @@ __global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__
 // the persistent kernel's pipeline never fills.  Same outputs as k_split_count.
 template <class K>
 __global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_tile(const DevCtx *__restrict__ c, u32 cur) {
+    pdl_entry();
     __shared__ u32 hist[GMAX];
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
@@ -415,6 +421,7 @@ __device__ __forceinline__ u32 block_excl_scan_1024(u32 v, u32 *wsum, u32 &total
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(const u32 *__restrict__ in, u64 n, u32 *__restrict__ bsum) {
+    pdl_entry();
     __shared__ u32 wsum[33];
     u64 base = (u64)blockIdx.x * SCAN_CHUNK + (u64)threadIdx.x * SCAN_ITEMS;
     u32 s = 0;
@@ -426,6 +433,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(const u32 *__res
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_bsums(u32 *__restrict__ bsum, u32 nb) {
+    pdl_entry();
     __shared__ u32 wsum[33];
     u32 carry = 0;
     for (u32 base = 0; base < nb; base += SCAN_THREADS) {
@@ -440,6 +448,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_bsums(u32 *__restrict__ b
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const u32 *__restrict__ in, u64 n, const u32 *__restrict__ bsum,
                                                              u32 *__restrict__ out) {
+    pdl_entry();
     __shared__ u32 wsum[33];
     u64 base = (u64)blockIdx.x * SCAN_CHUNK + (u64)threadIdx.x * SCAN_ITEMS;
     u32 v[SCAN_ITEMS];
@@ -454,6 +463,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const u32 *__restri
 
 // Same three phases over the count matrix of a split round, sizes from the plan.
 __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_partials(const DevCtx *__restrict__ c) {
+    pdl_entry();
     __shared__ u32 wsum[33];
     const RoundPlan pl = *c->plan;
     for (u32 b = blockIdx.x; b < pl.nblk; b += gridDim.x) {
@@ -468,6 +478,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_partials(const DevCtx *_
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_bsums(const DevCtx *__restrict__ c) {
+    pdl_entry();
     __shared__ u32 wsum[33];
     const u32 nb = c->plan->nblk;
     u32 carry = 0;
@@ -482,6 +493,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_bsums(const DevCtx *__re
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_final(const DevCtx *__restrict__ c) {
+    pdl_entry();
     __shared__ u32 wsum[33];
     const RoundPlan pl = *c->plan;
     for (u32 b = blockIdx.x; b < pl.nblk; b += gridDim.x) {
@@ -501,6 +513,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_final(const DevCtx *__re
 // split (one CTA).  Splits that do not fit the count matrix are carried over to
 // the next round's list; the next list's counter is reset here.
 __global__ void __launch_bounds__(1024) k_round_plan(const DevCtx *__restrict__ c, u32 cur) {
+    pdl_entry();
     __shared__ u32 wsum[33];
     __shared__ unsigned long long wsum64[33];
     __shared__ u32 cut_s;
@@ -580,6 +593,7 @@ __global__ void __launch_bounds__(1024) k_round_plan(const DevCtx *__restrict__ 
 // k_scan_partials/k_scan_bsums pass over cnt+1), T[i] = floor(b_i*gamma/alpha)+1
 // (R7), digest of b and the level-1 dump for the pass log.
 __global__ void __launch_bounds__(SCAN_THREADS) k_fit_final(const DevCtx *__restrict__ c, u32 node, const u32 *__restrict__ bsum) {
+    pdl_entry();
     __shared__ u32 wsum[33];
     __shared__ unsigned long long dsum;
     if (*c->nan_flag) return;
@@ -780,6 +794,7 @@ template <class K>
 #define PCF_SC_MINB 2
 #endif
 __global__ void __launch_bounds__(SC_THREADS, PCF_SC_MINB) k_split_scatter(const DevCtx *__restrict__ c, u32 cur) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char sc_smem_raw[];
     SplitScatterSmem &S = *reinterpret_cast<SplitScatterSmem *>(sc_smem_raw);
     if (*c->nan_flag) return;
@@ -846,6 +861,7 @@ __device__ __forceinline__ void make_run_task(const DevCtx *c, const SplitTask &
 
 constexpr int TG_THREADS = 256;
 __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__restrict__ c, u32 cur) {
+    pdl_entry();
     __shared__ u32 dcnt[GMAX];
     __shared__ u8 dpack[GMAX];
     __shared__ u32 rd0[GMAX], rd1[GMAX], rk[GMAX];   // packed runs of the split (warp 0)
@@ -955,6 +971,7 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
 }
 
 __global__ void k_k7_advance(const DevCtx *__restrict__ c) {
+    pdl_entry();
     *c->k7_begin = *c->k7_count;
     *c->k7_next = 0;
 }

@@ -657,6 +657,7 @@ __device__ __forceinline__ void push_root(const DevCtx *c, K7Smem &S, u32 e) {
 
 template <class K>
 __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kernel(const DevCtx *__restrict__ c) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char k7_smem_raw[];
     K7Smem &S = *reinterpret_cast<K7Smem *>(k7_smem_raw);
     if (*c->nan_flag) return;
