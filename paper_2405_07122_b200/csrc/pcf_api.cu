@@ -394,7 +394,6 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             CK(launch_pdl(k_minmax<K>, grid, MM_THREADS, 0, st, dc, idx));
             tm.end();
             tm.begin(PH_FIT);
-            CK(launch_pdl(k_node_model<K>, 1, 1, 0, st, dc, idx));
             u32 alpha = g.alpha;
             CK(launch_pdl(k_fit_sample<K>, (alpha + 255) / 256, 256, 0, st, dc, idx));
             {
@@ -407,7 +406,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             }
             tm.end();
             CK(cudaGetLastError());
-            launches += 6;
+            launches += 5;
             bytes[PH_MINMAX] += 8ull * m;
             bytes[PH_FIT] += 8ull * alpha + 8ull * (P + 2);
             stats.global_nodes++;

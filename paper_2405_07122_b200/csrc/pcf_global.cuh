@@ -102,18 +102,27 @@ __global__ void k_node_model(const DevCtx *__restrict__ c, u32 node) {
     if (!ok) push_item(c, g.off, g.m, g.level, g.src, 1u);   // Standard-Sort the whole segment
 }
 
+// The node's model (from the min/max) is built by every thread (cheap, one
+// launch less); thread 0 of block 0 publishes it (and the degenerate verdict,
+// R9/R10) for the later kernels.
 template <class K>
 __global__ void k_fit_sample(const DevCtx *__restrict__ c, u32 node) {
     pdl_entry();
     if (*c->nan_flag) return;
-    const GNode &g = c->nodes[node];
-    if (g.degenerate) return;
+    GNode &g = c->nodes[node];
+    Model md;
+    const bool ok = make_model<K>(g.kmin, g.kmax, g.beta, md);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        g.md = md;
+        g.degenerate = ok ? 0u : 1u;
+        if (!ok) push_item(c, g.off, g.m, g.level, g.src, 1u);   // Standard-Sort the whole segment
+    }
+    if (!ok) return;
     const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= g.alpha) return;
     const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
     const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, g.off), k, g.m);
     const u64 raw = c->buf[g.src][g.off + pos];
-    const Model md = g.md;
     atomicAdd(&g.cnt[interval_index<K>(K::to_okey(raw), md)], 1u);
 }
 
