@@ -84,7 +84,7 @@ struct Counters {             // zeroed at the start of every call
 };
 
 struct Layout {
-    size_t ctx, counters, tmp, digs, tmap, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
+    size_t ctx, counters, tmp, digs, tmap, k7_order, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
 };
 
 static Layout layout_for(const Caps &c) {
@@ -100,6 +100,7 @@ static Layout layout_for(const Caps &c) {
     L.acc = take((size_t)c.node_cap * sizeof(NodeAcc));
     L.arena = take(c.arena_u32 * 4);
     L.k7 = take((size_t)c.k7_cap * sizeof(K7Task));
+    L.k7_order = take((size_t)c.k7_cap * 4);
     L.splits_a = take((size_t)c.split_cap * sizeof(SplitTask));
     L.splits_b = take((size_t)c.split_cap * sizeof(SplitTask));
     L.items = take((size_t)c.items_cap * sizeof(SegItem));
@@ -306,6 +307,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.buf[1] = (u64 *)(ws + L.tmp);
         hc.nodes = (GNode *)(ws + L.nodes);
         hc.k7 = (K7Task *)(ws + L.k7);
+        hc.k7_order = (u32 *)(ws + L.k7_order);
         hc.k7_cap = caps.k7_cap;
         hc.splits[0] = (SplitTask *)(ws + L.splits_a);
         hc.splits[1] = (SplitTask *)(ws + L.splits_b);
@@ -482,11 +484,12 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             CK(cudaGetLastError());
             // K7 over every group produced so far (persistent grid; reads the task count on the device)
             tm.begin(PH_K7);
+            CK(launch_pdl(k_k7_order, 1, 1024, 0, st, (const DevCtx *)d_ctx));
             CK(launch_pdl(k7_kernel<K>, nsm * k7_ctas_per_sm<K>(), K7_THREADS, k7_smem_bytes(), st, (const DevCtx *)d_ctx));
             CK(launch_pdl(k_k7_advance, 1, 1, 0, st, (const DevCtx *)d_ctx));
             tm.end();
             CK(cudaGetLastError());
-            launches += 2;
+            launches += 3;
             Counters hcnt;
             CK(cudaMemcpyAsync(&hcnt, d_cnt, sizeof hcnt, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));

@@ -270,6 +270,7 @@ struct DevCtx {
     GNode *nodes;
     // K7 queue
     K7Task *k7;
+    u32 *k7_order;          // claim order of the current K7 launch's tasks (largest first), or NULL
     u32 *k7_count;
     u32 k7_cap;
     u32 *k7_next;

@@ -979,6 +979,36 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
     }
 }
 
+// Claim order of the tasks [k7_begin, k7_count) for the next K7 launch:
+// largest first (64 size classes of S_CAP/64 keys, a counting sort in one CTA),
+// so the persistent grid ends on small tasks (shorter tail) -- for launches of
+// up to ~16 tasks per SM; larger ones keep the order taskgen produced them in
+// (neighbouring tasks are neighbours in memory, measured 2 % faster on c5f).
+__global__ void __launch_bounds__(1024) k_k7_order(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    __shared__ u32 cnt[64];
+    const u32 b = *c->k7_begin, e = min(*c->k7_count, c->k7_cap);
+    if (e - b > 16u * 148u) {   // many tasks per CTA: the tail is short anyway; keep the produced
+        for (u32 i = b + threadIdx.x; i < e; i += blockDim.x) c->k7_order[i] = i;   // (memory-local) order
+        return;
+    }
+    if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    auto cls = [&](u32 i) { return 63u - min(c->k7[i].size / (u32)(S_CAP / 64), 63u); };
+    for (u32 i = b + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&cnt[cls(i)], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {   // exclusive scan of the 64 class counts
+        const u32 a0 = cnt[2 * threadIdx.x], a1 = cnt[2 * threadIdx.x + 1];
+        u32 x = a0 + a1;
+        for (int o = 1; o < 32; o <<= 1) { const u32 y = __shfl_up_sync(0xffffffffu, x, o); if (threadIdx.x >= (u32)o) x += y; }
+        const u32 ex = x - a0 - a1;
+        cnt[2 * threadIdx.x] = b + ex;
+        cnt[2 * threadIdx.x + 1] = b + ex + a0;
+    }
+    __syncthreads();
+    for (u32 i = b + threadIdx.x; i < e; i += blockDim.x) c->k7_order[atomicAdd(&cnt[cls(i)], 1u)] = i;
+}
+
 __global__ void k_k7_advance(const DevCtx *__restrict__ c) {
     pdl_entry();
     *c->k7_begin = *c->k7_count;

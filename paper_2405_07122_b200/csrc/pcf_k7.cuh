@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
         mbar_init(&S.tbar, 1);
         mbar_init_fence();
         S.nidx = begin + atomicAdd(c->k7_next, 1u);
-        if (S.nidx < ntasks) { S.ntask = c->k7[S.nidx]; k7_issue(c, S, S.ntask); }
+        if (S.nidx < ntasks) { S.ntask = c->k7[c->k7_order ? c->k7_order[S.nidx] : S.nidx]; k7_issue(c, S, S.ntask); }
     }
     __syncthreads();
     for (u32 it = 0;; ++it) {
@@ -827,7 +827,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
         }
         if (threadIdx.x == 0) {   // B is free: the next task streams in while this one is stored
             S.nidx = nclaim;
-            if (nclaim < ntasks) { S.ntask = c->k7[nclaim]; k7_issue(c, S, S.ntask); }
+            if (nclaim < ntasks) { S.ntask = c->k7[c->k7_order ? c->k7_order[nclaim] : nclaim]; k7_issue(c, S, S.ntask); }
         }
         store_task<K>(S, gout, M);
         prof_mark(c, S, 13);
