@@ -48,6 +48,8 @@ extern "C" {
 #define PCF_FLAG_SAMPLE_ALL 2u  /* test mode (reading R14): sample = whole segment, alpha = m      */
 #define PCF_FLAG_TIMING     4u  /* record CUDA events per phase into stats->phase_ms (implies SYNC) */
 #define PCF_FLAG_PROFILE    8u  /* K7 per-phase SM cycle counters into stats->k7_cycles (with SYNC) */
+#define PCF_FLAG_EXACT_RANKS 16u /* test mode: the split scatter always takes its exact (source-
+                                    index) re-rank path instead of trusting the atomic ranks      */
 
 /* One record per bucketing node, i.e. per call of Alg. 1 that reaches its
  * model-based bucketing step.  Identical layout to the

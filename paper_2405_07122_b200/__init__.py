@@ -16,7 +16,7 @@ __all__ = ["build", "lib", "sort", "sort_host", "workspace_bytes", "host_workspa
            "FLAG_SYNC", "FLAG_SAMPLE_ALL", "FLAG_TIMING", "PHASES"]
 
 KEY_F64, KEY_U64 = 0, 1
-FLAG_SYNC, FLAG_SAMPLE_ALL, FLAG_TIMING, FLAG_PROFILE = 1, 2, 4, 8
+FLAG_SYNC, FLAG_SAMPLE_ALL, FLAG_TIMING, FLAG_PROFILE, FLAG_EXACT_RANKS = 1, 2, 4, 8, 16
 PHASES = ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "total"]
 STATUS = {0: "PCF_OK", 1: "PCF_ERR_INVALID_ARG", 2: "PCF_ERR_NAN", 3: "PCF_ERR_WORKSPACE_TOO_SMALL",
           4: "PCF_ERR_OOM", 5: "PCF_ERR_CUDA", 6: "PCF_ERR_LOG_OVERFLOW", 7: "PCF_ERR_INTERNAL"}
@@ -128,7 +128,7 @@ class SortInfo:
 
 def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False, log: bool = False,
          timing: bool = False, stats: bool = False, sync: bool = True, workspace=None, node_capacity=None,
-         profile: bool = False, stream=None):
+         profile: bool = False, exact_ranks: bool = False, stream=None):
     """Sort a 1-D CUDA tensor of float64 or uint64 keys ascending (totalOrder for f64).
 
     Returns ``out`` (a new tensor unless given; ``out is x`` sorts in place), or
@@ -150,7 +150,7 @@ def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False,
     if out is None:
         out = torch.empty_like(x)
     flags = (FLAG_SYNC if sync else 0) | (FLAG_SAMPLE_ALL if sample_all else 0) | (FLAG_TIMING if timing else 0) \
-        | (FLAG_PROFILE if profile else 0)
+        | (FLAG_PROFILE if profile else 0) | (FLAG_EXACT_RANKS if exact_ranks else 0)
     p = make_params(tau, seed, flags)
     if workspace is not None:
         p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()

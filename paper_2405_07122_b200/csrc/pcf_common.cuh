@@ -341,6 +341,7 @@ __device__ __forceinline__ void pdl_entry() {
 }
 
 constexpr u32 FLAG_SAMPLE_ALL = 2u;
+constexpr u32 FLAG_EXACT_RANKS = 16u;
 constexpr int K7_PROF_SLOTS = 16;
 
 }  // namespace pcf

@@ -779,7 +779,7 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
         }
         y[S.goff[b & 0xffffu] + i] = S.buf[i];
     }
-    if (!__syncthreads_or(inv)) return;
+    if (!__syncthreads_or(inv || (c->flags & FLAG_EXACT_RANKS))) return;
     for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) {
         const u32 e = S.dsrc[i];
         const u32 d = e & 0xffffu;

@@ -27,7 +27,7 @@ def pcf():
 DEV = "cuda:0"
 
 
-def compare(pcf, x, tau=64, seed=0, sample_all=False, check_nodes=True, inplace=False):
+def compare(pcf, x, tau=64, seed=0, sample_all=False, check_nodes=True, inplace=False, exact_ranks=False):
     flags = oracle.FLAG_SAMPLE_ALL if sample_all else 0
     ref = oracle.learned_sort(x, tau=tau, seed=seed, flags=flags, log=check_nodes, check=True)
     xt = torch.from_numpy(x.copy()).to(DEV)
@@ -35,7 +35,8 @@ def compare(pcf, x, tau=64, seed=0, sample_all=False, check_nodes=True, inplace=
         out, info = pcf.sort(xt, xt, tau=tau, seed=seed, sample_all=sample_all, log=check_nodes, stats=True)
         assert out.data_ptr() == xt.data_ptr()
     else:
-        out, info = pcf.sort(xt, tau=tau, seed=seed, sample_all=sample_all, log=check_nodes, stats=True)
+        out, info = pcf.sort(xt, tau=tau, seed=seed, sample_all=sample_all, log=check_nodes, stats=True,
+                             exact_ranks=exact_ranks)
         assert np.array_equal(xt.cpu().numpy().view(np.uint64), x.view(np.uint64)), "input was modified"
     got = out.cpu().numpy()
     assert np.array_equal(got.view(np.uint64), ref.out.view(np.uint64)), "sorted output differs"
@@ -165,3 +166,10 @@ def test_full_size_c2_exact(pcf):
 
 def test_full_size_c1_exact(pcf):
     compare(pcf, synth.config("c1"))
+
+
+@pytest.mark.parametrize("name,n", [("c2", 2_000_000), ("c5f", 1_000_000), ("c3", 500_000)])
+def test_split_scatter_exact_rank_path(pcf, name, n):
+    """The split scatter's fallback (exact re-rank of every same-chunk, same-digit
+    group by source index), forced on every tile: identical output and records."""
+    compare(pcf, synth.config(name, n=n), exact_ranks=True)
