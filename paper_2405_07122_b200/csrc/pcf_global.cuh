@@ -918,17 +918,22 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
         }
         if (threadIdx.x == 0) nrun = 0;
         __syncthreads();
-        if (threadIdx.x < 32) {
-        // warp 0: greedy next-fit packing of the packable digits, 32 digits per step
-        u32 run_d0 = 0, run_keys = 0;
+        {
+        // every warp: greedy next-fit packing of the packable digits of its own range of
+        // the split's digits (32 digits per step); runs never cross a warp's range, which
+        // only costs a few more (smaller) tasks and keeps the latency of a split short
+        const u32 w = threadIdx.x >> 5;
+        const u32 RW = ((st.G + TG_THREADS / 32 * 32 - 1) / (TG_THREADS / 32 * 32)) * 32;
+        const u32 dbeg = min(st.G, w * RW), dend = min(st.G, dbeg + RW);
+        u32 run_d0 = dbeg, run_keys = 0;
         auto emit = [&](u32 d0, u32 d1, u32 keys) {   // lane 0
             if (keys == 0) return;
-            const u32 r = nrun++;
+            const u32 r = atomicAdd(&nrun, 1u);
             rd0[r] = d0; rd1[r] = d1; rk[r] = keys;
         };
-        for (u32 base = 0; base < st.G; base += 32) {
+        for (u32 base = dbeg; base < dend; base += 32) {
             const u32 d = base + lane;
-            const bool valid = d < st.G;
+            const bool valid = d < dend;
             const u32 cn = valid ? dcnt[d] : 0;
             const bool pk = valid ? dpack[d] != 0 : true;
             const u32 dhi = valid ? min(st.jlo + ((d + 1) << st.shift), st.jhi) : 0;
@@ -957,7 +962,7 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
             }
             if (s < 32 && lane == 0) atomicOr(c->err_flag, 2u);   // unreachable: the loop retires a lane per step
         }
-        if (lane == 0 && run_d0 < st.G) emit(run_d0, st.G - 1, run_keys);
+        if (lane == 0 && run_d0 < dend) emit(run_d0, dend - 1, run_keys);
         }
         __syncthreads();
         // all threads: reserve the K7 slots of the split's runs at once, write the tasks
