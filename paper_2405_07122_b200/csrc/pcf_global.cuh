@@ -667,7 +667,9 @@ struct SplitScatterSmem {
     u32 scan_tmp[SC_WARPS + 1];
 };
 
-template <class K>
+// FULL: the tile holds SPLIT_TILE keys (every tile but the last of a split), so
+// the per-slot validity tests compile away.
+template <class K, bool FULL>
 __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c, SplitScatterSmem &S, const SplitTask &st,
                                                    u32 lt, const u32 *__restrict__ P) {
     const u32 deg = c->nodes[st.node].degenerate;   // checked after the tile's loads are issued
@@ -685,7 +687,7 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
 #pragma unroll
     for (u32 q = 0; q < SC_KPL; ++q) {
         const u32 k = r0 + q * 32 + lane;
-        const bool v = k < k1;
+        const bool v = FULL || k < k1;
         key[q] = v ? x[k] : 0ull;
         pk[q] = v ? (u32)dg[k] : 0xffffffffu;
     }
@@ -703,7 +705,7 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
 #pragma unroll
     for (u32 q = 0; q < SC_KPL; ++q) {
         const u32 d = pk[q];
-        if (d != 0xffffffffu) {
+        if (FULL || d != 0xffffffffu) {
             const u32 old = atomicAdd(&S.wc[w][d >> 1], (d & 1u) ? 0x10000u : 1u);
             pk[q] = d | ((((d & 1u) ? old >> 16 : old) & 0xffffu) << 16);
         }
@@ -755,7 +757,7 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
     // stage in digit order: digit run, then warp, then in-warp rank
 #pragma unroll
     for (u32 q = 0; q < SC_KPL; ++q) {
-        if (pk[q] != 0xffffffffu) {
+        if (FULL || pk[q] != 0xffffffffu) {
             const u32 d = pk[q] & 0xffffu;
             const u32 wo = (S.wc[w][d >> 1] >> ((d & 1u) * 16)) & 0xffffu;
             const u32 lp = S.tstart[d] + wo + (pk[q] >> 16);
@@ -812,7 +814,9 @@ __global__ void __launch_bounds__(SC_THREADS, PCF_SC_MINB) k_split_scatter(const
     const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
     if (tile >= pl.tiles) return;
     const SplitTask st = L[c->tmap[tile]];
-    split_scatter_tile<K>(c, S, st, tile - st.tile_begin, c->pmat);
+    const u32 lt = tile - st.tile_begin;
+    if ((lt + 1) * SPLIT_TILE <= st.m) split_scatter_tile<K, true>(c, S, st, lt, c->pmat);
+    else split_scatter_tile<K, false>(c, S, st, lt, c->pmat);
 }
 
 __host__ __device__ inline u32 ceil_log2_u32(u32 v) {   // v >= 1
