@@ -84,7 +84,7 @@ struct Counters {             // zeroed at the start of every call
 };
 
 struct Layout {
-    size_t ctx, counters, tmp, digs, tmap, k7_order, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
+    size_t ctx, counters, tmp, digs, tmap, k7_order, bmm, bfs, bnl, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
 };
 
 static Layout layout_for(const Caps &c) {
@@ -101,6 +101,10 @@ static Layout layout_for(const Caps &c) {
     L.arena = take(c.arena_u32 * 4);
     L.k7 = take((size_t)c.k7_cap * sizeof(K7Task));
     L.k7_order = take((size_t)c.k7_cap * 4);
+    // batched global nodes: chunk -> node maps (+ first chunk per node) and the node list
+    L.bmm = take((c.n / MMB_CHUNK + 2ull * c.node_cap + 64) * 4);
+    L.bfs = take((c.n / FSB_CHUNK + 2ull * c.node_cap + 64) * 4);
+    L.bnl = take(((u64)c.node_cap + 64) * 4);
     L.splits_a = take((size_t)c.split_cap * sizeof(SplitTask));
     L.splits_b = take((size_t)c.split_cap * sizeof(SplitTask));
     L.items = take((size_t)c.items_cap * sizeof(SegItem));
@@ -364,7 +368,11 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         u32 *arena = (u32 *)(ws + L.arena);
         u32 node_count = 0;
         std::vector<SplitTask> list;
-        auto add_node = [&](u64 off, u32 m, u32 level, u32 src) -> int {
+        std::vector<u32> batch;   // nodes whose fit is launched together
+        std::vector<GNode> batch_nodes;
+        u64 batch_arena0 = 0;
+        std::vector<u32> node_m, node_alpha;
+        auto add_node = [&](u64 off, u32 m, u32 level, u32 src, bool batched) -> int {
             if (node_count >= caps.node_cap) return fail(PCF_ERR_INTERNAL, "global node capacity exceeded");
             GNode g;
             memset(&g, 0, sizeof g);
@@ -380,16 +388,27 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             g.H = g.T + (P + 2);
             arena_used += need_u32;
             const u32 sh0 = choose_shift(P + 1, m);
-            if (m >= (1u << BND_MIN_LOG2) && arena_used + GMAX <= caps.arena_u32) {
+            if (!batched && m >= (1u << BND_MIN_LOG2) && arena_used + GMAX <= caps.arena_u32) {
                 g.bnd = arena + arena_used;
                 arena_used += GMAX;
                 g.bshift = sh0;
                 g.bG = (P + 1 + (1u << sh0) - 1) >> sh0;
             }
             u32 idx = node_count++;
-            CK(cudaMemcpyAsync(hc.nodes + idx, &g, sizeof g, cudaMemcpyHostToDevice, st));
-            CK(cudaMemsetAsync(g.cnt, 0, need_u32 * 4, st));
+            node_m.push_back(m);
+            node_alpha.push_back(g.alpha);
+            if (!batched) {
+                CK(cudaMemcpyAsync(hc.nodes + idx, &g, sizeof g, cudaMemcpyHostToDevice, st));
+                CK(cudaMemsetAsync(g.cnt, 0, need_u32 * 4, st));
+            }
             const DevCtx *dc = d_ctx;
+            if (batched) {   // uploaded (nodes, zeroed tables) with the rest of the batch
+                if (batch.empty()) batch_arena0 = (u64)(g.cnt - arena);
+                batch_nodes.push_back(g);
+                batch.push_back(idx);
+                bytes[PH_MINMAX] += 8ull * m;
+                bytes[PH_FIT] += 8ull * g.alpha + 8ull * (P + 2);
+            } else {
             tm.begin(PH_MINMAX);
             u64 nvec = m / 2 + 1;
             u32 grid = (u32)std::min<u64>(148ull * 8, (nvec + MM_THREADS * MM_UNROLL - 1) / (MM_THREADS * MM_UNROLL));
@@ -411,6 +430,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             launches += 5;
             bytes[PH_MINMAX] += 8ull * m;
             bytes[PH_FIT] += 8ull * alpha + 8ull * (P + 2);
+            }
             stats.global_nodes++;
             global_nodes.push_back(idx);
             SplitTask s;
@@ -426,7 +446,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         // host-side list of splits to append to the device list of the next round
-        rc = add_node(0, (u32)n, 1, 0);
+        rc = add_node(0, (u32)n, 1, 0, false);
         if (rc) return rc;
         u32 round = 0;
         u32 pending = 0;   // splits already in the device list splits[round & 1]
@@ -505,8 +525,47 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
                 CK(cudaMemsetAsync(&d_cnt->nitems, 0, 4, st));
             }
             for (const SegItem &it : items) {
-                if (it.kind == 0) { rc = add_node(it.off, it.m, it.level, it.src); if (rc) return rc; }
+                if (it.kind == 0) { rc = add_node(it.off, it.m, it.level, it.src, true); if (rc) return rc; }
                 else fallbacks.push_back(it);
+            }
+            if (!batch.empty()) {   // one min/max, one sampling and one fit launch for every new node
+                std::vector<u32> cmm, fmm, cfs, ffs;
+                u64 nkeys = 0;
+                // the batch's node records (consecutive indices) and its zeroed table range
+                CK(cudaMemcpyAsync(hc.nodes + batch[0], batch_nodes.data(), batch_nodes.size() * sizeof(GNode),
+                                   cudaMemcpyHostToDevice, st));
+                CK(cudaMemsetAsync(arena + batch_arena0, 0, (arena_used - batch_arena0) * 4, st));
+                for (u32 idx : batch) {
+                    fmm.push_back((u32)cmm.size());
+                    ffs.push_back((u32)cfs.size());
+                    const u32 m = node_m[idx], al = node_alpha[idx];
+                    for (u32 q = 0; q < (m + MMB_CHUNK - 1) / MMB_CHUNK; ++q) cmm.push_back(idx);
+                    for (u32 q = 0; q < (al + FSB_CHUNK - 1) / FSB_CHUNK; ++q) cfs.push_back(idx);
+                    nkeys += m;
+                }
+                // first-chunk tables are indexed by node: scatter them into node-sized arrays
+                std::vector<u32> nfm(node_count, 0), nfs(node_count, 0);
+                for (size_t i = 0; i < batch.size(); ++i) { nfm[batch[i]] = fmm[i]; nfs[batch[i]] = ffs[i]; }
+                u32 *d_cmm = (u32 *)(ws + L.bmm), *d_nfm = d_cmm + cmm.size();
+                u32 *d_cfs = (u32 *)(ws + L.bfs), *d_nfs = d_cfs + cfs.size();
+                u32 *d_nl = (u32 *)(ws + L.bnl);
+                CK(cudaMemcpyAsync(d_cmm, cmm.data(), cmm.size() * 4, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(d_nfm, nfm.data(), nfm.size() * 4, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(d_cfs, cfs.data(), cfs.size() * 4, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(d_nfs, nfs.data(), nfs.size() * 4, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(d_nl, batch.data(), batch.size() * 4, cudaMemcpyHostToDevice, st));
+                tm.begin(PH_MINMAX);
+                CK(launch_pdl(k_minmax_batch<K>, (u32)cmm.size(), MM_THREADS, 0, st, (const DevCtx *)d_ctx,
+                              (const u32 *)d_cmm, (const u32 *)d_nfm));
+                tm.end();
+                tm.begin(PH_FIT);
+                CK(launch_pdl(k_fit_sample_batch<K>, (u32)cfs.size(), FSB_CHUNK, 0, st, (const DevCtx *)d_ctx,
+                              (const u32 *)d_cfs, (const u32 *)d_nfs));
+                CK(launch_pdl(k_fit_batch, (u32)batch.size(), SCAN_THREADS, 0, st, (const DevCtx *)d_ctx, (const u32 *)d_nl));
+                tm.end();
+                launches += 3;
+                batch.clear();
+                batch_nodes.clear();
             }
             bytes[PH_COUNT] = 8ull * hcnt.split_keys;
             bytes[PH_SCATTER] = 16ull * hcnt.split_keys;

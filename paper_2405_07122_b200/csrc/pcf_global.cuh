@@ -126,6 +126,71 @@ __global__ void k_fit_sample(const DevCtx *__restrict__ c, u32 node) {
     atomicAdd(&g.cnt[interval_index<K>(K::to_okey(raw), md)], 1u);
 }
 
+// ------------------------------------------------------------------ batched global nodes
+// The recursing buckets too large for a K7 CTA that one batch produces (up to
+// thousands for skewed inputs at 10^8-10^9 keys) are fitted together: one
+// min/max launch, one sampling launch and one fit launch for all of them,
+// instead of five launches per node.  A chunk list maps every CTA to its node
+// (cnode[b]) and its first chunk (nfirst[node]).
+constexpr int MMB_CHUNK = 16384;   // keys per min/max CTA
+constexpr int FSB_CHUNK = 256;     // samples per sampling CTA
+
+template <class K>
+__global__ void __launch_bounds__(MM_THREADS) k_minmax_batch(const DevCtx *__restrict__ c, const u32 *__restrict__ cnode,
+                                                            const u32 *__restrict__ nfirst) {
+    pdl_entry();
+    if (*c->nan_flag) return;
+    const u32 node = cnode[blockIdx.x];
+    GNode &g = c->nodes[node];
+    const u64 s0 = (u64)(blockIdx.x - nfirst[node]) * MMB_CHUNK, s1 = min((u64)g.m, s0 + MMB_CHUNK);
+    const u64 *x = c->buf[g.src] + g.off;
+    u64 mn = ~0ull, mx = 0;
+    bool nan = false;
+    constexpr int U = MMB_CHUNK / MM_THREADS;   // 64 keys per thread, 8 loads in flight
+#pragma unroll 8
+    for (int q = 0; q < U; ++q) {
+        const u64 i = s0 + threadIdx.x + (u64)q * MM_THREADS;
+        if (i < s1) mm_acc<K>(x[i], mn, mx, nan);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        u64 a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn; mx = b > mx ? b : mx;
+    }
+    __shared__ u64 smn[MM_THREADS / 32], smx[MM_THREADS / 32];
+    if ((threadIdx.x & 31) == 0) { smn[threadIdx.x >> 5] = mn; smx[threadIdx.x >> 5] = mx; }
+    if (__syncthreads_or(nan) && threadIdx.x == 0) atomicOr(c->nan_flag, 1u);
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < MM_THREADS / 32; ++w) { mn = smn[w] < mn ? smn[w] : mn; mx = smx[w] > mx ? smx[w] : mx; }
+        atomicMin(&g.kmin, mn);
+        atomicMax(&g.kmax, mx);
+    }
+}
+
+// alpha samples of every node -> per-bin counts; the first CTA of a node
+// publishes its model (and the R9/R10 verdict) like k_fit_sample.
+template <class K>
+__global__ void __launch_bounds__(FSB_CHUNK) k_fit_sample_batch(const DevCtx *__restrict__ c, const u32 *__restrict__ cnode,
+                                                               const u32 *__restrict__ nfirst) {
+    pdl_entry();
+    if (*c->nan_flag) return;
+    const u32 node = cnode[blockIdx.x];
+    GNode &g = c->nodes[node];
+    Model md;
+    const bool ok = make_model<K>(g.kmin, g.kmax, g.beta, md);
+    const u32 cb = blockIdx.x - nfirst[node];
+    if (cb == 0 && threadIdx.x == 0) {
+        g.md = md;
+        g.degenerate = ok ? 0u : 1u;
+        if (!ok) push_item(c, g.off, g.m, g.level, g.src, 1u);   // Standard-Sort the whole segment
+    }
+    if (!ok) return;
+    const u32 k = cb * FSB_CHUNK + threadIdx.x;
+    if (k >= g.alpha) return;
+    const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
+    const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, g.off), k, g.m);
+    atomicAdd(&g.cnt[interval_index<K>(K::to_okey(c->buf[g.src][g.off + pos]), md)], 1u);
+}
+
 // ------------------------------------------------------------------ splits
 __device__ __forceinline__ u32 find_split(const SplitTask *L, u32 ns, u32 tile) {
     u32 lo = 0, hi = ns - 1;
@@ -639,6 +704,48 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_fit_final(const DevCtx *__rest
             if (logging) db += digest_term(i, e);
             if (copy_l1 && i - 1 < c->l1_cap) c->l1_b[i - 1] = e;
         }
+    }
+    if (logging) {
+        for (int o = 16; o > 0; o >>= 1) db += __shfl_xor_sync(0xffffffffu, db, o);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&dsum, (unsigned long long)db);
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd((unsigned long long *)&g.digest_b, dsum);
+    }
+}
+
+// b = prefix of the counts and T of one node per CTA (the batched nodes have
+// up to a few thousand bins: the CTA walks them SCAN_CHUNK at a time).
+__global__ void __launch_bounds__(SCAN_THREADS) k_fit_batch(const DevCtx *__restrict__ c, const u32 *__restrict__ nlist) {
+    pdl_entry();
+    __shared__ u32 wsum[33];
+    __shared__ unsigned long long dsum;
+    if (*c->nan_flag) return;
+    GNode &g = c->nodes[nlist[blockIdx.x]];
+    if (g.degenerate) return;
+    const u64 nb = (u64)g.beta + 1;
+    const bool logging = c->rec != nullptr;
+    u32 *in = g.cnt + 1;
+    if (threadIdx.x == 0) dsum = 0;
+    u32 carry = 0;
+    u64 db = 0;
+    for (u64 base0 = 0; base0 < nb; base0 += SCAN_CHUNK) {
+        const u64 base = base0 + (u64)threadIdx.x * SCAN_ITEMS;
+        u32 v[SCAN_ITEMS], sm = 0;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) { v[k] = base + k < nb ? in[base + k] : 0; sm += v[k]; }
+        u32 total;
+        u32 e = block_excl_scan_1024(sm, wsum, total) + carry;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) {
+            e += v[k];
+            if (base + k < nb) {
+                const u64 i = base + k + 1;
+                in[base + k] = e;
+                g.T[i] = bucket_of(e, g.alpha, g.gamma);
+                if (logging) db += digest_term(i, e);
+            }
+        }
+        carry += total;
     }
     if (logging) {
         for (int o = 16; o > 0; o >>= 1) db += __shfl_xor_sync(0xffffffffu, db, o);

@@ -173,3 +173,11 @@ def test_split_scatter_exact_rank_path(pcf, name, n):
     """The split scatter's fallback (exact re-rank of every same-chunk, same-digit
     group by source index), forced on every tile: identical output and records."""
     compare(pcf, synth.config(name, n=n), exact_ranks=True)
+
+
+def test_batched_global_nodes(pcf):
+    """LogNormal at 2e7 keys: hundreds of level-1 buckets are too large for a K7 CTA and
+    become global nodes fitted in one batch (k_minmax_batch / k_fit_sample_batch /
+    k_fit_batch); output, every node record and level-1 b/H must still match."""
+    _, info = compare(pcf, synth.config("c2", n=20_000_000))
+    assert info.stats["global_nodes"] > 100
