@@ -597,8 +597,9 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
                 u64 *cur = dst0;
                 for (u64 w = K8_TILE; w < m; w *= 2) {
                     u64 *nxt = cur == bo ? bt : bo;
-                    k8_partition<K><<<(nblk + 255) / 256, 256, 0, st>>>(cur, m, w, nblk, k8_sp, flag);
-                    k8_merge<K><<<nblk, K8_THREADS, K8_MERGE_SMEM, st>>>(cur, nxt, m, w, k8_sp, flag, 2 * w >= m ? 1u : 0u);
+                    const u32 nmt = (u32)((m + K8_MTILE - 1) / K8_MTILE);
+                    k8_partition<K><<<(nmt + 255) / 256, 256, 0, st>>>(cur, m, w, nmt, k8_sp, flag);
+                    k8_merge<K><<<nmt, K8_MTHREADS, K8_MERGE_SMEM, st>>>(cur, nxt, m, w, k8_sp, flag, 2 * w >= m ? 1u : 0u);
                     cur = nxt;
                     launches += 2;
                 }

@@ -17,7 +17,16 @@ namespace pcf {
 constexpr int K8_THREADS = 512;
 constexpr int K8_TILE = 4096;
 constexpr int K8_IPT = K8_TILE / K8_THREADS;   // 8
-constexpr int K8_MERGE_SMEM = K8_TILE * 8;
+#ifndef PCF_K8_MTILE
+#define PCF_K8_MTILE 1024
+#endif
+#ifndef PCF_K8_MTHREADS
+#define PCF_K8_MTHREADS 256
+#endif
+constexpr int K8_MTILE = PCF_K8_MTILE;            // outputs of one merge CTA
+constexpr int K8_MTHREADS = PCF_K8_MTHREADS;
+constexpr int K8_MIPT = K8_MTILE / K8_MTHREADS;   // outputs per merge thread
+constexpr int K8_MERGE_SMEM = K8_MTILE * 8;
 constexpr int K8_SORT_SMEM = 2 * K8_TILE * 8;
 
 // flag[0] = 1 if the bucket holds two different keys; flag[1] = first key
@@ -44,10 +53,11 @@ __device__ __forceinline__ u32 k8_split(const u64 *A, u32 la, const u64 *B, u32 
 }
 
 // K8_IPT consecutive outputs of merge(A, B) starting at A[ia], B[ib] into o[].
-__device__ __forceinline__ void k8_merge_seq(const u64 *A, u32 la, const u64 *B, u32 lb, u32 ia, u32 ib, u64 (&o)[K8_IPT]) {
+template <int NO>
+__device__ __forceinline__ void k8_merge_seq(const u64 *A, u32 la, const u64 *B, u32 lb, u32 ia, u32 ib, u64 (&o)[NO]) {
     u64 xa = ia < la ? A[ia] : ~0ull, xb = ib < lb ? B[ib] : ~0ull;
 #pragma unroll
-    for (int k = 0; k < K8_IPT; ++k) {
+    for (int k = 0; k < NO; ++k) {
         const bool ta = ib >= lb || (ia < la && xa <= xb);
         o[k] = ta ? xa : xb;
         if (ta) { ++ia; xa = ia < la ? A[ia] : ~0ull; }
@@ -104,7 +114,7 @@ __global__ void __launch_bounds__(K8_THREADS) k8_blocksort(const u64 *__restrict
         const u32 p0 = (t0 / (2 * run)) * (2 * run), d = t0 - p0;
         const u64 *A = sa + p0, *B = sa + p0 + run;
         const u32 ia = k8_split(A, run, B, run, d);
-        k8_merge_seq(A, run, B, run, ia, d - ia, r);
+        k8_merge_seq<K8_IPT>(A, run, B, run, ia, d - ia, r);
 #pragma unroll
         for (int k = 0; k < K8_IPT; ++k) sb[t0 + k] = r[k];
         __syncthreads();
@@ -120,7 +130,7 @@ __global__ void k8_partition(const u64 *__restrict__ src, u64 m, u64 width, u32 
                              const u32 *__restrict__ flag) {
     const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntiles || *flag == 0) return;
-    const u64 o0 = (u64)t * K8_TILE;
+    const u64 o0 = (u64)t * K8_MTILE;
     const u64 pair0 = (o0 / (2 * width)) * (2 * width);
     const u64 na = min(pair0 + width, m) - pair0, nb = min(pair0 + 2 * width, m) - min(pair0 + width, m);
     const u64 d = o0 - pair0;
@@ -134,45 +144,45 @@ __global__ void k8_partition(const u64 *__restrict__ src, u64 m, u64 width, u32 
 }
 
 template <class K>
-__global__ void __launch_bounds__(K8_THREADS) k8_merge(const u64 *__restrict__ src, u64 *__restrict__ dst, u64 m, u64 width,
+__global__ void __launch_bounds__(K8_MTHREADS) k8_merge(const u64 *__restrict__ src, u64 *__restrict__ dst, u64 m, u64 width,
                                                       const u32 *__restrict__ sp, const u32 *__restrict__ flag, u32 last) {
     extern __shared__ __align__(16) u64 k8_smem[];   // K8_TILE input keys
     u64 *sa = k8_smem;
     if (*flag == 0) return;
     const u32 t = blockIdx.x;
-    const u64 o0 = (u64)t * K8_TILE;
+    const u64 o0 = (u64)t * K8_MTILE;
     if (o0 >= m) return;
     const u64 pair0 = (o0 / (2 * width)) * (2 * width);
     const u64 na = min(pair0 + width, m) - pair0, nb = min(pair0 + 2 * width, m) - min(pair0 + width, m);
-    const u64 d0 = o0 - pair0, d1 = min(d0 + K8_TILE, na + nb);
+    const u64 d0 = o0 - pair0, d1 = min(d0 + K8_MTILE, na + nb);
     const u32 ia0 = sp[t];
     const u32 ia1 = d1 == na + nb ? (u32)na : sp[t + 1];
     const u32 ib0 = (u32)(d0 - ia0), ib1 = (u32)(d1 - ia1);
     const u32 la = ia1 - ia0, lb = ib1 - ib0, tot = la + lb;
     const u64 *A = src + pair0, *B = src + pair0 + na;
     {   // all loads of a thread in flight at once, then the stores to shared memory
-        u64 v[K8_IPT];
+        u64 v[K8_MIPT];
 #pragma unroll
-        for (int j = 0; j < K8_IPT; ++j) {
-            const u32 k = threadIdx.x + j * K8_THREADS;
+        for (int j = 0; j < K8_MIPT; ++j) {
+            const u32 k = threadIdx.x + j * K8_MTHREADS;
             v[j] = k < la ? A[ia0 + k] : k < tot ? B[ib0 + (k - la)] : 0ull;
         }
 #pragma unroll
-        for (int j = 0; j < K8_IPT; ++j) {
-            const u32 k = threadIdx.x + j * K8_THREADS;
+        for (int j = 0; j < K8_MIPT; ++j) {
+            const u32 k = threadIdx.x + j * K8_MTHREADS;
             if (k < tot) sa[k] = v[j];
         }
     }
     __syncthreads();
     // per thread: K8_IPT consecutive outputs from its own merge-path split, stored
     // straight from registers (a warp writes 32 x 64 contiguous bytes)
-    const u32 dd = min(threadIdx.x * K8_IPT, tot);
+    const u32 dd = min(threadIdx.x * K8_MIPT, tot);
     const u32 ia = k8_split(sa, la, sa + la, lb, dd);
-    u64 r[K8_IPT];
-    k8_merge_seq(sa, la, sa + la, lb, ia, dd - ia, r);
+    u64 r[K8_MIPT];
+    k8_merge_seq<K8_MIPT>(sa, la, sa + la, lb, ia, dd - ia, r);
     u64 *outp = dst + o0 + dd;
 #pragma unroll
-    for (int k = 0; k < K8_IPT; ++k) if (dd + k < tot) outp[k] = last ? K::from_okey(r[k]) : r[k];
+    for (int k = 0; k < K8_MIPT; ++k) if (dd + k < tot) outp[k] = last ? K::from_okey(r[k]) : r[k];
 }
 
 }  // namespace pcf
