@@ -14,8 +14,14 @@
 
 namespace pcf {
 
-constexpr int K8_THREADS = 512;
-constexpr int K8_TILE = 4096;
+#ifndef PCF_K8_THREADS
+#define PCF_K8_THREADS 512
+#endif
+constexpr int K8_THREADS = PCF_K8_THREADS;
+#ifndef PCF_K8_TILE
+#define PCF_K8_TILE 4096
+#endif
+constexpr int K8_TILE = PCF_K8_TILE;
 constexpr int K8_IPT = K8_TILE / K8_THREADS;   // 8
 #ifndef PCF_K8_MTILE
 #define PCF_K8_MTILE 1024
