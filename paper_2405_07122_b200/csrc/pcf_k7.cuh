@@ -15,15 +15,18 @@
 //
 // Work split inside the CTA:
 //  * CTA-wide (16 warps): the K7_GROUP placement by the global model, and any
-//    node of more than GCAP keys (its children are < delta <= 861 keys).
-//  * Node groups (4 groups of 4 warps, named barriers 1..4): every other node
-//    is run, start to finish, by one group, with its keys held in registers
-//    (<= 16 per thread): min/max, alpha seeded samples (R3) ->
-//    per-bin counts, b = prefix, T, classify + per-warp
-//    counts, one column pass (bucket sizes, destinations, Alg. 1
-//    dispatch), placement, and Standard-Sort of the leaf buckets.  Recursing
-//    buckets go onto the group's stack; groups take the task's level-1 nodes
-//    from a shared list.  Groups never wait for each other inside a task.
+//    node of more than 2 GCAP keys (its children are < delta <= 861 keys).
+//  * Every other node is run, start to finish, by as few warps as hold its keys
+//    in registers (<= 16 per thread): double teams of 8 warps (nodes <= 4096,
+//    named barriers 5-6), teams of 4 (<= 2048, barriers 1-4), single warps
+//    (<= 512, with their whole subtrees, depth-first on a per-warp stack).
+//    A node step: min/max, alpha seeded samples (R3) -> per-bin
+//    counts, b = prefix, T, classify + per-warp counts, one
+//    column pass (bucket sizes, destinations, Alg. 1 lines 160-167 dispatch),
+//    placement, and Standard-Sort of the leaf buckets.  Teams publish their
+//    children to a small-node list that the single warps drain; no set of warps
+//    waits for another inside a task.  The next task is claimed early and
+//    bulk-copied into B while the current one is written out.
 //  * Buffers: a node at relative depth r lives in A (r even) or B (r odd);
 //    recursing buckets are placed into the other buffer, leaf buckets of
 //    >= 2 keys into B (scratch) and then sorted into A, single keys straight
