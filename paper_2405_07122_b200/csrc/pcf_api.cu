@@ -474,7 +474,11 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             CK(launch_pdl(k_tile_map, nsm * 2, 256, 0, st, (const DevCtx *)d_ctx, cur));
             tm.end();
             tm.begin(PH_COUNT);
-            if (n <= (1ull << 25)) CK(launch_pdl(k_split_count_tile<K>, tile_grid, SC_THREADS, 0, st, (const DevCtx *)d_ctx, cur));
+            // one CTA per tile for small sorts and for rounds after the first (their T
+            // gathers are local to a split: they need L1, which the persistent kernel's
+            // 2 x 111 KB of staging takes); the persistent bulk-copy kernel for the first
+            // round of a large sort (gather-free digit table)
+            if (n <= (1ull << 25) || round > 0) CK(launch_pdl(k_split_count_tile<K>, tile_grid, SC_THREADS, 0, st, (const DevCtx *)d_ctx, cur));
             else CK(launch_pdl(k_split_count<K>, nsm * count_ctas_per_sm<K>(), CNT_THREADS, sizeof(CountSmem), st, (const DevCtx *)d_ctx, cur));
             tm.end();
             tm.begin(PH_OTHER);
