@@ -164,7 +164,7 @@ struct PhaseTimer {
 
 enum { PH_MINMAX = 0, PH_FIT = 1, PH_COUNT = 2, PH_SCATTER = 3, PH_K7 = 4, PH_K8 = 5, PH_OTHER = 6, PH_TOTAL = 7 };
 
-static int k7_smem_bytes() { return (int)sizeof(K7Smem); }
+static int k7_smem_bytes(u32 tau = 2) { return (int)(sizeof(K7Smem) + k7_lists_bytes(tau < 2 ? 2 : tau)); }
 static int split_smem_bytes() { return (int)sizeof(SplitScatterSmem); }
 
 // Launch with programmatic stream serialization (see pdl_entry()).
@@ -356,7 +356,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         u32 one = 1;
         CK(cudaMemcpyAsync(&d_cnt->k7_count, &one, 4, cudaMemcpyHostToDevice, st));
         tm.begin(PH_K7);
-        k7_kernel<K><<<1, K7_THREADS, k7_smem_bytes(), st>>>(d_ctx);
+        k7_kernel<K><<<1, K7_THREADS, k7_smem_bytes(p.tau), st>>>(d_ctx);
         CK(cudaGetLastError());
         tm.end();
         launches++;
@@ -509,7 +509,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             // K7 over every group produced so far (persistent grid; reads the task count on the device)
             tm.begin(PH_K7);
             CK(launch_pdl(k_k7_order, 1, 1024, 0, st, (const DevCtx *)d_ctx));
-            CK(launch_pdl(k7_kernel<K>, nsm * k7_ctas_per_sm<K>(), K7_THREADS, k7_smem_bytes(), st, (const DevCtx *)d_ctx));
+            CK(launch_pdl(k7_kernel<K>, nsm * k7_ctas_per_sm<K>(), K7_THREADS, k7_smem_bytes(p.tau), st, (const DevCtx *)d_ctx));
             CK(launch_pdl(k_k7_advance, 1, 1, 0, st, (const DevCtx *)d_ctx));
             tm.end();
             CK(cudaGetLastError());

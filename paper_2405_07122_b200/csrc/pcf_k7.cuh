@@ -54,8 +54,14 @@ constexpr int CCOLS = NB_CAP + 2;                  // counter columns (CTA view)
 constexpr int WCOLS = 128;                         // T / size columns per warp slice: >= iroot34(WCAP) + 2 = 109;
                                                    // a team's slices give 512 >= iroot34(GCAP) + 2 = 306
 constexpr u32 SMALL_MAX = 64;                      // leaves up to this size: key-parallel rank sort
-constexpr int LIST_CAP = S_CAP / 2;                // nodes hold >= tau >= 2 keys
-constexpr int LSM_CAP = LIST_CAP + K7_WARPS + 16;  // small-node list: + one over-claimed ticket per warp
+// Node lists live after K7Smem, sized for tau (nodes hold >= tau keys): the
+// small-node list holds <= S_CAP / tau entries (+ one over-claimed ticket per
+// warp), a warp's DFS stack <= WCAP / tau.  For the default tau = 64 that is
+// ~1 KB instead of the 33 KB tau = 2 needs, which leaves L1 to the T gathers.
+__host__ __device__ inline u32 k7_list_cap(u32 tau) { return (u32)S_CAP / tau > 0 ? (u32)S_CAP / tau : 1u; }
+__host__ __device__ inline u32 k7_lsm_cap(u32 tau) { return k7_list_cap(tau) + K7_WARPS + 16; }
+__host__ __device__ inline u32 k7_stk_cap(u32 tau) { return (u32)WCAP / tau > 0 ? (u32)WCAP / tau : 1u; }
+__host__ __device__ inline size_t k7_lists_bytes(u32 tau) { return 4ull * (k7_lsm_cap(tau) + (u64)K7_WARPS * k7_stk_cap(tau)); }
 constexpr int LBIG_CAP = 32;                       // nodes > WCAP keys of one task (<= 16)
 constexpr int STK_CAP = WCAP / 2;                  // per-warp DFS stack
 constexpr int BL_CAP = 128;                        // leaves > SMALL_MAX keys of one node: <= S_CAP / 65
@@ -81,9 +87,7 @@ struct K7Smem {
     u16 T16[TCOLS];    // bucket table of the current node (slices of the node's warps)
     u16 hcol[TCOLS];   // bucket sizes of the current node (same slices)
     u16 LC[S_CAP];                // per position: bucket column of a B-leaf key, 0 otherwise
-    u32 lsm[LSM_CAP];             // nodes <= WCAP keys (tickets; 0 = not yet pushed)
     u32 lbig[LBIG_CAP];           // nodes > WCAP keys
-    u32 stk[K7_WARPS][STK_CAP];   // per-warp DFS stacks (a team's first stack: its children before publication)
     u32 bl[BL_CAP];               // leaves > SMALL_MAX keys of the current node (slices of the node's warps)
     u64 wmn[K7_WARPS], wmx[K7_WARPS];
     u32 wsum[K7_WARPS];
@@ -103,9 +107,15 @@ struct K7Smem {
     u32 gdelta, glevel, gjlo, gjhi;
     long long prof_t;                       // PCF_FLAG_PROFILE bookkeeping (thread 0)
     unsigned long long prof[K7_PROF_SLOTS];
+    u32 *lsm;                     // nodes <= WCAP keys (tickets; 0 = not yet pushed)   [lsm_cap]
+    u32 *stk;                     // per-warp DFS stacks, row w at stk + w * stk_cap (a team's rows:
+                                  // its children before publication)                     [K7_WARPS * stk_cap]
+    u32 lsm_cap, list_cap, stk_cap;
+    unsigned char tail[];         // the lists (dynamic shared memory past the struct)
 };
 
-static_assert(sizeof(K7Smem) <= 232448, "K7 shared memory exceeds 227 KB");
+static_assert(sizeof(K7Smem) + 4 * ((S_CAP / 2) + K7_WARPS + 16 + K7_WARPS * (WCAP / 2)) <= 232448,
+              "K7 shared memory (tau = 2) exceeds 227 KB");
 
 // K7 phase profiling (PCF_FLAG_PROFILE): thread 0 charges the cycles since the
 // previous mark to slot `id` (barrier waits included).  Slots: 0 claim, 1 load,
@@ -484,10 +494,10 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
                             if (sl < (u32)LBIG_CAP) S.lbig[sl] = e; else atomicOr(c->err_flag, 2u);
                         } else if (CTA) {
                             const u32 sl = atomicAdd(&S.stot, 1u);
-                            if (sl < (u32)LIST_CAP) S.lsm[sl] = e; else atomicOr(c->err_flag, 2u);
+                            if (sl < S.list_cap) S.lsm[sl] = e; else atomicOr(c->err_flag, 2u);
                         } else {   // warp: own stack; team: staged in its warps' stacks (contiguous rows)
                             const u32 sl = atomicAdd(&S.top[w0], 1u);
-                            if (sl < (u32)(STK_CAP * NW)) (&S.stk[w0][0])[sl] = e; else atomicOr(c->err_flag, 2u);
+                            if (sl < S.stk_cap * NW) S.stk[w0 * S.stk_cap + sl] = e; else atomicOr(c->err_flag, 2u);
                         }
                     } else if (hh > SMALL_MAX) {
                         const u32 sl = atomicAdd(&S.nbl[w0], 1u);
@@ -548,7 +558,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
             __threadfence_block();
             for (u32 i = t; i < nc; i += NT) {
                 const u32 sl = atomicAdd(&S.stot, 1u);
-                if (sl < (u32)LIST_CAP) *(volatile u32 *)&S.lsm[sl] = (&S.stk[w0][0])[i]; else atomicOr(c->err_flag, 2u);
+                if (sl < S.list_cap) *(volatile u32 *)&S.lsm[sl] = S.stk[w0 * S.stk_cap + i]; else atomicOr(c->err_flag, 2u);
             }
         }
     }
@@ -654,7 +664,7 @@ __device__ __forceinline__ void push_root(const DevCtx *c, K7Smem &S, u32 e) {
         if (sl < (u32)LBIG_CAP) S.lbig[sl] = e; else atomicOr(c->err_flag, 2u);
     } else {
         const u32 sl = atomicAdd(&S.stot, 1u);
-        if (sl < (u32)LIST_CAP) S.lsm[sl] = e; else atomicOr(c->err_flag, 2u);
+        if (sl < S.list_cap) S.lsm[sl] = e; else atomicOr(c->err_flag, 2u);
     }
 }
 
@@ -671,7 +681,13 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
     const Grp<GW> GG{1 + w / GW, threadIdx.x % GT, (w / GW) * GW};            // barriers 1..4
     const Grp<2 * GW> GH{1 + NGRP + w / (2 * GW), threadIdx.x % (2 * GT), (w / (2 * GW)) * (2 * GW)};   // 5..6
     const Grp<1> GS{w, lane, w};
-    for (u32 i = threadIdx.x; i < (u32)LSM_CAP; i += K7_THREADS) S.lsm[i] = 0;   // tickets read 0 until pushed
+    if (threadIdx.x == 0) {
+        S.lsm_cap = k7_lsm_cap(c->tau); S.list_cap = k7_list_cap(c->tau); S.stk_cap = k7_stk_cap(c->tau);
+        S.lsm = reinterpret_cast<u32 *>(S.tail);
+        S.stk = S.lsm + S.lsm_cap;
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < S.lsm_cap; i += K7_THREADS) S.lsm[i] = 0;   // tickets read 0 until pushed
     if (c->k7_prof && threadIdx.x == 0) {
         for (int i = 0; i < K7_PROF_SLOTS; ++i) S.prof[i] = 0;
         S.prof_t = clock64();
@@ -802,10 +818,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 u32 e = 0;
                 if (lane == 0) {
                     if (S.top[w] > 0) {
-                        e = S.stk[w][--S.top[w]];
+                        e = S.stk[w * S.stk_cap + (--S.top[w])];
                     } else {
                         const u32 tk = atomicAdd(&S.snext, 1u);
-                        volatile u32 *slot = &S.lsm[tk < (u32)LSM_CAP ? tk : LSM_CAP - 1];
+                        volatile u32 *slot = &S.lsm[tk < S.lsm_cap ? tk : S.lsm_cap - 1];
                         u32 ns = 32;
                         for (;;) {   // wait (backing off, so the working teams keep the issue slots)
                             e = *slot;
