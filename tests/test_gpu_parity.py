@@ -181,3 +181,17 @@ def test_batched_global_nodes(pcf):
     k_fit_batch); output, every node record and level-1 b/H must still match."""
     _, info = compare(pcf, synth.config("c2", n=20_000_000))
     assert info.stats["global_nodes"] > 100
+
+
+def test_batched_degenerate_and_sample_all_nodes(pcf):
+    """Oversized recursing buckets that are degenerate (one repeated value: R9, the
+    whole node goes to Standard-Sort) or fitted in SAMPLE_ALL mode, through the
+    batched global-node path."""
+    rng = np.random.default_rng(5)
+    x = synth.generate("uniform", 3_000_000, 3)
+    for v in (0.25, 0.5, 0.75):                  # 20 000 copies each: buckets > S_CAP, < delta
+        idx = rng.choice(x.size, 20_000, replace=False)
+        x[idx] = v
+    _, info = compare(pcf, x)
+    assert info.stats["global_nodes"] > 1
+    compare(pcf, synth.config("c2", n=3_000_000), sample_all=True)
