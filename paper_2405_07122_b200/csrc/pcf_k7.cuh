@@ -294,7 +294,8 @@ __device__ __forceinline__ void classify_slots(const u64 (&key)[KPT], u32 (&pk)[
 }
 
 template <class K, int NW, int MODE>
-__device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos, u32 m, u32 L, u32 rel, u64 gbase) {
+__device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos, u32 m, u32 L, u32 rel, u64 gbase,
+                          const u64 *raw = nullptr) {   // MODE_GLOBAL: raw keys (bulk-copied task) instead of A
     constexpr u32 NT = NW * 32;
     constexpr bool CTA = NW == K7_WARPS;
     // bins / columns per thread: node <= S_CAP (CTA, 862 bins; 1024 group columns) or <= GCAP (group, 305)
@@ -327,7 +328,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
     for (int q = 0; q < KPT; ++q) {
         const u32 f = f0 + q * 32 + lane;
         const bool v = f < f1;
-        key[q] = X[pos + (v ? f : 0u)];
+        key[q] = (MODE == MODE_GLOBAL && raw) ? K::to_okey(raw[v ? f : 0u]) : X[pos + (v ? f : 0u)];
         pk[q] = v ? 0u : NONE;
         mn = v && key[q] < mn ? key[q] : mn;
         mx = v && key[q] > mx ? key[q] : mx;
@@ -717,7 +718,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
         u64 *dst = sort_task ? S.B : S.A;
         bool nan_here = false;
         mbar_wait(&S.tbar, it & 1u);
-        if (S.ldirect) {
+        // a K7_GROUP task's placement reads the raw bulk-copied keys itself (no pass over B)
+        const bool raw_group = task.kind == K7_GROUP && !S.ldirect;
+        if (raw_group) {
+        } else if (S.ldirect) {
             nan_here = load_task<K>(dst, c->buf[task.src] + task.off, M);
         } else {   // raw keys at B[lhead + i] -> ordered keys at dst[i]
             const u32 hd = S.lhead;
@@ -757,7 +761,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 }
                 __syncthreads();
                 Lb = S.glevel;
-                node_step<K, K7_WARPS, MODE_GLOBAL>(c, S, CT, 0, M, Lb, 0, task.off);
+                node_step<K, K7_WARPS, MODE_GLOBAL>(c, S, CT, 0, M, Lb, 0, task.off, raw_group ? S.B + S.lhead : nullptr);
                 prof_mark(c, S, 2);
             } else {   // K7_NODE: a fresh Learned-Sort call on the whole task
                 Lb = task.level;
