@@ -303,12 +303,13 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     value = m * args.steps / dt
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json recipe)",
         "config": {"workload": WORKLOADS.get(args.config, args.config), "n": n, "dist": cfg["dist"],
-                   "seed": cfg["seed"], "parallelism": "1 CPU thread"},
+                   "seed": cfg["seed"],
+                   "parallelism": f"oracle on 1 CPU thread (rank 0 of the --gpus {args.gpus} launch)"},
         "cpu_baseline": {"value": value, "unit": "keys/s", "cores": 1, "kind": "oracle",
                          "sample": f"{args.config} recipe at n={m}, {args.steps} timed runs"},
         "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
