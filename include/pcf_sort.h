@@ -38,6 +38,7 @@ extern "C" {
 #define PCF_ERR_CUDA 5                 /* a CUDA runtime call failed (see pcf_last_error())            */
 #define PCF_ERR_LOG_OVERFLOW 6         /* pass log capacity exceeded (records beyond capacity dropped) */
 #define PCF_ERR_INTERNAL 7             /* internal capacity bound violated (bug)                       */
+#define PCF_ERR_DEGENERATE 8           /* pcf_bucket_counts_f64: x_max == x_min, M_PCF undefined (R9)   */
 
 /* ---- key types ---------------------------------------------------------- */
 #define PCF_KEY_F64 0   /* IEEE binary64, ascending under IEEE-754 totalOrder (-0.0 before +0.0) */
@@ -144,6 +145,27 @@ int pcf_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const pcf_params *
  * before return.  in_host == out_host is allowed. */
 int pcf_sort_f64_host(const double *in_host, double *out_host, size_t n, const pcf_params *p, void *stream);
 int pcf_sort_u64_host(const uint64_t *in_host, uint64_t *out_host, size_t n, const pcf_params *p, void *stream);
+
+/* ---- the paper's bucketing-failure experiment (§4.3, Fig. 4)
+ * One model-based bucketing step M_PCF (Alg. 1, PAPER.md:152-158;
+ * model PAPER.md:288-308) of n float64 keys with DECOUPLED alpha, beta, gamma
+ * (the sort fixes alpha = beta = gamma = delta = floor(n^{3/4})):
+ *   sample a_k = keys[pos_k], k = 0..alpha-1, pos_k from the sampler of reading
+ *     R3 for the root node (level 1, offset 0) and `seed`, with replacement;
+ *   b[i] = |{k : i(a_k) <= i}|, i = 1..beta+1, with i(x) of reading R6;
+ *   H[j] = |c_j| = |{x : floor(b[i(x)] * gamma / alpha) + 1 = j}|, j = 1..gamma+1 (R7).
+ * The paper's "bucketing failure" is max_j |c_j| > delta (the caller compares).
+ * keys:       DEVICE, n f64 keys, 8-byte aligned, not modified.
+ * b_out:      DEVICE, beta + 1 uint32 (b[1..beta+1], stored 0-based), overwritten.
+ * H_out:      DEVICE, gamma + 1 uint32 (|c_1|..|c_{gamma+1}|), overwritten.
+ * max_bucket: HOST, receives max_j |c_j|; may be NULL.
+ * Synchronous on `stream` (one 24-byte device scratch, stream-ordered alloc).
+ * Errors: PCF_ERR_INVALID_ARG (NULL pointer, n < 2 or n >= 2^32, alpha, beta or
+ * gamma 0 or >= 2^32, beta + 1 or gamma + 1 overflow) before any launch;
+ * PCF_ERR_NAN if a key is NaN; PCF_ERR_DEGENERATE if all keys are equal (b_out,
+ * H_out unspecified after either); PCF_ERR_CUDA / PCF_ERR_OOM. */
+int pcf_bucket_counts_f64(const double *keys, size_t n, uint64_t alpha, uint64_t beta, uint64_t gamma,
+                          uint64_t seed, uint32_t *b_out, uint32_t *H_out, uint64_t *max_bucket, void *stream);
 
 /* Human-readable name of a status code (static storage). */
 const char *pcf_status_string(int status);

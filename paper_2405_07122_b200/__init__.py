@@ -12,14 +12,15 @@ import os
 
 from ._build import LIB_PATH, build  # noqa: F401
 
-__all__ = ["build", "lib", "sort", "sort_host", "workspace_bytes", "host_workspace_bytes", "PCFError", "KEY_F64", "KEY_U64",
+__all__ = ["build", "lib", "sort", "bucket_counts", "sort_host", "workspace_bytes", "host_workspace_bytes", "PCFError", "KEY_F64", "KEY_U64",
            "FLAG_SYNC", "FLAG_SAMPLE_ALL", "FLAG_TIMING", "PHASES"]
 
 KEY_F64, KEY_U64 = 0, 1
 FLAG_SYNC, FLAG_SAMPLE_ALL, FLAG_TIMING, FLAG_PROFILE, FLAG_EXACT_RANKS = 1, 2, 4, 8, 16
 PHASES = ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "total"]
 STATUS = {0: "PCF_OK", 1: "PCF_ERR_INVALID_ARG", 2: "PCF_ERR_NAN", 3: "PCF_ERR_WORKSPACE_TOO_SMALL",
-          4: "PCF_ERR_OOM", 5: "PCF_ERR_CUDA", 6: "PCF_ERR_LOG_OVERFLOW", 7: "PCF_ERR_INTERNAL"}
+          4: "PCF_ERR_OOM", 5: "PCF_ERR_CUDA", 6: "PCF_ERR_LOG_OVERFLOW", 7: "PCF_ERR_INTERNAL",
+          8: "PCF_ERR_DEGENERATE"}
 
 
 class NodeRecord(ctypes.Structure):
@@ -70,7 +71,8 @@ class PCFError(RuntimeError):
 
 _lib = None
 SYMBOLS = ["pcf_params_init", "pcf_workspace_bytes", "pcf_sort_f64", "pcf_sort_u64", "pcf_sort_f64_host",
-           "pcf_sort_u64_host", "pcf_status_string", "pcf_last_error", "pcf_abi_version"]
+           "pcf_sort_u64_host", "pcf_status_string", "pcf_last_error", "pcf_abi_version",
+           "pcf_bucket_counts_f64"]
 
 
 def lib():
@@ -93,6 +95,9 @@ def lib():
         L.pcf_status_string.argtypes = [i32]; L.pcf_status_string.restype = ctypes.c_char_p
         L.pcf_last_error.argtypes = []; L.pcf_last_error.restype = ctypes.c_char_p
         L.pcf_abi_version.argtypes = []; L.pcf_abi_version.restype = i32
+        u64 = ctypes.c_uint64
+        L.pcf_bucket_counts_f64.argtypes = [vp, sz, u64, u64, u64, u64, vp, vp, ctypes.POINTER(u64), vp]
+        L.pcf_bucket_counts_f64.restype = i32
         _ = u32
         _lib = L
     return _lib
@@ -189,6 +194,30 @@ def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False,
         info.level1_b = b.cpu().numpy().view(np.uint32)
         info.level1_h = h.cpu().numpy().view(np.uint32)
     return out, info
+
+
+def bucket_counts(x, alpha: int, beta: int, gamma: int, *, seed: int = 0, b=None, H=None, stream=None):
+    """One M_PCF bucketing step with decoupled alpha, beta, gamma (the §4.3
+    failure experiment) through ``pcf_bucket_counts_f64``.
+
+    x: 1-D CUDA float64 tensor.  Returns ``(b, H, max_bucket)``: b[1..beta+1]
+    and H = |c_1|..|c_{gamma+1}| as CUDA uint32 tensors (0-based), and
+    max_j |c_j| (the experiment's failure is ``max_bucket > delta``).
+    """
+    import torch
+
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float64:
+        raise TypeError("x must be a CUDA float64 tensor (no CPU fallback)")
+    x = x.contiguous()
+    if b is None:
+        b = torch.empty(beta + 1, dtype=torch.uint32, device=x.device)
+    if H is None:
+        H = torch.empty(gamma + 1, dtype=torch.uint32, device=x.device)
+    mx = ctypes.c_uint64(0)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
+    _check(lib().pcf_bucket_counts_f64(x.data_ptr(), x.numel(), alpha, beta, gamma, seed & 0xFFFFFFFFFFFFFFFF,
+                                       b.data_ptr(), H.data_ptr(), ctypes.byref(mx), st))
+    return b, H, int(mx.value)
 
 
 def NODE_DTYPE():

@@ -21,6 +21,7 @@
 #include "pcf_global.cuh"
 #include "pcf_k7.cuh"
 #include "pcf_k8.cuh"
+#include "pcf_bucketing.cuh"
 
 namespace pcf {
 
@@ -706,6 +707,52 @@ static int sort_host(const u64 *in_h, u64 *out_h, size_t n, const pcf_params *pp
     return rc;
 }
 
+// §4.3 experiment: one M_PCF step with decoupled alpha, beta, gamma (pcf_bucketing.cuh)
+static int bucket_counts_f64(const u64 *x, size_t n, u64 alpha, u64 beta, u64 gamma, u64 seed, u32 *b, u32 *H,
+                             uint64_t *max_bucket, cudaStream_t st) {
+    if (!x || !b || !H) return fail(PCF_ERR_INVALID_ARG, "NULL pointer");
+    if (n < 2 || n >= (1ull << 32)) return fail(PCF_ERR_INVALID_ARG, "n must be in [2, 2^32)");
+    if (!alpha || !beta || !gamma || alpha >= (1ull << 32) || beta >= 0xffffffffull || gamma >= 0xffffffffull)
+        return fail(PCF_ERR_INVALID_ARG, "alpha, beta, gamma must be in [1, 2^32 - 1)");
+    u64 *mm = nullptr;
+    CK(cudaMallocAsync(&mm, 3 * sizeof(u64), st));
+    int rc = PCF_OK;
+    u64 h[3] = {0, 0, 0};
+    auto run = [&]() -> int {
+        CK(cudaMemsetAsync(mm, 0xff, sizeof(u64), st));
+        CK(cudaMemsetAsync(mm + 1, 0, 2 * sizeof(u64), st));
+        CK(cudaMemsetAsync(b, 0, (beta + 1) * sizeof(u32), st));
+        CK(cudaMemsetAsync(H, 0, (gamma + 1) * sizeof(u32), st));
+        int dev = 0, sms = 148;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const u32 gx = (u32)std::min<u64>((n + BK_THREADS - 1) / BK_THREADS, (u64)sms * 8);
+        const u32 ga = (u32)std::min<u64>((alpha + BK_THREADS - 1) / BK_THREADS, (u64)sms * 8);
+        const u32 gh = (u32)std::min<u64>((gamma + BK_THREADS) / BK_THREADS, (u64)sms * 8);
+        k_bk_minmax<<<gx, BK_THREADS, 0, st>>>(x, n, mm);
+        k_bk_train<<<ga, BK_THREADS, 0, st>>>(x, n, (u32)alpha, (u32)beta, seed, mm, b);
+        k_bk_scan<<<1, 1024, 0, st>>>(b, (u32)(beta + 1));
+        k_bk_classify<<<gx, BK_THREADS, 0, st>>>(x, n, (u32)alpha, (u32)beta, (u32)gamma, mm, b, H);
+        k_bk_max<<<gh, BK_THREADS, 0, st>>>(H, (u32)(gamma + 1), mm);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h, mm, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return PCF_OK;
+    };
+    rc = run();
+    cudaFreeAsync(mm, st);
+    if (rc) return rc;
+    double lo, hi;
+    const u64 rlo = KeyF64::from_okey(h[0]), rhi = KeyF64::from_okey(h[1]);
+    memcpy(&lo, &rlo, 8);
+    memcpy(&hi, &rhi, 8);
+    if (lo != lo || hi != hi) return fail(PCF_ERR_NAN, "NaN key");
+    if (!(hi - lo > 0.0) || !(hi - lo <= 1.7976931348623157e308))
+        return fail(PCF_ERR_DEGENERATE, "x_max - x_min is not in (0, inf): M_PCF undefined");
+    if (max_bucket) *max_bucket = h[2];
+    return PCF_OK;
+}
+
 }  // namespace pcf
 
 // ---------------------------------------------------------------- C ABI
@@ -756,8 +803,15 @@ const char *pcf_status_string(int s) {
         case PCF_ERR_CUDA: return "PCF_ERR_CUDA";
         case PCF_ERR_LOG_OVERFLOW: return "PCF_ERR_LOG_OVERFLOW";
         case PCF_ERR_INTERNAL: return "PCF_ERR_INTERNAL";
+        case PCF_ERR_DEGENERATE: return "PCF_ERR_DEGENERATE";
         default: return "PCF_ERR_UNKNOWN";
     }
+}
+
+int pcf_bucket_counts_f64(const double *keys, size_t n, uint64_t alpha, uint64_t beta, uint64_t gamma,
+                          uint64_t seed, uint32_t *b_out, uint32_t *H_out, uint64_t *max_bucket, void *stream) {
+    return pcf::bucket_counts_f64(reinterpret_cast<const pcf::u64 *>(keys), n, alpha, beta, gamma, seed, b_out, H_out,
+                                  max_bucket, (cudaStream_t)stream);
 }
 
 const char *pcf_last_error(void) { return pcf::g_last_error.c_str(); }

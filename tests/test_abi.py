@@ -80,6 +80,17 @@ def test_argument_errors_before_any_launch(L):
     assert b"struct_size" in L.pcf_last_error()
 
 
+def test_bucket_counts_argument_errors_before_any_launch(L):
+    f, dp = L.pcf_bucket_counts_f64, ctypes.c_void_p
+    assert f(None, 10, 4, 4, 4, 0, dp(8192), dp(16384), None, None) == 1      # NULL keys
+    assert f(dp(4096), 10, 4, 4, 4, 0, None, dp(16384), None, None) == 1     # NULL b
+    assert f(dp(4096), 1, 4, 4, 4, 0, dp(8192), dp(16384), None, None) == 1  # n < 2
+    assert f(dp(4096), 1 << 32, 4, 4, 4, 0, dp(8192), dp(16384), None, None) == 1
+    for a, b, g in [(0, 4, 4), (4, 0, 4), (4, 4, 0), (1 << 32, 4, 4), (4, (1 << 32) - 1, 4)]:
+        assert f(dp(4096), 10, a, b, g, 0, dp(8192), dp(16384), None, None) == 1
+    assert b"alpha" in L.pcf_last_error()
+
+
 def test_product_path_does_not_touch_oracle():
     """The product package and its CUDA sources never reference oracle/ (③)."""
     pkg = os.path.join(ROOT, "paper_2405_07122_b200")
