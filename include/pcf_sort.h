@@ -160,7 +160,7 @@ int pcf_sort_u64_host(const uint64_t *in_host, uint64_t *out_host, size_t n, con
  * H_out:      DEVICE, gamma + 1 uint32 (|c_1|..|c_{gamma+1}|), overwritten.
  * max_bucket: HOST, receives max_j |c_j|; may be NULL.
  * Synchronous on `stream` (one 24-byte device scratch, stream-ordered alloc).
- * Errors: PCF_ERR_INVALID_ARG (NULL pointer, n < 2 or n >= 2^32, alpha, beta or
+ * Errors: PCF_ERR_INVALID_ARG (NULL or misaligned pointer, n < 2 or n >= 2^32, alpha, beta or
  * gamma 0 or >= 2^32, beta + 1 or gamma + 1 overflow) before any launch;
  * PCF_ERR_NAN if a key is NaN; PCF_ERR_DEGENERATE if all keys are equal (b_out,
  * H_out unspecified after either); PCF_ERR_CUDA / PCF_ERR_OOM. */

@@ -711,6 +711,8 @@ static int sort_host(const u64 *in_h, u64 *out_h, size_t n, const pcf_params *pp
 static int bucket_counts_f64(const u64 *x, size_t n, u64 alpha, u64 beta, u64 gamma, u64 seed, u32 *b, u32 *H,
                              uint64_t *max_bucket, cudaStream_t st) {
     if (!x || !b || !H) return fail(PCF_ERR_INVALID_ARG, "NULL pointer");
+    if (((uintptr_t)x & 7) || ((uintptr_t)b & 3) || ((uintptr_t)H & 3))
+        return fail(PCF_ERR_INVALID_ARG, "misaligned pointer (keys 8-byte, b/H 4-byte)");
     if (n < 2 || n >= (1ull << 32)) return fail(PCF_ERR_INVALID_ARG, "n must be in [2, 2^32)");
     if (!alpha || !beta || !gamma || alpha >= (1ull << 32) || beta >= 0xffffffffull || gamma >= 0xffffffffull)
         return fail(PCF_ERR_INVALID_ARG, "alpha, beta, gamma must be in [1, 2^32 - 1)");

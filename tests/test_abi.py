@@ -89,6 +89,9 @@ def test_bucket_counts_argument_errors_before_any_launch(L):
     for a, b, g in [(0, 4, 4), (4, 0, 4), (4, 4, 0), (1 << 32, 4, 4), (4, (1 << 32) - 1, 4)]:
         assert f(dp(4096), 10, a, b, g, 0, dp(8192), dp(16384), None, None) == 1
     assert b"alpha" in L.pcf_last_error()
+    assert f(dp(4097), 10, 4, 4, 4, 0, dp(8192), dp(16384), None, None) == 1   # misaligned keys
+    assert f(dp(4096), 10, 4, 4, 4, 0, dp(8194), dp(16384), None, None) == 1   # misaligned b
+    assert b"misaligned" in L.pcf_last_error()
 
 
 def test_product_path_does_not_touch_oracle():
