@@ -30,7 +30,12 @@ constexpr int NB_CAP = 1024;             // max buckets of one K7 CTA-level part
 constexpr int WMAX = 1024;               // largest segment a single warp runs Alg. 1 on
 constexpr int WNB = 184;                 // >= iroot34(WMAX) + 2 (warp scratch bins)
 constexpr int WSTACK = 320;              // warp DFS stack entries (bound: DESIGN.md §5.3)
-constexpr int GMAX = 1024;               // digits per global split pass
+#ifndef PCF_GMAX
+#define PCF_GMAX 1024
+#endif
+constexpr int GMAX = PCF_GMAX;           // digits per global split pass (a power of two)
+static_assert((GMAX & (GMAX - 1)) == 0 && GMAX >= 256, "GMAX must be a power of two >= 256");
+constexpr unsigned GMAX_LOG2 = GMAX >= 4096 ? 12 : GMAX >= 2048 ? 11 : GMAX >= 1024 ? 10 : GMAX >= 512 ? 9 : 8;
 constexpr int SPLIT_THREADS = 512;       // split count kernel block
 constexpr int SC_WARPS = 12;             // split scatter: warps per CTA
 constexpr int SC_THREADS = SC_WARPS * 32;

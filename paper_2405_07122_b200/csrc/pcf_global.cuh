@@ -940,7 +940,7 @@ __host__ __device__ inline u32 floor_log2_u64(u64 v) {  // v >= 1
 // G = ceil(W / 2^s) <= GMAX, expected group ~ S_CAP/2 keys, G >= 2.
 __host__ __device__ inline u32 choose_shift(u32 W, u32 c) {
     u32 cl = ceil_log2_u32(W);
-    u32 smin = cl > 10 ? cl - 10 : 0;
+    u32 smin = cl > GMAX_LOG2 ? cl - GMAX_LOG2 : 0;
     u64 q = ((u64)(S_CAP / 2) * W) / (c ? c : 1);
     u32 st = floor_log2_u64(q ? q : 1);
     u32 s = st < 10 ? st : 10;
