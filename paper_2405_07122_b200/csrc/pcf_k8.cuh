@@ -44,6 +44,10 @@ __global__ void __launch_bounds__(256) k8_check(const u64 *__restrict__ src, u64
     if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
+#ifndef PCF_K8_WARPSORT
+#define PCF_K8_WARPSORT 1
+#endif
+
 // Compare-exchange of two registers (ascending).
 __device__ __forceinline__ void k8_cx(u64 &a, u64 &b) { const u64 x = a < b ? a : b; b = a < b ? b : a; a = x; }
 
@@ -111,12 +115,47 @@ __global__ void __launch_bounds__(K8_THREADS) k8_blocksort(const u64 *__restrict
     k8_cx(r[0], r[4]); k8_cx(r[1], r[5]); k8_cx(r[2], r[6]); k8_cx(r[3], r[7]);
     k8_cx(r[2], r[4]); k8_cx(r[3], r[5]);
     k8_cx(r[1], r[2]); k8_cx(r[3], r[4]); k8_cx(r[5], r[6]);
+#if PCF_K8_WARPSORT
+    // 16 .. 256 keys: the warp's 32 ascending runs of 8 merged in registers by a
+    // bitonic network (each stage: compare element i with its mirror i ^ (k - 1),
+    // then half-cleaners i ^ j), shuffles across lanes, no shared memory
+    static_assert(K8_IPT == 8, "register merge assumes 8 keys per lane");
+    {
+        const u32 L = threadIdx.x & 31;
+#pragma unroll
+        for (u32 k = 16; k <= 256; k <<= 1) {
+            {
+                const bool lo = (L & (k / 16)) == 0;
+                u64 p[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) p[q] = __shfl_xor_sync(0xffffffffu, r[7 - q], k / 8 - 1);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) r[q] = (lo == (p[q] < r[q])) ? p[q] : r[q];
+            }
+#pragma unroll
+            for (u32 j = k / 4; j >= 8; j >>= 1) {
+                const bool lo = (L & (j / 8)) == 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const u64 p = __shfl_xor_sync(0xffffffffu, r[q], j / 8);
+                    r[q] = (lo == (p < r[q])) ? p : r[q];
+                }
+            }
+            k8_cx(r[0], r[4]); k8_cx(r[1], r[5]); k8_cx(r[2], r[6]); k8_cx(r[3], r[7]);
+            k8_cx(r[0], r[2]); k8_cx(r[1], r[3]); k8_cx(r[4], r[6]); k8_cx(r[5], r[7]);
+            k8_cx(r[0], r[1]); k8_cx(r[2], r[3]); k8_cx(r[4], r[5]); k8_cx(r[6], r[7]);
+        }
+    }
+    constexpr u32 RUN0 = 32 * K8_IPT;
+#else
+    constexpr u32 RUN0 = K8_IPT;
+#endif
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K8_IPT; ++k) a[t0 + k] = r[k];
     __syncthreads();
     u64 *sa = a, *sb = b;
-    for (u32 run = K8_IPT; run < (u32)K8_TILE; run <<= 1) {
+    for (u32 run = RUN0; run < (u32)K8_TILE; run <<= 1) {
         const u32 p0 = (t0 / (2 * run)) * (2 * run), d = t0 - p0;
         const u64 *A = sa + p0, *B = sa + p0 + run;
         const u32 ia = k8_split(A, run, B, run, d);
