@@ -108,47 +108,58 @@ __global__ void __launch_bounds__(K8_THREADS) k8_blocksort(const u64 *__restrict
     u64 r[K8_IPT];
 #pragma unroll
     for (int k = 0; k < K8_IPT; ++k) r[k] = a[t0 + ((k + threadIdx.x) & (K8_IPT - 1))];   // rotated: fewer bank conflicts
-    // Batcher odd-even merge sort of 8
-    k8_cx(r[0], r[1]); k8_cx(r[2], r[3]); k8_cx(r[4], r[5]); k8_cx(r[6], r[7]);
-    k8_cx(r[0], r[2]); k8_cx(r[1], r[3]); k8_cx(r[4], r[6]); k8_cx(r[5], r[7]);
-    k8_cx(r[1], r[2]); k8_cx(r[5], r[6]);
-    k8_cx(r[0], r[4]); k8_cx(r[1], r[5]); k8_cx(r[2], r[6]); k8_cx(r[3], r[7]);
-    k8_cx(r[2], r[4]); k8_cx(r[3], r[5]);
-    k8_cx(r[1], r[2]); k8_cx(r[3], r[4]); k8_cx(r[5], r[6]);
+    // Batcher odd-even merge sort of each 8 registers
+#define K8_BATCHER8(o)                                                                                   \
+    k8_cx(r[o + 0], r[o + 1]); k8_cx(r[o + 2], r[o + 3]); k8_cx(r[o + 4], r[o + 5]); k8_cx(r[o + 6], r[o + 7]); \
+    k8_cx(r[o + 0], r[o + 2]); k8_cx(r[o + 1], r[o + 3]); k8_cx(r[o + 4], r[o + 6]); k8_cx(r[o + 5], r[o + 7]); \
+    k8_cx(r[o + 1], r[o + 2]); k8_cx(r[o + 5], r[o + 6]);                                                   \
+    k8_cx(r[o + 0], r[o + 4]); k8_cx(r[o + 1], r[o + 5]); k8_cx(r[o + 2], r[o + 6]); k8_cx(r[o + 3], r[o + 7]); \
+    k8_cx(r[o + 2], r[o + 4]); k8_cx(r[o + 3], r[o + 5]);                                                   \
+    k8_cx(r[o + 1], r[o + 2]); k8_cx(r[o + 3], r[o + 4]); k8_cx(r[o + 5], r[o + 6]);
+#pragma unroll
+    for (int o = 0; o < K8_IPT; o += 8) { K8_BATCHER8(o) }
+#undef K8_BATCHER8
+    static_assert(K8_IPT == 8 || K8_IPT == 16, "K8_IPT must be 8 or 16");
 #if PCF_K8_WARPSORT
-    // 16 .. 256 keys: the warp's 32 ascending runs of 8 merged in registers by a
-    // bitonic network (each stage: compare element i with its mirror i ^ (k - 1),
-    // then half-cleaners i ^ j), shuffles across lanes, no shared memory
-    static_assert(K8_IPT == 8, "register merge assumes 8 keys per lane");
+    // 16 .. 32 * K8_IPT keys: the warp's ascending runs of 8 merged in registers by a
+    // bitonic network (each stage: compare element i = K8_IPT * lane + q with its
+    // mirror i ^ (k - 1), then half-cleaners i ^ j), lane shuffles, no shared memory
     {
         const u32 L = threadIdx.x & 31;
 #pragma unroll
-        for (u32 k = 16; k <= 256; k <<= 1) {
-            {
-                const bool lo = (L & (k / 16)) == 0;
-                u64 p[8];
+        for (u32 k = 16; k <= 32u * K8_IPT; k <<= 1) {
+            if (k <= (u32)K8_IPT) {   // mirror inside the lane
 #pragma unroll
-                for (int q = 0; q < 8; ++q) p[q] = __shfl_xor_sync(0xffffffffu, r[7 - q], k / 8 - 1);
+                for (u32 q = 0; q < (u32)K8_IPT; ++q)
+                    if (!(q & (k / 2))) k8_cx(r[q], r[q ^ (k - 1)]);
+            } else {
+                const bool lo = (L & (k / (2 * K8_IPT))) == 0;
+                u64 p[K8_IPT];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) r[q] = (lo == (p[q] < r[q])) ? p[q] : r[q];
+                for (int q = 0; q < K8_IPT; ++q) p[q] = __shfl_xor_sync(0xffffffffu, r[K8_IPT - 1 - q], k / K8_IPT - 1);
+#pragma unroll
+                for (int q = 0; q < K8_IPT; ++q) r[q] = (lo == (p[q] < r[q])) ? p[q] : r[q];
             }
 #pragma unroll
-            for (u32 j = k / 4; j >= 8; j >>= 1) {
-                const bool lo = (L & (j / 8)) == 0;
+            for (u32 j = k / 4; j >= 1; j >>= 1) {
+                if (j >= (u32)K8_IPT) {
+                    const bool lo = (L & (j / K8_IPT)) == 0;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const u64 p = __shfl_xor_sync(0xffffffffu, r[q], j / 8);
-                    r[q] = (lo == (p < r[q])) ? p : r[q];
+                    for (int q = 0; q < K8_IPT; ++q) {
+                        const u64 p = __shfl_xor_sync(0xffffffffu, r[q], j / K8_IPT);
+                        r[q] = (lo == (p < r[q])) ? p : r[q];
+                    }
+                } else {
+#pragma unroll
+                    for (u32 q = 0; q < (u32)K8_IPT; ++q)
+                        if (!(q & j)) k8_cx(r[q], r[q | j]);
                 }
             }
-            k8_cx(r[0], r[4]); k8_cx(r[1], r[5]); k8_cx(r[2], r[6]); k8_cx(r[3], r[7]);
-            k8_cx(r[0], r[2]); k8_cx(r[1], r[3]); k8_cx(r[4], r[6]); k8_cx(r[5], r[7]);
-            k8_cx(r[0], r[1]); k8_cx(r[2], r[3]); k8_cx(r[4], r[5]); k8_cx(r[6], r[7]);
         }
     }
     constexpr u32 RUN0 = 32 * K8_IPT;
 #else
-    constexpr u32 RUN0 = K8_IPT;
+    constexpr u32 RUN0 = 8;   // each lane holds K8_IPT / 8 sorted runs of 8
 #endif
     __syncthreads();
 #pragma unroll
