@@ -27,14 +27,53 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "float64 keys/sec sorted at 1×B200; per-pass HBM GB/s as fraction of peak"
-WORKLOADS = {   # BASELINE.json configs; c2 = configs[1] is the bench line
+WORKLOADS = {   # BASELINE.json configs; the bench line is c5f = configs[4] (largest single-GPU config)
     "c1": "c1_uniform_1e6", "c2": "c2_lognormal_1e7", "c3": "c3_gaussmix8_dup10_1e8",
     "c4": "c4_exp700u4_1e8", "c5f": "c5_exponential_1e9", "c5u": "c5_u64_uniform_1e9",
 }
 # per-pass algorithmic bytes: phase -> what one key costs in that phase
-PASS_NOTE = {"minmax": "8 B/key read", "fit": "8 B/sample gather + tables", "classify_hist": "8 B/key read",
-             "scatter": "8 B/key read + 8 B/key write", "smem_subtree": "8 B/key read + 8 B/key write",
+PASS_NOTE = {"minmax": "8 B/key read, once per global node", "fit": "8 B/sample gather + tables",
+             "classify_hist": "8 B/key read, once per bucketing level (SURVEY.md 8(d))",
+             "scatter": "8 B/key read + 8 B/key write, once per bucketing level (SURVEY.md 8(d))",
+             "smem_subtree": "8 B/key read + 8 B/key write per key handed to K7",
              "fallback_sort": "16 B/key per merge pass"}
+
+
+def workload_config(name, n):
+    """The `config` dict of both arms (identical, so the driver can pair them)."""
+    import synth
+    cfg = synth.CONFIGS[name]
+    return {"workload": WORKLOADS.get(name, name), "n": n, "dist": cfg["dist"], "seed": cfg["seed"],
+            "key_type": "u64" if cfg["dist"] == "u64" else "f64", "tau": 64,
+            "alpha=beta=gamma=delta": "floor(n^{3/4})",
+            "l2": "flushed before every step (2 x L2 write, outside the events); inputs 8n B > L2"}
+
+
+def host_cpu():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+def run_pinned_1core(fn):
+    """Run fn() with this process pinned to one core (the taskset -c <core> of SURVEY.md 8(d))."""
+    try:
+        allowed = sorted(os.sched_getaffinity(0))
+    except AttributeError:
+        return fn(), None
+    core = allowed[0]
+    os.sched_setaffinity(0, {core})
+    try:
+        return fn(), core
+    finally:
+        os.sched_setaffinity(0, set(allowed))
 
 
 def load_peaks():
@@ -126,14 +165,15 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def traffic_from_profiles(kernel_phase):
-    """ncu dram bytes per launch of the dominant kernel, from the committed summary."""
+def traffic_from_profiles(config, kernel_phase):
+    """ncu dram read+write bytes per launch of the dominant kernel on this config,
+    from the committed `ncu --set full` summary (profiles/traffic.json), or None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
         d = json.load(f)
-    v = d.get(kernel_phase)
+    v = d.get(config, {}).get(kernel_phase)
     return v if isinstance(v, (int, float)) else None
 
 
@@ -165,12 +205,16 @@ def run_gpu(args):
         flush.fill_(1)
         step(True)
     torch.cuda.synchronize()
-    # correctness of the benchmarked configuration (sortedness + permutation), cheap
+    # correctness of the benchmarked configuration: the output equals an independent
+    # library sort of the same keys (the sorted permutation is unique under totalOrder)
+    def total_order_i64(t):
+        s64 = t.view(torch.int64)
+        if t.dtype == torch.float64:
+            return s64 ^ ((s64 >> 63) & 0x7FFFFFFFFFFFFFFF)
+        return s64 ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=t.device)
+    ok_sorted = bool(torch.equal(total_order_i64(out), torch.sort(total_order_i64(x)).values))
+    torch.cuda.empty_cache()
     o = out.cpu().numpy()
-    bits = o.view(np.uint64)
-    if o.dtype == np.float64:   # totalOrder key: flip sign bit of positives, complement negatives
-        bits = bits ^ np.where(bits >> np.uint64(63), np.uint64(0xFFFFFFFFFFFFFFFF), np.uint64(1 << 63))
-    ok_sorted = bool(np.all(bits[1:] >= bits[:-1]))
 
     sampler = ClockSampler(local)
     if rank == 0:
@@ -178,7 +222,7 @@ def run_gpu(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    times, phase_ms, phase_bytes, launches = [], {}, {}, 0
+    times, phase_ms, phase_bytes, launches, split_moved = [], {}, {}, 0, 0
     t_wall0 = time.perf_counter()
     for _ in range(args.steps):          # the headline: no per-phase instrumentation
         flush.fill_(1)
@@ -205,6 +249,7 @@ def run_gpu(args):
             phase_ms[k] = phase_ms.get(k, 0.0) + v
         for k, v in st["phase_bytes"].items():
             phase_bytes[k] = phase_bytes.get(k, 0) + v
+        split_moved = st["split_keys_moved"]
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -244,7 +289,7 @@ def run_gpu(args):
     dom = max((k for k in passes if "gbs" in passes[k]), key=lambda k: passes[k]["ms_per_step"], default=None)
     roof = None
     if dom:
-        tr = traffic_from_profiles(dom)
+        tr = traffic_from_profiles(args.config, dom)
         roof = {"bound": "hbm", "kernel": dom, "achieved": passes[dom]["gbs"], "peak": peak, "unit": "GB/s",
                 "frac": passes[dom]["frac"], "traffic": tr, "peak_source": peak_src,
                 "share_of_step": round(passes[dom]["ms_per_step"] / (sum(prof_times) / args.steps), 3),
@@ -252,6 +297,7 @@ def run_gpu(args):
     # ---- CPU baseline: the oracle, single thread, on the same workload (rank 0, N = 1 only)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
+        del host, pin_in, pin_out
         cpu = cpu_baseline(args.config, n, args.cpu_sample)
     value = world * n * args.steps / (total_ms * 1e-3)
     line = {
@@ -259,10 +305,9 @@ def run_gpu(args):
         "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64" if host.dtype == np.float64 else "u64",
         "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md §4)",
-        "config": {"workload": WORKLOADS.get(args.config, args.config), "n": n, "dist": cfg["dist"],
-                   "seed": cfg["seed"], "tau": 64, "alpha=beta=gamma=delta": "floor(n^{3/4})",
-                   "l2": "flushed before every step (2 x L2 write, outside the events)",
-                   "parallelism": f"replicas{world}" if world > 1 else "1gpu"},
+        "config": workload_config(args.config, n),
+        "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+        "split_keys_moved_per_step": split_moved,
         "passes": passes, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
         "e2e": {"value": world * n * args.steps / (e2e_ms * 1e-3), "unit": "keys/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
@@ -274,18 +319,28 @@ def run_gpu(args):
 
 
 def cpu_baseline(config, n, sample):
+    """The oracle (single thread, pinned to one core) on a bounded sample of the
+    workload: the first `sample` keys of the same seeded stream."""
     import oracle
     import synth
     m = min(n, sample)
     x = synth.config(config, n=m)
-    t0 = time.perf_counter()
-    oracle.learned_sort(x, check=False)
-    dt = time.perf_counter() - t0
+
+    def run():
+        t0 = time.perf_counter()
+        oracle.learned_sort(x, check=False)
+        return time.perf_counter() - t0
+    dt, core = run_pinned_1core(run)
+    model, ncpu = host_cpu()
     return {"value": m / dt, "unit": "keys/s", "cores": 1, "kind": "oracle",
-            "sample": f"{config} recipe at n={m} (first {m} keys of the same stream), 1 run, {dt:.2f} s"}
+            "sample": f"{config} recipe, first {m} keys of the same stream (n={m}: its own level parameters), "
+                      f"1 run, {dt:.2f} s",
+            "pinned_core": core, "host_cpu": model, "host_nproc": ncpu}
 
 
 def run_reference(args):
+    """--impl reference: the CPU oracle as it stands (single thread, pinned to one
+    core), each step a bounded sample (the first --ref-sample keys) of the workload."""
     import oracle
     import synth
     rank = int(os.environ.get("RANK", "0"))
@@ -293,25 +348,31 @@ def run_reference(args):
         return
     cfg = synth.CONFIGS[args.config]
     n = cfg["n"] if args.n is None else args.n
-    m = min(n, args.cpu_sample)
+    m = min(n, args.ref_sample)
     x = synth.config(args.config, n=m)
-    for _ in range(args.warmup):
-        oracle.learned_sort(x, check=False)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.learned_sort(x, check=False)
-    dt = time.perf_counter() - t0
+
+    def run():
+        for _ in range(args.warmup):
+            oracle.learned_sort(x, check=False)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle.learned_sort(x, check=False)
+        return time.perf_counter() - t0
+    dt, core = run_pinned_1core(run)
     value = m * args.steps / dt
+    model, ncpu = host_cpu()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, BASELINE.json recipe)",
-        "config": {"workload": WORKLOADS.get(args.config, args.config), "n": n, "dist": cfg["dist"],
-                   "seed": cfg["seed"],
-                   "parallelism": f"oracle on 1 CPU thread (rank 0 of the --gpus {args.gpus} launch)"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64" if cfg["dist"] == "u64" else "f64",
+        "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md §4)",
+        "config": workload_config(args.config, n),
+        "parallelism": f"oracle on 1 pinned CPU core (rank 0 of the --gpus {args.gpus} launch)",
         "cpu_baseline": {"value": value, "unit": "keys/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{args.config} recipe at n={m}, {args.steps} timed runs"},
+                         "sample": f"{args.config} recipe, first {m} keys of the same stream per step, "
+                                   f"{args.steps} timed steps",
+                         "pinned_core": core, "host_cpu": model, "host_nproc": ncpu},
         "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -323,9 +384,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c5f", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=None, help="override n (parity-test sizes)")
-    ap.add_argument("--cpu-sample", type=int, default=10_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=200_000_000,
+                    help="keys of the workload the cpu_baseline oracle run sorts (~10-30 s)")
+    ap.add_argument("--ref-sample", type=int, default=20_000_000,
+                    help="keys per --impl reference step (the whole run stays within a few minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

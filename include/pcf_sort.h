@@ -90,7 +90,7 @@ typedef struct pcf_stats {
     uint32_t host_syncs;       /* stream synchronisations performed inside the call          */
     uint32_t reserved;
     uint64_t groups_smem;      /* bucket groups finished in shared memory (K7 tasks)         */
-    uint64_t split_tasks;      /* oversized groups re-partitioned in global memory            */
+    uint64_t split_keys_moved; /* keys moved by the global digit-split rounds (all rounds)    */
     uint64_t global_nodes;     /* bucketing nodes run by the global (multi-CTA) path          */
     uint64_t fallback_keys_global; /* keys sorted by the global fallback sort               */
     /* PCF_FLAG_TIMING: milliseconds per phase, CUDA events on `stream`:

@@ -41,7 +41,7 @@ class PassLog(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_uint32), ("rounds", ctypes.c_uint32),
                 ("host_syncs", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
-                ("groups_smem", ctypes.c_uint64), ("split_tasks", ctypes.c_uint64),
+                ("groups_smem", ctypes.c_uint64), ("split_keys_moved", ctypes.c_uint64),
                 ("global_nodes", ctypes.c_uint64), ("fallback_keys_global", ctypes.c_uint64),
                 ("phase_ms", ctypes.c_float * 8), ("phase_bytes", ctypes.c_uint64 * 8),
                 ("k7_cycles", ctypes.c_uint64 * 16)]
@@ -49,7 +49,7 @@ class Stats(ctypes.Structure):
     def as_dict(self):
         return {"kernel_launches": self.kernel_launches, "rounds": self.rounds,
                 "host_syncs": self.host_syncs, "groups_smem": self.groups_smem,
-                "split_tasks": self.split_tasks, "global_nodes": self.global_nodes,
+                "split_keys_moved": self.split_keys_moved, "global_nodes": self.global_nodes,
                 "fallback_keys_global": self.fallback_keys_global,
                 "phase_ms": {PHASES[i]: float(self.phase_ms[i]) for i in range(8)},
                 "phase_bytes": {PHASES[i]: int(self.phase_bytes[i]) for i in range(8)},
@@ -103,6 +103,29 @@ def lib():
     return _lib
 
 
+def _check_device_buffer(t, dtype, n, device, name):
+    """The library writes n elements of `dtype` through t's pointer: refuse anything else."""
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.numel() != n:
+        raise ValueError(f"{name} must have {n} elements, got {t.numel()}")
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, keys are on {device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _check_workspace(ws, device):
+    import torch
+
+    if not isinstance(ws, torch.Tensor) or not ws.is_cuda or ws.device != device or not ws.is_contiguous():
+        raise ValueError(f"workspace must be a contiguous CUDA tensor on {device}")
+
+
 def make_params(tau: int = 64, seed: int = 0, flags: int = FLAG_SYNC, workspace=None, workspace_bytes=0):
     p = Params()
     lib().pcf_params_init(ctypes.byref(p))
@@ -154,6 +177,9 @@ def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False,
     n = x.numel()
     if out is None:
         out = torch.empty_like(x)
+    _check_device_buffer(out, x.dtype, n, x.device, "out")
+    if workspace is not None:
+        _check_workspace(workspace, x.device)
     flags = (FLAG_SYNC if sync else 0) | (FLAG_SAMPLE_ALL if sample_all else 0) | (FLAG_TIMING if timing else 0) \
         | (FLAG_PROFILE if profile else 0) | (FLAG_EXACT_RANKS if exact_ranks else 0)
     p = make_params(tau, seed, flags)
@@ -213,6 +239,8 @@ def bucket_counts(x, alpha: int, beta: int, gamma: int, *, seed: int = 0, b=None
         b = torch.empty(beta + 1, dtype=torch.uint32, device=x.device)
     if H is None:
         H = torch.empty(gamma + 1, dtype=torch.uint32, device=x.device)
+    _check_device_buffer(b, torch.uint32, beta + 1, x.device, "b")
+    _check_device_buffer(H, torch.uint32, gamma + 1, x.device, "H")
     mx = ctypes.c_uint64(0)
     st = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
     _check(lib().pcf_bucket_counts_f64(x.data_ptr(), x.numel(), alpha, beta, gamma, seed & 0xFFFFFFFFFFFFFFFF,
@@ -244,21 +272,38 @@ def sort_host(x, out=None, *, tau: int = 64, seed: int = 0, workspace=None, stre
     if isinstance(x, torch.Tensor):
         if x.is_cuda:
             raise TypeError("sort_host expects host memory")
+        if x.dtype not in (torch.float64, torch.uint64):
+            raise TypeError(f"keys must be float64 or uint64, got {x.dtype}")
+        if x.dim() != 1 or not x.is_contiguous():
+            raise ValueError("x must be a contiguous 1-D tensor")
         ptr, n, dt = x.data_ptr(), x.numel(), x.dtype
         is_f64 = dt == torch.float64
         if out is None:
             out = torch.empty_like(x)
+        if not isinstance(out, torch.Tensor) or out.is_cuda or out.dtype != dt or out.numel() != n \
+                or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous host tensor of {n} {dt} keys")
         optr = out.data_ptr()
     else:
+        x = np.asarray(x)
+        if x.dtype not in (np.float64, np.uint64):
+            raise TypeError(f"keys must be float64 or uint64, got {x.dtype}")
+        if x.ndim != 1:
+            raise ValueError("x must be 1-D")
         x = np.ascontiguousarray(x)
         ptr, n = x.ctypes.data, x.size
         is_f64 = x.dtype == np.float64
         if out is None:
             out = np.empty_like(x)
+        if not isinstance(out, np.ndarray) or out.dtype != x.dtype or out.size != n or not out.flags.c_contiguous \
+                or not out.flags.writeable:
+            raise ValueError(f"out must be a writeable contiguous numpy array of {n} {x.dtype} keys")
         optr = out.ctypes.data
     fn = lib().pcf_sort_f64_host if is_f64 else lib().pcf_sort_u64_host
     p = make_params(tau, seed, FLAG_SYNC)
     if workspace is not None:
+        if not isinstance(workspace, torch.Tensor) or not workspace.is_cuda or not workspace.is_contiguous():
+            raise ValueError("workspace must be a contiguous CUDA tensor")
         p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
     s = stream if stream is not None else torch.cuda.current_stream()
     rc = fn(ctypes.c_void_p(ptr), ctypes.c_void_p(optr), n, ctypes.byref(p), ctypes.c_void_p(s.cuda_stream))

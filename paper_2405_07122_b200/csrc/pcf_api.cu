@@ -184,38 +184,50 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
 }
 
+// Per-device caches: occupancy results and the raised shared-memory limits apply to
+// the device they were queried / set on (cudaFuncSetAttribute is per device).
+constexpr int MAX_DEVS = 64;
+static int cur_dev() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAX_DEVS) d = 0;
+    return d;
+}
+
 template <class K>
 static int k7_ctas_per_sm() {   // resident K7 CTAs per SM (persistent grid size)
-    static thread_local int v = 0;
-    if (!v) {
+    static thread_local int v[MAX_DEVS] = {0};
+    const int d = cur_dev();
+    if (!v[d]) {
         int b = 1;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k7_kernel<K>, K7_THREADS, k7_smem_bytes()) != cudaSuccess || b < 1) b = 1;
-        v = b;
+        v[d] = b;
     }
-    return v;
+    return v[d];
 }
 
 template <class K>
 static int count_ctas_per_sm() {
-    static thread_local int v = 0;
-    if (!v) {
+    static thread_local int v[MAX_DEVS] = {0};
+    const int d = cur_dev();
+    if (!v[d]) {
         int b = 1;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_split_count<K>, CNT_THREADS, (int)sizeof(CountSmem)) != cudaSuccess || b < 1) b = 1;
-        v = b;
+        v[d] = b;
     }
-    return v;
+    return v[d];
 }
 
 template <class K>
 static int configure_kernels() {
-    static thread_local bool done = false;
-    if (done) return PCF_OK;
+    static thread_local bool done[MAX_DEVS] = {false};
+    const int d = cur_dev();
+    if (done[d]) return PCF_OK;
     CK(cudaFuncSetAttribute(k7_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
     CK(cudaFuncSetAttribute(k8_merge<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
     CK(cudaFuncSetAttribute(k8_blocksort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_SORT_SMEM));
-    done = true;
+    done[d] = true;
     return PCF_OK;
 }
 
@@ -345,7 +357,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     u32 launches = 0;
     int status = PCF_OK;
     std::vector<SegItem> fallbacks;
-    u64 k7_tasks = 0;
+    u64 k7_tasks = 0, split_moved = 0, global_keys = 0;
     u64 bytes[PCF_PHASES] = {0};
     std::vector<u32> global_nodes;   // indices (for the pass-log finalisation)
 
@@ -572,14 +584,19 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
                 batch.clear();
                 batch_nodes.clear();
             }
-            bytes[PH_COUNT] = 8ull * hcnt.split_keys;
-            bytes[PH_SCATTER] = 16ull * hcnt.split_keys;
+            split_moved = hcnt.split_keys;
             bytes[PH_K7] = 16ull * hcnt.k7_keys;
             if (pending == 0 && list.empty()) break;
             rounds_per_batch = 2;
         }
         stats.rounds = round;
-        stats.split_tasks = 0;
+        stats.split_keys_moved = split_moved;
+        // one classify (8 B/key) and one stable scatter (16 B/key) per
+        // bucketing level of every key the global path buckets; extra digit rounds are
+        // traffic, not algorithmic bytes (reported as split_keys_moved)
+        for (u32 m_ : node_m) global_keys += m_;
+        bytes[PH_COUNT] = 8ull * global_keys;
+        bytes[PH_SCATTER] = 16ull * global_keys;
         if (status == PCF_OK) {
             // K8: global Standard-Sort of large buckets (flags in pmat, merge splits in cmat:
             // both are free once the split rounds are done)
