@@ -277,11 +277,13 @@ def run_gpu(args):
         return
     peak, peak_src = load_peaks()
     passes = {}
-    for k in ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other"]:
+    notes = {"other": "round plans, count-matrix scans, task generation",
+             "deep_batches": "device-driven batches of oversized recursing buckets (all phases; CUDA-graph loop)"}
+    for k in ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "deep_batches"]:
         ms = phase_ms.get(k, 0.0)
         by = phase_bytes.get(k, 0)
         if ms > 0 and by == 0:
-            passes[k] = {"ms_per_step": ms / args.steps, "note": "round plans, count-matrix scans, task generation"}
+            passes[k] = {"ms_per_step": ms / args.steps, "note": notes.get(k, "")}
         elif ms > 0 and by > 0:
             gbs = by / (ms * 1e-3) / 1e9
             passes[k] = {"ms_per_step": ms / args.steps, "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
@@ -295,6 +297,7 @@ def run_gpu(args):
                 "share_of_step": round(passes[dom]["ms_per_step"] / (sum(prof_times) / args.steps), 3),
                 "phase_timing_step_ms": sum(prof_times) / args.steps}
     # ---- CPU baseline: the oracle, single thread, on the same workload (rank 0, N = 1 only)
+    key_dtype = "f64" if host.dtype == np.float64 else "u64"
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         del host, pin_in, pin_out
@@ -303,7 +306,7 @@ def run_gpu(args):
     line = {
         "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if host.dtype == np.float64 else "u64",
+        "scaling": "weak", "vs_baseline": None, "dtype": key_dtype,
         "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md §4)",
         "config": workload_config(args.config, n),
         "parallelism": f"replicas{world}" if world > 1 else "1gpu",

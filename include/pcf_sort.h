@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PCF_ABI_VERSION 1
+#define PCF_ABI_VERSION 2   /* 2: pcf_params.status_out, pcf_stats.device_batches, 9 phases */
 
 /* ---- status codes (every entry point returns one) ---------------------- */
 #define PCF_OK 0
@@ -45,7 +45,8 @@ extern "C" {
 #define PCF_KEY_U64 1   /* uint64_t, ascending numeric order                                      */
 
 /* ---- flags -------------------------------------------------------------- */
-#define PCF_FLAG_SYNC       1u  /* synchronise the stream before returning and report NaN/overflow */
+#define PCF_FLAG_SYNC       1u  /* synchronise the stream once before returning, report NaN/overflow
+                                   and fill *stats; without it the call never synchronises       */
 #define PCF_FLAG_SAMPLE_ALL 2u  /* test mode (reading R14): sample = whole segment, alpha = m      */
 #define PCF_FLAG_TIMING     4u  /* record CUDA events per phase into stats->phase_ms (implies SYNC) */
 #define PCF_FLAG_PROFILE    8u  /* K7 per-phase SM cycle counters into stats->k7_cycles (with SYNC) */
@@ -81,21 +82,26 @@ typedef struct pcf_pass_log {
     uint64_t level1_capacity;  /* entries available in level1_b / level1_h           */
 } pcf_pass_log;
 
-/* Host-side statistics, filled when params->stats != NULL and the call is
- * synchronous (PCF_FLAG_SYNC or PCF_FLAG_TIMING). */
-#define PCF_PHASES 8
+/* Host-side statistics, written when params->stats != NULL.  Fields read from
+ * device counters (rounds, groups_smem, split_keys_moved, global_nodes,
+ * fallback_keys_global, device_batches, phase_bytes, k7_cycles, and the
+ * device-driven part of kernel_launches) are filled only by synchronous calls
+ * (PCF_FLAG_SYNC or PCF_FLAG_TIMING); asynchronous calls leave them 0. */
+#define PCF_PHASES 9
 typedef struct pcf_stats {
     uint32_t kernel_launches;  /* kernels this call launched                                  */
     uint32_t rounds;           /* device work rounds (global bucketing / split waves)        */
-    uint32_t host_syncs;       /* stream synchronisations performed inside the call          */
-    uint32_t reserved;
+    uint32_t host_syncs;       /* stream synchronisations inside the call: 1 with SYNC, else 0 */
+    uint32_t device_batches;   /* device-driven batches of oversized recursing buckets run    */
     uint64_t groups_smem;      /* bucket groups finished in shared memory (K7 tasks)         */
     uint64_t split_keys_moved; /* keys moved by the global digit-split rounds (all rounds)    */
     uint64_t global_nodes;     /* bucketing nodes run by the global (multi-CTA) path          */
     uint64_t fallback_keys_global; /* keys sorted by the global fallback sort               */
     /* PCF_FLAG_TIMING: milliseconds per phase, CUDA events on `stream`:
      * [0] min/max  [1] sample+fit  [2] classify+histogram  [3] stable scatter
-     * [4] smem subtree (K7)  [5] global fallback sort  [6] other  [7] total */
+     * [4] smem subtree (K7)  [5] global fallback sort + pass-log records  [6] other
+     * [7] total  [8] device-driven batches of oversized recursing buckets (all their
+     * phases: the host cannot place events inside the device-driven loop) */
     float phase_ms[PCF_PHASES];
     uint64_t phase_bytes[PCF_PHASES];  /* algorithmic bytes per phase */
     /* PCF_FLAG_PROFILE: clock64 cycles summed over K7 CTAs per phase (see pcf_k7.cuh prof_mark) */
@@ -112,7 +118,12 @@ typedef struct pcf_params {
     size_t workspace_bytes;    /*   library allocates stream-ordered (cudaMallocAsync)     */
     pcf_pass_log *log;         /* host struct pointing at device buffers, or NULL          */
     pcf_stats *stats;          /* host struct, or NULL                                     */
+    /* ABI v2: device (or mapped pinned host) int that receives, in stream order after
+     * all of the sort's work, PCF_OK, PCF_ERR_NAN, PCF_ERR_LOG_OVERFLOW or
+     * PCF_ERR_INTERNAL -- the status of an asynchronous call.  NULL = not written. */
+    int *status_out;
 } pcf_params;
+#define PCF_PARAMS_V1_SIZE ((uint32_t)offsetof(pcf_params, status_out))   /* v1 callers: no status_out */
 
 /* Fill *p with the defaults above.  Never fails. */
 void pcf_params_init(pcf_params *p);
@@ -122,24 +133,29 @@ void pcf_params_init(pcf_params *p);
  * histograms and work queues.  Pure host arithmetic; no CUDA call. */
 size_t pcf_workspace_bytes(size_t n, int key_type, const pcf_params *p);
 
-/* Sort n keys.  in/out: DEVICE pointers to n contiguous keys, 8-byte aligned.
- * `in` is never written unless in == out (in-place is allowed); any other
- * overlap of [in, in+n) and [out, out+n) is PCF_ERR_INVALID_ARG.  `out` is
- * fully overwritten with the ascending permutation of `in`.
+/* Sort n keys (Alg. 1).  in/out: DEVICE pointers to n
+ * contiguous keys, 8-byte aligned.  `in` is never written unless in == out
+ * (in-place is allowed); any other overlap of [in, in+n) and [out, out+n) is
+ * PCF_ERR_INVALID_ARG.  `out` is fully overwritten with the ascending
+ * permutation of `in`.
+ * Execution: every kernel is enqueued on `stream`; the recursion over buckets
+ * too large for one CTA and the fallback sort run from CUDA
+ * graphs whose loops are decided on the device, so the host never waits for the
+ * GPU inside the call.  Without PCF_FLAG_SYNC the call returns right after
+ * enqueueing (stats->host_syncs == 0); with it, it synchronises `stream` once.
  * Errors: argument errors return before any launch.  NaN (f64) is detected on
- * the device by the first pass; later kernels do no work; with PCF_FLAG_SYNC the
- * call returns PCF_ERR_NAN (out unspecified), otherwise PCF_OK is returned
- * after enqueueing and the NaN is only visible through a later synchronous call
- * (asynchronous error reporting is not provided in ABI v1).
- * Without PCF_FLAG_SYNC the call may still synchronise internally when the
- * input needs more than one global bucketing round (skewed data); see
- * DESIGN.md §5. */
+ * the device by the first pass (the level-1 min/max), which sets a
+ * device flag; every later kernel then exits without work.  With PCF_FLAG_SYNC
+ * the call returns PCF_ERR_NAN (out unspecified); without it the call returns
+ * PCF_OK after enqueueing and the NaN is reported through params->status_out.
+ * Device capacity violations (a bug) are PCF_ERR_INTERNAL the same way. */
 int pcf_sort_f64(const double *in, double *out, size_t n, const pcf_params *p, void *stream);
 int pcf_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const pcf_params *p, void *stream);
 
 /* End-to-end entry: HOST pointers (pinned memory recommended).  Copies the n
- * keys to the device, sorts them with pcf_sort_*, copies the result back and
- * synchronises `stream`.  If p->workspace holds at least
+ * keys to the device, sorts them with pcf_sort_* (asynchronously), copies the
+ * result back and synchronises `stream` once; returns the sort's status
+ * (PCF_ERR_NAN etc.; also written to p->status_out if set).  If p->workspace holds at least
  * round_up(8n, 256) + pcf_workspace_bytes(n) bytes it is used as [device keys |
  * sort workspace]; otherwise device buffers are stream-ordered allocations freed
  * before return.  in_host == out_host is allowed. */
@@ -166,6 +182,11 @@ int pcf_sort_u64_host(const uint64_t *in_host, uint64_t *out_host, size_t n, con
  * H_out unspecified after either); PCF_ERR_CUDA / PCF_ERR_OOM. */
 int pcf_bucket_counts_f64(const double *keys, size_t n, uint64_t alpha, uint64_t beta, uint64_t gamma,
                           uint64_t seed, uint32_t *b_out, uint32_t *H_out, uint64_t *max_bucket, void *stream);
+
+/* Entries the pass log's level1_b / level1_h arrays need for a sort of n keys:
+ * beta + 1 = gamma + 1 = floor(n^{3/4}) + 1 (reading R5), plus one
+ * spare.  Pure host arithmetic. */
+size_t pcf_level1_entries(size_t n, const pcf_params *p);
 
 /* Human-readable name of a status code (static storage). */
 const char *pcf_status_string(int status);

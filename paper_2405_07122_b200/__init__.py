@@ -17,7 +17,9 @@ __all__ = ["build", "lib", "sort", "bucket_counts", "sort_host", "workspace_byte
 
 KEY_F64, KEY_U64 = 0, 1
 FLAG_SYNC, FLAG_SAMPLE_ALL, FLAG_TIMING, FLAG_PROFILE, FLAG_EXACT_RANKS = 1, 2, 4, 8, 16
-PHASES = ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "total"]
+PHASES = ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "total",
+          "deep_batches"]
+NPHASES = len(PHASES)
 STATUS = {0: "PCF_OK", 1: "PCF_ERR_INVALID_ARG", 2: "PCF_ERR_NAN", 3: "PCF_ERR_WORKSPACE_TOO_SMALL",
           4: "PCF_ERR_OOM", 5: "PCF_ERR_CUDA", 6: "PCF_ERR_LOG_OVERFLOW", 7: "PCF_ERR_INTERNAL",
           8: "PCF_ERR_DEGENERATE"}
@@ -40,19 +42,20 @@ class PassLog(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_uint32), ("rounds", ctypes.c_uint32),
-                ("host_syncs", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("host_syncs", ctypes.c_uint32), ("device_batches", ctypes.c_uint32),
                 ("groups_smem", ctypes.c_uint64), ("split_keys_moved", ctypes.c_uint64),
                 ("global_nodes", ctypes.c_uint64), ("fallback_keys_global", ctypes.c_uint64),
-                ("phase_ms", ctypes.c_float * 8), ("phase_bytes", ctypes.c_uint64 * 8),
+                ("phase_ms", ctypes.c_float * NPHASES), ("phase_bytes", ctypes.c_uint64 * NPHASES),
                 ("k7_cycles", ctypes.c_uint64 * 16)]
 
     def as_dict(self):
         return {"kernel_launches": self.kernel_launches, "rounds": self.rounds,
-                "host_syncs": self.host_syncs, "groups_smem": self.groups_smem,
+                "host_syncs": self.host_syncs, "device_batches": self.device_batches,
+                "groups_smem": self.groups_smem,
                 "split_keys_moved": self.split_keys_moved, "global_nodes": self.global_nodes,
                 "fallback_keys_global": self.fallback_keys_global,
-                "phase_ms": {PHASES[i]: float(self.phase_ms[i]) for i in range(8)},
-                "phase_bytes": {PHASES[i]: int(self.phase_bytes[i]) for i in range(8)},
+                "phase_ms": {PHASES[i]: float(self.phase_ms[i]) for i in range(NPHASES)},
+                "phase_bytes": {PHASES[i]: int(self.phase_bytes[i]) for i in range(NPHASES)},
                 "k7_cycles": [int(v) for v in self.k7_cycles]}
 
 
@@ -60,7 +63,8 @@ class Params(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("tau", ctypes.c_uint32),
                 ("seed", ctypes.c_uint64), ("flags", ctypes.c_uint32), ("reserved0", ctypes.c_uint32),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("log", ctypes.POINTER(PassLog)), ("stats", ctypes.POINTER(Stats))]
+                ("log", ctypes.POINTER(PassLog)), ("stats", ctypes.POINTER(Stats)),
+                ("status_out", ctypes.c_void_p)]
 
 
 class PCFError(RuntimeError):
@@ -72,7 +76,7 @@ class PCFError(RuntimeError):
 _lib = None
 SYMBOLS = ["pcf_params_init", "pcf_workspace_bytes", "pcf_sort_f64", "pcf_sort_u64", "pcf_sort_f64_host",
            "pcf_sort_u64_host", "pcf_status_string", "pcf_last_error", "pcf_abi_version",
-           "pcf_bucket_counts_f64"]
+           "pcf_bucket_counts_f64", "pcf_level1_entries"]
 
 
 def lib():
@@ -98,6 +102,7 @@ def lib():
         u64 = ctypes.c_uint64
         L.pcf_bucket_counts_f64.argtypes = [vp, sz, u64, u64, u64, u64, vp, vp, ctypes.POINTER(u64), vp]
         L.pcf_bucket_counts_f64.restype = i32
+        L.pcf_level1_entries.argtypes = [sz, PP]; L.pcf_level1_entries.restype = sz
         _ = u32
         _lib = L
     return _lib
@@ -156,11 +161,14 @@ class SortInfo:
 
 def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False, log: bool = False,
          timing: bool = False, stats: bool = False, sync: bool = True, workspace=None, node_capacity=None,
-         profile: bool = False, exact_ranks: bool = False, stream=None):
+         profile: bool = False, exact_ranks: bool = False, stream=None, status=None):
     """Sort a 1-D CUDA tensor of float64 or uint64 keys ascending (totalOrder for f64).
 
     Returns ``out`` (a new tensor unless given; ``out is x`` sorts in place), or
     ``(out, SortInfo)`` when ``log``/``timing``/``stats`` is requested.
+    ``sync=False`` returns right after enqueueing (no host synchronisation); the
+    call's status (0 = PCF_OK, 2 = PCF_ERR_NAN, ...) is then written, in stream
+    order, to ``status`` (a 1-element CUDA int32 tensor) if given.
     """
     import torch
 
@@ -185,17 +193,16 @@ def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False,
     p = make_params(tau, seed, flags)
     if workspace is not None:
         p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    if status is not None:
+        _check_device_buffer(status, torch.int32, 1, x.device, "status")
+        p.status_out = status.data_ptr()
     info = SortInfo() if (log or timing or stats or profile) else None
     keep = []
     if log:
         cap = node_capacity if node_capacity is not None else min(n, 12 * (n // max(tau, 1))) + 64
         recs = torch.zeros(cap * 9, dtype=torch.int64, device=x.device)   # 72-byte records
         cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
-        from math import isqrt
-        l1 = 2
-        if n:
-            # floor(n^{3/4}) + 2 upper bound without the library: isqrt(isqrt(n^3)) + 2
-            l1 = isqrt(isqrt(n ** 3)) + 2
+        l1 = int(lib().pcf_level1_entries(n, ctypes.byref(p))) if n else 2   # the library sizes it
         b = torch.zeros(l1, dtype=torch.int32, device=x.device)
         h = torch.zeros(l1, dtype=torch.int32, device=x.device)
         pl = PassLog(recs.data_ptr(), cap, cnt.data_ptr(), b.data_ptr(), h.data_ptr(), l1)

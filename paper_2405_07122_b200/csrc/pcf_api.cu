@@ -55,20 +55,22 @@ struct Caps {
     u64 bsum_cap;
 };
 
-constexpr u32 BND_MIN_LOG2 = 24;   // nodes of >= 2^20 keys get the gather-free digit table
+constexpr u32 BND_MIN_LOG2 = 24;   // nodes of >= 2^24 keys get the gather-free digit table
 
 static Caps caps_for(u64 n) {
     Caps c;
     c.n = n;
     c.P = (u32)iroot34(n);
-    c.node_cap = (u32)(n / S_CAP + 2);
+    // global nodes hold > S_CAP keys; nodes of one level are disjoint, and a global
+    // node nests in another only if the parent has > S_CAP^{4/3} keys: 2 n / S_CAP bounds them
+    c.node_cap = (u32)(2 * (n / S_CAP) + 64);
     // root tables + every oversized node: sum of 3*(m^{3/4}+2) over disjoint m > S_CAP
-    // is <= 3*(n^{3/4} + n / S_CAP^{1/4} + 2*node_cap)  (S_CAP^{1/4} > 9.5)
-    c.arena_u32 = 3ull * ((u64)c.P + 2) + 3ull * (n * 2 / 19 + 2ull * c.node_cap) + 64
+    // is <= 3*(n^{3/4} + n / S_CAP^{1/4} + 2*node_cap)  (S_CAP^{1/4} > 9.5), twice for nesting
+    c.arena_u32 = 3ull * ((u64)c.P + 2) + 6ull * (n * 2 / 19 + 2ull * c.node_cap) + 64
                   + (u64)GMAX * ((n >> BND_MIN_LOG2) + 1);   // digit boundaries of large nodes
     c.k7_cap = (u32)std::min<u64>(n / 32 + 65536, 0xffffffffull);
     c.split_cap = (u32)(n / 1024 + 4096);
-    c.items_cap = (u32)(n / S_CAP + 64);
+    c.items_cap = (u32)(2 * (n / S_CAP) + 64);   // items hold > S_CAP keys (see node_cap)
     // every split of a round has <= GMAX digits and ceil(m/SPLIT_TILE) tiles; a round's
     // splits are disjoint segments of > S_CAP keys (or of wider-than-NB_CAP bucket ranges)
     c.cmat_cap = (n / SPLIT_TILE + n / S_CAP + 64) * (u64)GMAX;
@@ -76,16 +78,9 @@ static Caps caps_for(u64 n) {
     return c;
 }
 
-struct Counters {             // zeroed at the start of every call
-    u32 nan_flag, err_flag, k7_count, k7_next;
-    u32 nsplits[2], nitems, k7_begin;
-    unsigned long long rec_count, k7_keys, split_keys, pad;
-    RoundPlan plan;
-    unsigned long long k7_prof[K7_PROF_SLOTS];
-};
-
 struct Layout {
-    size_t ctx, counters, tmp, digs, tmap, k7_order, bmm, bfs, bnl, nodes, acc, arena, k7, splits_a, splits_b, items, cmat, pmat, bsum, total;
+    size_t ctx, counters, tmp, digs, tmap, k7_order, bpre_mm, bpre_fs, nodes, arena, k7, splits_a, splits_b, items, fb,
+        k8_tb, k8_mb, k8_flag, cmat, pmat, bsum, status, total;
 };
 
 static Layout layout_for(const Caps &c) {
@@ -94,22 +89,24 @@ static Layout layout_for(const Caps &c) {
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
     L.ctx = take(sizeof(DevCtx));
     L.counters = take(sizeof(Counters));
+    L.status = take(16);
     L.tmp = take(c.n * 8);
     L.digs = take(c.n * 2);
     L.tmap = take((c.n / SPLIT_TILE + c.split_cap + 64) * 4);
     L.nodes = take((size_t)c.node_cap * sizeof(GNode));
-    L.acc = take((size_t)c.node_cap * sizeof(NodeAcc));
     L.arena = take(c.arena_u32 * 4);
     L.k7 = take((size_t)c.k7_cap * sizeof(K7Task));
     L.k7_order = take((size_t)c.k7_cap * 4);
-    // batched global nodes: chunk -> node maps (+ first chunk per node) and the node list
-    L.bmm = take((c.n / MMB_CHUNK + 2ull * c.node_cap + 64) * 4);
-    L.bfs = take((c.n / FSB_CHUNK + 2ull * c.node_cap + 64) * 4);
-    L.bnl = take(((u64)c.node_cap + 64) * 4);
+    L.bpre_mm = take(((u64)c.node_cap + 1) * 4);   // a batch's chunk prefix sums
+    L.bpre_fs = take(((u64)c.node_cap + 1) * 4);
     L.splits_a = take((size_t)c.split_cap * sizeof(SplitTask));
     L.splits_b = take((size_t)c.split_cap * sizeof(SplitTask));
     L.items = take((size_t)c.items_cap * sizeof(SegItem));
-    L.cmat = take(c.cmat_cap * 4);
+    L.fb = take((size_t)c.items_cap * sizeof(SegItem));   // fallback (K8) segments
+    L.k8_tb = take(((u64)c.items_cap + 1) * 4);
+    L.k8_mb = take(((u64)c.items_cap + 1) * 4);
+    L.k8_flag = take(((u64)c.items_cap + 1) * 4);
+    L.cmat = take(c.cmat_cap * 4);   // also the K8 merge-path splits (n / K8_MTILE + segments < cmat_cap)
     L.pmat = take(c.cmat_cap * 4);
     L.bsum = take(c.bsum_cap * 4);
     L.total = off;
@@ -117,8 +114,8 @@ static Layout layout_for(const Caps &c) {
 }
 
 static size_t small_layout_bytes() {
-    // n <= S_CAP: ctx + counters + one K7 task
-    return align_up(sizeof(DevCtx), 256) + align_up(sizeof(Counters), 256) + align_up(sizeof(K7Task), 256);
+    // n <= S_CAP: ctx + counters + status + one K7 task
+    return align_up(sizeof(DevCtx), 256) + align_up(sizeof(Counters), 256) + 256 + align_up(sizeof(K7Task), 256);
 }
 
 static size_t workspace_bytes_impl(size_t n) {
@@ -163,7 +160,8 @@ struct PhaseTimer {
     }
 };
 
-enum { PH_MINMAX = 0, PH_FIT = 1, PH_COUNT = 2, PH_SCATTER = 3, PH_K7 = 4, PH_K8 = 5, PH_OTHER = 6, PH_TOTAL = 7 };
+enum { PH_MINMAX = 0, PH_FIT = 1, PH_COUNT = 2, PH_SCATTER = 3, PH_K7 = 4, PH_K8 = 5, PH_OTHER = 6, PH_TOTAL = 7,
+       PH_BATCHES = 8 };
 
 static int k7_smem_bytes(u32 tau = 2) { return (int)(sizeof(K7Smem) + k7_lists_bytes(tau < 2 ? 2 : tau)); }
 static int split_smem_bytes() { return (int)sizeof(SplitScatterSmem); }
@@ -231,32 +229,220 @@ static int configure_kernels() {
     return PCF_OK;
 }
 
+// ---------------------------------------------------------------- launch helpers
+struct Launch {   // the kernel-launch configuration of this device
+    int nsm;
+    int k7_grid;
+    int count_grid;
+    int tau_smem;
+};
+
+// ---------------------------------------------------------------- device-driven tail (CUDA graph)
+// Everything after the host-launched first batch runs from one executable graph:
+//   k_items_to_nodes -> k_batch_cond -> WHILE (more work) {
+//       batched min/max, sampling, fit of the new global nodes;
+//       two split rounds (plan, tile map, count, scan x3, scatter, taskgen);
+//       K7 (order, kernel, advance); k_items_to_nodes; k_batch_cond }
+//   [phase boundary]
+//   k8_plan -> k8_check -> k8_blocksort -> WHILE (merge passes left) {
+//       k8_partition, k8_merge, k8_pass_end } -> k_log_finalize
+// The loop conditions are set on the device (cudaGraphSetConditional), so the
+// recursion over oversized buckets needs no host round trip.
+// Graphs depend only on (device, key type, DevCtx address, tau); they are cached
+// per thread (a repeated sort with the same workspace reuses them).
+struct TailGraph {
+    int dev;
+    int kt;
+    const void *ctx;
+    u32 tau;
+    cudaGraph_t g[2];
+    cudaGraphExec_t ex[2];
+    u32 body_kernels, parent_kernels[2], k8_body_kernels;
+};
+
+static thread_local std::vector<TailGraph> g_tails;
+static thread_local cudaStream_t g_cap[2] = {nullptr, nullptr};
+
+template <class K>
+static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32 *nk) {
+    CK(launch_pdl(k_round_plan, 1, 1024, 0, cs, d_ctx));
+    CK(launch_pdl(k_tile_map, lc.nsm * 2, 256, 0, cs, d_ctx));
+    CK(launch_pdl(k_split_count_tile<K>, lc.nsm * 8, SC_THREADS, 0, cs, d_ctx));
+    CK(launch_pdl(k_scanp_partials, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
+    CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, cs, d_ctx));
+    CK(launch_pdl(k_scanp_final, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
+    CK(launch_pdl(k_split_scatter<K>, lc.nsm * 2 * 4, SC_THREADS, split_smem_bytes(), cs, d_ctx));
+    CK(launch_pdl(k_split_taskgen, lc.nsm * 2, TG_THREADS, 0, cs, d_ctx));
+    *nk += 8;
+    return PCF_OK;
+}
+
+template <class K>
+static int add_k7(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32 *nk) {
+    CK(launch_pdl(k_k7_order, 1, 1024, 0, cs, d_ctx));
+    CK(launch_pdl(k7_kernel<K>, lc.k7_grid, K7_THREADS, lc.tau_smem, cs, d_ctx));
+    CK(launch_pdl(k_k7_advance, 1, 1, 0, cs, d_ctx));
+    *nk += 3;
+    return PCF_OK;
+}
+
+// Add a WHILE node after the current capture dependencies of `cs`, capture its
+// body from `body` (launched on the second capture stream), and continue the
+// capture of `cs` after the node.
+template <class F>
+static int add_while(cudaStream_t cs, cudaGraphConditionalHandle h, F body) {
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t cg;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t ndeps = 0;
+    CK(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &ndeps));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, cg, deps, ndeps, &cp));
+    cudaGraph_t bg = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(g_cap[1], bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    const int rc = body(g_cap[1]);
+    cudaGraph_t tmp;
+    const cudaError_t e = cudaStreamEndCapture(g_cap[1], &tmp);
+    if (rc) return rc;
+    CK(e);
+    CK(cudaStreamUpdateCaptureDependencies(cs, &node, 1, cudaStreamSetCaptureDependencies));
+    return PCF_OK;
+}
+
+template <class K>
+static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
+    for (int i = 0; i < 2; ++i)
+        if (!g_cap[i]) CK(cudaStreamCreateWithFlags(&g_cap[i], cudaStreamNonBlocking));
+    cudaStream_t cs = g_cap[0];
+    tg.body_kernels = 0;
+    tg.k8_body_kernels = 0;
+    // ---- graph 0: the device-driven batches of oversized recursing buckets
+    {
+        CK(cudaGraphCreate(&tg.g[0], 0));
+        cudaGraphConditionalHandle hb;
+        CK(cudaGraphConditionalHandleCreate(&hb, tg.g[0], 0, cudaGraphCondAssignDefault));
+        CK(cudaStreamBeginCaptureToGraph(cs, tg.g[0], nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        int rc = PCF_OK;
+        auto cap = [&]() -> int {
+            CK(launch_pdl(k_items_to_nodes<K>, 1, 1024, 0, cs, d_ctx));
+            CK(launch_pdl(k_batch_cond, 1, 1, 0, cs, d_ctx, hb, 0u));
+            return add_while(cs, hb, [&](cudaStream_t bs) -> int {
+                u32 nk = 0;
+                CK(launch_pdl(k_minmax_batch<K>, lc.nsm * 8, MM_THREADS, 0, bs, d_ctx));
+                CK(launch_pdl(k_fit_sample_batch<K>, lc.nsm * 8, FSB_CHUNK, 0, bs, d_ctx));
+                CK(launch_pdl(k_fit_batch, lc.nsm * 2, SCAN_THREADS, 0, bs, d_ctx));
+                nk += 3;
+                for (int r = 0; r < 2; ++r) { int e = add_round<K>(bs, d_ctx, lc, &nk); if (e) return e; }
+                int e = add_k7<K>(bs, d_ctx, lc, &nk);
+                if (e) return e;
+                CK(launch_pdl(k_items_to_nodes<K>, 1, 1024, 0, bs, d_ctx));
+                CK(launch_pdl(k_batch_cond, 1, 1, 0, bs, d_ctx, hb, 1u));
+                nk += 2;
+                tg.body_kernels = nk;
+                return PCF_OK;
+            });
+        };
+        rc = cap();
+        cudaGraph_t out;
+        const cudaError_t e = cudaStreamEndCapture(cs, &out);
+        if (rc) return rc;
+        CK(e);
+        tg.parent_kernels[0] = 2;
+    }
+    // ---- graph 1: the segmented fallback sort (K8) and the pass-log records
+    {
+        CK(cudaGraphCreate(&tg.g[1], 0));
+        cudaGraphConditionalHandle hk;
+        CK(cudaGraphConditionalHandleCreate(&hk, tg.g[1], 0, cudaGraphCondAssignDefault));
+        CK(cudaStreamBeginCaptureToGraph(cs, tg.g[1], nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        auto cap = [&]() -> int {
+            CK(launch_pdl(k8_plan, 1, 1024, 0, cs, d_ctx, hk));
+            CK(launch_pdl(k8_check, lc.nsm * 8, 256, 0, cs, d_ctx));
+            CK(launch_pdl(k8_blocksort<K>, lc.nsm * 3, K8_THREADS, K8_SORT_SMEM, cs, d_ctx));
+            int rc = add_while(cs, hk, [&](cudaStream_t bs) -> int {
+                CK(launch_pdl(k8_partition<K>, lc.nsm * 4, 256, 0, bs, d_ctx));
+                CK(launch_pdl(k8_merge<K>, lc.nsm * 8, K8_MTHREADS, K8_MERGE_SMEM, bs, d_ctx));
+                CK(launch_pdl(k8_pass_end, 1, 1, 0, bs, d_ctx, hk));
+                tg.k8_body_kernels = 3;
+                return PCF_OK;
+            });
+            if (rc) return rc;
+            CK(launch_pdl(k_log_finalize<K>, lc.nsm * 4, 256, 0, cs, d_ctx));
+            return PCF_OK;
+        };
+        const int rc = cap();
+        cudaGraph_t out;
+        const cudaError_t e = cudaStreamEndCapture(cs, &out);
+        if (rc) return rc;
+        CK(e);
+        tg.parent_kernels[1] = 4;
+    }
+    for (int i = 0; i < 2; ++i) CK(cudaGraphInstantiate(&tg.ex[i], tg.g[i], 0));
+    return PCF_OK;
+}
+
+template <class K>
+static int get_tail(const DevCtx *d_ctx, u32 tau, const Launch &lc, TailGraph **out) {
+    const int dev = cur_dev();
+    const int kt = K::is_f64 ? 0 : 1;
+    for (auto &t : g_tails)
+        if (t.dev == dev && t.kt == kt && t.ctx == d_ctx && t.tau == tau) { *out = &t; return PCF_OK; }
+    constexpr size_t MAX_TAILS = 8;
+    if (g_tails.size() >= MAX_TAILS) {   // evict the oldest
+        TailGraph &o = g_tails.front();
+        for (int i = 0; i < 2; ++i) { cudaGraphExecDestroy(o.ex[i]); cudaGraphDestroy(o.g[i]); }
+        g_tails.erase(g_tails.begin());
+    }
+    TailGraph tg;
+    memset(&tg, 0, sizeof tg);
+    tg.dev = dev; tg.kt = kt; tg.ctx = d_ctx; tg.tau = tau;
+    const int rc = build_tail<K>(tg, d_ctx, lc);
+    if (rc) {
+        for (int i = 0; i < 2; ++i) { if (tg.ex[i]) cudaGraphExecDestroy(tg.ex[i]); if (tg.g[i]) cudaGraphDestroy(tg.g[i]); }
+        return rc;
+    }
+    g_tails.push_back(tg);
+    *out = &g_tails.back();
+    return PCF_OK;
+}
+
 // ---------------------------------------------------------------- the sort
 template <class K>
 static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, cudaStream_t st) {
     pcf_params p;
     pcf_params_init(&p);
     if (pp) {
-        if (pp->struct_size < sizeof(pcf_params)) return fail(PCF_ERR_INVALID_ARG, "pcf_params.struct_size too small");
-        p = *pp;
+        if (pp->struct_size < PCF_PARAMS_V1_SIZE) return fail(PCF_ERR_INVALID_ARG, "pcf_params.struct_size too small");
+        memcpy(&p, pp, std::min<size_t>(pp->struct_size, sizeof(pcf_params)));
+        p.struct_size = sizeof(pcf_params);
     }
     if (p.tau < 2) return fail(PCF_ERR_INVALID_ARG, "tau must be >= 2");
-    if (n == 0) return PCF_OK;
-    if (!in || !out) return fail(PCF_ERR_INVALID_ARG, "NULL key pointer with n > 0");
+    if (!in || !out) { if (n) return fail(PCF_ERR_INVALID_ARG, "NULL key pointer with n > 0"); }
     if (n >= (1ull << 32)) return fail(PCF_ERR_INVALID_ARG, "n must be < 2^32 in ABI v1");
     if (((uintptr_t)in & 7) || ((uintptr_t)out & 7)) return fail(PCF_ERR_INVALID_ARG, "keys must be 8-byte aligned");
-    if (in != out) {
+    if (n && in != out) {
         uintptr_t a0 = (uintptr_t)in, a1 = a0 + n * 8, b0 = (uintptr_t)out, b1 = b0 + n * 8;
         if (a0 < b1 && b0 < a1) return fail(PCF_ERR_INVALID_ARG, "in and out overlap (only in == out is allowed)");
+    }
+    if (p.log && !p.log->count) return fail(PCF_ERR_INVALID_ARG, "pass log needs a count pointer");
+    const bool timing = (p.flags & PCF_FLAG_TIMING) != 0;
+    const bool sync = timing || (p.flags & PCF_FLAG_SYNC) != 0;
+    pcf_stats stats;
+    memset(&stats, 0, sizeof stats);
+    if (n == 0) {
+        if (p.status_out) CK(cudaMemsetAsync(p.status_out, 0, sizeof(int), st));
+        if (p.stats) *p.stats = stats;
+        return PCF_OK;
     }
     int rc = configure_kernels<K>();
     if (rc) return rc;
 
-    const bool timing = (p.flags & PCF_FLAG_TIMING) != 0;
-    const bool sync = timing || (p.flags & PCF_FLAG_SYNC) != 0;
     const bool logging = p.log != nullptr;
-    pcf_stats stats;
-    memset(&stats, 0, sizeof stats);
     PhaseTimer tm;
     tm.on = timing;
     tm.st = st;
@@ -297,7 +483,6 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.l1_b = p.log->level1_b;
         hc.l1_h = p.log->level1_h;
         hc.l1_cap = p.log->level1_capacity;
-        if (!p.log->count) return fail(PCF_ERR_INVALID_ARG, "pass log needs a count pointer");
         hc.rec_count = reinterpret_cast<unsigned long long *>(p.log->count);
         if (!hc.rec) hc.rec = reinterpret_cast<NodeRec *>(1);   // non-null marks logging on; cap 0
         CK(cudaMemsetAsync(p.log->count, 0, 8, st));
@@ -306,13 +491,16 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     const bool small = n <= (size_t)S_CAP;
     DevCtx *d_ctx;
     Counters *d_cnt;
+    int *d_status;
     Caps caps;
     Layout L;
     memset(&L, 0, sizeof L);
+    memset(&caps, 0, sizeof caps);
     if (small) {
         d_ctx = (DevCtx *)ws;
         d_cnt = (Counters *)(ws + align_up(sizeof(DevCtx), 256));
-        K7Task *d_task = (K7Task *)(ws + align_up(sizeof(DevCtx), 256) + align_up(sizeof(Counters), 256));
+        d_status = (int *)(ws + align_up(sizeof(DevCtx), 256) + align_up(sizeof(Counters), 256));
+        K7Task *d_task = (K7Task *)((char *)d_status + 256);
         hc.k7 = d_task;
         hc.k7_cap = 1;
         hc.buf[1] = nullptr;
@@ -321,8 +509,14 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         L = layout_for(caps);
         d_ctx = (DevCtx *)(ws + L.ctx);
         d_cnt = (Counters *)(ws + L.counters);
+        d_status = (int *)(ws + L.status);
         hc.buf[1] = (u64 *)(ws + L.tmp);
         hc.nodes = (GNode *)(ws + L.nodes);
+        hc.node_cap = caps.node_cap;
+        hc.arena = (u32 *)(ws + L.arena);
+        hc.arena_cap = caps.arena_u32;
+        hc.bpre_mm = (u32 *)(ws + L.bpre_mm);
+        hc.bpre_fs = (u32 *)(ws + L.bpre_fs);
         hc.k7 = (K7Task *)(ws + L.k7);
         hc.k7_order = (u32 *)(ws + L.k7_order);
         hc.k7_cap = caps.k7_cap;
@@ -331,6 +525,12 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.splits_cap = caps.split_cap;
         hc.items = (SegItem *)(ws + L.items);
         hc.items_cap = caps.items_cap;
+        hc.fb = (SegItem *)(ws + L.fb);
+        hc.fb_cap = caps.items_cap;
+        hc.k8_tb = (u32 *)(ws + L.k8_tb);
+        hc.k8_mb = (u32 *)(ws + L.k8_mb);
+        hc.k8_flag = (u32 *)(ws + L.k8_flag);
+        hc.k8_sp = (u32 *)(ws + L.cmat);   // free once the split rounds are done
         hc.cmat = (u32 *)(ws + L.cmat);
         hc.pmat = (u32 *)(ws + L.pmat);
         hc.bsum = (u32 *)(ws + L.bsum);
@@ -338,6 +538,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.digs = (u16 *)(ws + L.digs);
         hc.tmap = (u32 *)(ws + L.tmap);
     }
+    hc.cnt = d_cnt;
     hc.nan_flag = &d_cnt->nan_flag;
     hc.err_flag = &d_cnt->err_flag;
     hc.k7_count = &d_cnt->k7_count;
@@ -350,326 +551,184 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     hc.plan = &d_cnt->plan;
     hc.k7_prof = (p.flags & PCF_FLAG_PROFILE) ? d_cnt->k7_prof : nullptr;
     if (!logging) hc.rec_count = &d_cnt->rec_count;
-    CK(cudaMemcpyAsync(d_ctx, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(d_cnt, 0, sizeof(Counters), st));
 
     const bool sample_all = (p.flags & PCF_FLAG_SAMPLE_ALL) != 0;
-    u32 launches = 0;
-    int status = PCF_OK;
-    std::vector<SegItem> fallbacks;
-    u64 k7_tasks = 0, split_moved = 0, global_keys = 0;
-    u64 bytes[PCF_PHASES] = {0};
-    std::vector<u32> global_nodes;   // indices (for the pass-log finalisation)
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    Launch lc;
+    lc.nsm = nsm;
+    lc.k7_grid = nsm * k7_ctas_per_sm<K>();
+    lc.count_grid = nsm * count_ctas_per_sm<K>();
+    lc.tau_smem = k7_smem_bytes(p.tau);
 
+    // initial counters (host-built: the root node and its tables are carved here)
+    Counters h0;
+    memset(&h0, 0, sizeof h0);
+    u32 launches = 0;
+    u64 bytes[PCF_PHASES] = {0};
+    TailGraph *tail = nullptr;
     if (small) {
+        h0.k7_count = 1;
+        CK(cudaMemcpyAsync(d_ctx, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_cnt, &h0, sizeof h0, cudaMemcpyHostToDevice, st));
         K7Task t;
         memset(&t, 0, sizeof t);
         t.off = 0; t.size = (u32)n; t.kind = K7_NODE; t.src = 0; t.level = 1;
         CK(cudaMemcpyAsync(hc.k7, &t, sizeof t, cudaMemcpyHostToDevice, st));
-        u32 one = 1;
-        CK(cudaMemcpyAsync(&d_cnt->k7_count, &one, 4, cudaMemcpyHostToDevice, st));
         tm.begin(PH_K7);
-        k7_kernel<K><<<1, K7_THREADS, k7_smem_bytes(p.tau), st>>>(d_ctx);
+        k7_kernel<K><<<1, K7_THREADS, lc.tau_smem, st>>>(d_ctx);
         CK(cudaGetLastError());
         tm.end();
         launches++;
-        k7_tasks = 1;
         bytes[PH_K7] += 16ull * n;
     } else {
-        // ------------------------------------------------ global nodes
-        u64 arena_used = 0;
-        u32 *arena = (u32 *)(ws + L.arena);
-        u32 node_count = 0;
-        std::vector<SplitTask> list;
-        std::vector<u32> batch;   // nodes whose fit is launched together
-        std::vector<GNode> batch_nodes;
-        u64 batch_arena0 = 0;
-        std::vector<u32> node_m, node_alpha;
-        auto add_node = [&](u64 off, u32 m, u32 level, u32 src, bool batched) -> int {
-            if (node_count >= caps.node_cap) return fail(PCF_ERR_INTERNAL, "global node capacity exceeded");
-            GNode g;
-            memset(&g, 0, sizeof g);
-            u32 P = (u32)iroot34(m);
-            g.off = off; g.m = m; g.level = level;
-            g.kmin = ~0ull; g.kmax = 0;
-            g.alpha = sample_all ? m : P; g.beta = P; g.gamma = P; g.delta = P;
-            g.src = src;
-            u64 need_u32 = 3ull * ((u64)P + 2);
-            if (arena_used + need_u32 > caps.arena_u32) return fail(PCF_ERR_INTERNAL, "node table arena exceeded");
-            g.cnt = arena + arena_used;
-            g.T = g.cnt + (P + 2);
-            g.H = g.T + (P + 2);
-            arena_used += need_u32;
-            const u32 sh0 = choose_shift(P + 1, m);
-            if (!batched && m >= (1u << BND_MIN_LOG2) && arena_used + GMAX <= caps.arena_u32) {
-                g.bnd = arena + arena_used;
-                arena_used += GMAX;
-                g.bshift = sh0;
-                g.bG = (P + 1 + (1u << sh0) - 1) >> sh0;
-            }
-            u32 idx = node_count++;
-            node_m.push_back(m);
-            node_alpha.push_back(g.alpha);
-            if (!batched) {
-                CK(cudaMemcpyAsync(hc.nodes + idx, &g, sizeof g, cudaMemcpyHostToDevice, st));
-                CK(cudaMemsetAsync(g.cnt, 0, need_u32 * 4, st));
-            }
-            const DevCtx *dc = d_ctx;
-            if (batched) {   // uploaded (nodes, zeroed tables) with the rest of the batch
-                if (batch.empty()) batch_arena0 = (u64)(g.cnt - arena);
-                batch_nodes.push_back(g);
-                batch.push_back(idx);
-                bytes[PH_MINMAX] += 8ull * m;
-                bytes[PH_FIT] += 8ull * g.alpha + 8ull * (P + 2);
-            } else {
-            tm.begin(PH_MINMAX);
-            u64 nvec = m / 2 + 1;
-            u32 grid = (u32)std::min<u64>(148ull * 8, (nvec + MM_THREADS * MM_UNROLL - 1) / (MM_THREADS * MM_UNROLL));
-            CK(launch_pdl(k_minmax<K>, grid, MM_THREADS, 0, st, dc, idx));
-            tm.end();
-            tm.begin(PH_FIT);
-            u32 alpha = g.alpha;
-            CK(launch_pdl(k_fit_sample<K>, (alpha + 255) / 256, 256, 0, st, dc, idx));
-            {
-                u64 nbins = (u64)P + 1;
-                u32 nblk = (u32)((nbins + SCAN_CHUNK - 1) / SCAN_CHUNK);
-                u32 *bs = (u32 *)(ws + L.bsum);
-                CK(launch_pdl(k_scan_partials, nblk, SCAN_THREADS, 0, st, (const u32 *)(g.cnt + 1), (u64)nbins, bs));
-                CK(launch_pdl(k_scan_bsums, 1, SCAN_THREADS, 0, st, bs, nblk));
-                CK(launch_pdl(k_fit_final, nblk, SCAN_THREADS, 0, st, dc, idx, (const u32 *)bs));
-            }
-            tm.end();
-            CK(cudaGetLastError());
-            launches += 5;
-            bytes[PH_MINMAX] += 8ull * m;
-            bytes[PH_FIT] += 8ull * alpha + 8ull * (P + 2);
-            }
-            stats.global_nodes++;
-            global_nodes.push_back(idx);
-            SplitTask s;
-            memset(&s, 0, sizeof s);
-            s.off = off; s.m = m; s.node = idx; s.jlo = 1; s.jhi = P + 2;
-            s.shift = sh0;
-            s.G = (P + 1 + (1u << s.shift) - 1) >> s.shift;
-            s.src = src; s.dst = src == 1 ? 2 : 1;
-            list.push_back(s);
-            return PCF_OK;
-        };
-        int dev = 0, nsm = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        // host-side list of splits to append to the device list of the next round
-        rc = add_node(0, (u32)n, 1, 0, false);
-        if (rc) return rc;
-        u32 round = 0;
-        u32 pending = 0;   // splits already in the device list splits[round & 1]
-        auto flush_list = [&]() -> int {
-            if (list.empty()) return PCF_OK;
-            const u32 cur = round & 1u;
-            if (pending + list.size() > caps.split_cap) return fail(PCF_ERR_INTERNAL, "split list capacity exceeded");
-            CK(cudaMemcpyAsync(hc.splits[cur] + pending, list.data(), list.size() * sizeof(SplitTask),
-                               cudaMemcpyHostToDevice, st));
-            pending += (u32)list.size();
-            CK(cudaMemcpyAsync(&d_cnt->nsplits[cur], &pending, 4, cudaMemcpyHostToDevice, st));
-            list.clear();
-            return PCF_OK;
-        };
-        // upper bound on the tiles of the next round: its keys are <= n and it has at most
-        // (splits in it) partial tiles; the first round has 1 split, the second <= GMAX
-        u64 splits_bound = 0;   // upper bound on the splits of the round being enqueued
-        auto enqueue_round = [&]() -> int {
-            const u32 cur = round & 1u;
+        // ------------------------------------------------ level 1 (host-launched, exact grids)
+        const u32 P = (u32)iroot34(n);
+        GNode g;
+        memset(&g, 0, sizeof g);
+        g.off = 0; g.m = (u32)n; g.level = 1;
+        g.kmin = ~0ull; g.kmax = 0;
+        g.alpha = sample_all ? (u32)n : P; g.beta = P; g.gamma = P; g.delta = P;
+        g.src = 0;
+        u64 arena_used = 3ull * ((u64)P + 2);
+        u32 *arena = hc.arena;
+        g.cnt = arena;
+        g.T = g.cnt + (P + 2);
+        g.H = g.T + (P + 2);
+        const u32 sh0 = choose_shift(P + 1, (u32)n);
+        if (n >= (1ull << BND_MIN_LOG2)) {   // digit boundaries: gather-free digits in the first count pass
+            g.bnd = arena + arena_used;
+            arena_used += GMAX;
+            g.bshift = sh0;
+            g.bG = (P + 1 + (1u << sh0) - 1) >> sh0;
+        }
+        SplitTask s0;
+        memset(&s0, 0, sizeof s0);
+        s0.off = 0; s0.m = (u32)n; s0.node = 0; s0.jlo = 1; s0.jhi = P + 2;
+        s0.shift = sh0;
+        s0.G = (P + 1 + (1u << sh0) - 1) >> sh0;
+        s0.src = 0; s0.dst = 1;
+        h0.node_count = 1;
+        h0.arena_used = arena_used;
+        h0.nsplits[0] = 1;
+        h0.global_keys = n;
+        CK(cudaMemcpyAsync(d_ctx, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_cnt, &h0, sizeof h0, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(hc.nodes, &g, sizeof g, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(hc.splits[0], &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(g.cnt, 0, 3ull * ((u64)P + 2) * 4, st));
+        const DevCtx *dc = d_ctx;
+        tm.begin(PH_MINMAX);
+        {
+            const u64 nvec = n / 2 + 1;
+            const u32 grid = (u32)std::min<u64>(148ull * 8, (nvec + MM_THREADS * MM_UNROLL - 1) / (MM_THREADS * MM_UNROLL));
+            CK(launch_pdl(k_minmax<K>, grid, MM_THREADS, 0, st, dc, 0u));
+        }
+        tm.end();
+        tm.begin(PH_FIT);
+        {
+            CK(launch_pdl(k_fit_sample<K>, (g.alpha + 255) / 256, 256, 0, st, dc, 0u));
+            const u64 nbins = (u64)P + 1;
+            const u32 nblk = (u32)((nbins + SCAN_CHUNK - 1) / SCAN_CHUNK);
+            u32 *bs = hc.bsum;
+            CK(launch_pdl(k_scan_partials, nblk, SCAN_THREADS, 0, st, (const u32 *)(g.cnt + 1), (u64)nbins, bs));
+            CK(launch_pdl(k_scan_bsums, 1, SCAN_THREADS, 0, st, bs, nblk));
+            CK(launch_pdl(k_fit_final, nblk, SCAN_THREADS, 0, st, dc, 0u, (const u32 *)bs));
+        }
+        tm.end();
+        CK(cudaGetLastError());
+        launches += 5;
+        bytes[PH_MINMAX] += 8ull * n;
+        bytes[PH_FIT] += 8ull * g.alpha + 8ull * (P + 2);
+        // two split rounds with grids sized from n (an upper bound on each round's tiles)
+        u64 splits_bound = 1;
+        for (int r = 0; r < 2; ++r) {
             const u32 tile_grid = (u32)std::min<u64>(n / SPLIT_TILE + 1 + splits_bound, 0x7fffffffull);
-            // each split yields <= GMAX next splits; overflow carry-over adds <= the current ones
             splits_bound = std::min<u64>(splits_bound * (GMAX + 1), caps.split_cap);
             tm.begin(PH_OTHER);
-            CK(launch_pdl(k_round_plan, 1, 1024, 0, st, (const DevCtx *)d_ctx, cur));
-            CK(launch_pdl(k_tile_map, nsm * 2, 256, 0, st, (const DevCtx *)d_ctx, cur));
+            CK(launch_pdl(k_round_plan, 1, 1024, 0, st, dc));
+            CK(launch_pdl(k_tile_map, nsm * 2, 256, 0, st, dc));
             tm.end();
             tm.begin(PH_COUNT);
-            // one CTA per tile for small sorts and for rounds after the first (their T
-            // gathers are local to a split: they need L1, which the persistent kernel's
-            // 2 x 111 KB of staging takes); the persistent bulk-copy kernel for the first
-            // round of a large sort (gather-free digit table)
-            if (n <= (1ull << 25) || round > 0) CK(launch_pdl(k_split_count_tile<K>, tile_grid, SC_THREADS, 0, st, (const DevCtx *)d_ctx, cur));
-            else CK(launch_pdl(k_split_count<K>, nsm * count_ctas_per_sm<K>(), CNT_THREADS, sizeof(CountSmem), st, (const DevCtx *)d_ctx, cur));
+            // one CTA per tile for small sorts and the second round (their T gathers are
+            // local to a split: they need L1, which the persistent kernel's 2 x 111 KB of
+            // staging takes); the persistent bulk-copy kernel for the first round of a
+            // large sort (gather-free digit table)
+            if (n <= (1ull << 25) || r > 0) CK(launch_pdl(k_split_count_tile<K>, tile_grid, SC_THREADS, 0, st, dc));
+            else CK(launch_pdl(k_split_count<K>, lc.count_grid, CNT_THREADS, sizeof(CountSmem), st, dc));
             tm.end();
             tm.begin(PH_OTHER);
-            CK(launch_pdl(k_scanp_partials, nsm * 2, SCAN_THREADS, 0, st, (const DevCtx *)d_ctx));
-            CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, st, (const DevCtx *)d_ctx));
-            CK(launch_pdl(k_scanp_final, nsm * 2, SCAN_THREADS, 0, st, (const DevCtx *)d_ctx));
+            CK(launch_pdl(k_scanp_partials, nsm * 2, SCAN_THREADS, 0, st, dc));
+            CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, st, dc));
+            CK(launch_pdl(k_scanp_final, nsm * 2, SCAN_THREADS, 0, st, dc));
             tm.end();
             tm.begin(PH_SCATTER);
-            CK(launch_pdl(k_split_scatter<K>, tile_grid, SC_THREADS, split_smem_bytes(), st, (const DevCtx *)d_ctx, cur));
+            CK(launch_pdl(k_split_scatter<K>, tile_grid, SC_THREADS, split_smem_bytes(), st, dc));
             tm.end();
             tm.begin(PH_OTHER);
-            CK(launch_pdl(k_split_taskgen, nsm * 2, TG_THREADS, 0, st, (const DevCtx *)d_ctx, cur));
+            CK(launch_pdl(k_split_taskgen, nsm * 2, TG_THREADS, 0, st, dc));
             tm.end();
             launches += 8;
-            round++;
-            return PCF_OK;
-        };
-        u32 rounds_per_batch = 2;   // enough for 10^6..10^9 keys of well-modelled data
-        for (;;) {
-            rc = flush_list();
+        }
+        // K7 over every group produced so far (persistent grid; reads the task count on the device)
+        tm.begin(PH_K7);
+        {
+            u32 nk = 0;
+            rc = add_k7<K>(st, dc, lc, &nk);
             if (rc) return rc;
-            splits_bound = pending;
-            for (u32 k = 0; k < rounds_per_batch; ++k) {
-                rc = enqueue_round();
-                if (rc) return rc;
-            }
-            CK(cudaGetLastError());
-            // K7 over every group produced so far (persistent grid; reads the task count on the device)
-            tm.begin(PH_K7);
-            CK(launch_pdl(k_k7_order, 1, 1024, 0, st, (const DevCtx *)d_ctx));
-            CK(launch_pdl(k7_kernel<K>, nsm * k7_ctas_per_sm<K>(), K7_THREADS, k7_smem_bytes(p.tau), st, (const DevCtx *)d_ctx));
-            CK(launch_pdl(k_k7_advance, 1, 1, 0, st, (const DevCtx *)d_ctx));
-            tm.end();
-            CK(cudaGetLastError());
-            launches += 3;
-            Counters hcnt;
-            CK(cudaMemcpyAsync(&hcnt, d_cnt, sizeof hcnt, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            stats.host_syncs++;
-            if (hcnt.nan_flag) { status = PCF_ERR_NAN; break; }
-            if (hcnt.err_flag) return fail(PCF_ERR_INTERNAL, "device work-queue capacity exceeded (err_flag=" + std::to_string(hcnt.err_flag) + ")");
-            k7_tasks = hcnt.k7_count;
-            pending = hcnt.nsplits[round & 1u];
-            std::vector<SegItem> items(hcnt.nitems);
-            if (hcnt.nitems) {
-                CK(cudaMemcpyAsync(items.data(), hc.items, hcnt.nitems * sizeof(SegItem), cudaMemcpyDeviceToHost, st));
-                CK(cudaStreamSynchronize(st));
-                CK(cudaMemsetAsync(&d_cnt->nitems, 0, 4, st));
-            }
-            for (const SegItem &it : items) {
-                if (it.kind == 0) { rc = add_node(it.off, it.m, it.level, it.src, true); if (rc) return rc; }
-                else fallbacks.push_back(it);
-            }
-            if (!batch.empty()) {   // one min/max, one sampling and one fit launch for every new node
-                std::vector<u32> cmm, fmm, cfs, ffs;
-                u64 nkeys = 0;
-                // the batch's node records (consecutive indices) and its zeroed table range
-                CK(cudaMemcpyAsync(hc.nodes + batch[0], batch_nodes.data(), batch_nodes.size() * sizeof(GNode),
-                                   cudaMemcpyHostToDevice, st));
-                CK(cudaMemsetAsync(arena + batch_arena0, 0, (arena_used - batch_arena0) * 4, st));
-                for (u32 idx : batch) {
-                    fmm.push_back((u32)cmm.size());
-                    ffs.push_back((u32)cfs.size());
-                    const u32 m = node_m[idx], al = node_alpha[idx];
-                    for (u32 q = 0; q < (m + MMB_CHUNK - 1) / MMB_CHUNK; ++q) cmm.push_back(idx);
-                    for (u32 q = 0; q < (al + FSB_CHUNK - 1) / FSB_CHUNK; ++q) cfs.push_back(idx);
-                    nkeys += m;
-                }
-                // first-chunk tables are indexed by node: scatter them into node-sized arrays
-                std::vector<u32> nfm(node_count, 0), nfs(node_count, 0);
-                for (size_t i = 0; i < batch.size(); ++i) { nfm[batch[i]] = fmm[i]; nfs[batch[i]] = ffs[i]; }
-                u32 *d_cmm = (u32 *)(ws + L.bmm), *d_nfm = d_cmm + cmm.size();
-                u32 *d_cfs = (u32 *)(ws + L.bfs), *d_nfs = d_cfs + cfs.size();
-                u32 *d_nl = (u32 *)(ws + L.bnl);
-                CK(cudaMemcpyAsync(d_cmm, cmm.data(), cmm.size() * 4, cudaMemcpyHostToDevice, st));
-                CK(cudaMemcpyAsync(d_nfm, nfm.data(), nfm.size() * 4, cudaMemcpyHostToDevice, st));
-                CK(cudaMemcpyAsync(d_cfs, cfs.data(), cfs.size() * 4, cudaMemcpyHostToDevice, st));
-                CK(cudaMemcpyAsync(d_nfs, nfs.data(), nfs.size() * 4, cudaMemcpyHostToDevice, st));
-                CK(cudaMemcpyAsync(d_nl, batch.data(), batch.size() * 4, cudaMemcpyHostToDevice, st));
-                tm.begin(PH_MINMAX);
-                CK(launch_pdl(k_minmax_batch<K>, (u32)cmm.size(), MM_THREADS, 0, st, (const DevCtx *)d_ctx,
-                              (const u32 *)d_cmm, (const u32 *)d_nfm));
-                tm.end();
-                tm.begin(PH_FIT);
-                CK(launch_pdl(k_fit_sample_batch<K>, (u32)cfs.size(), FSB_CHUNK, 0, st, (const DevCtx *)d_ctx,
-                              (const u32 *)d_cfs, (const u32 *)d_nfs));
-                CK(launch_pdl(k_fit_batch, (u32)batch.size(), SCAN_THREADS, 0, st, (const DevCtx *)d_ctx, (const u32 *)d_nl));
-                tm.end();
-                launches += 3;
-                batch.clear();
-                batch_nodes.clear();
-            }
-            split_moved = hcnt.split_keys;
-            bytes[PH_K7] = 16ull * hcnt.k7_keys;
-            if (pending == 0 && list.empty()) break;
-            rounds_per_batch = 2;
+            launches += nk;
         }
-        stats.rounds = round;
-        stats.split_keys_moved = split_moved;
-        // one classify (8 B/key) and one stable scatter (16 B/key) per
-        // bucketing level of every key the global path buckets; extra digit rounds are
-        // traffic, not algorithmic bytes (reported as split_keys_moved)
-        for (u32 m_ : node_m) global_keys += m_;
-        bytes[PH_COUNT] = 8ull * global_keys;
-        bytes[PH_SCATTER] = 16ull * global_keys;
-        if (status == PCF_OK) {
-            // K8: global Standard-Sort of large buckets (flags in pmat, merge splits in cmat:
-            // both are free once the split rounds are done)
-            u32 *k8_flags = hc.pmat, *k8_sp = hc.cmat;
-            if (!fallbacks.empty()) CK(cudaMemsetAsync(k8_flags, 0, 4 * fallbacks.size(), st));
-            for (size_t fi = 0; fi < fallbacks.size(); ++fi) {
-                const SegItem &it = fallbacks[fi];
-                const u64 m = it.m;
-                u64 *src = (it.src == 0 ? const_cast<u64 *>(in) : it.src == 1 ? hc.buf[1] : out) + it.off;
-                u64 *bo = out + it.off, *bt = hc.buf[1] + it.off;
-                u32 *flag = k8_flags + fi;
-                u32 npass = 1;
-                for (u64 w = K8_TILE; w < m; w *= 2) npass++;
-                // pass k writes `out` iff (npass - 1 - k) is even, so the last pass lands in out
-                u64 *dst0 = ((npass - 1) % 2 == 0) ? bo : bt;
-                const u32 nblk = (u32)((m + K8_TILE - 1) / K8_TILE);
-                tm.begin(PH_K8);
-                k8_check<<<(u32)std::min<u64>(4ull * nsm, (m + 255) / 256), 256, 0, st>>>(src, m, flag);
-                k8_blocksort<K><<<nblk, K8_THREADS, K8_SORT_SMEM, st>>>(src, dst0, bo, m, flag);
-                u64 *cur = dst0;
-                for (u64 w = K8_TILE; w < m; w *= 2) {
-                    u64 *nxt = cur == bo ? bt : bo;
-                    const u32 nmt = (u32)((m + K8_MTILE - 1) / K8_MTILE);
-                    k8_partition<K><<<(nmt + 255) / 256, 256, 0, st>>>(cur, m, w, nmt, k8_sp, flag);
-                    k8_merge<K><<<nmt, K8_MTHREADS, K8_MERGE_SMEM, st>>>(cur, nxt, m, w, k8_sp, flag, 2 * w >= m ? 1u : 0u);
-                    cur = nxt;
-                    launches += 2;
-                }
-                tm.end();
-                launches += 2;
-                CK(cudaGetLastError());
-                bytes[PH_K8] += 24ull * m;   // check + block sort; the merge passes are added below (timing)
-                stats.fallback_keys_global += m;
-            }
-            if (timing && !fallbacks.empty()) {   // merge passes run only for buckets with two distinct keys
-                std::vector<u32> fl(fallbacks.size());
-                CK(cudaMemcpyAsync(fl.data(), k8_flags, 4 * fl.size(), cudaMemcpyDeviceToHost, st));
-                CK(cudaStreamSynchronize(st));
-                for (size_t fi = 0; fi < fl.size(); ++fi) {
-                    u32 npass = 1;
-                    for (u64 w = K8_TILE; w < fallbacks[fi].m; w *= 2) npass++;
-                    if (fl[fi]) bytes[PH_K8] += 16ull * fallbacks[fi].m * (npass - 1);
-                }
-            }
-            // pass log: records of the global nodes (need the complete H)
-            if (logging) {
-                NodeAcc *acc = (NodeAcc *)(ws + L.acc);
-                CK(cudaMemsetAsync(acc, 0, sizeof(NodeAcc) * node_count, st));
-                for (u32 idx : global_nodes) {
-                    k_node_finalize_acc<<<64, 256, 0, st>>>(d_ctx, idx, acc + idx);
-                    k_node_finalize_rec<K><<<1, 1, 0, st>>>(d_ctx, idx, acc + idx);
-                    launches += 2;
-                }
-                CK(cudaGetLastError());
-            }
-        }
+        tm.end();
+        CK(cudaGetLastError());
+        // ------------------------------------------------ everything after: device-driven (graphs)
+        rc = get_tail<K>(d_ctx, p.tau, lc, &tail);
+        if (rc) return rc;
+        tm.begin(PH_BATCHES);
+        CK(cudaGraphLaunch(tail->ex[0], st));
+        tm.end();
+        tm.begin(PH_K8);
+        CK(cudaGraphLaunch(tail->ex[1], st));
+        tm.end();
+        launches += tail->parent_kernels[0] + tail->parent_kernels[1];
     }
-    stats.groups_smem = k7_tasks;
+    if (p.status_out) {
+        k_status<<<1, 1, 0, st>>>(d_ctx, p.status_out);
+        CK(cudaGetLastError());
+        launches++;
+    }
     if (timing) cudaEventRecord(ev_total1, st);
+    int status = PCF_OK;
     if (sync) {
         Counters hcnt;
         CK(cudaMemcpyAsync(&hcnt, d_cnt, sizeof hcnt, cudaMemcpyDeviceToHost, st));
+        unsigned long long rcnt = 0;
+        if (logging) CK(cudaMemcpyAsync(&rcnt, p.log->count, 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        stats.host_syncs++;
-        if (hcnt.nan_flag) status = PCF_ERR_NAN;
+        stats.host_syncs = 1;
+        if (hcnt.nan_flag) status = fail(PCF_ERR_NAN, "input contains NaN");
         else if (hcnt.err_flag) status = fail(PCF_ERR_INTERNAL, "device capacity exceeded (err_flag=" + std::to_string(hcnt.err_flag) + ")");
-        if (status == PCF_OK && logging) {
-            unsigned long long cnt = 0;
-            CK(cudaMemcpy(&cnt, p.log->count, 8, cudaMemcpyDeviceToHost));
-            if (cnt > p.log->capacity) status = fail(PCF_ERR_LOG_OVERFLOW, "pass log capacity exceeded");
-        }
-        if (status == PCF_ERR_NAN) fail(PCF_ERR_NAN, "input contains NaN");
+        else if (logging && rcnt > p.log->capacity) status = fail(PCF_ERR_LOG_OVERFLOW, "pass log capacity exceeded");
         for (int i = 0; i < K7_PROF_SLOTS; ++i) stats.k7_cycles[i] = hcnt.k7_prof[i];
+        stats.rounds = hcnt.round;
+        stats.groups_smem = hcnt.k7_count;
+        stats.global_nodes = small ? 0 : hcnt.node_count;
+        stats.split_keys_moved = hcnt.split_keys;
+        stats.fallback_keys_global = hcnt.fb_keys;
+        if (tail) {
+            launches += hcnt.iters * tail->body_kernels + hcnt.k8.max_merges * tail->k8_body_kernels;
+            stats.device_batches = hcnt.iters;
+        }
+        if (!small) {
+            // one classify (8 B/key) and one stable scatter (16 B/key) per
+            // bucketing level of every key the global path buckets; extra digit rounds are
+            // traffic, not algorithmic bytes (reported as split_keys_moved)
+            bytes[PH_COUNT] = 8ull * hcnt.global_keys;
+            bytes[PH_SCATTER] = 16ull * hcnt.global_keys;
+            bytes[PH_K7] = 16ull * hcnt.k7_keys;
+            bytes[PH_K8] = hcnt.k8_bytes;
+            bytes[PH_MINMAX] = 8ull * hcnt.global_keys;
+        }
     }
     stats.kernel_launches = launches;
     if (timing) {
@@ -696,8 +755,9 @@ static int sort_host(const u64 *in_h, u64 *out_h, size_t n, const pcf_params *pp
     pcf_params p;
     pcf_params_init(&p);
     if (pp) {
-        if (pp->struct_size < sizeof(pcf_params)) return fail(PCF_ERR_INVALID_ARG, "pcf_params.struct_size too small");
-        p = *pp;
+        if (pp->struct_size < PCF_PARAMS_V1_SIZE) return fail(PCF_ERR_INVALID_ARG, "pcf_params.struct_size too small");
+        memcpy(&p, pp, std::min<size_t>(pp->struct_size, sizeof(pcf_params)));
+        p.struct_size = sizeof(pcf_params);
     }
     const bool own_keys = !(p.workspace && p.workspace_bytes >= key_bytes + sort_ws);
     if (own_keys) {
@@ -710,6 +770,14 @@ static int sort_host(const u64 *in_h, u64 *out_h, size_t n, const pcf_params *pp
         p.workspace = (char *)p.workspace + key_bytes;
         p.workspace_bytes -= key_bytes;
     }
+    // one synchronisation for the whole call: the sort runs asynchronously and
+    // reports through a device status word read after the result's D2H copy
+    int *d_status = nullptr;
+    int *user_status = p.status_out;
+    e = cudaMallocAsync((void **)&d_status, sizeof(int), st);
+    if (e != cudaSuccess) { cudaGetLastError(); if (own_keys) cudaFreeAsync(d, st); return fail(PCF_ERR_OOM, "cudaMallocAsync status failed"); }
+    p.status_out = d_status;
+    p.flags &= ~(PCF_FLAG_SYNC | PCF_FLAG_TIMING);
     int rc = PCF_OK;
     e = cudaMemcpyAsync(d, in_h, n * 8, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
@@ -718,9 +786,17 @@ static int sort_host(const u64 *in_h, u64 *out_h, size_t n, const pcf_params *pp
         e = cudaMemcpyAsync(out_h, d, n * 8, cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
     }
+    int hs = PCF_OK;
+    if (!rc) {
+        e = cudaMemcpyAsync(&hs, d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
+        if (!rc && user_status) cudaMemcpyAsync(user_status, d_status, sizeof(int), cudaMemcpyDefault, st);
+    }
+    cudaFreeAsync(d_status, st);
     if (own_keys) cudaFreeAsync(d, st);
     e = cudaStreamSynchronize(st);
     if (!rc && e != cudaSuccess) rc = fail(PCF_ERR_CUDA, cudaGetErrorString(e));
+    if (!rc && hs != PCF_OK) rc = fail(hs, hs == PCF_ERR_NAN ? "input contains NaN" : "device status " + std::to_string(hs));
     return rc;
 }
 
@@ -784,6 +860,7 @@ void pcf_params_init(pcf_params *p) {
     p->tau = 64;
     p->seed = 0;
     p->flags = PCF_FLAG_SYNC;
+    p->status_out = NULL;
 }
 
 size_t pcf_workspace_bytes(size_t n, int key_type, const pcf_params *p) {
@@ -831,6 +908,11 @@ int pcf_bucket_counts_f64(const double *keys, size_t n, uint64_t alpha, uint64_t
                           uint64_t seed, uint32_t *b_out, uint32_t *H_out, uint64_t *max_bucket, void *stream) {
     return pcf::bucket_counts_f64(reinterpret_cast<const pcf::u64 *>(keys), n, alpha, beta, gamma, seed, b_out, H_out,
                                   max_bucket, (cudaStream_t)stream);
+}
+
+size_t pcf_level1_entries(size_t n, const pcf_params *p) {
+    (void)p;
+    return n ? (size_t)pcf::iroot34(n) + 2 : 2;
 }
 
 const char *pcf_last_error(void) { return pcf::g_last_error.c_str(); }

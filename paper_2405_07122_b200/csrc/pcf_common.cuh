@@ -46,6 +46,7 @@ constexpr int SC_KPL = PCF_SC_KPL;             // keys per lane held in register
 constexpr int SC_PER_WARP = SC_KPL * 32; // 512 consecutive keys per warp
 constexpr int SPLIT_TILE = SC_WARPS * SC_PER_WARP;   // 5376 keys per split tile
 constexpr u64 GOLDEN = 0x9E3779B97F4A7C15ull;
+#define K7_PROF_SLOTS_DECL 16
 
 // ---------------------------------------------------------------- key transforms
 // totalOrder on binary64 == unsigned order of the "flipped" bits: set the sign
@@ -261,13 +262,48 @@ struct RoundPlan {
     u32 nblk;      // scan blocks over the count matrix
     u32 next_count;   // dynamic tile claims of k_split_count
     u32 next_scatter; // dynamic tile claims of k_split_scatter
-    u32 pad;
+    u32 cur;       // split list this round consumes (splits[cur]); the next round's is cur ^ 1
     u64 ctot;      // count-matrix entries
     u64 mtot;      // keys moved
 };
 
+// The batch of global nodes created on the device from the oversized recursing
+// buckets of the previous batch (k_items_to_nodes): nodes [first, first + nb),
+// their tables in arena[a0, a1), and the CTA chunk prefix sums of the batched
+// min/max (MMB_CHUNK keys per chunk) and sampling (FSB_CHUNK samples) kernels.
+struct BatchInfo {
+    u32 first, nb;
+    u32 mm_chunks, fs_chunks;   // totals
+    u64 a0, a1;
+};
+
+// Segmented fallback sort (K8) over every Standard-Sort bucket of > S_CAP keys.
+struct K8Plan {
+    u32 nseg;
+    u32 tiles;       // block-sort tiles over all segments
+    u32 mtiles;      // merge tiles over all segments
+    u32 max_merges;  // merge passes of the largest segment
+    u32 pass;        // current merge pass
+    u32 pad;
+};
+
+// Device counters of one sort (zeroed / initialised by the host at the start of
+// every call; read back only when the caller asks for a synchronous call).
+struct Counters {
+    u32 nan_flag, err_flag, k7_count, k7_next;
+    u32 nsplits[2], nitems, k7_begin;
+    unsigned long long rec_count, k7_keys, split_keys, global_keys;
+    RoundPlan plan;
+    u32 round, node_count, fb_count, iters;   // iters: device-driven batches run
+    unsigned long long arena_used, k8_bytes, fb_keys;
+    BatchInfo batch;
+    K8Plan k8;
+    unsigned long long k7_prof[K7_PROF_SLOTS_DECL];
+};
+
 struct DevCtx {
     u64 *buf[3];            // in (const, never written unless in==out), tmp, out
+    Counters *cnt;          // device counters of this call
     u64 n;
     u64 seed;
     u32 tau;
@@ -299,6 +335,17 @@ struct DevCtx {
     u32 *nan_flag;
     u32 *err_flag;          // bit0 capacity overflow, bit1 internal
     unsigned long long *k7_keys;   // keys handed to K7 (for the byte accounting)
+    // device-driven batches (k_items_to_nodes): node table and arena capacities,
+    // CTA chunk prefix sums of the current batch
+    u32 node_cap;
+    u32 *arena;
+    u64 arena_cap;
+    u32 *bpre_mm, *bpre_fs;   // [node_cap + 1]
+    // fallback (K8) segments
+    SegItem *fb;
+    u32 fb_cap;
+    u32 *k8_tb, *k8_mb, *k8_flag;   // per segment: first tile, first merge tile, "two distinct keys"
+    u32 *k8_sp;                     // merge-path split of every merge tile
     // pass log
     NodeRec *rec;
     unsigned long long *rec_count;
@@ -347,6 +394,6 @@ __device__ __forceinline__ void pdl_entry() {
 
 constexpr u32 FLAG_SAMPLE_ALL = 2u;
 constexpr u32 FLAG_EXACT_RANKS = 16u;
-constexpr int K7_PROF_SLOTS = 16;
+constexpr int K7_PROF_SLOTS = K7_PROF_SLOTS_DECL;
 
 }  // namespace pcf

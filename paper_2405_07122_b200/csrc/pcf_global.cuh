@@ -90,6 +90,54 @@ __device__ __forceinline__ void push_item(const DevCtx *c, u64 off, u32 m, u32 l
     }
 }
 
+// --- exclusive scan of a u32 array (3 phases)
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
+
+__device__ __forceinline__ u32 block_excl_scan_1024(u32 v, u32 *wsum, u32 &total) {
+    const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u32 x = v;
+    for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= (u32)o) x += y; }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        u32 s = wsum[lane];
+        u32 t = s;
+        for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, t, o); if (lane >= (u32)o) t += y; }
+        wsum[lane] = t - s;
+        if (lane == 31) wsum[32] = t;
+    }
+    __syncthreads();
+    u32 r = wsum[w] + x - v;
+    total = wsum[32];
+    __syncthreads();
+    return r;
+}
+
+__host__ __device__ inline u32 ceil_log2_u32(u32 v) {   // v >= 1
+    u32 r = 0;
+    while ((1ull << r) < v) ++r;
+    return r;
+}
+__host__ __device__ inline u32 floor_log2_u64(u64 v) {  // v >= 1
+    u32 r = 0;
+    while (v >> (r + 1)) ++r;
+    return r;
+}
+// Digit shift for splitting W >= 2 consecutive buckets holding c keys:
+// G = ceil(W / 2^s) <= GMAX, expected group ~ S_CAP/2 keys, G >= 2.
+__host__ __device__ inline u32 choose_shift(u32 W, u32 c) {
+    u32 cl = ceil_log2_u32(W);
+    u32 smin = cl > GMAX_LOG2 ? cl - GMAX_LOG2 : 0;
+    u64 q = ((u64)(S_CAP / 2) * W) / (c ? c : 1);
+    u32 st = floor_log2_u64(q ? q : 1);
+    u32 s = st < 10 ? st : 10;
+    if (s < smin) s = smin;
+    if (s > cl - 1) s = cl - 1;
+    return s;
+}
+
 template <class K>
 __global__ void k_node_model(const DevCtx *__restrict__ c, u32 node) {
     pdl_entry();
@@ -128,67 +176,244 @@ __global__ void k_fit_sample(const DevCtx *__restrict__ c, u32 node) {
 
 // ------------------------------------------------------------------ batched global nodes
 // The recursing buckets too large for a K7 CTA that one batch produces (up to
-// thousands for skewed inputs at 10^8-10^9 keys) are fitted together: one
-// min/max launch, one sampling launch and one fit launch for all of them,
-// instead of five launches per node.  A chunk list maps every CTA to its node
-// (cnode[b]) and its first chunk (nfirst[node]).
-constexpr int MMB_CHUNK = 16384;   // keys per min/max CTA
-constexpr int FSB_CHUNK = 256;     // samples per sampling CTA
+// thousands for skewed inputs at 10^8-10^9 keys) become global nodes on the
+// device (k_items_to_nodes) and are fitted together: one min/max launch, one
+// sampling launch and one fit launch for all of them.  Both chunked kernels are
+// grid-stride over the batch's chunks; a chunk finds its node by a binary search
+// over the batch's chunk prefix sums (bpre_mm / bpre_fs, built by k_items_to_nodes).
+constexpr int MMB_CHUNK = 16384;   // keys per min/max chunk
+constexpr int FSB_CHUNK = 256;     // samples per sampling chunk
+
+__device__ __forceinline__ u32 batch_node_of(const u32 *__restrict__ pre, u32 nb, u32 chunk) {
+    u32 lo = 0, hi = nb - 1;   // last k with pre[k] <= chunk
+    while (lo < hi) {
+        const u32 mid = (lo + hi + 1) >> 1;
+        if (pre[mid] <= chunk) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
 
 template <class K>
-__global__ void __launch_bounds__(MM_THREADS) k_minmax_batch(const DevCtx *__restrict__ c, const u32 *__restrict__ cnode,
-                                                            const u32 *__restrict__ nfirst) {
+__global__ void __launch_bounds__(MM_THREADS) k_minmax_batch(const DevCtx *__restrict__ c) {
     pdl_entry();
     if (*c->nan_flag) return;
-    const u32 node = cnode[blockIdx.x];
-    GNode &g = c->nodes[node];
-    const u64 s0 = (u64)(blockIdx.x - nfirst[node]) * MMB_CHUNK, s1 = min((u64)g.m, s0 + MMB_CHUNK);
-    const u64 *x = c->buf[g.src] + g.off;
-    u64 mn = ~0ull, mx = 0;
-    bool nan = false;
-    constexpr int U = MMB_CHUNK / MM_THREADS;   // 64 keys per thread, 8 loads in flight
-#pragma unroll 8
-    for (int q = 0; q < U; ++q) {
-        const u64 i = s0 + threadIdx.x + (u64)q * MM_THREADS;
-        if (i < s1) mm_acc<K>(x[i], mn, mx, nan);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        u64 a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
-        mn = a < mn ? a : mn; mx = b > mx ? b : mx;
+    const BatchInfo bi = c->cnt->batch;
+    if (bi.nb == 0) return;
+    {   // zero the batch's tables (per-bin counts, T, H) before the sampling kernel adds to them
+        u32 *a = c->arena;
+        for (u64 i = bi.a0 + (u64)blockIdx.x * MM_THREADS + threadIdx.x; i < bi.a1; i += (u64)gridDim.x * MM_THREADS) a[i] = 0u;
     }
     __shared__ u64 smn[MM_THREADS / 32], smx[MM_THREADS / 32];
-    if ((threadIdx.x & 31) == 0) { smn[threadIdx.x >> 5] = mn; smx[threadIdx.x >> 5] = mx; }
-    if (__syncthreads_or(nan) && threadIdx.x == 0) atomicOr(c->nan_flag, 1u);
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < MM_THREADS / 32; ++w) { mn = smn[w] < mn ? smn[w] : mn; mx = smx[w] > mx ? smx[w] : mx; }
-        atomicMin(&g.kmin, mn);
-        atomicMax(&g.kmax, mx);
+    for (u32 ch = blockIdx.x; ch < bi.mm_chunks; ch += gridDim.x) {
+        const u32 k = batch_node_of(c->bpre_mm, bi.nb, ch);
+        GNode &g = c->nodes[bi.first + k];
+        const u64 s0 = (u64)(ch - c->bpre_mm[k]) * MMB_CHUNK, s1 = min((u64)g.m, s0 + MMB_CHUNK);
+        const u64 *x = c->buf[g.src] + g.off;
+        u64 mn = ~0ull, mx = 0;
+        bool nan = false;
+        constexpr int U = MMB_CHUNK / MM_THREADS;   // 64 keys per thread, 8 loads in flight
+#pragma unroll 8
+        for (int q = 0; q < U; ++q) {
+            const u64 i = s0 + threadIdx.x + (u64)q * MM_THREADS;
+            if (i < s1) mm_acc<K>(x[i], mn, mx, nan);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            u64 a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = a < mn ? a : mn; mx = b > mx ? b : mx;
+        }
+        if ((threadIdx.x & 31) == 0) { smn[threadIdx.x >> 5] = mn; smx[threadIdx.x >> 5] = mx; }
+        if (__syncthreads_or(nan) && threadIdx.x == 0) atomicOr(c->nan_flag, 1u);
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < MM_THREADS / 32; ++w) { mn = smn[w] < mn ? smn[w] : mn; mx = smx[w] > mx ? smx[w] : mx; }
+            atomicMin(&g.kmin, mn);
+            atomicMax(&g.kmax, mx);
+        }
+        __syncthreads();
     }
 }
 
-// alpha samples of every node -> per-bin counts; the first CTA of a node
+// alpha samples of every node -> per-bin counts; the first chunk of a node
 // publishes its model (and the R9/R10 verdict) like k_fit_sample.
 template <class K>
-__global__ void __launch_bounds__(FSB_CHUNK) k_fit_sample_batch(const DevCtx *__restrict__ c, const u32 *__restrict__ cnode,
-                                                               const u32 *__restrict__ nfirst) {
+__global__ void __launch_bounds__(FSB_CHUNK) k_fit_sample_batch(const DevCtx *__restrict__ c) {
     pdl_entry();
     if (*c->nan_flag) return;
-    const u32 node = cnode[blockIdx.x];
-    GNode &g = c->nodes[node];
-    Model md;
-    const bool ok = make_model<K>(g.kmin, g.kmax, g.beta, md);
-    const u32 cb = blockIdx.x - nfirst[node];
-    if (cb == 0 && threadIdx.x == 0) {
-        g.md = md;
-        g.degenerate = ok ? 0u : 1u;
-        if (!ok) push_item(c, g.off, g.m, g.level, g.src, 1u);   // Standard-Sort the whole segment
-    }
-    if (!ok) return;
-    const u32 k = cb * FSB_CHUNK + threadIdx.x;
-    if (k >= g.alpha) return;
+    const BatchInfo bi = c->cnt->batch;
+    if (bi.nb == 0) return;
     const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
-    const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, g.off), k, g.m);
-    atomicAdd(&g.cnt[interval_index<K>(K::to_okey(c->buf[g.src][g.off + pos]), md)], 1u);
+    for (u32 ch = blockIdx.x; ch < bi.fs_chunks; ch += gridDim.x) {
+        const u32 kb = batch_node_of(c->bpre_fs, bi.nb, ch);
+        GNode &g = c->nodes[bi.first + kb];
+        Model md;
+        const bool ok = make_model<K>(g.kmin, g.kmax, g.beta, md);
+        const u32 cb = ch - c->bpre_fs[kb];
+        if (cb == 0 && threadIdx.x == 0) {
+            g.md = md;
+            g.degenerate = ok ? 0u : 1u;
+            if (!ok) push_item(c, g.off, g.m, g.level, g.src, 1u);   // Standard-Sort the whole segment
+        }
+        if (!ok) continue;
+        const u32 k = cb * FSB_CHUNK + threadIdx.x;
+        if (k >= g.alpha) continue;
+        const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, g.off), k, g.m);
+        atomicAdd(&g.cnt[interval_index<K>(K::to_okey(c->buf[g.src][g.off + pos]), md)], 1u);
+    }
+}
+
+// Oversized recursing buckets (items of kind 0) -> new global nodes of the next
+// batch, with their tables carved from the arena and their first split appended
+// to the next round's list; Standard-Sort items (kind 1) -> the K8 segment list.
+// One CTA; consumes every item and resets the item count.  This replaces the
+// host round trip of the previous design (recursion per bucket).
+template <class K>
+__global__ void __launch_bounds__(1024) k_items_to_nodes(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    __shared__ u32 wsum[33];
+    __shared__ unsigned long long wsum64[33];
+    Counters &C = *c->cnt;
+    const u32 nit = min(C.nitems, c->items_cap);
+    const u32 t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
+    const u32 first = C.node_count;
+    const u64 a0 = C.arena_used;
+    const u32 cur = C.round & 1u;   // the list the next round consumes
+    u32 nb = 0, nfb = 0, cmm = 0, cfs = 0;
+    u64 arena = a0;
+    for (u32 base = 0; base < nit; base += 1024) {
+        const u32 i = base + t;
+        SegItem it;
+        it.kind = 2;
+        if (i < nit) it = c->items[i];
+        const bool isn = !C.nan_flag && it.kind == 0, isf = !C.nan_flag && it.kind == 1;
+        u32 P = 0, al = 0, need = 0, nmm = 0, nfs = 0;
+        if (isn) {
+            P = (u32)iroot34(it.m);
+            al = sample_all ? it.m : P;
+            need = 3u * (P + 2u);
+            nmm = (it.m + MMB_CHUNK - 1) / MMB_CHUNK;
+            nfs = (al + FSB_CHUNK - 1) / FSB_CHUNK;
+        }
+        u32 tot;
+        const u32 ex_n = block_excl_scan_1024(isn ? 1u : 0u, wsum, tot);
+        const u32 tot_n = tot;
+        const u32 ex_f = block_excl_scan_1024(isf ? 1u : 0u, wsum, tot);
+        const u32 tot_f = tot;
+        const u32 ex_mm = block_excl_scan_1024(nmm, wsum, tot);
+        const u32 tot_mm = tot;
+        const u32 ex_fs = block_excl_scan_1024(nfs, wsum, tot);
+        const u32 tot_fs = tot;
+        // u64 exclusive scan of the table sizes
+        u64 x = need;
+        for (int o = 1; o < 32; o <<= 1) { u64 y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= (u32)o) x += y; }
+        if (lane == 31) wsum64[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            u64 sv = wsum64[lane], t2 = sv;
+            for (int o = 1; o < 32; o <<= 1) { u64 y = __shfl_up_sync(0xffffffffu, t2, o); if (lane >= (u32)o) t2 += y; }
+            wsum64[lane] = t2 - sv;
+            if (lane == 31) wsum64[32] = t2;
+        }
+        __syncthreads();
+        const u64 ex_a = wsum64[w] + x - need, tot_a = wsum64[32];
+        __syncthreads();
+        if (isn) {
+            const u32 k = nb + ex_n, idx = first + k;
+            const u64 ao = arena + ex_a;
+            if (idx < c->node_cap && ao + need <= c->arena_cap) {
+                GNode g;
+                memset(&g, 0, sizeof g);
+                g.off = it.off; g.m = it.m; g.level = it.level;
+                g.kmin = ~0ull; g.kmax = 0;
+                g.alpha = al; g.beta = P; g.gamma = P; g.delta = P;
+                g.src = it.src;
+                g.cnt = c->arena + ao;
+                g.T = g.cnt + (P + 2);
+                g.H = g.T + (P + 2);
+                g.bnd = nullptr;
+                c->nodes[idx] = g;
+                c->bpre_mm[k] = cmm + ex_mm;
+                c->bpre_fs[k] = cfs + ex_fs;
+                SplitTask s;
+                s.off = it.off; s.m = it.m; s.node = idx; s.jlo = 1; s.jhi = P + 2;
+                s.shift = choose_shift(P + 1, it.m);
+                s.G = (P + 1 + (1u << s.shift) - 1) >> s.shift;
+                s.src = it.src; s.dst = it.src == 1 ? 2 : 1;
+                s.tile_begin = 0; s.ntiles = 0; s.cbase = 0; s.mbase = 0;
+                const u32 slot = atomicAdd(&C.nsplits[cur], 1u);
+                if (slot < c->splits_cap) c->splits[cur][slot] = s;
+                else atomicOr(c->err_flag, 1u);
+            } else {
+                atomicOr(c->err_flag, 8u);   // node table / arena capacity
+            }
+            atomicAdd(&C.global_keys, (unsigned long long)it.m);
+        }
+        if (isf) {
+            const u32 k = nfb + ex_f, fi = C.fb_count + k;
+            if (fi < c->fb_cap) c->fb[fi] = it;
+            else atomicOr(c->err_flag, 1u);
+        }
+        nb += tot_n; nfb += tot_f; cmm += tot_mm; cfs += tot_fs; arena += tot_a;
+    }
+    __syncthreads();
+    if (t == 0) {
+        const u32 nbc = first + nb <= c->node_cap ? nb : (c->node_cap > first ? c->node_cap - first : 0u);
+        BatchInfo bi;
+        bi.first = first; bi.nb = nbc; bi.mm_chunks = nbc == nb ? cmm : 0u; bi.fs_chunks = nbc == nb ? cfs : 0u;
+        bi.a0 = a0; bi.a1 = arena <= c->arena_cap ? arena : a0;
+        if (nbc != nb) bi.nb = 0;
+        C.batch = bi;
+        C.node_count = first + bi.nb;
+        C.arena_used = bi.a1;
+        C.fb_count = min(C.fb_count + nfb, c->fb_cap);
+        C.nitems = 0;
+    }
+}
+
+// b = prefix of the counts and T of one node per CTA (the batched nodes have
+// up to a few thousand bins: the CTA walks them SCAN_CHUNK at a time); grid-stride
+// over the batch's nodes.
+__global__ void __launch_bounds__(SCAN_THREADS) k_fit_batch(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    __shared__ u32 wsum[33];
+    __shared__ unsigned long long dsum;
+    if (*c->nan_flag) return;
+    const BatchInfo bi = c->cnt->batch;
+    const bool logging = c->rec != nullptr;
+    for (u32 k = blockIdx.x; k < bi.nb; k += gridDim.x) {
+        GNode &g = c->nodes[bi.first + k];
+        if (g.degenerate) continue;   // uniform per CTA
+        const u64 nb = (u64)g.beta + 1;
+        u32 *in = g.cnt + 1;
+        if (threadIdx.x == 0) dsum = 0;
+        u32 carry = 0;
+        u64 db = 0;
+        for (u64 base0 = 0; base0 < nb; base0 += SCAN_CHUNK) {
+            const u64 base = base0 + (u64)threadIdx.x * SCAN_ITEMS;
+            u32 v[SCAN_ITEMS], sm = 0;
+#pragma unroll
+            for (int q = 0; q < SCAN_ITEMS; ++q) { v[q] = base + q < nb ? in[base + q] : 0; sm += v[q]; }
+            u32 total;
+            u32 e = block_excl_scan_1024(sm, wsum, total) + carry;
+#pragma unroll
+            for (int q = 0; q < SCAN_ITEMS; ++q) {
+                e += v[q];
+                if (base + q < nb) {
+                    const u64 i = base + q + 1;
+                    in[base + q] = e;
+                    g.T[i] = bucket_of(e, g.alpha, g.gamma);
+                    if (logging) db += digest_term(i, e);
+                }
+            }
+            carry += total;
+        }
+        if (logging) {
+            for (int o = 16; o > 0; o >>= 1) db += __shfl_xor_sync(0xffffffffu, db, o);
+            if ((threadIdx.x & 31) == 0) atomicAdd(&dsum, (unsigned long long)db);
+            __syncthreads();
+            if (threadIdx.x == 0) atomicAdd((unsigned long long *)&g.digest_b, dsum);
+        }
+        __syncthreads();
+    }
 }
 
 // ------------------------------------------------------------------ splits
@@ -203,10 +428,10 @@ __device__ __forceinline__ u32 find_split(const SplitTask *L, u32 ns, u32 tile) 
 
 // Split of every tile of round `cur` (one thread per tile): the count and
 // scatter CTAs read it instead of each searching the split list.
-__global__ void k_tile_map(const DevCtx *__restrict__ c, u32 cur) {
+__global__ void k_tile_map(const DevCtx *__restrict__ c) {
     pdl_entry();
     const RoundPlan pl = *c->plan;
-    const SplitTask *__restrict__ L = c->splits[cur];
+    const SplitTask *__restrict__ L = c->splits[pl.cur];
     for (u32 si = blockIdx.x; si < pl.ns; si += gridDim.x) {   // one CTA per split
         const u32 tb = L[si].tile_begin, nt = L[si].ntiles;
         for (u32 t = threadIdx.x; t < nt; t += blockDim.x) c->tmap[tb + t] = si;
@@ -249,7 +474,7 @@ struct CountSmem {
 };
 
 // Producer (one thread): metadata of `tile` and the bulk copy of its keys into stage `sg`.
-__device__ __forceinline__ void count_issue(const DevCtx *__restrict__ c, CountSmem &S, u32 cur, u32 tile, u32 sg) {
+__device__ __forceinline__ void count_issue(const DevCtx *__restrict__ c, CountSmem &S, u32 cur, u32 tile, u32 sg) {   // cur: plan.cur
     CountStage &m = S.meta[sg];
     const SplitTask &st = c->splits[cur][c->tmap[tile]];
     m.st = st;
@@ -283,12 +508,13 @@ __device__ __forceinline__ void count_issue(const DevCtx *__restrict__ c, CountS
 constexpr int CNT_THREADS = SC_THREADS + 32;   // 12 consumer warps + 1 producer warp
 
 template <class K>
-__global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__restrict__ c, u32 cur) {
+__global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__restrict__ c) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char cnt_smem_raw[];
     CountSmem &S = *reinterpret_cast<CountSmem *>(cnt_smem_raw);
     if (*c->nan_flag) return;
     const u32 ntiles = c->plan->tiles;
+    const u32 cur = c->plan->cur;
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         mbar_init(&S.full[0], 1); mbar_init(&S.full[1], 1);
@@ -411,19 +637,21 @@ __global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__
 // One CTA per tile (no pipeline): for rounds of few tiles per SM (n <= 2^25), where
 // the persistent kernel's pipeline never fills.  Same outputs as k_split_count.
 template <class K>
-__global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_tile(const DevCtx *__restrict__ c, u32 cur) {
+__global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_tile(const DevCtx *__restrict__ c) {
     pdl_entry();
     __shared__ u32 hist[GMAX];
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
-    const SplitTask *__restrict__ L = c->splits[cur];
+    const SplitTask *__restrict__ L = c->splits[pl.cur];
     u32 *__restrict__ C = c->cmat;
-    const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
-    if (tile >= pl.tiles) return;
+    // one tile per CTA when the grid covers the round (host-launched first rounds);
+    // grid-stride in the device-driven batches, whose grid cannot know the round's size
+    for (u32 tile = blockIdx.x; tile < pl.tiles; tile += gridDim.x) {
     const u32 s = c->tmap[tile];
     const SplitTask st = L[s];
     const u32 lt = tile - st.tile_begin;
     const GNode &g = c->nodes[st.node];
+    if (tile != blockIdx.x) __syncthreads();   // the previous tile's histogram is written out
     for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) hist[d] = 0;
     const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
     const bool deg = g.degenerate != 0;
@@ -467,31 +695,7 @@ __global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_tile(const DevCtx
     }
     __syncthreads();
     for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
-}
-
-// --- exclusive scan of a u32 array (3 phases)
-constexpr int SCAN_THREADS = 1024;
-constexpr int SCAN_ITEMS = 4;
-constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_ITEMS;
-
-__device__ __forceinline__ u32 block_excl_scan_1024(u32 v, u32 *wsum, u32 &total) {
-    const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    u32 x = v;
-    for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= (u32)o) x += y; }
-    if (lane == 31) wsum[w] = x;
-    __syncthreads();
-    if (w == 0) {
-        u32 s = wsum[lane];
-        u32 t = s;
-        for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, t, o); if (lane >= (u32)o) t += y; }
-        wsum[lane] = t - s;
-        if (lane == 31) wsum[32] = t;
     }
-    __syncthreads();
-    u32 r = wsum[w] + x - v;
-    total = wsum[32];
-    __syncthreads();
-    return r;
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_partials(const u32 *__restrict__ in, u64 n, u32 *__restrict__ bsum) {
@@ -586,11 +790,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_final(const DevCtx *__re
 // Plan split round `cur`: tiles, count-matrix offsets and key offsets of every
 // split (one CTA).  Splits that do not fit the count matrix are carried over to
 // the next round's list; the next list's counter is reset here.
-__global__ void __launch_bounds__(1024) k_round_plan(const DevCtx *__restrict__ c, u32 cur) {
+__global__ void __launch_bounds__(1024) k_round_plan(const DevCtx *__restrict__ c) {
     pdl_entry();
     __shared__ u32 wsum[33];
     __shared__ unsigned long long wsum64[33];
     __shared__ u32 cut_s;
+    const u32 cur = c->cnt->round & 1u;   // rounds alternate between the two split lists
     SplitTask *L = c->splits[cur];
     const u32 nxt = cur ^ 1u;
     u32 ns = *c->nan_flag ? 0u : min(c->nsplits[cur], c->splits_cap);
@@ -657,9 +862,10 @@ __global__ void __launch_bounds__(1024) k_round_plan(const DevCtx *__restrict__ 
         }
         pl.nblk = (u32)((pl.ctot + SCAN_CHUNK - 1) / SCAN_CHUNK);
         pl.next_count = 0; pl.next_scatter = 0;
-        pl.pad = 0;
+        pl.cur = cur;
         *c->plan = pl;
         atomicAdd(c->split_keys, (unsigned long long)pl.mtot);
+        c->cnt->round += 1;   // every reader of this round takes cur from the plan
     }
 }
 
@@ -704,48 +910,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_fit_final(const DevCtx *__rest
             if (logging) db += digest_term(i, e);
             if (copy_l1 && i - 1 < c->l1_cap) c->l1_b[i - 1] = e;
         }
-    }
-    if (logging) {
-        for (int o = 16; o > 0; o >>= 1) db += __shfl_xor_sync(0xffffffffu, db, o);
-        if ((threadIdx.x & 31) == 0) atomicAdd(&dsum, (unsigned long long)db);
-        __syncthreads();
-        if (threadIdx.x == 0) atomicAdd((unsigned long long *)&g.digest_b, dsum);
-    }
-}
-
-// b = prefix of the counts and T of one node per CTA (the batched nodes have
-// up to a few thousand bins: the CTA walks them SCAN_CHUNK at a time).
-__global__ void __launch_bounds__(SCAN_THREADS) k_fit_batch(const DevCtx *__restrict__ c, const u32 *__restrict__ nlist) {
-    pdl_entry();
-    __shared__ u32 wsum[33];
-    __shared__ unsigned long long dsum;
-    if (*c->nan_flag) return;
-    GNode &g = c->nodes[nlist[blockIdx.x]];
-    if (g.degenerate) return;
-    const u64 nb = (u64)g.beta + 1;
-    const bool logging = c->rec != nullptr;
-    u32 *in = g.cnt + 1;
-    if (threadIdx.x == 0) dsum = 0;
-    u32 carry = 0;
-    u64 db = 0;
-    for (u64 base0 = 0; base0 < nb; base0 += SCAN_CHUNK) {
-        const u64 base = base0 + (u64)threadIdx.x * SCAN_ITEMS;
-        u32 v[SCAN_ITEMS], sm = 0;
-#pragma unroll
-        for (int k = 0; k < SCAN_ITEMS; ++k) { v[k] = base + k < nb ? in[base + k] : 0; sm += v[k]; }
-        u32 total;
-        u32 e = block_excl_scan_1024(sm, wsum, total) + carry;
-#pragma unroll
-        for (int k = 0; k < SCAN_ITEMS; ++k) {
-            e += v[k];
-            if (base + k < nb) {
-                const u64 i = base + k + 1;
-                in[base + k] = e;
-                g.T[i] = bucket_of(e, g.alpha, g.gamma);
-                if (logging) db += digest_term(i, e);
-            }
-        }
-        carry += total;
     }
     if (logging) {
         for (int o = 16; o > 0; o >>= 1) db += __shfl_xor_sync(0xffffffffu, db, o);
@@ -911,42 +1075,21 @@ template <class K>
 #ifndef PCF_SC_MINB
 #define PCF_SC_MINB 2
 #endif
-__global__ void __launch_bounds__(SC_THREADS, PCF_SC_MINB) k_split_scatter(const DevCtx *__restrict__ c, u32 cur) {
+__global__ void __launch_bounds__(SC_THREADS, PCF_SC_MINB) k_split_scatter(const DevCtx *__restrict__ c) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char sc_smem_raw[];
     SplitScatterSmem &S = *reinterpret_cast<SplitScatterSmem *>(sc_smem_raw);
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
-    const SplitTask *__restrict__ L = c->splits[cur];
-    const u32 tile = blockIdx.x;   // one CTA per tile; the grid is an upper bound
-    if (tile >= pl.tiles) return;
-    const SplitTask st = L[c->tmap[tile]];
-    const u32 lt = tile - st.tile_begin;
-    if ((lt + 1) * SPLIT_TILE <= st.m) split_scatter_tile<K, true>(c, S, st, lt, c->pmat);
-    else split_scatter_tile<K, false>(c, S, st, lt, c->pmat);
-}
-
-__host__ __device__ inline u32 ceil_log2_u32(u32 v) {   // v >= 1
-    u32 r = 0;
-    while ((1ull << r) < v) ++r;
-    return r;
-}
-__host__ __device__ inline u32 floor_log2_u64(u64 v) {  // v >= 1
-    u32 r = 0;
-    while (v >> (r + 1)) ++r;
-    return r;
-}
-// Digit shift for splitting W >= 2 consecutive buckets holding c keys:
-// G = ceil(W / 2^s) <= GMAX, expected group ~ S_CAP/2 keys, G >= 2.
-__host__ __device__ inline u32 choose_shift(u32 W, u32 c) {
-    u32 cl = ceil_log2_u32(W);
-    u32 smin = cl > GMAX_LOG2 ? cl - GMAX_LOG2 : 0;
-    u64 q = ((u64)(S_CAP / 2) * W) / (c ? c : 1);
-    u32 st = floor_log2_u64(q ? q : 1);
-    u32 s = st < 10 ? st : 10;
-    if (s < smin) s = smin;
-    if (s > cl - 1) s = cl - 1;
-    return s;
+    const SplitTask *__restrict__ L = c->splits[pl.cur];
+    // one tile per CTA when the grid covers the round, grid-stride otherwise (device-driven batches)
+    for (u32 tile = blockIdx.x; tile < pl.tiles; tile += gridDim.x) {
+        if (tile != blockIdx.x) __syncthreads();   // the previous tile's stage is written out
+        const SplitTask st = L[c->tmap[tile]];
+        const u32 lt = tile - st.tile_begin;
+        if ((lt + 1) * SPLIT_TILE <= st.m) split_scatter_tile<K, true>(c, S, st, lt, c->pmat);
+        else split_scatter_tile<K, false>(c, S, st, lt, c->pmat);
+    }
 }
 
 __device__ __forceinline__ void push_k7(const DevCtx *c, const K7Task &t) {
@@ -980,7 +1123,7 @@ __device__ __forceinline__ void make_run_task(const DevCtx *c, const SplitTask &
 }
 
 constexpr int TG_THREADS = 256;
-__global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__restrict__ c, u32 cur) {
+__global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__restrict__ c) {
     pdl_entry();
     __shared__ u32 dcnt[GMAX];
     __shared__ u8 dpack[GMAX];
@@ -988,7 +1131,7 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
     __shared__ u32 nrun, rbase;
     if (*c->nan_flag) return;
     const RoundPlan pl = *c->plan;
-    const u32 nxt = cur ^ 1u;
+    const u32 cur = pl.cur, nxt = cur ^ 1u;
     const u32 *__restrict__ P = c->pmat;
     const u32 lane = threadIdx.x & 31;
     for (u32 si = blockIdx.x; si < pl.ns; si += gridDim.x) {   // one CTA per split
@@ -1131,50 +1274,75 @@ __global__ void k_k7_advance(const DevCtx *__restrict__ c) {
     *c->k7_next = 0;
 }
 
-// ------------------------------------------------------------------ pass-log finalisation of a global node
-struct NodeAcc {
-    unsigned long long dh;
-    u32 nf, ns, nr, pad;
-};
+// ------------------------------------------------------------------ end of a device-driven batch
+// Condition of the batch loop (a CUDA-graph WHILE node): another batch runs iff
+// the last one left new global nodes or unfinished splits (and no error).
+__global__ void k_batch_cond(const DevCtx *__restrict__ c, cudaGraphConditionalHandle h, u32 count_iter) {
+    pdl_entry();
+    Counters &C = *c->cnt;
+    const bool more = !C.nan_flag && !C.err_flag && (C.batch.nb > 0 || C.nsplits[C.round & 1u] > 0);
+    if (count_iter) C.iters += 1;
+    if (C.iters > 64u) atomicOr(c->err_flag, 16u);   // bound: depth <= 6 levels, a few rounds each
+    cudaGraphSetConditional(h, more && C.iters <= 64u ? 1u : 0u);
+}
 
-__global__ void k_node_finalize_acc(const DevCtx *__restrict__ c, u32 node, NodeAcc *acc) {
-    const GNode &g = c->nodes[node];
-    if (g.degenerate || *c->nan_flag) return;
-    const u32 tau = c->tau;
-    u64 dh = 0;
-    u32 nf = 0, ns = 0, nr = 0;
-    const bool copy_l1 = g.level == 1 && c->l1_h != nullptr;
-    for (u32 u = blockIdx.x * blockDim.x + threadIdx.x; u <= g.gamma; u += gridDim.x * blockDim.x) {
-        u32 h = g.H[u + 1];
-        dh += digest_term(u + 1, h);
-        if (h) { if (h >= g.delta) nf++; else if (h < tau) ns++; else nr++; }
-        if (copy_l1 && u < c->l1_cap) c->l1_h[u] = h;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        dh += __shfl_xor_sync(0xffffffffu, dh, o);
-        nf += __shfl_xor_sync(0xffffffffu, nf, o);
-        ns += __shfl_xor_sync(0xffffffffu, ns, o);
-        nr += __shfl_xor_sync(0xffffffffu, nr, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&acc->dh, dh);
-        atomicAdd(&acc->nf, nf); atomicAdd(&acc->ns, ns); atomicAdd(&acc->nr, nr);
+// ------------------------------------------------------------------ pass-log records of the global nodes
+// One CTA per global node (grid-stride): digest and dispatch counts of its
+// complete H (written by the split rounds and the K7 groups), then the record.
+template <class K>
+__global__ void __launch_bounds__(256) k_log_finalize(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    if (c->rec == nullptr || *c->nan_flag) return;
+    __shared__ unsigned long long sdh[8];
+    __shared__ u32 sn[8][3];
+    const u32 nn = c->cnt->node_count, tau = c->tau;
+    for (u32 node = blockIdx.x; node < nn; node += gridDim.x) {
+        const GNode &g = c->nodes[node];
+        if (g.degenerate) continue;   // uniform per CTA: Standard-Sort, no bucketing record (R9/R10)
+        u64 dh = 0;
+        u32 nf = 0, ns = 0, nr = 0;
+        const bool copy_l1 = g.level == 1 && c->l1_h != nullptr;
+        for (u32 u = threadIdx.x; u <= g.gamma; u += blockDim.x) {
+            const u32 h = g.H[u + 1];
+            dh += digest_term(u + 1, h);
+            if (h) { if (h >= g.delta) nf++; else if (h < tau) ns++; else nr++; }
+            if (copy_l1 && u < c->l1_cap) c->l1_h[u] = h;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            dh += __shfl_xor_sync(0xffffffffu, dh, o);
+            nf += __shfl_xor_sync(0xffffffffu, nf, o);
+            ns += __shfl_xor_sync(0xffffffffu, ns, o);
+            nr += __shfl_xor_sync(0xffffffffu, nr, o);
+        }
+        const u32 w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) { sdh[w] = dh; sn[w][0] = nf; sn[w][1] = ns; sn[w][2] = nr; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (u32 i = 1; i < blockDim.x / 32; ++i) { dh += sdh[i]; nf += sn[i][0]; ns += sn[i][1]; nr += sn[i][2]; }
+            const unsigned long long slot = atomicAdd(c->rec_count, 1ull);
+            if (slot < c->rec_cap) {
+                NodeRec r;
+                r.level = g.level; r.alpha = g.alpha; r.offset = g.off; r.m = g.m;
+                r.xmin_bits = K::from_okey(g.kmin); r.xmax_bits = K::from_okey(g.kmax);
+                r.digest_b = g.digest_b; r.digest_h = dh;
+                r.n_fallback = nf; r.n_small = ns; r.n_recurse = nr; r.reserved = 0;
+                c->rec[slot] = r;
+            }
+        }
+        __syncthreads();
     }
 }
 
-template <class K>
-__global__ void k_node_finalize_rec(const DevCtx *__restrict__ c, u32 node, const NodeAcc *acc) {
-    const GNode &g = c->nodes[node];
-    if (g.degenerate || *c->nan_flag) return;
-    unsigned long long slot = atomicAdd(c->rec_count, 1ull);
-    if (slot < c->rec_cap) {
-        NodeRec r;
-        r.level = g.level; r.alpha = g.alpha; r.offset = g.off; r.m = g.m;
-        r.xmin_bits = K::from_okey(g.kmin); r.xmax_bits = K::from_okey(g.kmax);
-        r.digest_b = g.digest_b; r.digest_h = acc->dh;
-        r.n_fallback = acc->nf; r.n_small = acc->ns; r.n_recurse = acc->nr; r.reserved = 0;
-        c->rec[slot] = r;
-    }
+// Status of the call for asynchronous callers: PCF_OK, PCF_ERR_NAN,
+// PCF_ERR_LOG_OVERFLOW or PCF_ERR_INTERNAL, written in stream order after all work.
+__global__ void k_status(const DevCtx *__restrict__ c, int *status) {
+    pdl_entry();
+    const Counters &C = *c->cnt;
+    int s = 0;                                   // PCF_OK
+    if (C.nan_flag) s = 2;                        // PCF_ERR_NAN
+    else if (C.err_flag) s = 7;                   // PCF_ERR_INTERNAL
+    else if (c->rec != nullptr && c->rec_count && *c->rec_count > c->rec_cap) s = 6;   // PCF_ERR_LOG_OVERFLOW
+    *status = s;
 }
 
 }  // namespace pcf

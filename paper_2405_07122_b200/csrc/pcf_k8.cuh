@@ -11,6 +11,7 @@
 // its tiles are copied straight to the output and the passes are skipped.
 #pragma once
 #include "pcf_common.cuh"
+#include "pcf_global.cuh"
 
 namespace pcf {
 
@@ -34,15 +35,6 @@ constexpr int K8_MTHREADS = PCF_K8_MTHREADS;
 constexpr int K8_MIPT = K8_MTILE / K8_MTHREADS;   // outputs per merge thread
 constexpr int K8_MERGE_SMEM = K8_MTILE * 8;
 constexpr int K8_SORT_SMEM = 2 * K8_TILE * 8;
-
-// flag[0] = 1 if the bucket holds two different keys; flag[1] = first key
-__global__ void __launch_bounds__(256) k8_check(const u64 *__restrict__ src, u64 m, u32 *__restrict__ flag) {
-    const u64 first = src[0];
-    bool diff = false;
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x)
-        diff |= src[i] != first;
-    if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(flag, 1u);
-}
 
 #ifndef PCF_K8_WARPSORT
 #define PCF_K8_WARPSORT 1
@@ -80,16 +72,9 @@ __device__ __forceinline__ void k8_merge_seq(const u64 *A, u32 la, const u64 *B,
 // of merge-path merges of sorted runs through shared memory (each thread
 // emits 8 consecutive outputs).  Padding with the largest ordered key sorts last.
 template <class K>
-__global__ void __launch_bounds__(K8_THREADS) k8_blocksort(const u64 *__restrict__ src, u64 *__restrict__ dst,
-                                                          u64 *__restrict__ out, u64 m, const u32 *__restrict__ flag) {
-    extern __shared__ __align__(16) u64 k8_bs[];   // 2 * K8_TILE keys
+__device__ __forceinline__ void k8_sort_tile(u64 *k8_bs, const u64 *__restrict__ src, u64 *__restrict__ dst, u64 m, u64 base) {
     u64 *a = k8_bs, *b = k8_bs + K8_TILE;
-    const u64 base = (u64)blockIdx.x * K8_TILE;
     const u32 n = (u32)min((u64)K8_TILE, m - base);
-    if (*flag == 0) {   // all keys equal: already sorted, final position
-        for (u32 k = threadIdx.x; k < n; k += K8_THREADS) out[base + k] = src[base + k];
-        return;
-    }
     {
         u64 v[K8_IPT];
 #pragma unroll
@@ -179,66 +164,201 @@ __global__ void __launch_bounds__(K8_THREADS) k8_blocksort(const u64 *__restrict
     for (u32 k = threadIdx.x; k < n; k += K8_THREADS) dst[base + k] = m <= (u64)K8_TILE ? K::from_okey(sa[k]) : sa[k];
 }
 
-// Merge-path split of output tile t (diagonal t*K8_TILE inside its run pair):
-// sp[t] = number of keys taken from the first run.  One thread per tile.
-template <class K>
-__global__ void k8_partition(const u64 *__restrict__ src, u64 m, u64 width, u32 ntiles, u32 *__restrict__ sp,
-                             const u32 *__restrict__ flag) {
-    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntiles || *flag == 0) return;
-    const u64 o0 = (u64)t * K8_MTILE;
-    const u64 pair0 = (o0 / (2 * width)) * (2 * width);
-    const u64 na = min(pair0 + width, m) - pair0, nb = min(pair0 + 2 * width, m) - min(pair0 + width, m);
-    const u64 d = o0 - pair0;
-    const u64 *A = src + pair0, *B = src + pair0 + na;
-    u64 lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
-    while (lo < hi) {   // first i with A[i] > B[d-1-i]  (A first among equal keys; ordered keys)
-        const u64 mid = (lo + hi) >> 1;
-        if (A[mid] <= B[d - 1 - mid]) lo = mid + 1; else hi = mid;
+// ------------------------------------------------------------------ segmented driver
+// Every Standard-Sort bucket of > S_CAP keys (the fallback segments collected by
+// k_items_to_nodes) is sorted by one chain of launches: k8_plan, k8_check,
+// k8_blocksort, then a CUDA-graph WHILE loop of (k8_partition, k8_merge,
+// k8_pass_end) over the merge passes of the largest segment.  Segment s has
+// merges(s) = ceil(log2(ceil(m_s / K8_TILE))) passes; its block sort writes to
+// out if merges(s) is even (tmp otherwise) and pass p writes to out iff
+// merges(s) - 1 - p is even, so its last pass lands in out.  All kernels are
+// grid-stride over the tiles of all segments and find their segment by a binary
+// search over the per-segment tile prefix sums.
+__device__ __forceinline__ u32 k8_merges(u64 m) {
+    u32 r = 0;
+    for (u64 w = K8_TILE; w < m; w *= 2) ++r;
+    return r;
+}
+__device__ __forceinline__ u32 k8_seg_of(const u32 *__restrict__ pre, u32 nseg, u32 x) {   // last s with pre[s] <= x
+    u32 lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        const u32 mid = (lo + hi + 1) >> 1;
+        if (pre[mid] <= x) lo = mid; else hi = mid - 1;
     }
-    sp[t] = (u32)lo;
+    return lo;
+}
+
+__global__ void __launch_bounds__(1024) k8_plan(const DevCtx *__restrict__ c, cudaGraphConditionalHandle h) {
+    pdl_entry();
+    __shared__ u32 wsum[33];
+    __shared__ u32 smax;
+    __shared__ unsigned long long sbytes, skeys;
+    Counters &C = *c->cnt;
+    const u32 nseg = C.nan_flag ? 0u : C.fb_count;
+    if (threadIdx.x == 0) { smax = 0; sbytes = 0; skeys = 0; }
+    __syncthreads();
+    u32 ct = 0, cm = 0, mx = 0;
+    unsigned long long by = 0, ks = 0;
+    for (u32 base = 0; base < nseg; base += 1024) {
+        const u32 s = base + threadIdx.x;
+        u32 nt = 0, nm = 0;
+        if (s < nseg) {
+            const u64 m = c->fb[s].m;
+            nt = (u32)((m + K8_TILE - 1) / K8_TILE);
+            nm = (u32)((m + K8_MTILE - 1) / K8_MTILE);
+            mx = max(mx, k8_merges(m));
+            by += 24ull * m;   // all-equal check (8 B/key) + block sort (16 B/key)
+            ks += m;
+            c->k8_flag[s] = 0;
+        }
+        u32 tot;
+        const u32 et = block_excl_scan_1024(nt, wsum, tot);
+        const u32 tt = tot;
+        const u32 em = block_excl_scan_1024(nm, wsum, tot);
+        if (s < nseg) { c->k8_tb[s] = ct + et; c->k8_mb[s] = cm + em; }
+        ct += tt; cm += tot;
+    }
+    atomicMax(&smax, mx);
+    atomicAdd(&sbytes, by);
+    atomicAdd(&skeys, ks);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        K8Plan pl;
+        pl.nseg = nseg; pl.tiles = ct; pl.mtiles = cm; pl.max_merges = smax; pl.pass = 0; pl.pad = 0;
+        C.k8 = pl;
+        C.k8_bytes = sbytes;
+        C.fb_keys = skeys;
+        cudaGraphSetConditional(h, smax > 0 ? 1u : 0u);
+    }
+}
+
+// "two distinct keys" flag per segment (an all-equal bucket, e.g. config c3's
+// duplicate-heavy one, is already sorted: copied, no merge passes)
+__global__ void __launch_bounds__(256) k8_check(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    const K8Plan pl = c->cnt->k8;
+    for (u32 t = blockIdx.x; t < pl.tiles; t += gridDim.x) {
+        const u32 s = k8_seg_of(c->k8_tb, pl.nseg, t);
+        const SegItem it = c->fb[s];
+        const u64 *src = c->buf[it.src] + it.off;
+        const u64 first = src[0];
+        const u64 b0 = (u64)(t - c->k8_tb[s]) * K8_TILE, b1 = min((u64)it.m, b0 + K8_TILE);
+        bool diff = false;
+        for (u64 i = b0 + threadIdx.x; i < b1; i += blockDim.x) diff |= src[i] != first;
+        if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(&c->k8_flag[s], 1u);
+    }
 }
 
 template <class K>
-__global__ void __launch_bounds__(K8_MTHREADS) k8_merge(const u64 *__restrict__ src, u64 *__restrict__ dst, u64 m, u64 width,
-                                                      const u32 *__restrict__ sp, const u32 *__restrict__ flag, u32 last) {
-    extern __shared__ __align__(16) u64 k8_smem[];   // K8_TILE input keys
-    u64 *sa = k8_smem;
-    if (*flag == 0) return;
-    const u32 t = blockIdx.x;
-    const u64 o0 = (u64)t * K8_MTILE;
-    if (o0 >= m) return;
-    const u64 pair0 = (o0 / (2 * width)) * (2 * width);
-    const u64 na = min(pair0 + width, m) - pair0, nb = min(pair0 + 2 * width, m) - min(pair0 + width, m);
-    const u64 d0 = o0 - pair0, d1 = min(d0 + K8_MTILE, na + nb);
-    const u32 ia0 = sp[t];
-    const u32 ia1 = d1 == na + nb ? (u32)na : sp[t + 1];
-    const u32 ib0 = (u32)(d0 - ia0), ib1 = (u32)(d1 - ia1);
-    const u32 la = ia1 - ia0, lb = ib1 - ib0, tot = la + lb;
-    const u64 *A = src + pair0, *B = src + pair0 + na;
-    {   // all loads of a thread in flight at once, then the stores to shared memory
-        u64 v[K8_MIPT];
-#pragma unroll
-        for (int j = 0; j < K8_MIPT; ++j) {
-            const u32 k = threadIdx.x + j * K8_MTHREADS;
-            v[j] = k < la ? A[ia0 + k] : k < tot ? B[ib0 + (k - la)] : 0ull;
+__global__ void __launch_bounds__(K8_THREADS) k8_blocksort(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    extern __shared__ __align__(16) u64 k8_bs[];   // 2 * K8_TILE keys
+    const K8Plan pl = c->cnt->k8;
+    u64 *out = c->buf[2], *tmp = c->buf[1];
+    for (u32 t = blockIdx.x; t < pl.tiles; t += gridDim.x) {
+        const u32 s = k8_seg_of(c->k8_tb, pl.nseg, t);
+        const SegItem it = c->fb[s];
+        const u64 *src = c->buf[it.src] + it.off;
+        const u64 base = (u64)(t - c->k8_tb[s]) * K8_TILE;
+        if (c->k8_flag[s] == 0) {   // all keys equal: already sorted, final position
+            const u32 n = (u32)min((u64)K8_TILE, (u64)it.m - base);
+            for (u32 k = threadIdx.x; k < n; k += K8_THREADS) out[it.off + base + k] = src[base + k];
+            continue;
         }
-#pragma unroll
-        for (int j = 0; j < K8_MIPT; ++j) {
-            const u32 k = threadIdx.x + j * K8_MTHREADS;
-            if (k < tot) sa[k] = v[j];
-        }
+        __syncthreads();   // the previous tile's shared-memory stage is drained
+        u64 *dst0 = ((k8_merges(it.m) & 1u) == 0 ? out : tmp) + it.off;
+        k8_sort_tile<K>(k8_bs, src, dst0, it.m, base);
     }
-    __syncthreads();
-    // per thread: K8_IPT consecutive outputs from its own merge-path split, stored
-    // straight from registers (a warp writes 32 x 64 contiguous bytes)
-    const u32 dd = min(threadIdx.x * K8_MIPT, tot);
-    const u32 ia = k8_split(sa, la, sa + la, lb, dd);
-    u64 r[K8_MIPT];
-    k8_merge_seq<K8_MIPT>(sa, la, sa + la, lb, ia, dd - ia, r);
-    u64 *outp = dst + o0 + dd;
+}
+
+// Merge pass `pl.pass` (width K8_TILE << pass): the merge-path split of every
+// output tile of every segment still merging (one thread per tile).
+template <class K>
+__global__ void k8_partition(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    const K8Plan pl = c->cnt->k8;
+    const u64 width = (u64)K8_TILE << pl.pass;
+    for (u32 gt = blockIdx.x * blockDim.x + threadIdx.x; gt < pl.mtiles; gt += gridDim.x * blockDim.x) {
+        const u32 s = k8_seg_of(c->k8_mb, pl.nseg, gt);
+        const SegItem it = c->fb[s];
+        const u32 mg = k8_merges(it.m);
+        if (pl.pass >= mg || c->k8_flag[s] == 0) continue;
+        const u32 t = gt - c->k8_mb[s];
+        const u64 m = it.m;
+        if (t == 0) atomicAdd(&c->cnt->k8_bytes, 16ull * m);
+        const u64 *src = (((mg - pl.pass) & 1u) == 0 ? c->buf[2] : c->buf[1]) + it.off;   // = dst of pass - 1
+        const u64 o0 = (u64)t * K8_MTILE;
+        const u64 pair0 = (o0 / (2 * width)) * (2 * width);
+        const u64 na = min(pair0 + width, m) - pair0, nb = min(pair0 + 2 * width, m) - min(pair0 + width, m);
+        const u64 d = o0 - pair0;
+        const u64 *A = src + pair0, *B = src + pair0 + na;
+        u64 lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+        while (lo < hi) {   // first i with A[i] > B[d-1-i]  (A first among equal keys; ordered keys)
+            const u64 mid = (lo + hi) >> 1;
+            if (A[mid] <= B[d - 1 - mid]) lo = mid + 1; else hi = mid;
+        }
+        c->k8_sp[gt] = (u32)lo;
+    }
+}
+
+template <class K>
+__global__ void __launch_bounds__(K8_MTHREADS) k8_merge(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    extern __shared__ __align__(16) u64 k8_smem[];   // K8_MTILE input keys
+    u64 *sa = k8_smem;
+    const K8Plan pl = c->cnt->k8;
+    const u64 width = (u64)K8_TILE << pl.pass;
+    for (u32 gt = blockIdx.x; gt < pl.mtiles; gt += gridDim.x) {
+        const u32 s = k8_seg_of(c->k8_mb, pl.nseg, gt);
+        const SegItem it = c->fb[s];
+        const u32 mg = k8_merges(it.m);
+        if (pl.pass >= mg || c->k8_flag[s] == 0) continue;   // uniform per CTA
+        __syncthreads();   // the previous tile's stage is drained
+        const u32 t = gt - c->k8_mb[s];
+        const u64 m = it.m;
+        const bool last = pl.pass + 1 == mg;
+        const u64 *src = (((mg - pl.pass) & 1u) == 0 ? c->buf[2] : c->buf[1]) + it.off;
+        u64 *dst = (((mg - 1 - pl.pass) & 1u) == 0 ? c->buf[2] : c->buf[1]) + it.off;
+        const u64 o0 = (u64)t * K8_MTILE;
+        const u64 pair0 = (o0 / (2 * width)) * (2 * width);
+        const u64 na = min(pair0 + width, m) - pair0, nb = min(pair0 + 2 * width, m) - min(pair0 + width, m);
+        const u64 d0 = o0 - pair0, d1 = min(d0 + K8_MTILE, na + nb);
+        const u32 ia0 = c->k8_sp[gt];
+        const u32 ia1 = d1 == na + nb ? (u32)na : c->k8_sp[gt + 1];
+        const u32 ib0 = (u32)(d0 - ia0), ib1 = (u32)(d1 - ia1);
+        const u32 la = ia1 - ia0, lb = ib1 - ib0, tot = la + lb;
+        const u64 *A = src + pair0, *B = src + pair0 + na;
+        {   // all loads of a thread in flight at once, then the stores to shared memory
+            u64 v[K8_MIPT];
 #pragma unroll
-    for (int k = 0; k < K8_MIPT; ++k) if (dd + k < tot) outp[k] = last ? K::from_okey(r[k]) : r[k];
+            for (int j = 0; j < K8_MIPT; ++j) {
+                const u32 k = threadIdx.x + j * K8_MTHREADS;
+                v[j] = k < la ? A[ia0 + k] : k < tot ? B[ib0 + (k - la)] : 0ull;
+            }
+#pragma unroll
+            for (int j = 0; j < K8_MIPT; ++j) {
+                const u32 k = threadIdx.x + j * K8_MTHREADS;
+                if (k < tot) sa[k] = v[j];
+            }
+        }
+        __syncthreads();
+        // per thread: K8_MIPT consecutive outputs from its own merge-path split, stored
+        // straight from registers (a warp writes 32 x 32 contiguous bytes)
+        const u32 dd = min(threadIdx.x * K8_MIPT, tot);
+        const u32 ia = k8_split(sa, la, sa + la, lb, dd);
+        u64 r[K8_MIPT];
+        k8_merge_seq<K8_MIPT>(sa, la, sa + la, lb, ia, dd - ia, r);
+        u64 *outp = dst + o0 + dd;
+#pragma unroll
+        for (int k = 0; k < K8_MIPT; ++k) if (dd + k < tot) outp[k] = last ? K::from_okey(r[k]) : r[k];
+    }
+}
+
+__global__ void k8_pass_end(const DevCtx *__restrict__ c, cudaGraphConditionalHandle h) {
+    pdl_entry();
+    K8Plan &pl = c->cnt->k8;
+    pl.pass += 1;
+    cudaGraphSetConditional(h, pl.pass < pl.max_merges && !c->cnt->err_flag ? 1u : 0u);
 }
 
 }  // namespace pcf

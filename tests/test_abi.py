@@ -43,7 +43,7 @@ def test_params_defaults(L):
 def test_status_strings_and_version(L):
     for code, name in pcf.STATUS.items():
         assert L.pcf_status_string(code).decode() == name
-    assert L.pcf_abi_version() == 1
+    assert L.pcf_abi_version() == 2
 
 
 def test_workspace_bytes(L):
@@ -55,7 +55,7 @@ def test_workspace_bytes(L):
         w = pcf.workspace_bytes(n)
         assert w >= 8 * n and w > prev
         prev = w
-    assert pcf.workspace_bytes(10 ** 9) < 16 * 10 ** 9   # one extra key buffer + tables/queues
+    assert pcf.workspace_bytes(10 ** 9) < 18 * 10 ** 9   # one extra key buffer + digits + tables/queues
 
 
 def test_argument_errors_before_any_launch(L):

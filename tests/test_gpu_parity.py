@@ -195,3 +195,63 @@ def test_batched_degenerate_and_sample_all_nodes(pcf):
     _, info = compare(pcf, x)
     assert info.stats["global_nodes"] > 1
     compare(pcf, synth.config("c2", n=3_000_000), sample_all=True)
+
+
+# ---------------------------------------------------------------- asynchronous calls
+@pytest.mark.parametrize("name,n", [("c2", None), ("c4", 2_000_000), ("c2", 100_000_000)])
+def test_async_no_host_sync(pcf, name, n):
+    """Without PCF_FLAG_SYNC the call never waits for the GPU: the recursion over
+    oversized buckets and the fallback sort are decided on the
+    device.  c2 (one device batch), c4 (a ~10^8-key fallback bucket, the K8 loop)
+    and LogNormal 1e8 (thousands of oversized recursing buckets, several device
+    batches); output and the status word must match the synchronous call / oracle."""
+    x = synth.config(name, n=n)
+    xt = torch.from_numpy(x).to(DEV)
+    status = torch.full((1,), -1, dtype=torch.int32, device=DEV)
+    out, info = pcf.sort(xt, sync=False, stats=True, status=status)
+    assert info.stats["host_syncs"] == 0
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    if n is None or n <= 2_000_000:
+        ref = oracle.learned_sort(x, check=False).out
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+    else:
+        s = xt.view(torch.int64)
+        key = s ^ ((s >> 63) & 0x7FFFFFFFFFFFFFFF)
+        o = out.view(torch.int64)
+        assert torch.equal(o ^ ((o >> 63) & 0x7FFFFFFFFFFFFFFF), torch.sort(key).values)
+    _, sinfo = pcf.sort(xt, stats=True)
+    assert sinfo.stats["host_syncs"] == 1
+    if name == "c2" and n is not None:
+        assert sinfo.stats["device_batches"] >= 1 and sinfo.stats["global_nodes"] > 100
+
+
+@pytest.mark.parametrize("n", [5000, 100_000, 3_000_000])
+def test_async_nan_status(pcf, n):
+    """NaN input without SYNC: PCF_OK returned after enqueueing, PCF_ERR_NAN (2) in the status word."""
+    x = synth.generate("uniform", n, 1)
+    x[n // 3] = np.nan
+    status = torch.full((1,), -1, dtype=torch.int32, device=DEV)
+    out, info = pcf.sort(torch.from_numpy(x).to(DEV), sync=False, stats=True, status=status)
+    assert info.stats["host_syncs"] == 0
+    torch.cuda.synchronize()
+    assert int(status.item()) == 2
+
+
+def test_host_entry_nan(pcf):
+    x = synth.generate("exponential", 300_000, 6)
+    x[7] = np.nan
+    with pytest.raises(pcf.PCFError) as e:
+        pcf.sort_host(x)
+    assert e.value.status == 2
+
+
+def test_repeated_calls_reuse_graphs(pcf):
+    """The device-driven tail is a cached CUDA graph keyed on the workspace: repeated
+    sorts with one workspace, then a different workspace, then the first again."""
+    xs = [synth.generate("lognormal", 3_000_000, s) for s in (1, 2)]
+    ws = [torch.empty(pcf.workspace_bytes(3_000_000), dtype=torch.uint8, device=DEV) for _ in range(2)]
+    for k in (0, 1, 0, 0, 1):
+        x = xs[k % 2]
+        out = pcf.sort(torch.from_numpy(x).to(DEV), workspace=ws[k])
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), oracle.learned_sort(x, check=False).out.view(np.uint64))
