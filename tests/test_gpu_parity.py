@@ -255,3 +255,35 @@ def test_repeated_calls_reuse_graphs(pcf):
         x = xs[k % 2]
         out = pcf.sort(torch.from_numpy(x).to(DEV), workspace=ws[k])
         assert np.array_equal(out.cpu().numpy().view(np.uint64), oracle.learned_sort(x, check=False).out.view(np.uint64))
+
+
+# ---------------------------------------------------------------- reading R6 at bin edges
+def test_r6_bin_edges_gpu(pcf):
+    """Keys within a few ulps of PCF bin edges (tests/golden/r6_bin_edges.json, derived in
+    exact rationals by tools/find_r6_cases.py): with the whole segment as the sample
+    (R14 test mode) the level-1 b[] counts every key's i(x), so b must equal the counts of
+    the R6 values -- and differs from the counts of the exact-rational values.  m = 1000
+    runs in K7 (one CTA), m = 20000 on the global path (min/max, fit, split kernels)."""
+    import json
+    import os
+    from fractions import Fraction
+    from test_oracle_pins import r6_by_rationals
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "r6_bin_edges.json")))
+    rng = np.random.default_rng(7)
+    for grp in g["groups"]:
+        m, beta = grp["m"], grp["beta"]
+        lo, hi = float.fromhex(grp["lo"]), float.fromhex(grp["hi"])
+        cases = [float.fromhex(c["x"]) for c in grp["cases"]]
+        ks = rng.integers(0, beta, m - 2 - len(cases))
+        filler = [(Fraction(lo) + (Fraction(hi) - Fraction(lo)) * (2 * int(k) + 1) / (2 * beta)) for k in ks]
+        filler = [f.numerator / f.denominator for f in filler]   # bin centres: far from every edge
+        x = np.array([lo, hi] + cases + filler, dtype=np.float64)
+        rng.shuffle(x)
+        i6 = np.array([r6_by_rationals(float(v), lo, hi, beta) for v in x])
+        iex = np.array([int((Fraction(float(v)) - Fraction(lo)) / (Fraction(hi) - Fraction(lo)) * beta // 1) + 1
+                        for v in x])
+        b_r6 = np.cumsum(np.bincount(i6, minlength=beta + 2)[1:]).astype(np.uint32)
+        b_ex = np.cumsum(np.bincount(iex, minlength=beta + 2)[1:]).astype(np.uint32)
+        assert not np.array_equal(b_r6, b_ex)
+        _, info = compare(pcf, x, sample_all=True)
+        assert np.array_equal(info.level1_b[: beta + 1], b_r6), f"m={m}: GPU i(x) differs from reading R6"

@@ -344,3 +344,46 @@ def test_determinism():
     a = oracle.learned_sort(x, seed=5, log=True)
     b = oracle.learned_sort(x, seed=5, log=True)
     assert np.array_equal(a.nodes, b.nodes) and np.array_equal(a.out, b.out)
+
+
+# ---------------------------------------------------------------- R6 at bin edges
+def _rn(q):
+    return q.numerator / q.denominator   # one correct rounding (CPython int/int true division)
+
+
+def r6_by_rationals(x, lo, hi, beta):
+    """Reading R6 derived in exact rationals, one RN per step (no FPU sub/div/mul)."""
+    d = _rn(Fraction(x) - Fraction(lo))
+    r = _rn(Fraction(hi) - Fraction(lo))
+    q = _rn(Fraction(d) / Fraction(r))
+    t = _rn(Fraction(q) * beta)
+    return int(t // 1) + 1
+
+
+def r6_cases():
+    g = _gold("r6_bin_edges.json")
+    for grp in g["groups"]:
+        lo, hi, beta = float.fromhex(grp["lo"]), float.fromhex(grp["hi"]), grp["beta"]
+        for c in grp["cases"]:
+            yield lo, hi, beta, float.fromhex(c["x"]), c
+
+
+def test_r6_golden_derivation():
+    """Each stored case is re-derived here: the R6 value, and that it differs from the
+    exact rational floor and/or from the fl(d * fl(beta / r)) op order (so the pin
+    discriminates between the readings)."""
+    n = 0
+    for lo, hi, beta, x, c in r6_cases():
+        assert r6_by_rationals(x, lo, hi, beta) == c["i_r6"]
+        ex = int((Fraction(x) - Fraction(lo)) / (Fraction(hi) - Fraction(lo)) * beta // 1) + 1
+        assert ex == c["i_exact"]
+        assert c["i_r6"] != c["i_exact"] or c["i_r6"] != c["i_other_order"]
+        n += 1
+    assert n >= 40
+
+
+def test_r6_oracle_at_bin_edges():
+    """The oracle's i(x) follows reading R6 (not the exact rational, not another op
+    order) on keys within a few ulps of bin edges."""
+    for lo, hi, beta, x, c in r6_cases():
+        assert oracle.interval_index(x, lo, hi, beta) == c["i_r6"], (x.hex(), c)
