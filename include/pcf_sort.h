@@ -43,6 +43,9 @@ extern "C" {
 /* ---- key types ---------------------------------------------------------- */
 #define PCF_KEY_F64 0   /* IEEE binary64, ascending under IEEE-754 totalOrder (-0.0 before +0.0) */
 #define PCF_KEY_U64 1   /* uint64_t, ascending numeric order                                      */
+/* or'ed into pcf_workspace_bytes' key_type for the key-value entry points: */
+#define PCF_KEY_ARGSORT 0x10  /* pcf_argsort_*: + one u32 index per key                      */
+#define PCF_KEY_PAIRS   0x20  /* pcf_sort_pairs_*: + the permutation buffer as well          */
 
 /* ---- flags -------------------------------------------------------------- */
 #define PCF_FLAG_SYNC       1u  /* synchronise the stream once before returning, report NaN/overflow
@@ -151,6 +154,36 @@ size_t pcf_workspace_bytes(size_t n, int key_type, const pcf_params *p);
  * Device capacity violations (a bug) are PCF_ERR_INTERNAL the same way. */
 int pcf_sort_f64(const double *in, double *out, size_t n, const pcf_params *p, void *stream);
 int pcf_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const pcf_params *p, void *stream);
+
+/* ---- key-value mode (not in the paper, which sorts keys only,
+ * PAPER.md:136-139).  Equal keys keep their input order: the result is THE stable
+ * sorting permutation (reading R17), bit-identical to oracle stable_argsort.
+ * The sort itself is unchanged (same buckets, same node records); every kernel that
+ * moves keys also moves the key's source index: the stable split scatter (global
+ * u32 indices), K7 (task-local u16 indices in shared memory, stable tie-break by
+ * index in its leaf sorts) and K8 (u32 indices; (key, index) block sort).  Needs
+ * tau >= 16 (PCF_ERR_INVALID_ARG otherwise: shared-memory room for the indices).
+ *
+ * pcf_argsort_*: in/out as pcf_sort_*; perm: DEVICE uint32_t[n], 4-byte aligned,
+ *   receives perm[k] = input index of out[k].  Workspace: pcf_workspace_bytes(n,
+ *   key_type | PCF_KEY_ARGSORT, p).  Other semantics (flags, errors, status_out) as
+ *   pcf_sort_*.  n < 2^32. */
+int pcf_argsort_f64(const double *in, double *out, uint32_t *perm, size_t n, const pcf_params *p, void *stream);
+int pcf_argsort_u64(const uint64_t *in, uint64_t *out, uint32_t *perm, size_t n, const pcf_params *p, void *stream);
+
+/* pcf_sort_pairs_<key>_<value>: keys_in/keys_out as pcf_sort_*; vals_in / vals_out:
+ * DEVICE arrays of n values (aligned to their size) that must not overlap each
+ * other; vals_out[k] = vals_in[perm[k]].  Workspace: pcf_workspace_bytes(n,
+ * key_type | PCF_KEY_PAIRS, p) (the permutation lives in it).  With PCF_FLAG_SYNC the
+ * call synchronises once, after the value gather. */
+int pcf_sort_pairs_f64_u32(const double *keys_in, const uint32_t *vals_in, double *keys_out, uint32_t *vals_out,
+                           size_t n, const pcf_params *p, void *stream);
+int pcf_sort_pairs_f64_u64(const double *keys_in, const uint64_t *vals_in, double *keys_out, uint64_t *vals_out,
+                           size_t n, const pcf_params *p, void *stream);
+int pcf_sort_pairs_u64_u32(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out, uint32_t *vals_out,
+                           size_t n, const pcf_params *p, void *stream);
+int pcf_sort_pairs_u64_u64(const uint64_t *keys_in, const uint64_t *vals_in, uint64_t *keys_out, uint64_t *vals_out,
+                           size_t n, const pcf_params *p, void *stream);
 
 /* End-to-end entry: HOST pointers (pinned memory recommended).  Copies the n
  * keys to the device, sorts them with pcf_sort_* (asynchronously), copies the

@@ -96,6 +96,7 @@ def lib():
         L.orc_standard_sort.argtypes = [vp, u64, i32]; L.orc_standard_sort.restype = None
         L.orc_learned_sort.argtypes = [i32, vp, u64, ctypes.POINTER(Ctx)]; L.orc_learned_sort.restype = i32
         L.orc_depth_bound.argtypes = [u64, u32]; L.orc_depth_bound.restype = u32
+        L.orc_stable_argsort.argtypes = [i32, vp, u64, vp]; L.orc_stable_argsort.restype = i32
         _lib = L
     return _lib
 
@@ -200,6 +201,18 @@ def standard_sort(x: np.ndarray) -> np.ndarray:
     a = _bits(x)
     lib().orc_standard_sort(_ptr(a), len(a), kt)
     return a.view(x.dtype)
+
+
+def stable_argsort(x: np.ndarray) -> np.ndarray:
+    """the stable sorting permutation of x (ascending, totalOrder
+    for float64; equal keys in increasing index order), as uint64 indices."""
+    kt = _kt(x)
+    a = _bits(x)
+    perm = np.empty(len(a), dtype=np.uint64)
+    rc = lib().orc_stable_argsort(kt, _ptr(a), len(a), _ptr(perm))
+    if rc:
+        raise OracleError(rc)
+    return perm
 
 
 def depth_bound(n: int, tau: int = 64) -> int:

@@ -114,6 +114,41 @@ void orc_standard_sort(uint64_t *x, uint64_t m, int kt)
 }
 
 /* ------------------------------------------------------------------------ */
+/* SURVEY.md 8(f) F1, key-value / argsort variant.  The paper sorts keys only
+ * (Alg. 1 input/output); carrying a payload needs a rule for
+ * equal keys, and the one permutation every stable sort produces is the plain
+ * definition: perm[k] = the index of the k-th smallest key, equal keys in
+ * increasing index order (reading R17 in DESIGN.md).  Plain top-down stable merge
+ * sort of the indices (ties keep the left run first). */
+static void argsort_rec(int kt, const uint64_t *x, uint64_t *p, uint64_t *tmp, uint64_t lo, uint64_t hi)
+{
+    if (hi - lo < 2) return;
+    uint64_t mid = lo + (hi - lo) / 2, i = lo, j = mid, k = lo;
+    argsort_rec(kt, x, p, tmp, lo, mid);
+    argsort_rec(kt, x, p, tmp, mid, hi);
+    while (i < mid && j < hi) {
+        if (key_less(kt, x[p[j]], x[p[i]])) tmp[k++] = p[j++];   /* strictly smaller right key first */
+        else tmp[k++] = p[i++];
+    }
+    while (i < mid) tmp[k++] = p[i++];
+    while (j < hi) tmp[k++] = p[j++];
+    for (k = lo; k < hi; ++k) p[k] = tmp[k];
+}
+
+int orc_stable_argsort(int kt, const uint64_t *x, uint64_t n, uint64_t *perm)
+{
+    for (uint64_t i = 0; i < n; ++i) {
+        if (kt == ORC_KEY_F64 && is_nan_bits(x[i])) return ORC_ERR_NAN;
+        perm[i] = i;
+    }
+    uint64_t *tmp = (uint64_t *)malloc((size_t)(n ? n : 1) * 8);
+    if (!tmp) return ORC_ERR_OOM;
+    argsort_rec(kt, x, perm, tmp, 0, n);
+    free(tmp);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* alpha = beta = gamma = delta = floor(m^{3/4})  (
  * reading R5): the largest c with c^4 <= m^3, in exact 128-bit integers. */
 uint64_t orc_iroot34(uint64_t m)   /* defined for m < 2^42 */

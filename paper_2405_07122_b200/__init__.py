@@ -12,10 +12,11 @@ import os
 
 from ._build import LIB_PATH, build  # noqa: F401
 
-__all__ = ["build", "lib", "sort", "bucket_counts", "sort_host", "workspace_bytes", "host_workspace_bytes", "PCFError", "KEY_F64", "KEY_U64",
+__all__ = ["build", "lib", "sort", "argsort", "sort_pairs", "bucket_counts", "sort_host", "workspace_bytes", "host_workspace_bytes", "PCFError", "KEY_F64", "KEY_U64",
            "FLAG_SYNC", "FLAG_SAMPLE_ALL", "FLAG_TIMING", "PHASES"]
 
 KEY_F64, KEY_U64 = 0, 1
+KEY_ARGSORT, KEY_PAIRS = 0x10, 0x20   # or'ed into key_type for workspace_bytes
 FLAG_SYNC, FLAG_SAMPLE_ALL, FLAG_TIMING, FLAG_PROFILE, FLAG_EXACT_RANKS = 1, 2, 4, 8, 16
 PHASES = ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "total",
           "deep_batches"]
@@ -76,7 +77,8 @@ class PCFError(RuntimeError):
 _lib = None
 SYMBOLS = ["pcf_params_init", "pcf_workspace_bytes", "pcf_sort_f64", "pcf_sort_u64", "pcf_sort_f64_host",
            "pcf_sort_u64_host", "pcf_status_string", "pcf_last_error", "pcf_abi_version",
-           "pcf_bucket_counts_f64", "pcf_level1_entries"]
+           "pcf_bucket_counts_f64", "pcf_level1_entries", "pcf_argsort_f64", "pcf_argsort_u64",
+           "pcf_sort_pairs_f64_u32", "pcf_sort_pairs_f64_u64", "pcf_sort_pairs_u64_u32", "pcf_sort_pairs_u64_u64"]
 
 
 def lib():
@@ -103,6 +105,14 @@ def lib():
         L.pcf_bucket_counts_f64.argtypes = [vp, sz, u64, u64, u64, u64, vp, vp, ctypes.POINTER(u64), vp]
         L.pcf_bucket_counts_f64.restype = i32
         L.pcf_level1_entries.argtypes = [sz, PP]; L.pcf_level1_entries.restype = sz
+        for name in ["pcf_argsort_f64", "pcf_argsort_u64"]:
+            f = getattr(L, name)
+            f.argtypes = [vp, vp, vp, sz, PP, vp]
+            f.restype = i32
+        for name in ["pcf_sort_pairs_f64_u32", "pcf_sort_pairs_f64_u64", "pcf_sort_pairs_u64_u32", "pcf_sort_pairs_u64_u64"]:
+            f = getattr(L, name)
+            f.argtypes = [vp, vp, vp, vp, sz, PP, vp]
+            f.restype = i32
         _ = u32
         _lib = L
     return _lib
@@ -227,6 +237,81 @@ def sort(x, out=None, *, tau: int = 64, seed: int = 0, sample_all: bool = False,
         info.level1_b = b.cpu().numpy().view(np.uint32)
         info.level1_h = h.cpu().numpy().view(np.uint32)
     return out, info
+
+
+def argsort(x, out=None, perm=None, *, tau: int = 64, seed: int = 0, sync: bool = True, workspace=None,
+            stream=None, status=None):
+    """Key-value mode: sort 1-D CUDA float64/uint64 keys and return
+    ``(out, perm)`` -- the sorted keys and the stable sorting permutation (uint32 CUDA
+    tensor, perm[k] = input index of out[k]; equal keys keep their input order)."""
+    import torch
+
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError("x must be a CUDA tensor (no CPU fallback)")
+    if x.dtype == torch.float64:
+        fn = lib().pcf_argsort_f64
+    elif x.dtype == torch.uint64:
+        fn = lib().pcf_argsort_u64
+    else:
+        raise TypeError(f"keys must be float64 or uint64, got {x.dtype}")
+    if x.dim() != 1 or not x.is_contiguous():
+        raise ValueError("x must be a contiguous 1-D tensor")
+    n = x.numel()
+    if out is None:
+        out = torch.empty_like(x)
+    if perm is None:
+        perm = torch.empty(n, dtype=torch.uint32, device=x.device)
+    _check_device_buffer(out, x.dtype, n, x.device, "out")
+    _check_device_buffer(perm, torch.uint32, n, x.device, "perm")
+    p = make_params(tau, seed, FLAG_SYNC if sync else 0)
+    if workspace is not None:
+        _check_workspace(workspace, x.device)
+        p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    if status is not None:
+        _check_device_buffer(status, torch.int32, 1, x.device, "status")
+        p.status_out = status.data_ptr()
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    with torch.cuda.device(x.device):
+        rc = fn(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(perm.data_ptr()), n,
+                ctypes.byref(p), ctypes.c_void_p(s.cuda_stream))
+    _check(rc)
+    return out, perm
+
+
+def sort_pairs(keys, vals, keys_out=None, vals_out=None, *, tau: int = 64, seed: int = 0, sync: bool = True,
+               workspace=None, stream=None):
+    """Key-value mode: sort keys (CUDA float64/uint64) and move vals (CUDA uint32/uint64,
+    same length) with them; equal keys keep their input order.  Returns (keys_out, vals_out)."""
+    import torch
+
+    if not isinstance(keys, torch.Tensor) or not keys.is_cuda or not isinstance(vals, torch.Tensor) or not vals.is_cuda:
+        raise TypeError("keys and vals must be CUDA tensors (no CPU fallback)")
+    kk = {torch.float64: "f64", torch.uint64: "u64"}.get(keys.dtype)
+    vk = {torch.uint32: "u32", torch.uint64: "u64", torch.int32: "u32", torch.int64: "u64"}.get(vals.dtype)
+    if kk is None or vk is None:
+        raise TypeError(f"unsupported key/value dtypes {keys.dtype}/{vals.dtype}")
+    if keys.dim() != 1 or vals.dim() != 1 or not keys.is_contiguous() or not vals.is_contiguous():
+        raise ValueError("keys and vals must be contiguous 1-D tensors")
+    n = keys.numel()
+    if vals.numel() != n or vals.device != keys.device:
+        raise ValueError("vals must have one value per key, on the keys' device")
+    if keys_out is None:
+        keys_out = torch.empty_like(keys)
+    if vals_out is None:
+        vals_out = torch.empty_like(vals)
+    _check_device_buffer(keys_out, keys.dtype, n, keys.device, "keys_out")
+    _check_device_buffer(vals_out, vals.dtype, n, keys.device, "vals_out")
+    fn = getattr(lib(), f"pcf_sort_pairs_{kk}_{vk}")
+    p = make_params(tau, seed, FLAG_SYNC if sync else 0)
+    if workspace is not None:
+        _check_workspace(workspace, keys.device)
+        p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    s = stream if stream is not None else torch.cuda.current_stream(keys.device)
+    with torch.cuda.device(keys.device):
+        rc = fn(ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(vals.data_ptr()), ctypes.c_void_p(keys_out.data_ptr()),
+                ctypes.c_void_p(vals_out.data_ptr()), n, ctypes.byref(p), ctypes.c_void_p(s.cuda_stream))
+    _check(rc)
+    return keys_out, vals_out
 
 
 def bucket_counts(x, alpha: int, beta: int, gamma: int, *, seed: int = 0, b=None, H=None, stream=None):

@@ -79,11 +79,11 @@ static Caps caps_for(u64 n) {
 }
 
 struct Layout {
-    size_t ctx, counters, tmp, digs, tmap, k7_order, bpre_mm, bpre_fs, nodes, arena, k7, splits_a, splits_b, items, fb,
+    size_t ctx, counters, tmp, tidx, digs, tmap, k7_order, bpre_mm, bpre_fs, nodes, arena, k7, splits_a, splits_b, items, fb,
         k8_tb, k8_mb, k8_flag, cmat, pmat, bsum, status, total;
 };
 
-static Layout layout_for(const Caps &c) {
+static Layout layout_for(const Caps &c, bool pr = false) {
     Layout L;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
@@ -91,6 +91,7 @@ static Layout layout_for(const Caps &c) {
     L.counters = take(sizeof(Counters));
     L.status = take(16);
     L.tmp = take(c.n * 8);
+    L.tidx = pr ? take(c.n * 4) : 0;   // key-value mode: source indices of tmp
     L.digs = take(c.n * 2);
     L.tmap = take((c.n / SPLIT_TILE + c.split_cap + 64) * 4);
     L.nodes = take((size_t)c.node_cap * sizeof(GNode));
@@ -118,10 +119,10 @@ static size_t small_layout_bytes() {
     return align_up(sizeof(DevCtx), 256) + align_up(sizeof(Counters), 256) + 256 + align_up(sizeof(K7Task), 256);
 }
 
-static size_t workspace_bytes_impl(size_t n) {
+static size_t workspace_bytes_impl(size_t n, bool pr = false) {
     if (n == 0) return 0;
     if (n <= (size_t)S_CAP) return small_layout_bytes();
-    return layout_for(caps_for(n)).total;
+    return layout_for(caps_for(n), pr).total;
 }
 
 // ---------------------------------------------------------------- phase timer
@@ -163,7 +164,12 @@ struct PhaseTimer {
 enum { PH_MINMAX = 0, PH_FIT = 1, PH_COUNT = 2, PH_SCATTER = 3, PH_K7 = 4, PH_K8 = 5, PH_OTHER = 6, PH_TOTAL = 7,
        PH_BATCHES = 8 };
 
-static int k7_smem_bytes(u32 tau = 2) { return (int)(sizeof(K7Smem) + k7_lists_bytes(tau < 2 ? 2 : tau)); }
+// K7 dynamic shared memory: the struct, the node lists (sized for tau) and, in
+// key-value mode, the two u16 source-index arrays IA / IB behind them
+static int k7_smem_bytes(u32 tau = 2, bool pr = false) {
+    return (int)(sizeof(K7Smem) + k7_lists_bytes(tau < 2 ? 2 : tau) + (pr ? 4ull * S_CAP : 0ull));
+}
+constexpr u32 PR_MIN_TAU = 16;   // key-value mode: smaller tau needs node lists that leave no room for IA / IB
 static int split_smem_bytes() { return (int)sizeof(SplitScatterSmem); }
 
 // Launch with programmatic stream serialization (see pdl_entry()).
@@ -191,13 +197,13 @@ static int cur_dev() {
     return d;
 }
 
-template <class K>
+template <class K, bool PR>
 static int k7_ctas_per_sm() {   // resident K7 CTAs per SM (persistent grid size)
     static thread_local int v[MAX_DEVS] = {0};
     const int d = cur_dev();
     if (!v[d]) {
         int b = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k7_kernel<K>, K7_THREADS, k7_smem_bytes()) != cudaSuccess || b < 1) b = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k7_kernel<K, PR>, K7_THREADS, k7_smem_bytes(PR ? PR_MIN_TAU : 2, PR)) != cudaSuccess || b < 1) b = 1;
         v[d] = b;
     }
     return v[d];
@@ -220,11 +226,14 @@ static int configure_kernels() {
     static thread_local bool done[MAX_DEVS] = {false};
     const int d = cur_dev();
     if (done[d]) return PCF_OK;
-    CK(cudaFuncSetAttribute(k7_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7_smem_bytes()));
+    CK(cudaFuncSetAttribute(k7_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7_smem_bytes()));
+    CK(cudaFuncSetAttribute(k7_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7_smem_bytes(PR_MIN_TAU, true)));
     CK(cudaFuncSetAttribute(k_split_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
-    CK(cudaFuncSetAttribute(k8_merge<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
-    CK(cudaFuncSetAttribute(k8_blocksort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_SORT_SMEM));
+    CK(cudaFuncSetAttribute(k8_merge<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
+    CK(cudaFuncSetAttribute(k8_blocksort<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_SORT_SMEM));
+    CK(cudaFuncSetAttribute(k8_merge<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
+    CK(cudaFuncSetAttribute(k8_blocksort<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_SORT_SMEM));
     done[d] = true;
     return PCF_OK;
 }
@@ -252,7 +261,7 @@ struct Launch {   // the kernel-launch configuration of this device
 // per thread (a repeated sort with the same workspace reuses them).
 struct TailGraph {
     int dev;
-    int kt;
+    int kt;   // key type * 2 + key-value mode
     const void *ctx;
     u32 tau;
     cudaGraph_t g[2];
@@ -277,10 +286,10 @@ static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32
     return PCF_OK;
 }
 
-template <class K>
+template <class K, bool PR>
 static int add_k7(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32 *nk) {
     CK(launch_pdl(k_k7_order, 1, 1024, 0, cs, d_ctx));
-    CK(launch_pdl(k7_kernel<K>, lc.k7_grid, K7_THREADS, lc.tau_smem, cs, d_ctx));
+    CK(launch_pdl(k7_kernel<K, PR>, lc.k7_grid, K7_THREADS, lc.tau_smem, cs, d_ctx));
     CK(launch_pdl(k_k7_advance, 1, 1, 0, cs, d_ctx));
     *nk += 3;
     return PCF_OK;
@@ -314,7 +323,7 @@ static int add_while(cudaStream_t cs, cudaGraphConditionalHandle h, F body) {
     return PCF_OK;
 }
 
-template <class K>
+template <class K, bool PR>
 static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
     for (int i = 0; i < 2; ++i)
         if (!g_cap[i]) CK(cudaStreamCreateWithFlags(&g_cap[i], cudaStreamNonBlocking));
@@ -338,7 +347,7 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
                 CK(launch_pdl(k_fit_batch, lc.nsm * 2, SCAN_THREADS, 0, bs, d_ctx));
                 nk += 3;
                 for (int r = 0; r < 2; ++r) { int e = add_round<K>(bs, d_ctx, lc, &nk); if (e) return e; }
-                int e = add_k7<K>(bs, d_ctx, lc, &nk);
+                int e = add_k7<K, PR>(bs, d_ctx, lc, &nk);
                 if (e) return e;
                 CK(launch_pdl(k_items_to_nodes<K>, 1, 1024, 0, bs, d_ctx));
                 CK(launch_pdl(k_batch_cond, 1, 1, 0, bs, d_ctx, hb, 1u));
@@ -363,10 +372,10 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
         auto cap = [&]() -> int {
             CK(launch_pdl(k8_plan, 1, 1024, 0, cs, d_ctx, hk));
             CK(launch_pdl(k8_check, lc.nsm * 8, 256, 0, cs, d_ctx));
-            CK(launch_pdl(k8_blocksort<K>, lc.nsm * 3, K8_THREADS, K8_SORT_SMEM, cs, d_ctx));
+            CK(launch_pdl(k8_blocksort<K, PR>, lc.nsm * 3, K8_THREADS, K8_SORT_SMEM, cs, d_ctx));
             int rc = add_while(cs, hk, [&](cudaStream_t bs) -> int {
                 CK(launch_pdl(k8_partition<K>, lc.nsm * 4, 256, 0, bs, d_ctx));
-                CK(launch_pdl(k8_merge<K>, lc.nsm * 8, K8_MTHREADS, K8_MERGE_SMEM, bs, d_ctx));
+                CK(launch_pdl(k8_merge<K, PR>, lc.nsm * 8, K8_MTHREADS, K8_MERGE_SMEM, bs, d_ctx));
                 CK(launch_pdl(k8_pass_end, 1, 1, 0, bs, d_ctx, hk));
                 tg.k8_body_kernels = 3;
                 return PCF_OK;
@@ -386,10 +395,10 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
     return PCF_OK;
 }
 
-template <class K>
+template <class K, bool PR>
 static int get_tail(const DevCtx *d_ctx, u32 tau, const Launch &lc, TailGraph **out) {
     const int dev = cur_dev();
-    const int kt = K::is_f64 ? 0 : 1;
+    const int kt = (K::is_f64 ? 0 : 2) + (PR ? 1 : 0);
     for (auto &t : g_tails)
         if (t.dev == dev && t.kt == kt && t.ctx == d_ctx && t.tau == tau) { *out = &t; return PCF_OK; }
     constexpr size_t MAX_TAILS = 8;
@@ -401,7 +410,7 @@ static int get_tail(const DevCtx *d_ctx, u32 tau, const Launch &lc, TailGraph **
     TailGraph tg;
     memset(&tg, 0, sizeof tg);
     tg.dev = dev; tg.kt = kt; tg.ctx = d_ctx; tg.tau = tau;
-    const int rc = build_tail<K>(tg, d_ctx, lc);
+    const int rc = build_tail<K, PR>(tg, d_ctx, lc);
     if (rc) {
         for (int i = 0; i < 2; ++i) { if (tg.ex[i]) cudaGraphExecDestroy(tg.ex[i]); if (tg.g[i]) cudaGraphDestroy(tg.g[i]); }
         return rc;
@@ -412,8 +421,10 @@ static int get_tail(const DevCtx *d_ctx, u32 tau, const Launch &lc, TailGraph **
 }
 
 // ---------------------------------------------------------------- the sort
-template <class K>
-static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, cudaStream_t st) {
+// in, out: device keys; perm (key-value mode, PR): device u32[n] that receives the
+// stable sorting permutation (reading R17), NULL otherwise.
+template <class K, bool PR = false>
+static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, cudaStream_t st, u32 *perm = nullptr) {
     pcf_params p;
     pcf_params_init(&p);
     if (pp) {
@@ -422,6 +433,9 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         p.struct_size = sizeof(pcf_params);
     }
     if (p.tau < 2) return fail(PCF_ERR_INVALID_ARG, "tau must be >= 2");
+    if (PR && p.tau < PR_MIN_TAU) return fail(PCF_ERR_INVALID_ARG, "key-value / argsort mode needs tau >= 16");
+    if (PR && n && !perm) return fail(PCF_ERR_INVALID_ARG, "NULL permutation pointer with n > 0");
+    if (PR && ((uintptr_t)perm & 3)) return fail(PCF_ERR_INVALID_ARG, "permutation must be 4-byte aligned");
     if (!in || !out) { if (n) return fail(PCF_ERR_INVALID_ARG, "NULL key pointer with n > 0"); }
     if (n >= (1ull << 32)) return fail(PCF_ERR_INVALID_ARG, "n must be < 2^32 in ABI v1");
     if (((uintptr_t)in & 7) || ((uintptr_t)out & 7)) return fail(PCF_ERR_INVALID_ARG, "keys must be 8-byte aligned");
@@ -453,7 +467,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         cudaEventRecord(ev_total0, st);
     }
 
-    const size_t need = workspace_bytes_impl(n);
+    const size_t need = workspace_bytes_impl(n, PR);
     char *ws = (char *)p.workspace;
     bool own = false;
     if (ws) {
@@ -506,7 +520,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.buf[1] = nullptr;
     } else {
         caps = caps_for(n);
-        L = layout_for(caps);
+        L = layout_for(caps, PR);
         d_ctx = (DevCtx *)(ws + L.ctx);
         d_cnt = (Counters *)(ws + L.counters);
         d_status = (int *)(ws + L.status);
@@ -537,7 +551,9 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.cmat_cap = caps.cmat_cap;
         hc.digs = (u16 *)(ws + L.digs);
         hc.tmap = (u32 *)(ws + L.tmap);
+        if (PR) hc.ibuf[1] = (u32 *)(ws + L.tidx);
     }
+    if (PR) hc.ibuf[2] = perm;   // ibuf[0] stays NULL: the input's index is its position
     hc.cnt = d_cnt;
     hc.nan_flag = &d_cnt->nan_flag;
     hc.err_flag = &d_cnt->err_flag;
@@ -558,9 +574,9 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     Launch lc;
     lc.nsm = nsm;
-    lc.k7_grid = nsm * k7_ctas_per_sm<K>();
+    lc.k7_grid = nsm * k7_ctas_per_sm<K, PR>();
     lc.count_grid = nsm * count_ctas_per_sm<K>();
-    lc.tau_smem = k7_smem_bytes(p.tau);
+    lc.tau_smem = k7_smem_bytes(p.tau, PR);
 
     // initial counters (host-built: the root node and its tables are carved here)
     Counters h0;
@@ -577,7 +593,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         t.off = 0; t.size = (u32)n; t.kind = K7_NODE; t.src = 0; t.level = 1;
         CK(cudaMemcpyAsync(hc.k7, &t, sizeof t, cudaMemcpyHostToDevice, st));
         tm.begin(PH_K7);
-        k7_kernel<K><<<1, K7_THREADS, lc.tau_smem, st>>>(d_ctx);
+        k7_kernel<K, PR><<<1, K7_THREADS, lc.tau_smem, st>>>(d_ctx);
         CK(cudaGetLastError());
         tm.end();
         launches++;
@@ -675,14 +691,14 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         tm.begin(PH_K7);
         {
             u32 nk = 0;
-            rc = add_k7<K>(st, dc, lc, &nk);
+            rc = add_k7<K, PR>(st, dc, lc, &nk);
             if (rc) return rc;
             launches += nk;
         }
         tm.end();
         CK(cudaGetLastError());
         // ------------------------------------------------ everything after: device-driven (graphs)
-        rc = get_tail<K>(d_ctx, p.tau, lc, &tail);
+        rc = get_tail<K, PR>(d_ctx, p.tau, lc, &tail);
         if (rc) return rc;
         tm.begin(PH_BATCHES);
         CK(cudaGraphLaunch(tail->ex[0], st));
@@ -800,6 +816,83 @@ static int sort_host(const u64 *in_h, u64 *out_h, size_t n, const pcf_params *pp
     return rc;
 }
 
+// ---------------------------------------------------------------- key-value mode
+// vals_out[p] = vals_in[perm[p]]: the payload follows its key's stable permutation.
+template <class V>
+__global__ void __launch_bounds__(256) k_gather_vals(const DevCtx *__restrict__ c, const u32 *__restrict__ perm,
+                                                     const V *__restrict__ vin, V *__restrict__ vout, u64 n) {
+    pdl_entry();
+    if (c && *c->nan_flag) return;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) vout[i] = vin[perm[i]];
+}
+
+static size_t pairs_perm_bytes(size_t n) { return align_up(n * 4, 256); }
+
+template <class K, class V>
+static int sort_pairs(const u64 *kin, const V *vin, u64 *kout, V *vout, size_t n, const pcf_params *pp, cudaStream_t st) {
+    pcf_params p;
+    pcf_params_init(&p);
+    if (pp) {
+        if (pp->struct_size < PCF_PARAMS_V1_SIZE) return fail(PCF_ERR_INVALID_ARG, "pcf_params.struct_size too small");
+        memcpy(&p, pp, std::min<size_t>(pp->struct_size, sizeof(pcf_params)));
+        p.struct_size = sizeof(pcf_params);
+    }
+    if (n == 0) return sort_device<K, true>(kin, kout, 0, &p, st, nullptr);
+    if (!vin || !vout) return fail(PCF_ERR_INVALID_ARG, "NULL value pointer with n > 0");
+    if (((uintptr_t)vin % sizeof(V)) || ((uintptr_t)vout % sizeof(V))) return fail(PCF_ERR_INVALID_ARG, "misaligned values");
+    {
+        const uintptr_t a0 = (uintptr_t)vin, a1 = a0 + n * sizeof(V), b0 = (uintptr_t)vout, b1 = b0 + n * sizeof(V);
+        if (a0 < b1 && b0 < a1) return fail(PCF_ERR_INVALID_ARG, "vals_in and vals_out must not overlap");
+    }
+    const size_t pb = pairs_perm_bytes(n), sw = workspace_bytes_impl(n, true);
+    char *ws = (char *)p.workspace;
+    bool own = false;
+    if (ws) {
+        if (p.workspace_bytes < pb + sw) return fail(PCF_ERR_WORKSPACE_TOO_SMALL, "workspace smaller than pcf_workspace_bytes(PCF_KEY_PAIRS)");
+        if ((uintptr_t)ws & 255) return fail(PCF_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+    } else {
+        if (cudaMallocAsync((void **)&ws, pb + sw, st) != cudaSuccess) { cudaGetLastError(); return fail(PCF_ERR_OOM, "cudaMallocAsync workspace failed"); }
+        own = true;
+    }
+    struct Freer {
+        bool own; char *ws; cudaStream_t st;
+        ~Freer() { if (own) cudaFreeAsync(ws, st); }
+    } freer{own, ws, st};
+    u32 *perm = (u32 *)ws;
+    const bool sync = (p.flags & (PCF_FLAG_SYNC | PCF_FLAG_TIMING)) != 0;
+    int *user_status = p.status_out;
+    int *d_status = nullptr;
+    if (sync) {   // the gather runs after the sort: synchronise once, after it
+        if (cudaMallocAsync((void **)&d_status, sizeof(int), st) != cudaSuccess) { cudaGetLastError(); return fail(PCF_ERR_OOM, "status alloc failed"); }
+        p.status_out = d_status;
+    }
+    p.flags &= ~(PCF_FLAG_SYNC | PCF_FLAG_TIMING);
+    p.workspace = ws + pb;
+    p.workspace_bytes = sw;
+    int rc = sort_device<K, true>(kin, kout, n, &p, st, perm);
+    if (!rc) {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const DevCtx *dc = n <= (size_t)S_CAP ? (const DevCtx *)p.workspace
+                                              : (const DevCtx *)((char *)p.workspace + layout_for(caps_for(n), true).ctx);
+        const u32 grid = (u32)std::min<u64>((n + 255) / 256, (u64)nsm * 16);
+        CK(launch_pdl(k_gather_vals<V>, grid, 256, 0, st, dc, (const u32 *)perm, vin, vout, (u64)n));
+    }
+    if (sync) {
+        int hs = PCF_OK;
+        if (!rc) {
+            if (user_status) CK(cudaMemcpyAsync(user_status, d_status, sizeof(int), cudaMemcpyDefault, st));
+            CK(cudaMemcpyAsync(&hs, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (p.stats) p.stats->host_syncs = 1;
+        }
+        cudaFreeAsync(d_status, st);
+        if (!rc && hs != PCF_OK) rc = fail(hs, hs == PCF_ERR_NAN ? "input contains NaN" : "device status " + std::to_string(hs));
+    }
+    return rc;
+}
+
 // §4.3 experiment: one M_PCF step with decoupled alpha, beta, gamma (pcf_bucketing.cuh)
 static int bucket_counts_f64(const u64 *x, size_t n, u64 alpha, u64 beta, u64 gamma, u64 seed, u32 *b, u32 *H,
                              uint64_t *max_bucket, cudaStream_t st) {
@@ -864,9 +957,9 @@ void pcf_params_init(pcf_params *p) {
 }
 
 size_t pcf_workspace_bytes(size_t n, int key_type, const pcf_params *p) {
-    (void)key_type;
     (void)p;
-    return pcf::workspace_bytes_impl(n);
+    if (key_type & PCF_KEY_PAIRS) return n ? pcf::pairs_perm_bytes(n) + pcf::workspace_bytes_impl(n, true) : 0;
+    return pcf::workspace_bytes_impl(n, (key_type & PCF_KEY_ARGSORT) != 0);
 }
 
 int pcf_sort_f64(const double *in, double *out, size_t n, const pcf_params *p, void *stream) {
@@ -877,6 +970,44 @@ int pcf_sort_f64(const double *in, double *out, size_t n, const pcf_params *p, v
 int pcf_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const pcf_params *p, void *stream) {
     return pcf::sort_device<pcf::KeyU64>(reinterpret_cast<const pcf::u64 *>(in), reinterpret_cast<pcf::u64 *>(out), n, p,
                                          (cudaStream_t)stream);
+}
+
+int pcf_argsort_f64(const double *in, double *out, uint32_t *perm, size_t n, const pcf_params *p, void *stream) {
+    return pcf::sort_device<pcf::KeyF64, true>(reinterpret_cast<const pcf::u64 *>(in), reinterpret_cast<pcf::u64 *>(out), n, p,
+                                               (cudaStream_t)stream, perm);
+}
+
+int pcf_argsort_u64(const uint64_t *in, uint64_t *out, uint32_t *perm, size_t n, const pcf_params *p, void *stream) {
+    return pcf::sort_device<pcf::KeyU64, true>(reinterpret_cast<const pcf::u64 *>(in), reinterpret_cast<pcf::u64 *>(out), n, p,
+                                               (cudaStream_t)stream, perm);
+}
+
+int pcf_sort_pairs_f64_u32(const double *keys_in, const uint32_t *vals_in, double *keys_out, uint32_t *vals_out, size_t n,
+                           const pcf_params *p, void *stream) {
+    return pcf::sort_pairs<pcf::KeyF64, uint32_t>(reinterpret_cast<const pcf::u64 *>(keys_in), vals_in,
+                                                  reinterpret_cast<pcf::u64 *>(keys_out), vals_out, n, p, (cudaStream_t)stream);
+}
+
+int pcf_sort_pairs_f64_u64(const double *keys_in, const uint64_t *vals_in, double *keys_out, uint64_t *vals_out, size_t n,
+                           const pcf_params *p, void *stream) {
+    return pcf::sort_pairs<pcf::KeyF64, unsigned long long>(reinterpret_cast<const pcf::u64 *>(keys_in),
+                                                            reinterpret_cast<const unsigned long long *>(vals_in),
+                                                            reinterpret_cast<pcf::u64 *>(keys_out),
+                                                            reinterpret_cast<unsigned long long *>(vals_out), n, p, (cudaStream_t)stream);
+}
+
+int pcf_sort_pairs_u64_u32(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out, uint32_t *vals_out, size_t n,
+                           const pcf_params *p, void *stream) {
+    return pcf::sort_pairs<pcf::KeyU64, uint32_t>(reinterpret_cast<const pcf::u64 *>(keys_in), vals_in,
+                                                  reinterpret_cast<pcf::u64 *>(keys_out), vals_out, n, p, (cudaStream_t)stream);
+}
+
+int pcf_sort_pairs_u64_u64(const uint64_t *keys_in, const uint64_t *vals_in, uint64_t *keys_out, uint64_t *vals_out, size_t n,
+                           const pcf_params *p, void *stream) {
+    return pcf::sort_pairs<pcf::KeyU64, unsigned long long>(reinterpret_cast<const pcf::u64 *>(keys_in),
+                                                            reinterpret_cast<const unsigned long long *>(vals_in),
+                                                            reinterpret_cast<pcf::u64 *>(keys_out),
+                                                            reinterpret_cast<unsigned long long *>(vals_out), n, p, (cudaStream_t)stream);
 }
 
 int pcf_sort_f64_host(const double *in_host, double *out_host, size_t n, const pcf_params *p, void *stream) {

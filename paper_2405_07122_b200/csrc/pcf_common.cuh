@@ -303,6 +303,8 @@ struct Counters {
 
 struct DevCtx {
     u64 *buf[3];            // in (const, never written unless in==out), tmp, out
+    u32 *ibuf[3];           // key-value mode: the source index of every
+                            // key of buf[i] (ibuf[0] == NULL: identity), or all NULL (keys only)
     Counters *cnt;          // device counters of this call
     u64 n;
     u64 seed;

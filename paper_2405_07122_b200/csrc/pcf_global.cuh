@@ -1044,6 +1044,11 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
     // (Fused with the write-out: if an inversion is found, every position of the
     // tile is written again from the exact ranks below.)
     bool inv = false;
+    // key-value mode: the source index of every key moves with it (gathered from the
+    // tile's source range of ibuf[src], identity for the input buffer)
+    const u32 *isrc = c->ibuf[st.src];
+    u32 *idst = c->ibuf[2] ? c->ibuf[st.dst] + st.off : nullptr;
+    auto src_index = [&](u32 tl) -> u32 { return isrc ? isrc[st.off + k0 + tl] : (u32)(st.off + k0 + tl); };
     for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) {
         const u32 b = S.dsrc[i];
         if (i > 0) {
@@ -1051,6 +1056,7 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
             inv |= (a >> 21) == (b >> 21) && (a & 0xffffu) == (b & 0xffffu) && (a >> 16) > (b >> 16);
         }
         y[S.goff[b & 0xffffu] + i] = S.buf[i];
+        if (idst) idst[S.goff[b & 0xffffu] + i] = src_index(b >> 16);
     }
     if (!__syncthreads_or(inv || (c->flags & FLAG_EXACT_RANKS))) return;
     for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) {
@@ -1068,6 +1074,7 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
             for (u32 j = a; j < b; ++j) pos += (S.dsrc[j] >> 16) < (e >> 16) ? 1u : 0u;
         }
         y[S.goff[d] + pos] = S.buf[i];
+        if (idst) idst[S.goff[d] + pos] = src_index(e >> 16);
     }
 }
 

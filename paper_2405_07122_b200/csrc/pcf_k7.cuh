@@ -107,6 +107,8 @@ struct K7Smem {
     u32 gdelta, glevel, gjlo, gjhi;
     long long prof_t;                       // PCF_FLAG_PROFILE bookkeeping (thread 0)
     unsigned long long prof[K7_PROF_SLOTS];
+    u16 *IA, *IB;                 // key-value mode (PR): task-local source index of every position
+                                  // of A / B (dynamic shared memory past the lists), else NULL
     u32 *lsm;                     // nodes <= WCAP keys (tickets; 0 = not yet pushed)   [lsm_cap]
     u32 *stk;                     // per-warp DFS stacks, row w at stk + w * stk_cap (a team's rows:
                                   // its children before publication)                     [K7_WARPS * stk_cap]
@@ -200,11 +202,17 @@ __device__ __forceinline__ void write_record(const DevCtx *c, u32 level, u32 alp
     }
 }
 
+// Key-value mode: the tie-break of equal keys is their task-local source index
+// (IA / IB), i.e. input order -- the stable permutation (reading R17).
+template <bool PR>
+__device__ __forceinline__ u32 tie_of(const u16 *I, u32 j) { return PR ? (u32)I[j] : j; }
+
 // ------------------------------------------------------------------ Standard-Sort (R2) on ordered keys
 // Rank of (v, p) among (B[j], j), j in [st, st + h): keys below v, and equal
 // keys before p.  One 96-bit subtract chain per comparison; PTX's carry after
 // it is set iff (B[j], j) >= (v, p), so r counts the others and rank = h - r.
-__device__ __forceinline__ u32 rank_in_leaf(const u64 *B, u32 st, u32 h, u64 v, u32 p) {
+template <bool PR = false>
+__device__ __forceinline__ u32 rank_in_leaf(const u64 *B, u32 st, u32 h, u64 v, u32 p, const u16 *IB = nullptr) {
     u32 r = 0;
     const u32 vlo = (u32)v, vhi = (u32)(v >> 32);
     for (u32 j = st; j < st + h; ++j) {
@@ -214,7 +222,7 @@ __device__ __forceinline__ u32 rank_in_leaf(const u64 *B, u32 st, u32 h, u64 v, 
             "subc.cc.u32 t, %3, %4;\n\t"
             "subc.cc.u32 t, %5, %6;\n\t"
             "addc.u32 %0, %0, 0;\n\t}"
-            : "+r"(r) : "r"(j), "r"(p), "r"((u32)x), "r"(vlo), "r"((u32)(x >> 32)), "r"(vhi));
+            : "+r"(r) : "r"(tie_of<PR>(IB, j)), "r"(p), "r"((u32)x), "r"(vlo), "r"((u32)(x >> 32)), "r"(vhi));
     }
     return h - r;
 }
@@ -222,8 +230,21 @@ __device__ __forceinline__ u32 rank_in_leaf(const u64 *B, u32 st, u32 h, u64 v, 
 // Bitonic network over a[0, n) by a thread set; all merges ascending (the
 // first step of each stage compares i with its mirror), so the virtual +inf
 // padding never moves.
-template <int NW>
-__device__ void set_bitonic(u64 *a, u32 n, const Grp<NW> &G) {
+// compare-exchange of positions lo < hi: (key, tie) ascending; key-value mode
+// carries (and breaks ties by) the source index
+template <bool PR>
+__device__ __forceinline__ void cx_pos(u64 *a, u16 *ia, u32 lo, u32 hi) {
+    const u64 x = a[lo], y = a[hi];
+    if (PR) {
+        const u16 ix = ia[lo], iy = ia[hi];
+        if (x > y || (x == y && ix > iy)) { a[lo] = y; a[hi] = x; ia[lo] = iy; ia[hi] = ix; }
+    } else if (x > y) {
+        a[lo] = y; a[hi] = x;
+    }
+}
+
+template <int NW, bool PR = false>
+__device__ void set_bitonic(u64 *a, u32 n, const Grp<NW> &G, u16 *ia = nullptr) {
     constexpr u32 NT = NW * 32;
     if (n <= 1) return;
     const u32 P = next_pow2(n);
@@ -233,14 +254,14 @@ __device__ void set_bitonic(u64 *a, u32 n, const Grp<NW> &G) {
         for (u32 t = G.t; t < (P >> 1); t += NT) {
             const u32 blk = t >> lh, w = t & ((1u << lh) - 1);
             const u32 lo = (blk << lk) + w, hi = (blk << lk) + k - 1 - w;
-            if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
+            if (hi < n) cx_pos<PR>(a, ia, lo, hi);
         }
         G.bar();
         for (int lj = (int)lh - 1; lj >= 0; --lj) {
             const u32 j = 1u << lj;
             for (u32 t = G.t; t < (P >> 1); t += NT) {
                 const u32 lo = ((t >> lj) << (lj + 1)) + (t & (j - 1)), hi = lo + j;
-                if (hi < n) { u64 x = a[lo], y = a[hi]; if (x > y) { a[lo] = y; a[hi] = x; } }
+                if (hi < n) cx_pos<PR>(a, ia, lo, hi);
             }
             G.bar();
         }
@@ -249,14 +270,18 @@ __device__ void set_bitonic(u64 *a, u32 n, const Grp<NW> &G) {
 
 // Standard-Sort of the leaf B[st, st + h) into A[st, st + h) by a thread set.
 // Ends with a barrier of the set.
-template <int NW>
+template <int NW, bool PR = false>
 __device__ void sort_range(K7Smem &S, u32 st, u32 h, const Grp<NW> &G) {
     constexpr u32 NT = NW * 32;
     if (h <= SMALL_MAX) {
-        for (u32 p = st + G.t; p < st + h; p += NT) S.A[st + rank_in_leaf(S.B, st, h, S.B[p], p)] = S.B[p];
+        for (u32 p = st + G.t; p < st + h; p += NT) {
+            const u32 r = st + rank_in_leaf<PR>(S.B, st, h, S.B[p], tie_of<PR>(S.IB, p), S.IB);
+            S.A[r] = S.B[p];
+            if (PR) S.IA[r] = S.IB[p];
+        }
     } else {
-        set_bitonic<NW>(S.B + st, h, G);
-        for (u32 p = st + G.t; p < st + h; p += NT) S.A[p] = S.B[p];
+        set_bitonic<NW, PR>(S.B + st, h, G, PR ? S.IB + st : nullptr);
+        for (u32 p = st + G.t; p < st + h; p += NT) { S.A[p] = S.B[p]; if (PR) S.IA[p] = S.IB[p]; }
     }
     G.bar();
 }
@@ -293,7 +318,7 @@ __device__ __forceinline__ void classify_slots(const u64 (&key)[KPT], u32 (&pk)[
     }
 }
 
-template <class K, int NW, int MODE>
+template <class K, int NW, int MODE, bool PR>
 __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos, u32 m, u32 L, u32 rel, u64 gbase,
                           const u64 *raw = nullptr) {   // MODE_GLOBAL: raw keys (bulk-copied task) instead of A
     constexpr u32 NT = NW * 32;
@@ -303,6 +328,8 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
     const u32 t = G.t, g = G.g, w = warp_id(), wg = w - G.w0, lane = lane_id();
     u64 *X = (rel & 1) ? S.B : S.A;
     u64 *Y = (rel & 1) ? S.A : S.B;
+    u16 *IX = (rel & 1) ? S.IB : S.IA;   // key-value mode: source indices (NULL otherwise)
+    u16 *IY = (rel & 1) ? S.IA : S.IB;
     u16 *Wg = S.W + G.w0 * CCOLS;
     u16 *Wrow = Wg + wg * CCOLS;
     u32 *row32 = reinterpret_cast<u32 *>(Wrow);
@@ -323,16 +350,22 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
     // to straight-line code with the keys in registers.
     u64 key[KPT];
     u32 pk[KPT];
+    u32 ix2[PR ? KPT / 2 : 1];   // key-value mode: two u16 source indices per register
     u64 mn = ~0ull, mx = 0;
 #pragma unroll
     for (int q = 0; q < KPT; ++q) {
         const u32 f = f0 + q * 32 + lane;
         const bool v = f < f1;
         key[q] = (MODE == MODE_GLOBAL && raw) ? K::to_okey(raw[v ? f : 0u]) : X[pos + (v ? f : 0u)];
+        if (PR) {
+            const u32 i = (MODE == MODE_GLOBAL && raw) ? f : (u32)IX[pos + (v ? f : 0u)];
+            if (q & 1) ix2[q / 2] |= i << 16; else ix2[q / 2] = i & 0xffffu;
+        }
         pk[q] = v ? 0u : NONE;
         mn = v && key[q] < mn ? key[q] : mn;
         mx = v && key[q] > mx ? key[q] : mx;
     }
+    auto idx_of = [&](int q) -> u16 { return PR ? (u16)((q & 1) ? ix2[q / 2] >> 16 : ix2[q / 2] & 0xffffu) : (u16)0; };
 
     if (c->k7_prof && t == 0) {   // node statistics: slots 7/8 group nodes / keys, 9/10 CTA nodes / keys
         atomicAdd(&S.prof[CTA ? 9 : 7], 1ull);
@@ -363,10 +396,11 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
             // R9/R10: the whole node goes to Standard-Sort (no bucketing, no record)
             if (!(rel & 1)) {
 #pragma unroll
-                for (int q = 0; q < KPT; ++q) if (pk[q] != NONE) S.B[pos + f0 + q * 32 + lane] = key[q];
+                for (int q = 0; q < KPT; ++q)
+                    if (pk[q] != NONE) { S.B[pos + f0 + q * 32 + lane] = key[q]; if (PR) S.IB[pos + f0 + q * 32 + lane] = idx_of(q); }
             }
             G.bar();
-            sort_range<NW>(S, pos, m, G);
+            sort_range<NW, PR>(S, pos, m, G);
             return;
         }
         // ---- alpha samples (R3, R4) -> per-bin counts
@@ -547,6 +581,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
             u64 *dst = (d & DEST_A) ? S.A : (d & DEST_B) ? S.B : Y;
             if (valid) {
                 dst[p] = key[q];
+                if (PR) ((d & DEST_A) ? S.IA : (d & DEST_B) ? S.IB : IY)[p] = idx_of(q);
                 S.LC[p] = (d & DEST_B) ? (u16)u : (u16)0;
             }
         }
@@ -572,14 +607,16 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         if (hh > SMALL_MAX) continue;
         const u32 st = pos + ((u32)Wg[cc] & POS_MASK);
         const u64 v = S.B[pos + p];
-        S.A[st + rank_in_leaf(S.B, st, hh, v, pos + p)] = v;
+        const u32 r = st + rank_in_leaf<PR>(S.B, st, hh, v, tie_of<PR>(S.IB, pos + p), S.IB);
+        S.A[r] = v;
+        if (PR) S.IA[r] = S.IB[pos + p];
     }
     const u32 nb = S.nbl[w0];
     for (u32 i = 0; i < nb; ++i) {
         const u32 e = bl[i];
         const u32 st = pos + (e & 0x1fffu), hh = e >> 13;
-        set_bitonic<NW>(S.B + st, hh, G);
-        for (u32 p = st + t; p < st + hh; p += NT) S.A[p] = S.B[p];
+        set_bitonic<NW, PR>(S.B + st, hh, G, PR ? S.IB + st : nullptr);
+        for (u32 p = st + t; p < st + hh; p += NT) { S.A[p] = S.B[p]; if (PR) S.IA[p] = S.IB[p]; }
     }
     if (MODE == MODE_NODE && logging && t == 0) {
         const u32 cc = S.ncnt[w0];
@@ -597,12 +634,13 @@ __device__ __forceinline__ ulonglong2 ld_stream2(const ulonglong2 *p) {
 }
 
 // Load src[0, m) into dst (A or B) as ordered keys; returns true if a NaN was seen (f64).
-template <class K>
-__device__ __forceinline__ bool load_task(u64 *dst, const u64 *src, u32 m) {
+template <class K, bool PR>
+__device__ __forceinline__ bool load_task(u64 *dst, u16 *idst, const u64 *src, u32 m) {
     bool nan = false;
     auto put = [&](u32 k, u64 raw) {
         if (K::is_f64) nan |= (raw & 0x7fffffffffffffffull) > 0x7ff0000000000000ull;
         dst[k] = K::to_okey(raw);
+        if (PR) idst[k] = (u16)k;
     };
     const u32 head = ((uintptr_t)src & 15) ? 1u : 0u;
     if (head && m && threadIdx.x == 0) put(0, src[0]);
@@ -620,6 +658,33 @@ __device__ __forceinline__ bool load_task(u64 *dst, const u64 *src, u32 m) {
     for (; i < nv; i += K7_THREADS) { ulonglong2 r = ld_stream2(v + i); put(head + 2 * i, r.x); put(head + 2 * i + 1, r.y); }
     if (m > head && ((m - head) & 1) && threadIdx.x == 0) put(m - 1, src[m - 1]);
     return nan;
+}
+
+// Key-value mode: the global source index of the task's output positions,
+// perm[off + p] = index of the key (ibuf[src][off + IA[p]], identity for the input
+// buffer), gathered into registers before any thread writes (ibuf[src] may be the
+// destination array itself).
+template <bool PR>
+__device__ __forceinline__ void store_task_idx(const DevCtx *c, const K7Smem &S, const K7Task &t, u32 m) {
+    if (!PR) return;
+    const u32 *isrc = c->ibuf[t.src];
+    u32 g[KPT];
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+        const u32 p = threadIdx.x + q * K7_THREADS;
+        g[q] = 0;
+        if (p < m) {
+            const u32 i = S.IA[p];
+            g[q] = isrc ? isrc[t.off + i] : (u32)(t.off + i);
+        }
+    }
+    __syncthreads();
+    u32 *idst = c->ibuf[2] + t.off;
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+        const u32 p = threadIdx.x + q * K7_THREADS;
+        if (p < m) idst[p] = g[q];
+    }
 }
 
 // Write A[0, m) (sorted ordered keys) to dst as raw keys, 16-byte stores.
@@ -669,7 +734,7 @@ __device__ __forceinline__ void push_root(const DevCtx *c, K7Smem &S, u32 e) {
     }
 }
 
-template <class K>
+template <class K, bool PR>
 __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kernel(const DevCtx *__restrict__ c) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char k7_smem_raw[];
@@ -686,6 +751,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
         S.lsm_cap = k7_lsm_cap(c->tau); S.list_cap = k7_list_cap(c->tau); S.stk_cap = k7_stk_cap(c->tau);
         S.lsm = reinterpret_cast<u32 *>(S.tail);
         S.stk = S.lsm + S.lsm_cap;
+        S.IA = PR ? reinterpret_cast<u16 *>(S.stk + K7_WARPS * S.stk_cap) : nullptr;
+        S.IB = PR ? S.IA + S_CAP : nullptr;
     }
     __syncthreads();
     for (u32 i = threadIdx.x; i < S.lsm_cap; i += K7_THREADS) S.lsm[i] = 0;   // tickets read 0 until pushed
@@ -722,7 +789,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
         const bool raw_group = task.kind == K7_GROUP && !S.ldirect;
         if (raw_group) {
         } else if (S.ldirect) {
-            nan_here = load_task<K>(dst, c->buf[task.src] + task.off, M);
+            nan_here = load_task<K, PR>(dst, sort_task ? S.IB : S.IA, c->buf[task.src] + task.off, M);
         } else {   // raw keys at B[lhead + i] -> ordered keys at dst[i]
             const u32 hd = S.lhead;
             u64 r[KPT];
@@ -738,6 +805,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 if (i < M) {
                     if (K::is_f64) nan_here |= (r[q] & 0x7fffffffffffffffull) > 0x7ff0000000000000ull;
                     dst[i] = K::to_okey(r[q]);
+                    if (PR) (sort_task ? S.IB : S.IA)[i] = (u16)i;
                 }
             }
         }
@@ -749,7 +817,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
         prof_mark(c, S, 1);
         if (threadIdx.x == 0 && c->k7_prof) { S.prof[11] += 1; S.prof[12] += M; }
         if (sort_task) {
-            sort_range<K7_WARPS>(S, 0, M, CT);
+            sort_range<K7_WARPS, PR>(S, 0, M, CT);
             prof_mark(c, S, 6);
         } else {
             u32 Lb;
@@ -761,7 +829,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 }
                 __syncthreads();
                 Lb = S.glevel;
-                node_step<K, K7_WARPS, MODE_GLOBAL>(c, S, CT, 0, M, Lb, 0, task.off, raw_group ? S.B + S.lhead : nullptr);
+                node_step<K, K7_WARPS, MODE_GLOBAL, PR>(c, S, CT, 0, M, Lb, 0, task.off, raw_group ? S.B + S.lhead : nullptr);
                 prof_mark(c, S, 2);
             } else {   // K7_NODE: a fresh Learned-Sort call on the whole task
                 Lb = task.level;
@@ -774,7 +842,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 if (ent_m(e) > (u32)(2 * GCAP)) {
                     __syncthreads();
                     if (threadIdx.x == 0) S.lbig[i] = 0;
-                    node_step<K, K7_WARPS, MODE_NODE>(c, S, CT, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                    node_step<K, K7_WARPS, MODE_NODE, PR>(c, S, CT, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
                 }
             }
             // double teams (2 x GW warps) take the nodes of (GCAP, 2 GCAP] keys
@@ -793,7 +861,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 GH.bar();
                 const u32 e = S.cur[GH.w0];
                 if (!e) break;
-                node_step<K, 2 * GW, MODE_NODE>(c, S, GH, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                node_step<K, 2 * GW, MODE_NODE, PR>(c, S, GH, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
             }
             prof_mark(c, S, 4);
             // teams of GW warps take the nodes of (WCAP, GCAP] keys (their children go to the small
@@ -813,7 +881,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 GG.bar();
                 const u32 e = S.cur[GG.w0];
                 if (!e) break;
-                node_step<K, GW, MODE_NODE>(c, S, GG, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                node_step<K, GW, MODE_NODE, PR>(c, S, GG, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
             }
             if (GG.t == 0) { __threadfence_block(); atomicSub(&S.big_active, 1u); }
             if (lane == 0) S.top[w] = 0;
@@ -843,7 +911,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 }
                 e = __shfl_sync(0xffffffffu, e, 0);
                 if (!e) break;
-                node_step<K, 1, MODE_NODE>(c, S, GS, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                node_step<K, 1, MODE_NODE, PR>(c, S, GS, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
             }
             __syncthreads();
             prof_mark(c, S, 5);
@@ -852,6 +920,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
             S.nidx = nclaim;
             if (nclaim < ntasks) { S.ntask = c->k7[c->k7_order ? c->k7_order[nclaim] : nclaim]; k7_issue(c, S, S.ntask); }
         }
+        store_task_idx<PR>(c, S, task, M);
         store_task<K>(S, gout, M);
         prof_mark(c, S, 13);
         __syncthreads();

@@ -33,7 +33,7 @@ constexpr int K8_IPT = K8_TILE / K8_THREADS;   // 8
 constexpr int K8_MTILE = PCF_K8_MTILE;            // outputs of one merge CTA
 constexpr int K8_MTHREADS = PCF_K8_MTHREADS;
 constexpr int K8_MIPT = K8_MTILE / K8_MTHREADS;   // outputs per merge thread
-constexpr int K8_MERGE_SMEM = K8_MTILE * 8;
+constexpr int K8_MERGE_SMEM = K8_MTILE * 12;   // keys (+ key-value mode: u32 indices)
 constexpr int K8_SORT_SMEM = 2 * K8_TILE * 8;
 
 #ifndef PCF_K8_WARPSORT
@@ -164,6 +164,39 @@ __device__ __forceinline__ void k8_sort_tile(u64 *k8_bs, const u64 *__restrict__
     for (u32 k = threadIdx.x; k < n; k += K8_THREADS) dst[base + k] = m <= (u64)K8_TILE ? K::from_okey(sa[k]) : sa[k];
 }
 
+// Key-value mode: a K8_TILE tile of (ordered key, source index)
+// pairs sorted by a shared-memory bitonic network on (key, index) -- equal keys in
+// index order, so the block sort is stable; the merge passes (A first among equal
+// keys) keep it stable.  Simpler than the keys-only register network: this mode is
+// not the benchmarked path.
+template <class K>
+__device__ __forceinline__ void k8_sort_tile_pr(u64 *a, u32 *ai, const u64 *__restrict__ src, const u32 *__restrict__ isrc,
+                                                u64 src_off, u64 *__restrict__ dst, u32 *__restrict__ idst, u64 m, u64 base) {
+    const u32 n = (u32)min((u64)K8_TILE, m - base);
+    for (u32 k = threadIdx.x; k < (u32)K8_TILE; k += K8_THREADS) {
+        a[k] = k < n ? K::to_okey(src[base + k]) : ~0ull;
+        ai[k] = k < n ? (isrc ? isrc[src_off + base + k] : (u32)(src_off + base + k)) : 0xffffffffu;
+    }
+    __syncthreads();
+    for (u32 k = 2; k <= (u32)K8_TILE; k <<= 1) {
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            for (u32 t = threadIdx.x; t < (u32)K8_TILE / 2; t += K8_THREADS) {
+                const u32 lo = ((t / j) * 2 * j) + (t % j), hi = lo + j;
+                const bool up = (lo & k) == 0;
+                const u64 x = a[lo], y = a[hi];
+                const u32 ix = ai[lo], iy = ai[hi];
+                const bool gt = x > y || (x == y && ix > iy);
+                if (gt == up) { a[lo] = y; a[hi] = x; ai[lo] = iy; ai[hi] = ix; }
+            }
+            __syncthreads();
+        }
+    }
+    for (u32 k = threadIdx.x; k < n; k += K8_THREADS) {
+        dst[base + k] = m <= (u64)K8_TILE ? K::from_okey(a[k]) : a[k];
+        idst[base + k] = ai[k];
+    }
+}
+
 // ------------------------------------------------------------------ segmented driver
 // Every Standard-Sort bucket of > S_CAP keys (the fallback segments collected by
 // k_items_to_nodes) is sorted by one chain of launches: k8_plan, k8_check,
@@ -249,25 +282,45 @@ __global__ void __launch_bounds__(256) k8_check(const DevCtx *__restrict__ c) {
     }
 }
 
-template <class K>
+template <class K, bool PR>
 __global__ void __launch_bounds__(K8_THREADS) k8_blocksort(const DevCtx *__restrict__ c) {
     pdl_entry();
-    extern __shared__ __align__(16) u64 k8_bs[];   // 2 * K8_TILE keys
+    extern __shared__ __align__(16) u64 k8_bs[];   // 2 * K8_TILE keys (PR: K8_TILE keys + indices)
     const K8Plan pl = c->cnt->k8;
     u64 *out = c->buf[2], *tmp = c->buf[1];
     for (u32 t = blockIdx.x; t < pl.tiles; t += gridDim.x) {
         const u32 s = k8_seg_of(c->k8_tb, pl.nseg, t);
         const SegItem it = c->fb[s];
         const u64 *src = c->buf[it.src] + it.off;
+        const u32 *isrc = PR ? c->ibuf[it.src] : nullptr;
         const u64 base = (u64)(t - c->k8_tb[s]) * K8_TILE;
         if (c->k8_flag[s] == 0) {   // all keys equal: already sorted, final position
             const u32 n = (u32)min((u64)K8_TILE, (u64)it.m - base);
+            constexpr u32 NQ = PR ? (u32)((K8_TILE + K8_THREADS - 1) / K8_THREADS) : 1u;
+            u32 g[NQ];
+            if (PR) {   // indices first: ibuf[src] may be ibuf[2] itself
+#pragma unroll
+                for (u32 q = 0; q < NQ; ++q) {
+                    const u32 k = threadIdx.x + q * K8_THREADS;
+                    g[q] = k < n ? (isrc ? isrc[it.off + base + k] : (u32)(it.off + base + k)) : 0u;
+                }
+            }
             for (u32 k = threadIdx.x; k < n; k += K8_THREADS) out[it.off + base + k] = src[base + k];
+            if (PR) {
+#pragma unroll
+                for (u32 q = 0; q < NQ; ++q) {
+                    const u32 k = threadIdx.x + q * K8_THREADS;
+                    if (k < n) c->ibuf[2][it.off + base + k] = g[q];
+                }
+            }
             continue;
         }
         __syncthreads();   // the previous tile's shared-memory stage is drained
-        u64 *dst0 = ((k8_merges(it.m) & 1u) == 0 ? out : tmp) + it.off;
-        k8_sort_tile<K>(k8_bs, src, dst0, it.m, base);
+        const bool to_out = (k8_merges(it.m) & 1u) == 0;
+        u64 *dst0 = (to_out ? out : tmp) + it.off;
+        if (PR) k8_sort_tile_pr<K>(k8_bs, reinterpret_cast<u32 *>(k8_bs + K8_TILE), src, isrc, it.off, dst0,
+                                   c->ibuf[to_out ? 2 : 1] + it.off, it.m, base);
+        else k8_sort_tile<K>(k8_bs, src, dst0, it.m, base);
     }
 }
 
@@ -301,11 +354,12 @@ __global__ void k8_partition(const DevCtx *__restrict__ c) {
     }
 }
 
-template <class K>
+template <class K, bool PR>
 __global__ void __launch_bounds__(K8_MTHREADS) k8_merge(const DevCtx *__restrict__ c) {
     pdl_entry();
-    extern __shared__ __align__(16) u64 k8_smem[];   // K8_MTILE input keys
+    extern __shared__ __align__(16) u64 k8_smem[];   // K8_MTILE input keys (+ PR: their indices)
     u64 *sa = k8_smem;
+    u32 *sai = reinterpret_cast<u32 *>(k8_smem + K8_MTILE);
     const K8Plan pl = c->cnt->k8;
     const u64 width = (u64)K8_TILE << pl.pass;
     for (u32 gt = blockIdx.x; gt < pl.mtiles; gt += gridDim.x) {
@@ -318,7 +372,10 @@ __global__ void __launch_bounds__(K8_MTHREADS) k8_merge(const DevCtx *__restrict
         const u64 m = it.m;
         const bool last = pl.pass + 1 == mg;
         const u64 *src = (((mg - pl.pass) & 1u) == 0 ? c->buf[2] : c->buf[1]) + it.off;
-        u64 *dst = (((mg - 1 - pl.pass) & 1u) == 0 ? c->buf[2] : c->buf[1]) + it.off;
+        const bool to_out = ((mg - 1 - pl.pass) & 1u) == 0;
+        u64 *dst = (to_out ? c->buf[2] : c->buf[1]) + it.off;
+        const u32 *isrc = PR ? (to_out ? c->ibuf[1] : c->ibuf[2]) + it.off : nullptr;
+        u32 *idst = PR ? (to_out ? c->ibuf[2] : c->ibuf[1]) + it.off : nullptr;
         const u64 o0 = (u64)t * K8_MTILE;
         const u64 pair0 = (o0 / (2 * width)) * (2 * width);
         const u64 na = min(pair0 + width, m) - pair0, nb = min(pair0 + 2 * width, m) - min(pair0 + width, m);
@@ -339,6 +396,7 @@ __global__ void __launch_bounds__(K8_MTHREADS) k8_merge(const DevCtx *__restrict
             for (int j = 0; j < K8_MIPT; ++j) {
                 const u32 k = threadIdx.x + j * K8_MTHREADS;
                 if (k < tot) sa[k] = v[j];
+                if (PR && k < tot) sai[k] = k < la ? isrc[pair0 + ia0 + k] : isrc[pair0 + na + ib0 + (k - la)];
             }
         }
         __syncthreads();
@@ -347,7 +405,18 @@ __global__ void __launch_bounds__(K8_MTHREADS) k8_merge(const DevCtx *__restrict
         const u32 dd = min(threadIdx.x * K8_MIPT, tot);
         const u32 ia = k8_split(sa, la, sa + la, lb, dd);
         u64 r[K8_MIPT];
-        k8_merge_seq<K8_MIPT>(sa, la, sa + la, lb, ia, dd - ia, r);
+        if (PR) {   // the same merge, by positions, so the indices follow their keys
+            u32 ja = ia, jb = dd - ia;
+#pragma unroll
+            for (int k = 0; k < K8_MIPT; ++k) {
+                const bool ta = jb >= lb || (ja < la && sa[ja] <= sa[la + jb]);
+                const u32 sp = ta ? ja : la + jb;
+                if (ta) ++ja; else ++jb;
+                if (dd + k < tot) { r[k] = sa[sp]; idst[o0 + dd + k] = sai[sp]; }
+            }
+        } else {
+            k8_merge_seq<K8_MIPT>(sa, la, sa + la, lb, ia, dd - ia, r);
+        }
         u64 *outp = dst + o0 + dd;
 #pragma unroll
         for (int k = 0; k < K8_MIPT; ++k) if (dd + k < tot) outp[k] = last ? K::from_okey(r[k]) : r[k];
