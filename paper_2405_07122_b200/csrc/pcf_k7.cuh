@@ -300,20 +300,11 @@ enum { MODE_NODE = 0, MODE_GLOBAL = 1 };
 // i(x) of every valid slot (pk != NONE) into pk: certified fast path for all
 // slots, the exact sub/div/mul evaluation (R6) only for the rare keys in the
 // guard band, behind one warp-uniform branch.
-#ifndef PCF_K7_SLOTSKIP
-#define PCF_K7_SLOTSKIP 1
-#endif
-// Slot q of a warp holds chunk q of the warp's range; chunks >= nch (uniform per
-// warp) hold no key, and with PCF_K7_SLOTSKIP their code is branched around
-// (the loops stay unrolled, so the keys stay in registers).
-__device__ __forceinline__ bool slot_live(int q, u32 nch) { return !PCF_K7_SLOTSKIP || (u32)q < nch; }
-
 template <class K>
-__device__ __forceinline__ void classify_slots(const u64 (&key)[KPT], u32 (&pk)[KPT], const Model &md, u32 nch) {
+__device__ __forceinline__ void classify_slots(const u64 (&key)[KPT], u32 (&pk)[KPT], const Model &md) {
     u32 bad = 0;
 #pragma unroll
     for (int q = 0; q < KPT; ++q) {
-        if (!slot_live(q, nch)) continue;
         bool ok;
         const u32 i = interval_index_fast<K>(key[q], md, ok);
         const bool v = pk[q] != NONE;
@@ -455,10 +446,9 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         }
         G.bar();
         // ---- classify (i(x) -> T) and count per (warp, column); unstable rank
-        classify_slots<K>(key, pk, md, nch);
+        classify_slots<K>(key, pk, md);
 #pragma unroll
         for (int q = 0; q < KPT; ++q) {
-            if (!slot_live(q, nch)) continue;
             const bool v = pk[q] != NONE;
             const u32 u = T16[v ? pk[q] : 1u];
             u32 old = 0;
@@ -473,10 +463,9 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         if (t == 0) S.nbl[w0] = 0;
         const u32 *gT = S.gT;
         const u32 jb = S.gjlo - 1u;
-        classify_slots<K>(key, pk, md, nch);
+        classify_slots<K>(key, pk, md);
 #pragma unroll
         for (int q = 0; q < KPT; ++q) {
-            if (!slot_live(q, nch)) continue;
             const bool v = pk[q] != NONE;
             u32 j = 0;
             if (v) j = __ldg(gT + pk[q]);
@@ -572,7 +561,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
     // ---- placement (chunk order: stable re-rank of recursing keys)
 #pragma unroll
     for (int q = 0; q < KPT; ++q) {
-        if (slot_live(q, nch)) {
+        {
             const u32 u = pk[q] & 0xffffu;
             const bool valid = pk[q] != NONE;
             u32 d = valid ? (u32)Wrow[u] + (pk[q] >> 16) : 0u;
