@@ -107,8 +107,10 @@ typedef struct pcf_stats {
      * phases: the host cannot place events inside the device-driven loop) */
     float phase_ms[PCF_PHASES];
     uint64_t phase_bytes[PCF_PHASES];  /* algorithmic bytes per phase */
-    /* PCF_FLAG_PROFILE: clock64 cycles summed over K7 CTAs per phase (see pcf_k7.cuh prof_mark) */
-    uint64_t k7_cycles[16];
+    /* PCF_FLAG_PROFILE: clock64 cycles summed over K7 CTAs per phase (see pcf_k7.cuh prof_mark);
+     * [16..19]: warp-cycles inside node steps of double teams / teams / single warps, and
+     * warp-cycles single warps spent waiting for small nodes */
+    uint64_t k7_cycles[24];
 } pcf_stats;
 
 typedef struct pcf_params {

@@ -47,7 +47,7 @@ class Stats(ctypes.Structure):
                 ("groups_smem", ctypes.c_uint64), ("split_keys_moved", ctypes.c_uint64),
                 ("global_nodes", ctypes.c_uint64), ("fallback_keys_global", ctypes.c_uint64),
                 ("phase_ms", ctypes.c_float * NPHASES), ("phase_bytes", ctypes.c_uint64 * NPHASES),
-                ("k7_cycles", ctypes.c_uint64 * 16)]
+                ("k7_cycles", ctypes.c_uint64 * 24)]
 
     def as_dict(self):
         return {"kernel_launches": self.kernel_launches, "rounds": self.rounds,

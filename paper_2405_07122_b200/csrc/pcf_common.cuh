@@ -46,7 +46,7 @@ constexpr int SC_KPL = PCF_SC_KPL;             // keys per lane held in register
 constexpr int SC_PER_WARP = SC_KPL * 32; // 512 consecutive keys per warp
 constexpr int SPLIT_TILE = SC_WARPS * SC_PER_WARP;   // 5376 keys per split tile
 constexpr u64 GOLDEN = 0x9E3779B97F4A7C15ull;
-#define K7_PROF_SLOTS_DECL 16
+#define K7_PROF_SLOTS_DECL 24
 
 // ---------------------------------------------------------------- key transforms
 // totalOrder on binary64 == unsigned order of the "flipped" bits: set the sign

@@ -767,6 +767,11 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
         if (S.nidx < ntasks) { S.ntask = c->k7[c->k7_order ? c->k7_order[S.nidx] : S.nidx]; k7_issue(c, S, S.ntask); }
     }
     __syncthreads();
+#ifndef PCF_K7_WPROF
+#define PCF_K7_WPROF 0   // per-warp busy / wait cycles (slots 16-19): profiling builds only (costs registers)
+#endif
+    const bool wprof = PCF_K7_WPROF && c->k7_prof != nullptr && lane == 0;
+    unsigned long long wcyc[4] = {0, 0, 0, 0};
     for (u32 it = 0;; ++it) {
         if (threadIdx.x == 0) {
             S.task_idx = S.nidx;
@@ -861,7 +866,9 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 GH.bar();
                 const u32 e = S.cur[GH.w0];
                 if (!e) break;
+                const long long t0 = wprof ? clock64() : 0;
                 node_step<K, 2 * GW, MODE_NODE, PR>(c, S, GH, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                if (wprof) wcyc[0] += clock64() - t0;
             }
             prof_mark(c, S, 4);
             // teams of GW warps take the nodes of (WCAP, GCAP] keys (their children go to the small
@@ -881,13 +888,16 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 GG.bar();
                 const u32 e = S.cur[GG.w0];
                 if (!e) break;
+                const long long t0 = wprof ? clock64() : 0;
                 node_step<K, GW, MODE_NODE, PR>(c, S, GG, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                if (wprof) wcyc[1] += clock64() - t0;
             }
             if (GG.t == 0) { __threadfence_block(); atomicSub(&S.big_active, 1u); }
             if (lane == 0) S.top[w] = 0;
             __syncwarp();
             for (;;) {
                 u32 e = 0;
+                const long long tw = wprof ? clock64() : 0;
                 if (lane == 0) {
                     if (S.top[w] > 0) {
                         e = S.stk[w * S.stk_cap + (--S.top[w])];
@@ -910,8 +920,11 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                     }
                 }
                 e = __shfl_sync(0xffffffffu, e, 0);
+                const long long t0 = wprof ? clock64() : 0;
+                if (wprof) wcyc[3] += t0 - tw;
                 if (!e) break;
                 node_step<K, 1, MODE_NODE, PR>(c, S, GS, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                if (wprof) wcyc[2] += clock64() - t0;
             }
             __syncthreads();
             prof_mark(c, S, 5);
@@ -923,6 +936,11 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
         store_task_idx<PR>(c, S, task, M);
         store_task<K>(S, gout, M);
         prof_mark(c, S, 13);
+        __syncthreads();
+    }
+    if (PCF_K7_WPROF) {
+        if (wprof)
+            for (int i = 0; i < 4; ++i) atomicAdd(&S.prof[16 + i], wcyc[i]);
         __syncthreads();
     }
     if (c->k7_prof && threadIdx.x == 0)

@@ -22,3 +22,9 @@ for i in SLOTS:
 for i in (7, 8, 9, 10):
     print(f"  {NAMES[i]:28s} {cy[i]:.0f}")
 print(f"  mean group node {cy[8] / max(cy[7], 1):.1f} keys, mean CTA node {cy[10] / max(cy[9], 1):.1f} keys")
+# warp utilisation of the node phases (slots 16-19: per-warp cycles, summed over warps and CTAs)
+nodes_cta = cy[4] + cy[5]   # thread 0's cycles from the end of the group placement to the end of the task
+busy = cy[16] + cy[17] + cy[18]
+print(f"  warp-cycles in node steps: double teams {cy[16]:.3e}, teams {cy[17]:.3e}, warps {cy[18]:.3e}; "
+      f"small-list waits {cy[19]:.3e}")
+print(f"  node-phase warp utilisation {busy / max(16 * nodes_cta, 1):.3f} (busy warp-cycles / (16 warps x node-phase cycles))")
