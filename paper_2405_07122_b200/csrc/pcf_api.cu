@@ -248,13 +248,15 @@ struct Launch {   // the kernel-launch configuration of this device
 
 // ---------------------------------------------------------------- device-driven tail (CUDA graph)
 // Everything after the host-launched first batch runs from one executable graph:
-//   k_items_to_nodes -> k_batch_cond -> WHILE (more work) {
+//   k_items_to_nodes -> WHILE (more work) {
 //       batched min/max, sampling, fit of the new global nodes;
 //       two split rounds (plan, tile map, count, scan x3, scatter, taskgen);
-//       K7 (order, kernel, advance); k_items_to_nodes; k_batch_cond }
+//       K7 (order, kernel, advance); k_items_to_nodes }
 //   [phase boundary]
-//   k8_plan -> k8_check -> k8_blocksort -> WHILE (merge passes left) {
-//       k8_partition, k8_merge, k8_pass_end } -> k_log_finalize
+//   k8_plan -> IF (fallback segments) { k8_check, k8_blocksort }
+//           -> WHILE (merge passes left) { k8_partition, k8_merge, k8_pass_end }
+//           -> IF (pass log) { k_log_finalize }
+// A sort with no oversized bucket runs two kernels here (k_items_to_nodes, k8_plan).
 // The loop conditions are set on the device (cudaGraphSetConditional), so the
 // recursion over oversized buckets needs no host round trip.
 // Graphs depend only on (device, key type, DevCtx address, tau); they are cached
@@ -295,11 +297,11 @@ static int add_k7(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32 *n
     return PCF_OK;
 }
 
-// Add a WHILE node after the current capture dependencies of `cs`, capture its
-// body from `body` (launched on the second capture stream), and continue the
-// capture of `cs` after the node.
+// Add a conditional node (WHILE / IF) after the current capture dependencies of
+// `cs`, capture its body from `body` (launched on the second capture stream), and
+// continue the capture of `cs` after the node.
 template <class F>
-static int add_while(cudaStream_t cs, cudaGraphConditionalHandle h, F body) {
+static int add_cond(cudaStream_t cs, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type, F body) {
     cudaStreamCaptureStatus cst;
     cudaGraph_t cg;
     const cudaGraphNode_t *deps = nullptr;
@@ -308,7 +310,7 @@ static int add_while(cudaStream_t cs, cudaGraphConditionalHandle h, F body) {
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = h;
-    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.type = type;
     cp.conditional.size = 1;
     cudaGraphNode_t node;
     CK(cudaGraphAddNode(&node, cg, deps, ndeps, &cp));
@@ -338,9 +340,8 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
         CK(cudaStreamBeginCaptureToGraph(cs, tg.g[0], nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         int rc = PCF_OK;
         auto cap = [&]() -> int {
-            CK(launch_pdl(k_items_to_nodes<K>, 1, 1024, 0, cs, d_ctx));
-            CK(launch_pdl(k_batch_cond, 1, 1, 0, cs, d_ctx, hb, 0u));
-            return add_while(cs, hb, [&](cudaStream_t bs) -> int {
+            CK(launch_pdl(k_items_to_nodes<K>, 1, 1024, 0, cs, d_ctx, hb, 0u));
+            return add_cond(cs, hb, cudaGraphCondTypeWhile, [&](cudaStream_t bs) -> int {
                 u32 nk = 0;
                 CK(launch_pdl(k_minmax_batch<K>, lc.nsm * 8, MM_THREADS, 0, bs, d_ctx));
                 CK(launch_pdl(k_fit_sample_batch<K>, lc.nsm * 8, FSB_CHUNK, 0, bs, d_ctx));
@@ -349,9 +350,8 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
                 for (int r = 0; r < 2; ++r) { int e = add_round<K>(bs, d_ctx, lc, &nk); if (e) return e; }
                 int e = add_k7<K, PR>(bs, d_ctx, lc, &nk);
                 if (e) return e;
-                CK(launch_pdl(k_items_to_nodes<K>, 1, 1024, 0, bs, d_ctx));
-                CK(launch_pdl(k_batch_cond, 1, 1, 0, bs, d_ctx, hb, 1u));
-                nk += 2;
+                CK(launch_pdl(k_items_to_nodes<K>, 1, 1024, 0, bs, d_ctx, hb, 1u));
+                nk += 1;
                 tg.body_kernels = nk;
                 return PCF_OK;
             });
@@ -361,19 +361,25 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
         const cudaError_t e = cudaStreamEndCapture(cs, &out);
         if (rc) return rc;
         CK(e);
-        tg.parent_kernels[0] = 2;
+        tg.parent_kernels[0] = 1;
     }
     // ---- graph 1: the segmented fallback sort (K8) and the pass-log records
     {
         CK(cudaGraphCreate(&tg.g[1], 0));
-        cudaGraphConditionalHandle hk;
+        cudaGraphConditionalHandle hs, hk, hl;
+        CK(cudaGraphConditionalHandleCreate(&hs, tg.g[1], 0, cudaGraphCondAssignDefault));
         CK(cudaGraphConditionalHandleCreate(&hk, tg.g[1], 0, cudaGraphCondAssignDefault));
+        CK(cudaGraphConditionalHandleCreate(&hl, tg.g[1], 0, cudaGraphCondAssignDefault));
         CK(cudaStreamBeginCaptureToGraph(cs, tg.g[1], nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         auto cap = [&]() -> int {
-            CK(launch_pdl(k8_plan, 1, 1024, 0, cs, d_ctx, hk));
-            CK(launch_pdl(k8_check, lc.nsm * 8, 256, 0, cs, d_ctx));
-            CK(launch_pdl(k8_blocksort<K, PR>, lc.nsm * 3, K8_THREADS, K8_SORT_SMEM, cs, d_ctx));
-            int rc = add_while(cs, hk, [&](cudaStream_t bs) -> int {
+            CK(launch_pdl(k8_plan, 1, 1024, 0, cs, d_ctx, hs, hk, hl));
+            int rc = add_cond(cs, hs, cudaGraphCondTypeIf, [&](cudaStream_t bs) -> int {
+                CK(launch_pdl(k8_check, lc.nsm * 8, 256, 0, bs, d_ctx));
+                CK(launch_pdl(k8_blocksort<K, PR>, lc.nsm * 3, K8_THREADS, K8_SORT_SMEM, bs, d_ctx));
+                return PCF_OK;
+            });
+            if (rc) return rc;
+            rc = add_cond(cs, hk, cudaGraphCondTypeWhile, [&](cudaStream_t bs) -> int {
                 CK(launch_pdl(k8_partition<K>, lc.nsm * 4, 256, 0, bs, d_ctx));
                 CK(launch_pdl(k8_merge<K, PR>, lc.nsm * 8, K8_MTHREADS, K8_MERGE_SMEM, bs, d_ctx));
                 CK(launch_pdl(k8_pass_end, 1, 1, 0, bs, d_ctx, hk));
@@ -381,15 +387,17 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
                 return PCF_OK;
             });
             if (rc) return rc;
-            CK(launch_pdl(k_log_finalize<K>, lc.nsm * 4, 256, 0, cs, d_ctx));
-            return PCF_OK;
+            return add_cond(cs, hl, cudaGraphCondTypeIf, [&](cudaStream_t bs) -> int {
+                CK(launch_pdl(k_log_finalize<K>, lc.nsm * 4, 256, 0, bs, d_ctx));
+                return PCF_OK;
+            });
         };
         const int rc = cap();
         cudaGraph_t out;
         const cudaError_t e = cudaStreamEndCapture(cs, &out);
         if (rc) return rc;
         CK(e);
-        tg.parent_kernels[1] = 4;
+        tg.parent_kernels[1] = 1;   // k8_plan; the IF bodies are counted from the device counters
     }
     for (int i = 0; i < 2; ++i) CK(cudaGraphInstantiate(&tg.ex[i], tg.g[i], 0));
     return PCF_OK;
@@ -732,7 +740,8 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         stats.split_keys_moved = hcnt.split_keys;
         stats.fallback_keys_global = hcnt.fb_keys;
         if (tail) {
-            launches += hcnt.iters * tail->body_kernels + hcnt.k8.max_merges * tail->k8_body_kernels;
+            launches += hcnt.iters * tail->body_kernels + hcnt.k8.max_merges * tail->k8_body_kernels
+                        + (hcnt.k8.nseg ? 2 : 0) + (logging ? 1 : 0);
             stats.device_batches = hcnt.iters;
         }
         if (!small) {

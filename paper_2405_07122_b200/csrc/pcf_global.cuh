@@ -266,7 +266,8 @@ __global__ void __launch_bounds__(FSB_CHUNK) k_fit_sample_batch(const DevCtx *__
 // One CTA; consumes every item and resets the item count.  This replaces the
 // host round trip of the previous design (recursion per bucket).
 template <class K>
-__global__ void __launch_bounds__(1024) k_items_to_nodes(const DevCtx *__restrict__ c) {
+__global__ void __launch_bounds__(1024) k_items_to_nodes(const DevCtx *__restrict__ c, cudaGraphConditionalHandle h,
+                                                        u32 count_iter) {
     pdl_entry();
     __shared__ u32 wsum[33];
     __shared__ unsigned long long wsum64[33];
@@ -366,6 +367,12 @@ __global__ void __launch_bounds__(1024) k_items_to_nodes(const DevCtx *__restric
         C.arena_used = bi.a1;
         C.fb_count = min(C.fb_count + nfb, c->fb_cap);
         C.nitems = 0;
+        // condition of the batch loop (a CUDA-graph WHILE node): another batch runs iff
+        // this one made new global nodes or left unfinished splits (and no error)
+        if (count_iter) C.iters += 1;
+        if (C.iters > 64u) atomicOr(c->err_flag, 16u);   // bound: depth <= 6 levels, a few rounds each
+        const bool more = !C.nan_flag && !C.err_flag && (bi.nb > 0 || C.nsplits[cur] > 0);
+        cudaGraphSetConditional(h, more && C.iters <= 64u ? 1u : 0u);
     }
 }
 
@@ -1279,18 +1286,6 @@ __global__ void k_k7_advance(const DevCtx *__restrict__ c) {
     pdl_entry();
     *c->k7_begin = *c->k7_count;
     *c->k7_next = 0;
-}
-
-// ------------------------------------------------------------------ end of a device-driven batch
-// Condition of the batch loop (a CUDA-graph WHILE node): another batch runs iff
-// the last one left new global nodes or unfinished splits (and no error).
-__global__ void k_batch_cond(const DevCtx *__restrict__ c, cudaGraphConditionalHandle h, u32 count_iter) {
-    pdl_entry();
-    Counters &C = *c->cnt;
-    const bool more = !C.nan_flag && !C.err_flag && (C.batch.nb > 0 || C.nsplits[C.round & 1u] > 0);
-    if (count_iter) C.iters += 1;
-    if (C.iters > 64u) atomicOr(c->err_flag, 16u);   // bound: depth <= 6 levels, a few rounds each
-    cudaGraphSetConditional(h, more && C.iters <= 64u ? 1u : 0u);
 }
 
 // ------------------------------------------------------------------ pass-log records of the global nodes

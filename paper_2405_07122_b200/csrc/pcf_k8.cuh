@@ -221,7 +221,10 @@ __device__ __forceinline__ u32 k8_seg_of(const u32 *__restrict__ pre, u32 nseg, 
     return lo;
 }
 
-__global__ void __launch_bounds__(1024) k8_plan(const DevCtx *__restrict__ c, cudaGraphConditionalHandle h) {
+// Also sets the conditions of the tail graph: hseg (any segment: check + block
+// sort), h (merge passes left: the pass loop) and hlog (pass log on: records).
+__global__ void __launch_bounds__(1024) k8_plan(const DevCtx *__restrict__ c, cudaGraphConditionalHandle hseg,
+                                                cudaGraphConditionalHandle h, cudaGraphConditionalHandle hlog) {
     pdl_entry();
     __shared__ u32 wsum[33];
     __shared__ u32 smax;
@@ -261,7 +264,9 @@ __global__ void __launch_bounds__(1024) k8_plan(const DevCtx *__restrict__ c, cu
         C.k8 = pl;
         C.k8_bytes = sbytes;
         C.fb_keys = skeys;
+        cudaGraphSetConditional(hseg, nseg > 0 ? 1u : 0u);
         cudaGraphSetConditional(h, smax > 0 ? 1u : 0u);
+        cudaGraphSetConditional(hlog, c->rec != nullptr && !C.nan_flag ? 1u : 0u);
     }
 }
 

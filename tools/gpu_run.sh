@@ -9,3 +9,6 @@ timeout 1800 python -m pytest tests -x -q -m gpu --durations=20 "$@" > gpurun_ou
 tail -30 gpurun_out/${TAG}_pytest.log
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
 tail -3 gpurun_out/${TAG}_bench.err
+for cfg in ${BENCH_EXTRA:-}; do
+  timeout 600 python bench.py --config $cfg --no-cpu-baseline > gpurun_out/${TAG}_bench_$cfg.json 2> gpurun_out/${TAG}_bench_$cfg.err; echo "bench $cfg rc=$?"
+done
