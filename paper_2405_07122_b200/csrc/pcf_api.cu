@@ -239,11 +239,14 @@ static int configure_kernels() {
 }
 
 // ---------------------------------------------------------------- launch helpers
-struct Launch {   // the kernel-launch configuration of this device
+struct Launch {   // the kernel-launch configuration of this device and sort size
     int nsm;
     int k7_grid;
     int count_grid;
     int tau_smem;
+    u32 tile_grid;    // one CTA per split tile of a round (upper bound; idle CTAs exit)
+    u32 k8_tiles;     // one CTA per block-sort tile of all fallback segments (upper bound)
+    u32 k8_mtiles;    // one CTA per merge tile (upper bound)
 };
 
 // ---------------------------------------------------------------- device-driven tail (CUDA graph)
@@ -266,6 +269,7 @@ struct TailGraph {
     int kt;   // key type * 2 + key-value mode
     const void *ctx;
     u32 tau;
+    u64 n;    // grid bounds depend on it
     cudaGraph_t g[2];
     cudaGraphExec_t ex[2];
     u32 body_kernels, parent_kernels[2], k8_body_kernels;
@@ -278,11 +282,11 @@ template <class K>
 static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32 *nk) {
     CK(launch_pdl(k_round_plan, 1, 1024, 0, cs, d_ctx));
     CK(launch_pdl(k_tile_map, lc.nsm * 2, 256, 0, cs, d_ctx));
-    CK(launch_pdl(k_split_count_tile<K>, lc.nsm * 8, SC_THREADS, 0, cs, d_ctx));
+    CK(launch_pdl(k_split_count_tile<K>, lc.tile_grid, SC_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_scanp_partials, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_scanp_final, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
-    CK(launch_pdl(k_split_scatter<K>, lc.nsm * 2 * 4, SC_THREADS, split_smem_bytes(), cs, d_ctx));
+    CK(launch_pdl(k_split_scatter<K>, lc.tile_grid, SC_THREADS, split_smem_bytes(), cs, d_ctx));
     CK(launch_pdl(k_split_taskgen, lc.nsm * 2, TG_THREADS, 0, cs, d_ctx));
     *nk += 8;
     return PCF_OK;
@@ -374,14 +378,14 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
         auto cap = [&]() -> int {
             CK(launch_pdl(k8_plan, 1, 1024, 0, cs, d_ctx, hs, hk, hl));
             int rc = add_cond(cs, hs, cudaGraphCondTypeIf, [&](cudaStream_t bs) -> int {
-                CK(launch_pdl(k8_check, lc.nsm * 8, 256, 0, bs, d_ctx));
-                CK(launch_pdl(k8_blocksort<K, PR>, lc.nsm * 3, K8_THREADS, K8_SORT_SMEM, bs, d_ctx));
+                CK(launch_pdl(k8_check, lc.k8_tiles, 256, 0, bs, d_ctx));
+                CK(launch_pdl(k8_blocksort<K, PR>, lc.k8_tiles, K8_THREADS, K8_SORT_SMEM, bs, d_ctx));
                 return PCF_OK;
             });
             if (rc) return rc;
             rc = add_cond(cs, hk, cudaGraphCondTypeWhile, [&](cudaStream_t bs) -> int {
-                CK(launch_pdl(k8_partition<K>, lc.nsm * 4, 256, 0, bs, d_ctx));
-                CK(launch_pdl(k8_merge<K, PR>, lc.nsm * 8, K8_MTHREADS, K8_MERGE_SMEM, bs, d_ctx));
+                CK(launch_pdl(k8_partition<K>, (lc.k8_mtiles + 255) / 256, 256, 0, bs, d_ctx));
+                CK(launch_pdl(k8_merge<K, PR>, lc.k8_mtiles, K8_MTHREADS, K8_MERGE_SMEM, bs, d_ctx));
                 CK(launch_pdl(k8_pass_end, 1, 1, 0, bs, d_ctx, hk));
                 tg.k8_body_kernels = 3;
                 return PCF_OK;
@@ -404,11 +408,11 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
 }
 
 template <class K, bool PR>
-static int get_tail(const DevCtx *d_ctx, u32 tau, const Launch &lc, TailGraph **out) {
+static int get_tail(const DevCtx *d_ctx, u32 tau, u64 n, const Launch &lc, TailGraph **out) {
     const int dev = cur_dev();
     const int kt = (K::is_f64 ? 0 : 2) + (PR ? 1 : 0);
     for (auto &t : g_tails)
-        if (t.dev == dev && t.kt == kt && t.ctx == d_ctx && t.tau == tau) { *out = &t; return PCF_OK; }
+        if (t.dev == dev && t.kt == kt && t.ctx == d_ctx && t.tau == tau && t.n == n) { *out = &t; return PCF_OK; }
     constexpr size_t MAX_TAILS = 8;
     if (g_tails.size() >= MAX_TAILS) {   // evict the oldest
         TailGraph &o = g_tails.front();
@@ -417,7 +421,7 @@ static int get_tail(const DevCtx *d_ctx, u32 tau, const Launch &lc, TailGraph **
     }
     TailGraph tg;
     memset(&tg, 0, sizeof tg);
-    tg.dev = dev; tg.kt = kt; tg.ctx = d_ctx; tg.tau = tau;
+    tg.dev = dev; tg.kt = kt; tg.ctx = d_ctx; tg.tau = tau; tg.n = n;
     const int rc = build_tail<K, PR>(tg, d_ctx, lc);
     if (rc) {
         for (int i = 0; i < 2; ++i) { if (tg.ex[i]) cudaGraphExecDestroy(tg.ex[i]); if (tg.g[i]) cudaGraphDestroy(tg.g[i]); }
@@ -585,6 +589,10 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     lc.k7_grid = nsm * k7_ctas_per_sm<K, PR>();
     lc.count_grid = nsm * count_ctas_per_sm<K>();
     lc.tau_smem = k7_smem_bytes(p.tau, PR);
+    // fallback segments hold > S_CAP keys each: <= n / S_CAP partial tiles
+    lc.tile_grid = (u32)std::min<u64>(n / SPLIT_TILE + 4096, 0x7fffffffull);
+    lc.k8_tiles = (u32)(n / K8_TILE + n / S_CAP + 2);
+    lc.k8_mtiles = (u32)(n / K8_MTILE + n / S_CAP + 2);
 
     // initial counters (host-built: the root node and its tables are carved here)
     Counters h0;
@@ -706,7 +714,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         tm.end();
         CK(cudaGetLastError());
         // ------------------------------------------------ everything after: device-driven (graphs)
-        rc = get_tail<K, PR>(d_ctx, p.tau, lc, &tail);
+        rc = get_tail<K, PR>(d_ctx, p.tau, n, lc, &tail);
         if (rc) return rc;
         tm.begin(PH_BATCHES);
         CK(cudaGraphLaunch(tail->ex[0], st));

@@ -48,6 +48,19 @@ constexpr int SPLIT_TILE = SC_WARPS * SC_PER_WARP;   // 5376 keys per split tile
 constexpr u64 GOLDEN = 0x9E3779B97F4A7C15ull;
 #define K7_PROF_SLOTS_DECL 24
 
+// ---------------------------------------------------------------- debug bounds checks
+// compute-sanitizer is not available on the GPU pool, so a debug build
+// (-DPCF_CHECKS=1, tools/checks.sh) asserts the shared- and global-memory index
+// bounds of the hot kernels: a violation sets err_flag bit 5 and the call returns
+// PCF_ERR_INTERNAL (the GPU parity suite run against that build must stay green).
+#ifndef PCF_CHECKS
+#define PCF_CHECKS 0
+#endif
+#define PCF_CHECK(ctx, cond)                                                              \
+    do {                                                                                  \
+        if (PCF_CHECKS && !(cond)) atomicOr((ctx)->err_flag, 32u);                        \
+    } while (0)
+
 // ---------------------------------------------------------------- key transforms
 // totalOrder on binary64 == unsigned order of the "flipped" bits: set the sign
 // bit of non-negative patterns, complement negative ones (R11).

@@ -630,6 +630,7 @@ __global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__
                 if (k < nt) {
                     const u32 d = ix[q];
                     dg[k] = (u16)d;
+                    PCF_CHECK(c, d < G);
                     atomicAdd(&S.hist[d], 1u);
                 }
             }
@@ -695,6 +696,7 @@ __global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_tile(const DevCtx
             const u32 k = r0 + q * 32;
             if (k < k1) {
                 const u32 d = (ix[q] - st.jlo) >> st.shift;
+                PCF_CHECK(c, ix[q] >= st.jlo && ix[q] < st.jhi && d < st.G);
                 dg[k] = (u16)d;
                 atomicAdd(&hist[d], 1u);
             }
@@ -1039,6 +1041,7 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
             const u32 d = pk[q] & 0xffffu;
             const u32 wo = (S.wc[w][d >> 1] >> ((d & 1u) * 16)) & 0xffffu;
             const u32 lp = S.tstart[d] + wo + (pk[q] >> 16);
+            PCF_CHECK(c, d < G && lp < ntile);
             S.buf[lp] = key[q];
             S.dsrc[lp] = d | ((w * SC_PER_WARP + q * 32 + lane) << 16);
         }
@@ -1062,6 +1065,7 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
             const u32 a = S.dsrc[i - 1];
             inv |= (a >> 21) == (b >> 21) && (a & 0xffffu) == (b & 0xffffu) && (a >> 16) > (b >> 16);
         }
+        PCF_CHECK(c, (b & 0xffffu) < G && S.goff[b & 0xffffu] + i < st.m);
         y[S.goff[b & 0xffffu] + i] = S.buf[i];
         if (idst) idst[S.goff[b & 0xffffu] + i] = src_index(b >> 16);
     }

@@ -450,8 +450,10 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
 #pragma unroll
         for (int q = 0; q < KPT; ++q) {
             const bool v = pk[q] != NONE;
+            PCF_CHECK(c, !v || (pk[q] >= 1u && pk[q] <= P + 1 && w0 * WCOLS + P + 1 < (u32)TCOLS));
             const u32 u = T16[v ? pk[q] : 1u];
             u32 old = 0;
+            PCF_CHECK(c, !v || (u >= 1u && u <= ncol));
             if (v) old = atomicAdd(&row32[u >> 1], (u & 1) ? 0x10000u : 1u);
             pk[q] = v ? u | ((((u & 1) ? old >> 16 : old) & 0xffffu) << 16) : NONE;
         }
@@ -468,6 +470,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         for (int q = 0; q < KPT; ++q) {
             const bool v = pk[q] != NONE;
             u32 j = 0;
+            PCF_CHECK(c, !v || (pk[q] >= 1u && pk[q] <= md.beta + 1));
             if (v) j = __ldg(gT + pk[q]);
             pk[q] = v ? j - jb : NONE;   // column 1 + (j - jlo)
         }
@@ -580,6 +583,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
             const u32 p = pos + (d & POS_MASK);
             u64 *dst = (d & DEST_A) ? S.A : (d & DEST_B) ? S.B : Y;
             if (valid) {
+                PCF_CHECK(c, p < pos + m && (d & POS_MASK) < m && u <= ncol);
                 dst[p] = key[q];
                 if (PR) ((d & DEST_A) ? S.IA : (d & DEST_B) ? S.IB : IY)[p] = idx_of(q);
                 S.LC[p] = (d & DEST_B) ? (u16)u : (u16)0;
@@ -608,6 +612,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         const u32 st = pos + ((u32)Wg[cc] & POS_MASK);
         const u64 v = S.B[pos + p];
         const u32 r = st + rank_in_leaf<PR>(S.B, st, hh, v, tie_of<PR>(S.IB, pos + p), S.IB);
+        PCF_CHECK(c, r >= st && r < st + hh && st + hh <= pos + m);
         S.A[r] = v;
         if (PR) S.IA[r] = S.IB[pos + p];
     }
