@@ -159,7 +159,7 @@ int pcf_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const pcf_params *
 
 /* ---- key-value mode (not in the paper, which sorts keys only,
  * PAPER.md:136-139).  Equal keys keep their input order: the result is THE stable
- * sorting permutation (reading R17), bit-identical to oracle stable_argsort.
+ * sorting permutation (reading R18), bit-identical to oracle stable_argsort.
  * The sort itself is unchanged (same buckets, same node records); every kernel that
  * moves keys also moves the key's source index: the stable split scatter (global
  * u32 indices), K7 (task-local u16 indices in shared memory, stable tie-break by

@@ -118,7 +118,7 @@ void orc_standard_sort(uint64_t *x, uint64_t m, int kt)
  * (Alg. 1 input/output); carrying a payload needs a rule for
  * equal keys, and the one permutation every stable sort produces is the plain
  * definition: perm[k] = the index of the k-th smallest key, equal keys in
- * increasing index order (reading R17 in DESIGN.md).  Plain top-down stable merge
+ * increasing index order (reading R18 in DESIGN.md).  Plain top-down stable merge
  * sort of the indices (ties keep the left run first). */
 static void argsort_rec(int kt, const uint64_t *x, uint64_t *p, uint64_t *tmp, uint64_t lo, uint64_t hi)
 {

@@ -379,6 +379,7 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
             CK(launch_pdl(k8_plan, 1, 1024, 0, cs, d_ctx, hs, hk, hl));
             int rc = add_cond(cs, hs, cudaGraphCondTypeIf, [&](cudaStream_t bs) -> int {
                 CK(launch_pdl(k8_check, lc.k8_tiles, 256, 0, bs, d_ctx));
+                CK(launch_pdl(k8_passes, 1, 1024, 0, bs, d_ctx, hk));
                 CK(launch_pdl(k8_blocksort<K, PR>, lc.k8_tiles, K8_THREADS, K8_SORT_SMEM, bs, d_ctx));
                 return PCF_OK;
             });
@@ -434,7 +435,7 @@ static int get_tail(const DevCtx *d_ctx, u32 tau, u64 n, const Launch &lc, TailG
 
 // ---------------------------------------------------------------- the sort
 // in, out: device keys; perm (key-value mode, PR): device u32[n] that receives the
-// stable sorting permutation (reading R17), NULL otherwise.
+// stable sorting permutation (reading R18), NULL otherwise.
 template <class K, bool PR = false>
 static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, cudaStream_t st, u32 *perm = nullptr) {
     pcf_params p;
@@ -749,7 +750,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         stats.fallback_keys_global = hcnt.fb_keys;
         if (tail) {
             launches += hcnt.iters * tail->body_kernels + hcnt.k8.max_merges * tail->k8_body_kernels
-                        + (hcnt.k8.nseg ? 2 : 0) + (logging ? 1 : 0);
+                        + (hcnt.k8.nseg ? 3 : 0) + (logging ? 1 : 0);
             stats.device_batches = hcnt.iters;
         }
         if (!small) {

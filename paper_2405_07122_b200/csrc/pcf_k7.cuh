@@ -203,7 +203,7 @@ __device__ __forceinline__ void write_record(const DevCtx *c, u32 level, u32 alp
 }
 
 // Key-value mode: the tie-break of equal keys is their task-local source index
-// (IA / IB), i.e. input order -- the stable permutation (reading R17).
+// (IA / IB), i.e. input order -- the stable permutation (reading R18).
 template <bool PR>
 __device__ __forceinline__ u32 tie_of(const u16 *I, u32 j) { return PR ? (u32)I[j] : j; }
 

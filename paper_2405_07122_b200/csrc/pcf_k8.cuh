@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(1024) k8_plan(const DevCtx *__restrict__ c, cu
         C.k8_bytes = sbytes;
         C.fb_keys = skeys;
         cudaGraphSetConditional(hseg, nseg > 0 ? 1u : 0u);
-        cudaGraphSetConditional(h, smax > 0 ? 1u : 0u);
+        (void)h;   // the pass loop's condition is set by k8_passes, after the all-equal check
         cudaGraphSetConditional(hlog, c->rec != nullptr && !C.nan_flag ? 1u : 0u);
     }
 }
@@ -284,6 +284,25 @@ __global__ void __launch_bounds__(256) k8_check(const DevCtx *__restrict__ c) {
         bool diff = false;
         for (u64 i = b0 + threadIdx.x; i < b1; i += blockDim.x) diff |= src[i] != first;
         if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(&c->k8_flag[s], 1u);
+    }
+}
+
+// Merge passes of the segments that hold two distinct keys (all-equal segments are
+// copied by the block sort and need none): sets the pass loop's condition.
+__global__ void __launch_bounds__(1024) k8_passes(const DevCtx *__restrict__ c, cudaGraphConditionalHandle h) {
+    pdl_entry();
+    __shared__ u32 smax;
+    Counters &C = *c->cnt;
+    if (threadIdx.x == 0) smax = 0;
+    __syncthreads();
+    u32 mx = 0;
+    for (u32 s = threadIdx.x; s < C.k8.nseg; s += blockDim.x)
+        if (c->k8_flag[s]) mx = max(mx, k8_merges(c->fb[s].m));
+    atomicMax(&smax, mx);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        C.k8.max_merges = smax;
+        cudaGraphSetConditional(h, smax > 0 && !C.err_flag ? 1u : 0u);
     }
 }
 

@@ -1,7 +1,7 @@
 """key-value / argsort mode.
 
 CPU (-m "not gpu"): the oracle's stable permutation (oracle.stable_argsort, the plain
-definition: reading R17) pinned against Python's stable `sorted` (a library routine)
+definition: reading R18) pinned against Python's stable `sorted` (a library routine)
 over every small array of an alphabet with duplicates, -0.0/+0.0 and infinities, and
 against numpy's stable argsort on random arrays; invariants.
 GPU (-m gpu): pcf_argsort_* / pcf_sort_pairs_* against the oracle, element by element.

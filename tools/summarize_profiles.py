@@ -1,5 +1,6 @@
-"""Summaries of a profile_round.sh pass for profiles/<round>/:
-python tools/summarize_profiles.py gpurun_out/prof profiles/r01
+"""Summaries of a profile_round.sh / profile_r02.sh pass for profiles/<round>/:
+python tools/summarize_profiles.py gpurun_out/prof profiles/r01 [c2]
+python tools/summarize_profiles.py gpurun_out/prof2 profiles/r02 c5f
  - launches_bench_c2.txt : per-kernel time share of one bench step (ncu launch list, cold, serialised)
  - <kernel>_<cfg>.txt    : key metrics of the ncu --set full capture + top source lines
  - traffic.json (repo profiles/): dram bytes per launch of the bench's dominant kernel (bench.py reads it)"""
@@ -12,11 +13,12 @@ import sys
 from collections import defaultdict
 
 src, dst = sys.argv[1], sys.argv[2]
+CFG = sys.argv[3] if len(sys.argv) > 3 else "c2"
 os.makedirs(dst, exist_ok=True)
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 # ---- launch list: one bench step = the kernels between two consecutive k_minmax launches
-rows = list(csv.reader(open(os.path.join(src, "launches_bench_c2.csv"))))
+rows = list(csv.reader(open(os.path.join(src, f"launches_bench_{CFG}.csv"))))
 hdr, out = None, []
 for r in rows:
     if r and r[0] == "ID":
@@ -38,9 +40,9 @@ for k, us in seg:
     agg[k][0] += 1
     agg[k][1] += us
 tot = sum(v[1] for v in agg.values())
-with open(os.path.join(dst, "launches_bench_c2.txt"), "w") as f:
-    f.write("# one c2 sort (10^7 lognormal f64) from `ncu --metrics gpu__time_duration.sum --clock-control none`\n")
-    f.write("# of `python bench.py --steps 2 --warmup 3`: cold-cache, serialised launches -> compare shares\n")
+with open(os.path.join(dst, f"launches_bench_{CFG}.txt"), "w") as f:
+    f.write(f"# one {CFG} sort from `ncu --metrics gpu__time_duration.sum --clock-control none`\n")
+    f.write("# of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline`: cold-cache, serialised launches -> compare shares\n")
     f.write(f"# {len(seg)} launches, {tot:.1f} us total\n")
     for k, (cnt, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         f.write(f"{us:10.1f} us {100 * us / tot:5.1f}%  x{cnt:<3d} {k}\n")
@@ -79,12 +81,16 @@ for fn in sorted(os.listdir(src)):
             f.write(f"{s:28s} {100 * c / tots:5.1f}%\n")
         f.write("\n# top source lines by stall samples (tools/ncu_lines.py)\n")
         f.write(lines)
-    if name == "k7_kernel_c2" and "dram__bytes_read.sum" in met:
+    if name.startswith("k7_kernel_") and "dram__bytes_read.sum" in met:
         def b(n):
             val, u = met[n]
             return float(val.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-        traffic["smem_subtree"] = b("dram__bytes_read.sum") + b("dram__bytes_write.sum")
+        traffic[name[len("k7_kernel_"):]] = {"smem_subtree": b("dram__bytes_read.sum") + b("dram__bytes_write.sum"),
+                                             "_from": f"{dst}/{name}.txt (one K7 launch = the sort's K7 work)"}
 if traffic:
-    with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
-        json.dump({**traffic, "_source": f"{dst}/k7_kernel_c2.txt (one K7 launch = the whole c2 sort's K7 work)"}, f, indent=1)
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    doc = json.load(open(path)) if os.path.exists(path) else {}
+    doc.update(traffic)
+    with open(path, "w") as f:
+        json.dump(doc, f, indent=1)
 print("wrote", dst)
