@@ -187,6 +187,45 @@ int pcf_sort_pairs_u64_u32(const uint64_t *keys_in, const uint32_t *vals_in, uin
 int pcf_sort_pairs_u64_u64(const uint64_t *keys_in, const uint64_t *vals_in, uint64_t *keys_out, uint64_t *vals_out,
                            size_t n, const pcf_params *p, void *stream);
 
+/* ---- sharded sort over R GPUs -------------------------
+ * One process per GPU; the caller (paper_2405_07122_b200/sharded.py) runs the
+ * collectives between the calls (NCCL all-reduce / all-gather / all-to-all over
+ * NVLink).  Rank r holds keys [offset, offset + n) of the global array of N keys.
+ * The result is Alg. 1 on the WHOLE array: the level-1 node's extremes, sample
+ * (the single-GPU positions over [0, N)), b, T and H are the single-GPU ones;
+ * bucket ranges of ~N/R keys go to ranks; rank r's output is the sorted slice of
+ * the global output starting at range[0], bit-identical to the single-GPU sort, and
+ * every node record is the single-GPU one (the level-1 record on rank 0 only).
+ * Sequence (device pointers; `state` of pcf_shard_state_bytes(N, R) bytes):
+ *   pcf_shard_minmax     -> all-reduce state mm[0] MIN, mm[1] MAX, mm[2] MAX (int64)
+ *   pcf_shard_counts     -> all-reduce SUM of the counts (uint32[beta + 2])
+ *   pcf_shard_histogram  -> all-gather of the local histogram into Hall (R rows)
+ *   pcf_shard_partition  -> keys_out = local keys grouped by destination rank (stable);
+ *                           send / recv counts (host) for the all-to-all; range (host):
+ *                           {global offset, size, J_lo, J_hi} of this rank's buckets
+ *   all-to-all (keys, in source-rank order)
+ *   pcf_shard_sort_range -> out = the sorted range (workspace pcf_shard_workspace_bytes)
+ * pcf_shard_views returns the device pointers the collectives act on. */
+typedef struct pcf_shard {
+    uint64_t N;        /* keys over all ranks, 2 <= N < 2^32                     */
+    uint64_t offset;   /* global index of this rank's first key                  */
+    uint32_t R, rank;  /* 1 <= R <= 64                                            */
+    void *state;       /* DEVICE, pcf_shard_state_bytes(N, R) bytes, 256-aligned  */
+    size_t state_bytes;
+} pcf_shard;
+size_t pcf_shard_state_bytes(uint64_t N, uint32_t R);
+size_t pcf_shard_workspace_bytes(size_t m, uint64_t N);
+/* views[0]: int64 mm[4]; [1]: uint32 counts[beta + 2]; [2]: uint32 Hloc[gamma + 2];
+ * [3]: uint32 Hall[R][gamma + 2]; sizes[i]: element counts */
+int pcf_shard_views(const pcf_shard *sh, void **views, uint64_t *sizes);
+int pcf_shard_minmax(const void *keys, size_t n, int key_type, const pcf_shard *sh, void *stream);
+int pcf_shard_counts(const void *keys, size_t n, int key_type, const pcf_shard *sh, const pcf_params *p, void *stream);
+int pcf_shard_histogram(const void *keys, size_t n, int key_type, const pcf_shard *sh, const pcf_params *p, void *stream);
+int pcf_shard_partition(const void *keys, size_t n, int key_type, const pcf_shard *sh, void *keys_out,
+                        uint64_t *send_counts, uint64_t *recv_counts, uint64_t *range, void *stream);
+int pcf_shard_sort_range(const void *keys, void *out, size_t m, int key_type, const pcf_shard *sh,
+                         const uint64_t *range, const pcf_params *p, void *stream);
+
 /* End-to-end entry: HOST pointers (pinned memory recommended).  Copies the n
  * keys to the device, sorts them with pcf_sort_* (asynchronously), copies the
  * result back and synchronises `stream` once; returns the sort's status

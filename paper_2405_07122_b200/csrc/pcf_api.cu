@@ -22,6 +22,7 @@
 #include "pcf_k7.cuh"
 #include "pcf_k8.cuh"
 #include "pcf_bucketing.cuh"
+#include "pcf_shard.cuh"
 
 namespace pcf {
 
@@ -57,10 +58,12 @@ struct Caps {
 
 constexpr u32 BND_MIN_LOG2 = 24;   // nodes of >= 2^24 keys get the gather-free digit table
 
-static Caps caps_for(u64 n) {
+// root_n: size of the level-1 node (n itself; N for a shard of a sharded sort, whose
+// root tables are the global node's)
+static Caps caps_for(u64 n, u64 root_n = 0) {
     Caps c;
     c.n = n;
-    c.P = (u32)iroot34(n);
+    c.P = (u32)iroot34(root_n > n ? root_n : n);
     // global nodes hold > S_CAP keys; nodes of one level are disjoint, and a global
     // node nests in another only if the parent has > S_CAP^{4/3} keys: 2 n / S_CAP bounds them
     c.node_cap = (u32)(2 * (n / S_CAP) + 64);
@@ -83,7 +86,7 @@ struct Layout {
         k8_tb, k8_mb, k8_flag, cmat, pmat, bsum, status, total;
 };
 
-static Layout layout_for(const Caps &c, bool pr = false) {
+static Layout layout_for(const Caps &c, bool pr = false) {   // (caps_for(n, root_n))
     Layout L;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
@@ -386,7 +389,7 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
             if (rc) return rc;
             rc = add_cond(cs, hk, cudaGraphCondTypeWhile, [&](cudaStream_t bs) -> int {
                 CK(launch_pdl(k8_partition<K>, (lc.k8_mtiles + 255) / 256, 256, 0, bs, d_ctx));
-                CK(launch_pdl(k8_merge<K, PR>, lc.k8_mtiles, K8_MTHREADS, K8_MERGE_SMEM, bs, d_ctx));
+                CK(launch_pdl(k8_merge<K, PR>, lc.nsm * 8, K8_MTHREADS, K8_MERGE_SMEM, bs, d_ctx));
                 CK(launch_pdl(k8_pass_end, 1, 1, 0, bs, d_ctx, hk));
                 tg.k8_body_kernels = 3;
                 return PCF_OK;
@@ -434,10 +437,36 @@ static int get_tail(const DevCtx *d_ctx, u32 tau, u64 n, const Launch &lc, TailG
 }
 
 // ---------------------------------------------------------------- the sort
+// A shard of a sharded sort (pcf_shard.cuh): the keys are buckets [jlo, jhi) of the
+// global level-1 node of N keys, at global offset range_off.
+struct ShardRoot {
+    u64 N, range_off;
+    u32 jlo, jhi;
+    u32 record;              // write the global level-1 record (and level-1 dumps) here
+    const ShardState *S;     // all-reduced extremes
+    const u32 *cnt;          // all-reduced per-bin sample counts [beta + 2]
+    const u32 *Hg;           // global bucket sizes [gamma + 2]
+};
+
+// Model and R9/R10 verdict of the shard's root (the global level-1 node); a
+// degenerate range sends the whole shard range to Standard-Sort.
+template <class K>
+__global__ void k_shard_root(const DevCtx *__restrict__ c, const ShardState *__restrict__ S, u64 m) {
+    GNode &g = c->nodes[0];
+    g.kmin = i64_to_okey(S->mm[0]);
+    g.kmax = i64_to_okey(S->mm[1]);
+    Model md;
+    const bool ok = make_model<K>(g.kmin, g.kmax, g.beta, md);
+    g.md = md;
+    g.degenerate = ok ? 0u : 1u;
+    if (!ok) push_item(c, 0, (u32)m, 1, 0, 1u);
+}
+
 // in, out: device keys; perm (key-value mode, PR): device u32[n] that receives the
 // stable sorting permutation (reading R18), NULL otherwise.
 template <class K, bool PR = false>
-static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, cudaStream_t st, u32 *perm = nullptr) {
+static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, cudaStream_t st, u32 *perm = nullptr,
+                       const ShardRoot *shard = nullptr) {
     pcf_params p;
     pcf_params_init(&p);
     if (pp) {
@@ -480,7 +509,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         cudaEventRecord(ev_total0, st);
     }
 
-    const size_t need = workspace_bytes_impl(n, PR);
+    const size_t need = shard ? layout_for(caps_for(n, shard->N), PR).total : workspace_bytes_impl(n, PR);
     char *ws = (char *)p.workspace;
     bool own = false;
     if (ws) {
@@ -504,18 +533,23 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     hc.seed = p.seed;
     hc.tau = p.tau;
     hc.flags = p.flags;
+    if (shard) {
+        hc.gbase = shard->range_off;
+        hc.root_external = shard->record ? 2u : 1u;
+    }
     if (logging) {
         hc.rec = reinterpret_cast<NodeRec *>(p.log->records);
         hc.rec_cap = p.log->records ? p.log->capacity : 0;
         hc.l1_b = p.log->level1_b;
         hc.l1_h = p.log->level1_h;
         hc.l1_cap = p.log->level1_capacity;
+        if (shard && !shard->record) { hc.l1_b = nullptr; hc.l1_h = nullptr; }
         hc.rec_count = reinterpret_cast<unsigned long long *>(p.log->count);
         if (!hc.rec) hc.rec = reinterpret_cast<NodeRec *>(1);   // non-null marks logging on; cap 0
         CK(cudaMemsetAsync(p.log->count, 0, 8, st));
     }
 
-    const bool small = n <= (size_t)S_CAP;
+    const bool small = n <= (size_t)S_CAP && !shard;
     DevCtx *d_ctx;
     Counters *d_cnt;
     int *d_status;
@@ -532,7 +566,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.k7_cap = 1;
         hc.buf[1] = nullptr;
     } else {
-        caps = caps_for(n);
+        caps = caps_for(n, shard ? shard->N : 0);
         L = layout_for(caps, PR);
         d_ctx = (DevCtx *)(ws + L.ctx);
         d_cnt = (Counters *)(ws + L.counters);
@@ -617,20 +651,23 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         bytes[PH_K7] += 16ull * n;
     } else {
         // ------------------------------------------------ level 1 (host-launched, exact grids)
-        const u32 P = (u32)iroot34(n);
+        const u64 rootn = shard ? shard->N : n;
+        const u32 P = (u32)iroot34(rootn);
         GNode g;
         memset(&g, 0, sizeof g);
-        g.off = 0; g.m = (u32)n; g.level = 1;
+        g.off = shard ? (u64)0 - shard->range_off : 0;   // the record's offset is gbase + off = 0
+        g.m = (u32)rootn; g.level = 1;
         g.kmin = ~0ull; g.kmax = 0;
-        g.alpha = sample_all ? (u32)n : P; g.beta = P; g.gamma = P; g.delta = P;
+        g.alpha = sample_all ? (u32)rootn : P; g.beta = P; g.gamma = P; g.delta = P;
         g.src = 0;
         u64 arena_used = 3ull * ((u64)P + 2);
         u32 *arena = hc.arena;
         g.cnt = arena;
         g.T = g.cnt + (P + 2);
         g.H = g.T + (P + 2);
-        const u32 sh0 = choose_shift(P + 1, (u32)n);
-        if (n >= (1ull << BND_MIN_LOG2)) {   // digit boundaries: gather-free digits in the first count pass
+        const u32 jlo0 = shard ? shard->jlo : 1u, jhi0 = shard ? shard->jhi : P + 2;
+        const u32 sh0 = choose_shift(jhi0 - jlo0, (u32)n);
+        if (!shard && n >= (1ull << BND_MIN_LOG2)) {   // digit boundaries: gather-free digits in the first count pass
             g.bnd = arena + arena_used;
             arena_used += GMAX;
             g.bshift = sh0;
@@ -638,9 +675,9 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         }
         SplitTask s0;
         memset(&s0, 0, sizeof s0);
-        s0.off = 0; s0.m = (u32)n; s0.node = 0; s0.jlo = 1; s0.jhi = P + 2;
+        s0.off = 0; s0.m = (u32)n; s0.node = 0; s0.jlo = jlo0; s0.jhi = jhi0;
         s0.shift = sh0;
-        s0.G = (P + 1 + (1u << sh0) - 1) >> sh0;
+        s0.G = (jhi0 - jlo0 + (1u << sh0) - 1) >> sh0;
         s0.src = 0; s0.dst = 1;
         h0.node_count = 1;
         h0.arena_used = arena_used;
@@ -652,6 +689,14 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         CK(cudaMemcpyAsync(hc.splits[0], &s0, sizeof s0, cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(g.cnt, 0, 3ull * ((u64)P + 2) * 4, st));
         const DevCtx *dc = d_ctx;
+        if (shard) {   // the global node: all-reduced counts and histogram, model from the all-reduced extremes
+            CK(cudaMemcpyAsync(g.cnt, shard->cnt, ((u64)P + 2) * 4, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(g.H, shard->Hg, ((u64)P + 2) * 4, cudaMemcpyDeviceToDevice, st));
+            k_shard_root<K><<<1, 1, 0, st>>>(d_ctx, shard->S, (u64)n);
+            CK(cudaGetLastError());
+            launches++;
+        }
+        if (!shard) {
         tm.begin(PH_MINMAX);
         {
             const u64 nvec = n / 2 + 1;
@@ -659,9 +704,10 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             CK(launch_pdl(k_minmax<K>, grid, MM_THREADS, 0, st, dc, 0u));
         }
         tm.end();
+        }
         tm.begin(PH_FIT);
         {
-            CK(launch_pdl(k_fit_sample<K>, (g.alpha + 255) / 256, 256, 0, st, dc, 0u));
+            if (!shard) CK(launch_pdl(k_fit_sample<K>, (g.alpha + 255) / 256, 256, 0, st, dc, 0u));
             const u64 nbins = (u64)P + 1;
             const u32 nblk = (u32)((nbins + SCAN_CHUNK - 1) / SCAN_CHUNK);
             u32 *bs = hc.bsum;
@@ -672,8 +718,8 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         tm.end();
         CK(cudaGetLastError());
         launches += 5;
-        bytes[PH_MINMAX] += 8ull * n;
-        bytes[PH_FIT] += 8ull * g.alpha + 8ull * (P + 2);
+        if (!shard) bytes[PH_MINMAX] += 8ull * n;
+        bytes[PH_FIT] += shard ? 8ull * (P + 2) : 8ull * g.alpha + 8ull * (P + 2);
         // two split rounds with grids sized from n (an upper bound on each round's tiles)
         u64 splits_bound = 1;
         for (int r = 0; r < 2; ++r) {
@@ -911,6 +957,150 @@ static int sort_pairs(const u64 *kin, const V *vin, u64 *kout, V *vout, size_t n
     return rc;
 }
 
+// ---------------------------------------------------------------- sharded sort (pcf_shard.cuh)
+struct ShardLayout {
+    size_t S, cnt, T, Hloc, Hall, Hg, C, Pm, bsum, total;
+    u32 P, ntmax;
+};
+static ShardLayout shard_layout(u64 N, u32 R) {
+    ShardLayout L;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    L.P = (u32)iroot34(N);
+    const u64 nb = (u64)L.P + 2;
+    L.ntmax = (u32)(N / SH_TILE + 1);
+    L.S = take(sizeof(ShardState));
+    L.cnt = take(nb * 4);
+    L.T = take(nb * 4);
+    L.Hloc = take(nb * 4);
+    L.Hall = take(nb * 4 * R);
+    L.Hg = take(nb * 4);
+    L.C = take((u64)R * L.ntmax * 4);
+    L.Pm = take((u64)R * L.ntmax * 4);
+    L.bsum = take(((u64)R * L.ntmax / SCAN_CHUNK + 2) * 4);
+    L.total = off;
+    return L;
+}
+
+static int shard_check(const pcf_shard *sh) {
+    if (!sh || !sh->state) return fail(PCF_ERR_INVALID_ARG, "NULL shard descriptor / state");
+    if (sh->R < 1 || sh->R > SHARD_RMAX || sh->rank >= sh->R) return fail(PCF_ERR_INVALID_ARG, "R must be in [1, 64], rank < R");
+    if (sh->N < 2 || sh->N >= (1ull << 32)) return fail(PCF_ERR_INVALID_ARG, "N must be in [2, 2^32)");
+    if (((uintptr_t)sh->state & 255) || sh->state_bytes < shard_layout(sh->N, sh->R).total)
+        return fail(PCF_ERR_WORKSPACE_TOO_SMALL, "shard state smaller than pcf_shard_state_bytes() or misaligned");
+    return PCF_OK;
+}
+
+template <class K>
+static int shard_minmax(const u64 *x, size_t n, const pcf_shard *sh, cudaStream_t st) {
+    int rc = shard_check(sh);
+    if (rc) return rc;
+    ShardState *S = (ShardState *)((char *)sh->state + shard_layout(sh->N, sh->R).S);
+    long long init[4] = {0x7fffffffffffffffll, (long long)0x8000000000000000ull, 0, 0};
+    CK(cudaMemcpyAsync(S->mm, init, sizeof init, cudaMemcpyHostToDevice, st));
+    if (n) {
+        k_shard_minmax<K><<<(u32)std::min<u64>((n + 255) / 256, 148ull * 8), 256, 0, st>>>(x, n, S);
+        CK(cudaGetLastError());
+    }
+    return PCF_OK;
+}
+
+template <class K>
+static int shard_counts(const u64 *x, size_t n, const pcf_shard *sh, const pcf_params *pp, cudaStream_t st) {
+    int rc = shard_check(sh);
+    if (rc) return rc;
+    pcf_params p;
+    pcf_params_init(&p);
+    if (pp) memcpy(&p, pp, std::min<size_t>(pp->struct_size, sizeof(pcf_params)));
+    const ShardLayout L = shard_layout(sh->N, sh->R);
+    char *b = (char *)sh->state;
+    u32 *cnt = (u32 *)(b + L.cnt);
+    CK(cudaMemsetAsync(cnt, 0, ((u64)L.P + 2) * 4, st));
+    const u32 alpha = (p.flags & PCF_FLAG_SAMPLE_ALL) ? (u32)sh->N : L.P;
+    k_shard_counts<K><<<(alpha + 255) / 256, 256, 0, st>>>(x, n, sh->offset, sh->N, alpha, L.P, p.seed, p.flags,
+                                                            (const ShardState *)(b + L.S), cnt);
+    CK(cudaGetLastError());
+    return PCF_OK;
+}
+
+template <class K>
+static int shard_histogram(const u64 *x, size_t n, const pcf_shard *sh, const pcf_params *pp, cudaStream_t st) {
+    int rc = shard_check(sh);
+    if (rc) return rc;
+    pcf_params p;
+    pcf_params_init(&p);
+    if (pp) memcpy(&p, pp, std::min<size_t>(pp->struct_size, sizeof(pcf_params)));
+    const ShardLayout L = shard_layout(sh->N, sh->R);
+    char *b = (char *)sh->state;
+    const u32 alpha = (p.flags & PCF_FLAG_SAMPLE_ALL) ? (u32)sh->N : L.P;
+    u32 *T = (u32 *)(b + L.T), *H = (u32 *)(b + L.Hloc);
+    ShardState *S = (ShardState *)(b + L.S);
+    k_shard_table<<<1, 1024, 0, st>>>((const u32 *)(b + L.cnt), L.P, alpha, L.P, T);
+    CK(cudaMemsetAsync(H, 0, ((u64)L.P + 2) * 4, st));
+    // a degenerate global range (R9/R10) puts every key in bucket 1: the plan then
+    // gives the whole array to rank 0, which Standard-Sorts it
+    k_shard_deg_hist<K><<<1, 1, 0, st>>>(S, L.P, (u64)n, H);
+    if (n) k_shard_hist<K><<<(u32)std::min<u64>((n + 255) / 256, 148ull * 8), 256, 0, st>>>(x, n, L.P, S, T, H);
+    CK(cudaGetLastError());
+    return PCF_OK;
+}
+
+template <class K>
+static int shard_partition(const u64 *x, size_t n, const pcf_shard *sh, u64 *y, uint64_t *send_h, uint64_t *recv_h,
+                           uint64_t *range_h, cudaStream_t st) {
+    int rc = shard_check(sh);
+    if (rc) return rc;
+    const ShardLayout L = shard_layout(sh->N, sh->R);
+    char *b = (char *)sh->state;
+    ShardState *S = (ShardState *)(b + L.S);
+    const u32 R = sh->R;
+    k_shard_plan<<<1, 1024, 0, st>>>((const u32 *)(b + L.Hall), R, sh->rank, L.P, sh->N, (u32 *)(b + L.Hg), S);
+    CK(cudaGetLastError());
+    if (n) {
+        const u32 nt = (u32)((n + SH_TILE - 1) / SH_TILE);
+        if (nt > L.ntmax) return fail(PCF_ERR_INVALID_ARG, "shard larger than N");
+        u32 *C = (u32 *)(b + L.C), *Pm = (u32 *)(b + L.Pm), *bs = (u32 *)(b + L.bsum);
+        const u32 *T = (const u32 *)(b + L.T);
+        k_shard_dcount<K><<<nt, SH_WARPS * 32, 0, st>>>(x, n, L.P, R, S, T, C, nt);
+        const u64 tot = (u64)R * nt;
+        const u32 nblk = (u32)((tot + SCAN_CHUNK - 1) / SCAN_CHUNK);
+        k_scan_partials<<<nblk, SCAN_THREADS, 0, st>>>(C, tot, bs);
+        k_scan_bsums<<<1, SCAN_THREADS, 0, st>>>(bs, nblk);
+        k_scan_final<<<nblk, SCAN_THREADS, 0, st>>>(C, tot, bs, Pm);
+        k_shard_dscatter<K><<<nt, SH_WARPS * 32, 0, st>>>(x, n, L.P, R, S, T, Pm, nt, y);
+        CK(cudaGetLastError());
+    }
+    ShardState hs;
+    CK(cudaMemcpyAsync(&hs, S, sizeof hs, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));   // the exchange needs the split sizes on the host (all-to-all)
+    for (u32 r = 0; r < R; ++r) { if (send_h) send_h[r] = hs.send[r]; if (recv_h) recv_h[r] = hs.recv[r]; }
+    if (range_h) { range_h[0] = hs.range_off; range_h[1] = hs.range_m; range_h[2] = hs.J[sh->rank]; range_h[3] = hs.J[sh->rank + 1]; }
+    if (hs.mm[2]) return fail(PCF_ERR_NAN, "input contains NaN");
+    return PCF_OK;
+}
+
+template <class K>
+static int shard_sort_range(const u64 *in, u64 *out, size_t m, const pcf_shard *sh, const uint64_t *range_h,
+                            const pcf_params *p, cudaStream_t st) {
+    int rc = shard_check(sh);
+    if (rc) return rc;
+    if (!range_h) return fail(PCF_ERR_INVALID_ARG, "NULL range");
+    if (range_h[1] != m) return fail(PCF_ERR_INVALID_ARG, "m differs from the planned range size");
+    const ShardLayout L = shard_layout(sh->N, sh->R);
+    char *b = (char *)sh->state;
+    ShardRoot sr;
+    sr.N = sh->N; sr.range_off = range_h[0];
+    sr.jlo = (u32)range_h[2]; sr.jhi = (u32)range_h[3];
+    sr.record = sh->rank == 0;
+    sr.S = (const ShardState *)(b + L.S);
+    sr.cnt = (const u32 *)(b + L.cnt);
+    sr.Hg = (const u32 *)(b + L.Hg);
+    if (m == 0) {   // nothing to sort here; the level-1 record still belongs to rank 0
+        if (!sr.record || !p || !p->log) return PCF_OK;
+    }
+    return sort_device<K, false>(in, out, m, p, st, nullptr, &sr);
+}
+
 // §4.3 experiment: one M_PCF step with decoupled alpha, beta, gamma (pcf_bucketing.cuh)
 static int bucket_counts_f64(const u64 *x, size_t n, u64 alpha, u64 beta, u64 gamma, u64 seed, u32 *b, u32 *H,
                              uint64_t *max_bucket, cudaStream_t st) {
@@ -1062,6 +1252,67 @@ int pcf_bucket_counts_f64(const double *keys, size_t n, uint64_t alpha, uint64_t
 size_t pcf_level1_entries(size_t n, const pcf_params *p) {
     (void)p;
     return n ? (size_t)pcf::iroot34(n) + 2 : 2;
+}
+
+size_t pcf_shard_state_bytes(uint64_t N, uint32_t R) { return pcf::shard_layout(N, R ? R : 1).total; }
+
+size_t pcf_shard_workspace_bytes(size_t m, uint64_t N) {
+    return pcf::layout_for(pcf::caps_for(m ? m : 1, N), false).total;
+}
+
+int pcf_shard_views(const pcf_shard *sh, void **views, uint64_t *sizes) {
+    int rc = pcf::shard_check(sh);
+    if (rc) return rc;
+    const pcf::ShardLayout L = pcf::shard_layout(sh->N, sh->R);
+    char *b = (char *)sh->state;
+    const uint64_t nb = (uint64_t)L.P + 2;
+    views[0] = b + L.S;   // mm is the first member of ShardState
+    views[1] = b + L.cnt;
+    views[2] = b + L.Hloc;
+    views[3] = b + L.Hall;
+    sizes[0] = 4; sizes[1] = nb; sizes[2] = nb; sizes[3] = nb * sh->R;
+    return PCF_OK;
+}
+
+#define PCF_SHARD_DISPATCH(call_f64, call_u64)                                                     \
+    do {                                                                                           \
+        if (key_type == PCF_KEY_F64) return call_f64;                                              \
+        if (key_type == PCF_KEY_U64) return call_u64;                                              \
+        return pcf::fail(PCF_ERR_INVALID_ARG, "key_type must be PCF_KEY_F64 or PCF_KEY_U64");      \
+    } while (0)
+
+int pcf_shard_minmax(const void *keys, size_t n, int key_type, const pcf_shard *sh, void *stream) {
+    const pcf::u64 *k = (const pcf::u64 *)keys;
+    PCF_SHARD_DISPATCH(pcf::shard_minmax<pcf::KeyF64>(k, n, sh, (cudaStream_t)stream),
+                       pcf::shard_minmax<pcf::KeyU64>(k, n, sh, (cudaStream_t)stream));
+}
+
+int pcf_shard_counts(const void *keys, size_t n, int key_type, const pcf_shard *sh, const pcf_params *p, void *stream) {
+    const pcf::u64 *k = (const pcf::u64 *)keys;
+    PCF_SHARD_DISPATCH(pcf::shard_counts<pcf::KeyF64>(k, n, sh, p, (cudaStream_t)stream),
+                       pcf::shard_counts<pcf::KeyU64>(k, n, sh, p, (cudaStream_t)stream));
+}
+
+int pcf_shard_histogram(const void *keys, size_t n, int key_type, const pcf_shard *sh, const pcf_params *p, void *stream) {
+    const pcf::u64 *k = (const pcf::u64 *)keys;
+    PCF_SHARD_DISPATCH(pcf::shard_histogram<pcf::KeyF64>(k, n, sh, p, (cudaStream_t)stream),
+                       pcf::shard_histogram<pcf::KeyU64>(k, n, sh, p, (cudaStream_t)stream));
+}
+
+int pcf_shard_partition(const void *keys, size_t n, int key_type, const pcf_shard *sh, void *keys_out,
+                        uint64_t *send_counts, uint64_t *recv_counts, uint64_t *range, void *stream) {
+    const pcf::u64 *k = (const pcf::u64 *)keys;
+    pcf::u64 *y = (pcf::u64 *)keys_out;
+    PCF_SHARD_DISPATCH(pcf::shard_partition<pcf::KeyF64>(k, n, sh, y, send_counts, recv_counts, range, (cudaStream_t)stream),
+                       pcf::shard_partition<pcf::KeyU64>(k, n, sh, y, send_counts, recv_counts, range, (cudaStream_t)stream));
+}
+
+int pcf_shard_sort_range(const void *keys, void *out, size_t m, int key_type, const pcf_shard *sh,
+                         const uint64_t *range, const pcf_params *p, void *stream) {
+    const pcf::u64 *k = (const pcf::u64 *)keys;
+    pcf::u64 *y = (pcf::u64 *)out;
+    PCF_SHARD_DISPATCH(pcf::shard_sort_range<pcf::KeyF64>(k, y, m, sh, range, p, (cudaStream_t)stream),
+                       pcf::shard_sort_range<pcf::KeyU64>(k, y, m, sh, range, p, (cudaStream_t)stream));
 }
 
 const char *pcf_last_error(void) { return pcf::g_last_error.c_str(); }

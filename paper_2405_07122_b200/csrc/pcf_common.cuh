@@ -320,9 +320,13 @@ struct DevCtx {
                             // key of buf[i] (ibuf[0] == NULL: identity), or all NULL (keys only)
     Counters *cnt;          // device counters of this call
     u64 n;
+    u64 gbase;              // global position of buffer position 0 (a shard of a sharded sort; else 0):
+                            // sampler keys (R4) and node records use gbase + offset
     u64 seed;
     u32 tau;
     u32 flags;
+    u32 root_external;      // sharded sort: node 0 is the global level-1 node, fitted across
+                            // ranks; its record is written only where root_external == 2
     GNode *nodes;
     // K7 queue
     K7Task *k7;

@@ -169,7 +169,7 @@ __global__ void k_fit_sample(const DevCtx *__restrict__ c, u32 node) {
     const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= g.alpha) return;
     const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
-    const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, g.off), k, g.m);
+    const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, c->gbase + g.off), k, g.m);
     const u64 raw = c->buf[g.src][g.off + pos];
     atomicAdd(&g.cnt[interval_index<K>(K::to_okey(raw), md)], 1u);
 }
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(FSB_CHUNK) k_fit_sample_batch(const DevCtx *__
         if (!ok) continue;
         const u32 k = cb * FSB_CHUNK + threadIdx.x;
         if (k >= g.alpha) continue;
-        const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, g.off), k, g.m);
+        const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, c->gbase + g.off), k, g.m);
         atomicAdd(&g.cnt[interval_index<K>(K::to_okey(c->buf[g.src][g.off + pos]), md)], 1u);
     }
 }
@@ -1305,6 +1305,7 @@ __global__ void __launch_bounds__(256) k_log_finalize(const DevCtx *__restrict__
     for (u32 node = blockIdx.x; node < nn; node += gridDim.x) {
         const GNode &g = c->nodes[node];
         if (g.degenerate) continue;   // uniform per CTA: Standard-Sort, no bucketing record (R9/R10)
+        if (node == 0 && c->root_external == 1) continue;   // sharded: another rank records the root
         u64 dh = 0;
         u32 nf = 0, ns = 0, nr = 0;
         const bool copy_l1 = g.level == 1 && c->l1_h != nullptr;
@@ -1328,7 +1329,7 @@ __global__ void __launch_bounds__(256) k_log_finalize(const DevCtx *__restrict__
             const unsigned long long slot = atomicAdd(c->rec_count, 1ull);
             if (slot < c->rec_cap) {
                 NodeRec r;
-                r.level = g.level; r.alpha = g.alpha; r.offset = g.off; r.m = g.m;
+                r.level = g.level; r.alpha = g.alpha; r.offset = c->gbase + g.off; r.m = g.m;
                 r.xmin_bits = K::from_okey(g.kmin); r.xmax_bits = K::from_okey(g.kmax);
                 r.digest_b = g.digest_b; r.digest_h = dh;
                 r.n_fallback = nf; r.n_small = ns; r.n_recurse = nr; r.reserved = 0;

@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 }
                 __syncthreads();
                 Lb = S.glevel;
-                node_step<K, K7_WARPS, MODE_GLOBAL, PR>(c, S, CT, 0, M, Lb, 0, task.off, raw_group ? S.B + S.lhead : nullptr);
+                node_step<K, K7_WARPS, MODE_GLOBAL, PR>(c, S, CT, 0, M, Lb, 0, c->gbase + task.off, raw_group ? S.B + S.lhead : nullptr);
                 prof_mark(c, S, 2);
             } else {   // K7_NODE: a fresh Learned-Sort call on the whole task
                 Lb = task.level;
@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 if (ent_m(e) > (u32)(2 * GCAP)) {
                     __syncthreads();
                     if (threadIdx.x == 0) S.lbig[i] = 0;
-                    node_step<K, K7_WARPS, MODE_NODE, PR>(c, S, CT, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                    node_step<K, K7_WARPS, MODE_NODE, PR>(c, S, CT, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), c->gbase + task.off);
                 }
             }
             // double teams (2 x GW warps) take the nodes of (GCAP, 2 GCAP] keys
@@ -872,7 +872,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 const u32 e = S.cur[GH.w0];
                 if (!e) break;
                 const long long t0 = wprof ? clock64() : 0;
-                node_step<K, 2 * GW, MODE_NODE, PR>(c, S, GH, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                node_step<K, 2 * GW, MODE_NODE, PR>(c, S, GH, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), c->gbase + task.off);
                 if (wprof) wcyc[0] += clock64() - t0;
             }
             prof_mark(c, S, 4);
@@ -894,7 +894,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 const u32 e = S.cur[GG.w0];
                 if (!e) break;
                 const long long t0 = wprof ? clock64() : 0;
-                node_step<K, GW, MODE_NODE, PR>(c, S, GG, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                node_step<K, GW, MODE_NODE, PR>(c, S, GG, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), c->gbase + task.off);
                 if (wprof) wcyc[1] += clock64() - t0;
             }
             if (GG.t == 0) { __threadfence_block(); atomicSub(&S.big_active, 1u); }
@@ -928,7 +928,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS == 512 ? 1 : 2) k7_kern
                 const long long t0 = wprof ? clock64() : 0;
                 if (wprof) wcyc[3] += t0 - tw;
                 if (!e) break;
-                node_step<K, 1, MODE_NODE, PR>(c, S, GS, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), task.off);
+                node_step<K, 1, MODE_NODE, PR>(c, S, GS, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), c->gbase + task.off);
                 if (wprof) wcyc[2] += clock64() - t0;
             }
             __syncthreads();

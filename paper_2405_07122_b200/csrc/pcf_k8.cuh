@@ -386,13 +386,34 @@ __global__ void __launch_bounds__(K8_MTHREADS) k8_merge(const DevCtx *__restrict
     u32 *sai = reinterpret_cast<u32 *>(k8_smem + K8_MTILE);
     const K8Plan pl = c->cnt->k8;
     const u64 width = (u64)K8_TILE << pl.pass;
-    for (u32 gt = blockIdx.x; gt < pl.mtiles; gt += gridDim.x) {
-        const u32 s = k8_seg_of(c->k8_mb, pl.nseg, gt);
-        const SegItem it = c->fb[s];
-        const u32 mg = k8_merges(it.m);
-        if (pl.pass >= mg || c->k8_flag[s] == 0) continue;   // uniform per CTA
+    // persistent CTAs, each over a contiguous run of merge tiles: the segment record
+    // is fetched once per segment, not once per 1024-output tile
+    const u32 per = (pl.mtiles + gridDim.x - 1) / gridDim.x;
+    const u32 g0 = blockIdx.x * per, g1 = min(pl.mtiles, g0 + per);
+    u32 s = 0, s_beg = 1, s_end = 0, mg = 0;
+    bool skip = true;
+    // merge-path splits of the tile (sp[gt], sp[gt + 1]) are loaded one tile ahead
+    u32 spa = g0 < g1 ? c->k8_sp[g0] : 0u, spb = g0 + 1 < g1 + 1 ? c->k8_sp[min(g0 + 1, pl.mtiles)] : 0u;
+    SegItem it;
+    it.off = 0; it.m = 0; it.level = 0; it.src = 0; it.kind = 0;
+    for (u32 gt = g0; gt < g1; ++gt) {
+        if (gt >= s_end || gt < s_beg) {   // entering a segment
+            s = k8_seg_of(c->k8_mb, pl.nseg, gt);
+            it = c->fb[s];
+            mg = k8_merges(it.m);
+            skip = pl.pass >= mg || c->k8_flag[s] == 0;   // uniform per CTA
+            s_beg = c->k8_mb[s];
+            s_end = s + 1 < pl.nseg ? c->k8_mb[s + 1] : pl.mtiles;
+        }
+        if (skip) {
+            gt = s_end - 1;
+            if (gt + 1 < g1) { spa = c->k8_sp[gt + 1]; spb = c->k8_sp[min(gt + 2, pl.mtiles)]; }
+            continue;
+        }
+        const u32 cur_a = spa, cur_b = spb;
+        if (gt + 1 < g1) { spa = cur_b; spb = c->k8_sp[min(gt + 2, pl.mtiles)]; }
         __syncthreads();   // the previous tile's stage is drained
-        const u32 t = gt - c->k8_mb[s];
+        const u32 t = gt - s_beg;
         const u64 m = it.m;
         const bool last = pl.pass + 1 == mg;
         const u64 *src = (((mg - pl.pass) & 1u) == 0 ? c->buf[2] : c->buf[1]) + it.off;
@@ -404,8 +425,8 @@ __global__ void __launch_bounds__(K8_MTHREADS) k8_merge(const DevCtx *__restrict
         const u64 pair0 = (o0 / (2 * width)) * (2 * width);
         const u64 na = min(pair0 + width, m) - pair0, nb = min(pair0 + 2 * width, m) - min(pair0 + width, m);
         const u64 d0 = o0 - pair0, d1 = min(d0 + K8_MTILE, na + nb);
-        const u32 ia0 = c->k8_sp[gt];
-        const u32 ia1 = d1 == na + nb ? (u32)na : c->k8_sp[gt + 1];
+        const u32 ia0 = cur_a;
+        const u32 ia1 = d1 == na + nb ? (u32)na : cur_b;
         const u32 ib0 = (u32)(d0 - ia0), ib1 = (u32)(d1 - ia1);
         const u32 la = ia1 - ia0, lb = ib1 - ib0, tot = la + lb;
         const u64 *A = src + pair0, *B = src + pair0 + na;
