@@ -174,3 +174,25 @@ def test_torchcomm_gloo_world2():
         assert np.array(u, dtype=np.int32).view(np.uint32).tolist() == [(2 * (2 ** 31 - 1) + 1) % 2 ** 32, 14]
         assert g == [0, 100, 1, 101] and sizes == [3, 4]
     assert got[0][4] == [0, 1000, 1001, 1002] and got[1][4] == [1, 2]
+
+
+@pytest.mark.gpu
+def test_sharded_nccl_world1(sharded):
+    """The production communicator (TorchComm over NCCL) in a world of one GPU: the
+    collectives the driver issues run through NCCL on device tensors."""
+    import socket
+    import torch.distributed as dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        x = synth.config("c2", n=1_000_000)
+        out, info = sharded.sort_sharded(torch.from_numpy(x).cuda(), sharded.TorchComm(), log=True)
+        ref = oracle.learned_sort(x, log=True, check=False)
+        assert info.offset == 0
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), ref.out.view(np.uint64))
+        a, b = oracle.sort_nodes(ref.nodes), np.sort(info.nodes, order=["level", "offset"])
+        assert len(a) == len(b) and all(np.array_equal(a[f], b[f]) for f in a.dtype.names)
+    finally:
+        dist.destroy_process_group()
