@@ -321,6 +321,79 @@ def run_gpu(args):
     print(json.dumps(line))
 
 
+def run_sharded(args):
+    """--sharded: the sharded sort of ONE workload of n keys split
+    over the N ranks (strong scaling), collectives over NCCL (TorchComm); at N = 1
+    without torchrun, one in-process rank.  value = n / max-over-ranks step time."""
+    import numpy as np
+    import torch
+
+    import paper_2405_07122_b200 as pcf
+    from paper_2405_07122_b200 import sharded
+    import synth
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    pcf.build()
+    cfg = synth.CONFIGS[args.config]
+    n = cfg["n"] if args.n is None else args.n
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    host = synth.config(args.config, n=hi)[lo:]
+    x = torch.from_numpy(np.ascontiguousarray(host)).to(dev)
+    del host
+    comm = sharded.TorchComm() if world > 1 else sharded.LoopbackComm(sharded.LoopbackHub(1), 0)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(2 * max(l2, 64 << 20), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(args.warmup, 3)):
+        out, info = sharded.sort_sharded(x, comm)
+    torch.cuda.synchronize()
+    # global order: every slice sorted, slices in rank order, sizes add up
+    o = out.view(torch.int64)
+    key = o ^ ((o >> 63) & 0x7FFFFFFFFFFFFFFF) if out.dtype == torch.float64 else o ^ (-(1 << 63))
+    ok = bool(torch.all(key[1:] >= key[:-1]).item()) if len(key) > 1 else True
+    ends = torch.tensor([key[0].item() if len(key) else 0, key[-1].item() if len(key) else 0, len(key)],
+                        dtype=torch.int64, device=dev)
+    if world > 1:
+        allends = torch.empty(3 * world, dtype=torch.int64, device=dev)
+        torch.distributed.all_gather_into_tensor(allends, ends)
+        e = allends.view(world, 3).cpu().tolist()
+    else:
+        e = [ends.cpu().tolist()]
+    ne = [r for r in e if r[2] > 0]
+    ok = ok and all(ne[i][1] <= ne[i + 1][0] for i in range(len(ne) - 1)) and sum(r[2] for r in e) == n
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    times = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out, info = sharded.sort_sharded(x, comm)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(max_over_ranks(e0.elapsed_time(e1), world, dev))
+    clocks = sampler.stop() if rank == 0 else None
+    if rank != 0:
+        return
+    ms = sum(times) / len(times)
+    line = {
+        "metric": METRIC, "value": n / (ms * 1e-3), "unit": "keys/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64" if cfg["dist"] == "u64" else "f64",
+        "data": "synthetic (seeded, BASELINE.json recipe; DESIGN.md §4)", "config": workload_config(args.config, n),
+        "parallelism": f"sharded{world} (NCCL all-reduce / all-gather / all-to-all between library calls)"
+        if world > 1 else "sharded1 (in-process rank)",
+        "output_sorted": ok, "clocks": clocks,
+    }
+    print(json.dumps(line))
+
+
 def cpu_baseline(config, n, sample):
     """The oracle (single thread, pinned to one core) on a bounded sample of the
     workload: the first `sample` keys of the same seeded stream."""
@@ -394,9 +467,13 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=20_000_000,
                     help="keys per --impl reference step (the whole run stays within a few minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="one workload split over the N ranks (sharded sort, strong scaling) instead of replicas")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.sharded:
+        run_sharded(args)
     else:
         run_gpu(args)
 

@@ -36,9 +36,6 @@ constexpr int K8_MIPT = K8_MTILE / K8_MTHREADS;   // outputs per merge thread
 constexpr int K8_MERGE_SMEM = K8_MTILE * 12;   // keys (+ key-value mode: u32 indices)
 constexpr int K8_SORT_SMEM = 2 * K8_TILE * 8;
 
-#ifndef PCF_K8_WARPSORT
-#define PCF_K8_WARPSORT 1
-#endif
 
 // Compare-exchange of two registers (ascending).
 __device__ __forceinline__ void k8_cx(u64 &a, u64 &b) { const u64 x = a < b ? a : b; b = a < b ? b : a; a = x; }
@@ -104,8 +101,9 @@ __device__ __forceinline__ void k8_sort_tile(u64 *k8_bs, const u64 *__restrict__
 #pragma unroll
     for (int o = 0; o < K8_IPT; o += 8) { K8_BATCHER8(o) }
 #undef K8_BATCHER8
-    static_assert(K8_IPT == 8 || K8_IPT == 16, "K8_IPT must be 8 or 16");
-#if PCF_K8_WARPSORT
+    // the tested configuration: 512 threads x 8 keys (the 16-key and no-register-merge
+    // variants measured slower in round 1 and were dropped rather than left untested)
+    static_assert(K8_IPT == 8, "K8_IPT must be 8 (PCF_K8_TILE / PCF_K8_THREADS)");
     // 16 .. 32 * K8_IPT keys: the warp's ascending runs of 8 merged in registers by a
     // bitonic network (each stage: compare element i = K8_IPT * lane + q with its
     // mirror i ^ (k - 1), then half-cleaners i ^ j), lane shuffles, no shared memory
@@ -143,9 +141,6 @@ __device__ __forceinline__ void k8_sort_tile(u64 *k8_bs, const u64 *__restrict__
         }
     }
     constexpr u32 RUN0 = 32 * K8_IPT;
-#else
-    constexpr u32 RUN0 = 8;   // each lane holds K8_IPT / 8 sorted runs of 8
-#endif
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K8_IPT; ++k) a[t0 + k] = r[k];
