@@ -80,6 +80,14 @@ __global__ void __launch_bounds__(MM_THREADS) k_minmax(const DevCtx *__restrict_
     }
 }
 
+// cnt[bin] += 1, one atomic per distinct bin of the warp: skewed samples (c3's
+// repeated value, c4's first bin) would otherwise serialise on one address.
+__device__ __forceinline__ void warp_agg_add(u32 *cnt, u32 bin) {
+    const u32 act = __activemask();
+    const u32 peers = __match_any_sync(act, bin);
+    if ((threadIdx.x & 31) == (u32)(__ffs(peers) - 1)) atomicAdd(&cnt[bin], (u32)__popc(peers));
+}
+
 __device__ __forceinline__ void push_item(const DevCtx *c, u64 off, u32 m, u32 level, u32 src, u32 kind) {
     u32 slot = atomicAdd(c->nitems, 1u);
     if (slot < c->items_cap) {
@@ -171,7 +179,7 @@ __global__ void k_fit_sample(const DevCtx *__restrict__ c, u32 node) {
     const bool sample_all = (c->flags & FLAG_SAMPLE_ALL) != 0;
     const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, c->gbase + g.off), k, g.m);
     const u64 raw = c->buf[g.src][g.off + pos];
-    atomicAdd(&g.cnt[interval_index<K>(K::to_okey(raw), md)], 1u);
+    warp_agg_add(&g.cnt[0], interval_index<K>(K::to_okey(raw), md));
 }
 
 // ------------------------------------------------------------------ batched global nodes
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(FSB_CHUNK) k_fit_sample_batch(const DevCtx *__
         const u32 k = cb * FSB_CHUNK + threadIdx.x;
         if (k >= g.alpha) continue;
         const u64 pos = sample_all ? (u64)k : sample_pos(node_key(c->seed, g.level, c->gbase + g.off), k, g.m);
-        atomicAdd(&g.cnt[interval_index<K>(K::to_okey(c->buf[g.src][g.off + pos]), md)], 1u);
+        warp_agg_add(&g.cnt[0], interval_index<K>(K::to_okey(c->buf[g.src][g.off + pos]), md));
     }
 }
 

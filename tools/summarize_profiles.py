@@ -87,10 +87,7 @@ for fn in sorted(os.listdir(src)):
             return float(val.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         traffic[name[len("k7_kernel_"):]] = {"smem_subtree": b("dram__bytes_read.sum") + b("dram__bytes_write.sum"),
                                              "_from": f"{dst}/{name}.txt (one K7 launch = the sort's K7 work)"}
-if traffic:
-    path = os.path.join(ROOT, "profiles", "traffic.json")
-    doc = json.load(open(path)) if os.path.exists(path) else {}
-    doc.update(traffic)
-    with open(path, "w") as f:
-        json.dump(doc, f, indent=1)
+if traffic:   # merged into profiles/traffic.json (bench.py's roofline.traffic) by tools/merge_traffic.py
+    with open(os.path.join(dst, "traffic_fragment.json"), "w") as f:
+        json.dump(traffic, f, indent=1)
 print("wrote", dst)
