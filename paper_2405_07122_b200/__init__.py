@@ -78,7 +78,9 @@ _lib = None
 SYMBOLS = ["pcf_params_init", "pcf_workspace_bytes", "pcf_sort_f64", "pcf_sort_u64", "pcf_sort_f64_host",
            "pcf_sort_u64_host", "pcf_status_string", "pcf_last_error", "pcf_abi_version",
            "pcf_bucket_counts_f64", "pcf_level1_entries", "pcf_argsort_f64", "pcf_argsort_u64",
-           "pcf_sort_pairs_f64_u32", "pcf_sort_pairs_f64_u64", "pcf_sort_pairs_u64_u32", "pcf_sort_pairs_u64_u64"]
+           "pcf_sort_pairs_f64_u32", "pcf_sort_pairs_f64_u64", "pcf_sort_pairs_u64_u32", "pcf_sort_pairs_u64_u64",
+           "pcf_shard_state_bytes", "pcf_shard_workspace_bytes", "pcf_shard_views", "pcf_shard_minmax",
+           "pcf_shard_counts", "pcf_shard_histogram", "pcf_shard_partition", "pcf_shard_sort_range"]
 
 
 def lib():
@@ -109,7 +111,9 @@ def lib():
             f = getattr(L, name)
             f.argtypes = [vp, vp, vp, sz, PP, vp]
             f.restype = i32
-        for name in ["pcf_sort_pairs_f64_u32", "pcf_sort_pairs_f64_u64", "pcf_sort_pairs_u64_u32", "pcf_sort_pairs_u64_u64"]:
+        for name in ["pcf_sort_pairs_f64_u32", "pcf_sort_pairs_f64_u64", "pcf_sort_pairs_u64_u32", "pcf_sort_pairs_u64_u64",
+           "pcf_shard_state_bytes", "pcf_shard_workspace_bytes", "pcf_shard_views", "pcf_shard_minmax",
+           "pcf_shard_counts", "pcf_shard_histogram", "pcf_shard_partition", "pcf_shard_sort_range"]:
             f = getattr(L, name)
             f.argtypes = [vp, vp, vp, vp, sz, PP, vp]
             f.restype = i32
