@@ -116,15 +116,29 @@ __device__ __forceinline__ double key_offset(u64 okey, const Model &md) {   // d
     if (K::is_f64) return __dsub_rn(__longlong_as_double((long long)K::from_okey(okey)), md.xmin);
     return __ull2double_rn(okey - md.umin);
 }
-// Branch-free fast path: floor(t') + 1 and whether it is certified (ok); the
-// caller takes interval_index_exact for the rare uncertified keys.
+// The same d from the raw key bits (no ordered-key round trip: for f64 keys
+// from_okey(to_okey(raw)) == raw, which the compiler cannot see).
 template <class K>
-__device__ __forceinline__ u32 interval_index_fast(u64 okey, const Model &md, bool &ok) {
-    const double t = __dmul_rn(key_offset<K>(okey, md), md.s);
+__device__ __forceinline__ double key_offset_raw(u64 raw, const Model &md) {
+    if (K::is_f64) return __dsub_rn(__longlong_as_double((long long)raw), md.xmin);
+    return __ull2double_rn(raw - md.umin);
+}
+__device__ __forceinline__ u32 fast_from_offset(double d, const Model &md, bool &ok) {
+    const double t = __dmul_rn(d, md.s);
     const double fl = floor(t);
     const double fr = __dsub_rn(t, fl);
     ok = fr >= md.eps && fr <= 1.0 - md.eps;
     return (u32)fl + 1u;
+}
+// Branch-free fast path: floor(t') + 1 and whether it is certified (ok); the
+// caller takes interval_index_exact for the rare uncertified keys.
+template <class K>
+__device__ __forceinline__ u32 interval_index_fast(u64 okey, const Model &md, bool &ok) {
+    return fast_from_offset(key_offset<K>(okey, md), md, ok);
+}
+template <class K>
+__device__ __forceinline__ u32 interval_index_fast_raw(u64 raw, const Model &md, bool &ok) {
+    return fast_from_offset(key_offset_raw<K>(raw, md), md, ok);
 }
 template <class K>
 __device__ __forceinline__ u32 interval_index(u64 okey, const Model &md) {

@@ -607,13 +607,13 @@ __global__ void __launch_bounds__(CNT_THREADS, 2) k_split_count(const DevCtx *__
 #pragma unroll
             for (u32 q = 0; q < SC_KPL; ++q) {
                 bool ok;
-                ix[q] = interval_index_fast<K>(K::to_okey(raw[q]), md, ok);
+                ix[q] = interval_index_fast_raw<K>(raw[q], md, ok);
                 bad |= ok ? 0u : (1u << q);
             }
             if (bad) {   // rare: keys in the fast path's guard band
 #pragma unroll
                 for (u32 q = 0; q < SC_KPL; ++q)
-                    if (bad & (1u << q)) ix[q] = interval_index_exact(key_offset<K>(K::to_okey(raw[q]), md), md.r, md.betad);
+                    if (bad & (1u << q)) ix[q] = interval_index_exact(key_offset_raw<K>(raw[q], md), md.r, md.betad);
             }
             if (tab) {
                 const u32 cs = S.tab_cs;
@@ -689,13 +689,13 @@ __global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_tile(const DevCtx
 #pragma unroll
         for (u32 q = 0; q < SC_KPL; ++q) {
             bool ok;
-            ix[q] = interval_index_fast<K>(K::to_okey(raw[q]), md, ok);
+            ix[q] = interval_index_fast_raw<K>(raw[q], md, ok);
             bad |= ok ? 0u : (1u << q);
         }
         if (bad) {   // rare: keys in the fast path's guard band
 #pragma unroll
             for (u32 q = 0; q < SC_KPL; ++q)
-                if (bad & (1u << q)) ix[q] = interval_index_exact(key_offset<K>(K::to_okey(raw[q]), md), md.r, md.betad);
+                if (bad & (1u << q)) ix[q] = interval_index_exact(key_offset_raw<K>(raw[q], md), md.r, md.betad);
         }
 #pragma unroll
         for (u32 q = 0; q < SC_KPL; ++q) ix[q] = __ldg(&T[ix[q]]);

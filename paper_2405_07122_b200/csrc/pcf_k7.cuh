@@ -300,13 +300,14 @@ enum { MODE_NODE = 0, MODE_GLOBAL = 1 };
 // i(x) of every valid slot (pk != NONE) into pk: certified fast path for all
 // slots, the exact sub/div/mul evaluation (R6) only for the rare keys in the
 // guard band, behind one warp-uniform branch.
-template <class K>
+// RAW: key[] holds the raw key bits (the K7_GROUP placement), else ordered keys.
+template <class K, bool RAW = false>
 __device__ __forceinline__ void classify_slots(const u64 (&key)[KPT], u32 (&pk)[KPT], const Model &md) {
     u32 bad = 0;
 #pragma unroll
     for (int q = 0; q < KPT; ++q) {
         bool ok;
-        const u32 i = interval_index_fast<K>(key[q], md, ok);
+        const u32 i = RAW ? interval_index_fast_raw<K>(key[q], md, ok) : interval_index_fast<K>(key[q], md, ok);
         const bool v = pk[q] != NONE;
         bad |= (v && !ok) ? (1u << q) : 0u;
         pk[q] = v ? i : NONE;
@@ -314,7 +315,8 @@ __device__ __forceinline__ void classify_slots(const u64 (&key)[KPT], u32 (&pk)[
     if (__any_sync(0xffffffffu, bad != 0)) {
 #pragma unroll
         for (int q = 0; q < KPT; ++q)
-            if (bad & (1u << q)) pk[q] = interval_index_exact(key_offset<K>(key[q], md), md.r, md.betad);
+            if (bad & (1u << q))
+                pk[q] = interval_index_exact(RAW ? key_offset_raw<K>(key[q], md) : key_offset<K>(key[q], md), md.r, md.betad);
     }
 }
 
@@ -356,7 +358,8 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
     for (int q = 0; q < KPT; ++q) {
         const u32 f = f0 + q * 32 + lane;
         const bool v = f < f1;
-        key[q] = (MODE == MODE_GLOBAL && raw) ? K::to_okey(raw[v ? f : 0u]) : X[pos + (v ? f : 0u)];
+        // the K7_GROUP placement classifies raw key bits (converted to ordered keys after)
+        key[q] = MODE == MODE_GLOBAL ? (raw ? raw[v ? f : 0u] : K::from_okey(X[pos + (v ? f : 0u)])) : X[pos + (v ? f : 0u)];
         if (PR) {
             const u32 i = (MODE == MODE_GLOBAL && raw) ? f : (u32)IX[pos + (v ? f : 0u)];
             if (q & 1) ix2[q / 2] |= i << 16; else ix2[q / 2] = i & 0xffffu;
@@ -465,7 +468,9 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         if (t == 0) S.nbl[w0] = 0;
         const u32 *gT = S.gT;
         const u32 jb = S.gjlo - 1u;
-        classify_slots<K>(key, pk, md);
+        classify_slots<K, true>(key, pk, md);
+#pragma unroll
+        for (int q = 0; q < KPT; ++q) key[q] = K::to_okey(key[q]);
 #pragma unroll
         for (int q = 0; q < KPT; ++q) {
             const bool v = pk[q] != NONE;
