@@ -169,10 +169,28 @@ enum { PH_MINMAX = 0, PH_FIT = 1, PH_COUNT = 2, PH_SCATTER = 3, PH_K7 = 4, PH_K8
 
 // K7 dynamic shared memory: the struct, the node lists (sized for tau) and, in
 // key-value mode, the two u16 source-index arrays IA / IB behind them
-static int k7_smem_bytes(u32 tau = 2, bool pr = false) {
-    return (int)(sizeof(K7Smem) + k7_lists_bytes(tau < 2 ? 2 : tau) + (pr ? 4ull * S_CAP : 0ull));
+namespace k7s = k7n512;    // 512 threads: every tau, key-value mode
+namespace k7w = k7n1024;   // 1024 threads: keys-only sorts with tau >= K7W_MIN_TAU
+constexpr u32 PR_MIN_TAU = 16;   constexpr u32 K7W_MIN_TAU = 32;
+constexpr int SMEM_MAX = 232448;
+// The wide variant (32 warps per SM) unless the sort is key-value, tau is small or
+// PCF_K7_VARIANT=512 is set (A/B experiments).
+static bool k7_wide(u32 tau, bool pr) {
+    static int force = -1;
+    if (force < 0) {
+        const char *e = getenv("PCF_K7_VARIANT");
+        force = e && !strcmp(e, "512") ? 1 : 0;
+    }
+    return !pr && !force && tau >= K7W_MIN_TAU && k7w::Variant::smem(tau, false) <= (size_t)SMEM_MAX;
 }
-constexpr u32 PR_MIN_TAU = 16;   // key-value mode: smaller tau needs node lists that leave no room for IA / IB
+static int k7_smem_bytes(u32 tau, bool pr) {
+    return (int)(k7_wide(tau, pr) ? k7w::Variant::smem(tau, pr) : k7s::Variant::smem(tau, pr));
+}
+template <class K, bool PR>
+static void (*k7_fn(bool wide))(const DevCtx *) {
+    if constexpr (!PR) { if (wide) return k7w::k7_kernel<K, false>; }
+    return k7s::k7_kernel<K, PR>;
+}
 static int split_smem_bytes() { return (int)sizeof(SplitScatterSmem); }
 
 // Launch with programmatic stream serialization (see pdl_entry()).
@@ -201,15 +219,17 @@ static int cur_dev() {
 }
 
 template <class K, bool PR>
-static int k7_ctas_per_sm() {   // resident K7 CTAs per SM (persistent grid size)
-    static thread_local int v[MAX_DEVS] = {0};
+static int k7_ctas_per_sm(bool wide) {   // resident K7 CTAs per SM (persistent grid size)
+    static thread_local int v[2][MAX_DEVS] = {{0}};
     const int d = cur_dev();
-    if (!v[d]) {
+    if (!v[wide][d]) {
         int b = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k7_kernel<K, PR>, K7_THREADS, k7_smem_bytes(PR ? PR_MIN_TAU : 2, PR)) != cudaSuccess || b < 1) b = 1;
-        v[d] = b;
+        const int nt = wide ? k7w::Variant::threads : k7s::Variant::threads;
+        const int sm = (int)(wide ? k7w::Variant::smem(K7W_MIN_TAU, false) : k7s::Variant::smem(PR ? PR_MIN_TAU : 2, PR));
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k7_fn<K, PR>(wide), nt, sm) != cudaSuccess || b < 1) b = 1;
+        v[wide][d] = b;
     }
-    return v[d];
+    return v[wide][d];
 }
 
 template <class K>
@@ -229,8 +249,9 @@ static int configure_kernels() {
     static thread_local bool done[MAX_DEVS] = {false};
     const int d = cur_dev();
     if (done[d]) return PCF_OK;
-    CK(cudaFuncSetAttribute(k7_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7_smem_bytes()));
-    CK(cudaFuncSetAttribute(k7_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, k7_smem_bytes(PR_MIN_TAU, true)));
+    CK(cudaFuncSetAttribute(k7s::k7_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7s::Variant::smem(2, false)));
+    CK(cudaFuncSetAttribute(k7s::k7_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7s::Variant::smem(PR_MIN_TAU, true)));
+    CK(cudaFuncSetAttribute(k7w::k7_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7w::Variant::smem(K7W_MIN_TAU, false)));
     CK(cudaFuncSetAttribute(k_split_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
     CK(cudaFuncSetAttribute(k8_merge<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
@@ -245,6 +266,8 @@ static int configure_kernels() {
 struct Launch {   // the kernel-launch configuration of this device and sort size
     int nsm;
     int k7_grid;
+    int k7_threads;
+    bool k7_wide;
     int count_grid;
     int tau_smem;
     u32 tile_grid;    // one CTA per split tile of a round (upper bound; idle CTAs exit)
@@ -298,7 +321,7 @@ static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32
 template <class K, bool PR>
 static int add_k7(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32 *nk) {
     CK(launch_pdl(k_k7_order, 1, 1024, 0, cs, d_ctx));
-    CK(launch_pdl(k7_kernel<K, PR>, lc.k7_grid, K7_THREADS, lc.tau_smem, cs, d_ctx));
+    CK(launch_pdl(k7_fn<K, PR>(lc.k7_wide), lc.k7_grid, lc.k7_threads, lc.tau_smem, cs, d_ctx));
     CK(launch_pdl(k_k7_advance, 1, 1, 0, cs, d_ctx));
     *nk += 3;
     return PCF_OK;
@@ -621,7 +644,9 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     Launch lc;
     lc.nsm = nsm;
-    lc.k7_grid = nsm * k7_ctas_per_sm<K, PR>();
+    lc.k7_wide = k7_wide(p.tau, PR);
+    lc.k7_threads = lc.k7_wide ? k7w::Variant::threads : k7s::Variant::threads;
+    lc.k7_grid = nsm * k7_ctas_per_sm<K, PR>(lc.k7_wide);
     lc.count_grid = nsm * count_ctas_per_sm<K>();
     lc.tau_smem = k7_smem_bytes(p.tau, PR);
     // fallback segments hold > S_CAP keys each: <= n / S_CAP partial tiles
@@ -644,7 +669,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         t.off = 0; t.size = (u32)n; t.kind = K7_NODE; t.src = 0; t.level = 1;
         CK(cudaMemcpyAsync(hc.k7, &t, sizeof t, cudaMemcpyHostToDevice, st));
         tm.begin(PH_K7);
-        k7_kernel<K, PR><<<1, K7_THREADS, lc.tau_smem, st>>>(d_ctx);
+        k7_fn<K, PR>(lc.k7_wide)<<<1, lc.k7_threads, lc.tau_smem, st>>>(d_ctx);
         CK(cudaGetLastError());
         tm.end();
         launches++;

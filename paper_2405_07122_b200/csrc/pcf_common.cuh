@@ -17,16 +17,11 @@ typedef unsigned short u16;
 typedef unsigned char u8;
 
 // ---------------------------------------------------------------- tunables
-#ifndef PCF_K7_THREADS
-#define PCF_K7_THREADS 512
-#endif
 #ifndef PCF_S_CAP
 #define PCF_S_CAP 8192
 #endif
-constexpr int K7_THREADS = PCF_K7_THREADS;   // smem-subtree kernel block
-constexpr int K7_WARPS = K7_THREADS / 32;
 constexpr int S_CAP = PCF_S_CAP;             // keys a K7 CTA holds (two 64 KB buffers)
-constexpr int NB_CAP = 1024;             // max buckets of one K7 CTA-level partition
+constexpr int NB_CAP = 862;              // max buckets of one K7 CTA-level partition (>= iroot34(S_CAP) + 1)
 constexpr int WMAX = 1024;               // largest segment a single warp runs Alg. 1 on
 constexpr int WNB = 184;                 // >= iroot34(WMAX) + 2 (warp scratch bins)
 constexpr int WSTACK = 320;              // warp DFS stack entries (bound: DESIGN.md §5.3)

@@ -135,12 +135,14 @@ __host__ __device__ inline u32 floor_log2_u64(u64 v) {  // v >= 1
 }
 // Digit shift for splitting W >= 2 consecutive buckets holding c keys:
 // G = ceil(W / 2^s) <= GMAX, expected group ~ S_CAP/2 keys, G >= 2.
+constexpr u32 NB_SHIFT_MAX = 9;
+static_assert((1u << NB_SHIFT_MAX) <= (u32)NB_CAP, "NB_SHIFT_MAX");
 __host__ __device__ inline u32 choose_shift(u32 W, u32 c) {
     u32 cl = ceil_log2_u32(W);
     u32 smin = cl > GMAX_LOG2 ? cl - GMAX_LOG2 : 0;
     u64 q = ((u64)(S_CAP / 2) * W) / (c ? c : 1);
     u32 st = floor_log2_u64(q ? q : 1);
-    u32 s = st < 10 ? st : 10;
+    u32 s = st < NB_SHIFT_MAX ? st : NB_SHIFT_MAX;   // a digit group of 2^s buckets fits a K7 task (NB_CAP)
     if (s < smin) s = smin;
     if (s > cl - 1) s = cl - 1;
     return s;
