@@ -252,7 +252,8 @@ static int configure_kernels() {
     CK(cudaFuncSetAttribute(k7s::k7_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7s::Variant::smem(2, false)));
     CK(cudaFuncSetAttribute(k7s::k7_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7s::Variant::smem(PR_MIN_TAU, true)));
     CK(cudaFuncSetAttribute(k7w::k7_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7w::Variant::smem(K7W_MIN_TAU, false)));
-    CK(cudaFuncSetAttribute(k_split_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
+    CK(cudaFuncSetAttribute(k_split_scatter<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
+    CK(cudaFuncSetAttribute(k_split_scatter<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
     CK(cudaFuncSetAttribute(k8_merge<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
     CK(cudaFuncSetAttribute(k8_blocksort<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_SORT_SMEM));
@@ -304,7 +305,7 @@ struct TailGraph {
 static thread_local std::vector<TailGraph> g_tails;
 static thread_local cudaStream_t g_cap[2] = {nullptr, nullptr};
 
-template <class K>
+template <class K, bool PR>
 static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32 *nk) {
     CK(launch_pdl(k_round_plan, 1, 1024, 0, cs, d_ctx));
     CK(launch_pdl(k_tile_map, lc.nsm * 2, 256, 0, cs, d_ctx));
@@ -312,7 +313,7 @@ static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32
     CK(launch_pdl(k_scanp_partials, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_scanp_final, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
-    CK(launch_pdl(k_split_scatter<K>, lc.tile_grid, SC_THREADS, split_smem_bytes(), cs, d_ctx));
+    CK(launch_pdl(k_split_scatter<K, PR>, lc.tile_grid, SC_THREADS, split_smem_bytes(), cs, d_ctx));
     CK(launch_pdl(k_split_taskgen, lc.nsm * 2, TG_THREADS, 0, cs, d_ctx));
     *nk += 8;
     return PCF_OK;
@@ -377,7 +378,7 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
                 CK(launch_pdl(k_fit_sample_batch<K>, lc.nsm * 8, FSB_CHUNK, 0, bs, d_ctx));
                 CK(launch_pdl(k_fit_batch, lc.nsm * 2, SCAN_THREADS, 0, bs, d_ctx));
                 nk += 3;
-                for (int r = 0; r < 2; ++r) { int e = add_round<K>(bs, d_ctx, lc, &nk); if (e) return e; }
+                for (int r = 0; r < 2; ++r) { int e = add_round<K, PR>(bs, d_ctx, lc, &nk); if (e) return e; }
                 int e = add_k7<K, PR>(bs, d_ctx, lc, &nk);
                 if (e) return e;
                 CK(launch_pdl(k_items_to_nodes<K>, 1, 1024, 0, bs, d_ctx, hb, 1u));
@@ -768,7 +769,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             CK(launch_pdl(k_scanp_final, nsm * 2, SCAN_THREADS, 0, st, dc));
             tm.end();
             tm.begin(PH_SCATTER);
-            CK(launch_pdl(k_split_scatter<K>, tile_grid, SC_THREADS, split_smem_bytes(), st, dc));
+            CK(launch_pdl(k_split_scatter<K, PR>, tile_grid, SC_THREADS, split_smem_bytes(), st, dc));
             tm.end();
             tm.begin(PH_OTHER);
             CK(launch_pdl(k_split_taskgen, nsm * 2, TG_THREADS, 0, st, dc));

@@ -959,7 +959,7 @@ struct SplitScatterSmem {
 
 // FULL: the tile holds SPLIT_TILE keys (every tile but the last of a split), so
 // the per-slot validity tests compile away.
-template <class K, bool FULL>
+template <class K, bool FULL, bool PR>
 __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c, SplitScatterSmem &S, const SplitTask &st,
                                                    u32 lt, const u32 *__restrict__ P) {
     const u32 deg = c->nodes[st.node].degenerate;   // checked after the tile's loads are issued
@@ -1066,18 +1066,18 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
     bool inv = false;
     // key-value mode: the source index of every key moves with it (gathered from the
     // tile's source range of ibuf[src], identity for the input buffer)
-    const u32 *isrc = c->ibuf[st.src];
-    u32 *idst = c->ibuf[2] ? c->ibuf[st.dst] + st.off : nullptr;
+    const u32 *isrc = PR ? c->ibuf[st.src] : nullptr;
+    u32 *idst = PR ? c->ibuf[st.dst] + st.off : nullptr;
     auto src_index = [&](u32 tl) -> u32 { return isrc ? isrc[st.off + k0 + tl] : (u32)(st.off + k0 + tl); };
     for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) {
         const u32 b = S.dsrc[i];
-        if (i > 0) {
+        if (i > 0) {   // same chunk (src >> 5) and digit, source indices out of order
             const u32 a = S.dsrc[i - 1];
-            inv |= (a >> 21) == (b >> 21) && (a & 0xffffu) == (b & 0xffffu) && (a >> 16) > (b >> 16);
+            inv |= ((a ^ b) & 0xffe0ffffu) == 0u && a > b;
         }
         PCF_CHECK(c, (b & 0xffffu) < G && S.goff[b & 0xffffu] + i < st.m);
         y[S.goff[b & 0xffffu] + i] = S.buf[i];
-        if (idst) idst[S.goff[b & 0xffffu] + i] = src_index(b >> 16);
+        if (PR) idst[S.goff[b & 0xffffu] + i] = src_index(b >> 16);
     }
     if (!__syncthreads_or(inv || (c->flags & FLAG_EXACT_RANKS))) return;
     for (u32 i = threadIdx.x; i < ntile; i += SC_THREADS) {
@@ -1095,14 +1095,14 @@ __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c,
             for (u32 j = a; j < b; ++j) pos += (S.dsrc[j] >> 16) < (e >> 16) ? 1u : 0u;
         }
         y[S.goff[d] + pos] = S.buf[i];
-        if (idst) idst[S.goff[d] + pos] = src_index(e >> 16);
+        if (PR) idst[S.goff[d] + pos] = src_index(e >> 16);
     }
 }
 
-template <class K>
 #ifndef PCF_SC_MINB
 #define PCF_SC_MINB 2
 #endif
+template <class K, bool PR>
 __global__ void __launch_bounds__(SC_THREADS, PCF_SC_MINB) k_split_scatter(const DevCtx *__restrict__ c) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char sc_smem_raw[];
@@ -1115,8 +1115,8 @@ __global__ void __launch_bounds__(SC_THREADS, PCF_SC_MINB) k_split_scatter(const
         if (tile != blockIdx.x) __syncthreads();   // the previous tile's stage is written out
         const SplitTask st = L[c->tmap[tile]];
         const u32 lt = tile - st.tile_begin;
-        if ((lt + 1) * SPLIT_TILE <= st.m) split_scatter_tile<K, true>(c, S, st, lt, c->pmat);
-        else split_scatter_tile<K, false>(c, S, st, lt, c->pmat);
+        if ((lt + 1) * SPLIT_TILE <= st.m) split_scatter_tile<K, true, PR>(c, S, st, lt, c->pmat);
+        else split_scatter_tile<K, false, PR>(c, S, st, lt, c->pmat);
     }
 }
 
