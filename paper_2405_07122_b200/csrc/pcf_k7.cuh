@@ -135,6 +135,15 @@ __device__ __forceinline__ ulonglong2 ld_stream2(const ulonglong2 *p) {
 // thread in registers; every tau) and 1024 threads (8 keys per thread, a quad
 // team tier; node lists sized for tau >= K7W_MIN_TAU, keys-only mode).  The host
 // picks one per sort (pcf_api.cu: k7_wide).
+#ifndef PCF_K7_NS0
+#define PCF_K7_NS0 32      // small-list wait: first back-off (ns)
+#endif
+#ifndef PCF_K7_NSMAX
+#define PCF_K7_NSMAX 512   // small-list wait: largest back-off (ns; longer sleeps delay the task end)
+#endif
+#ifndef PCF_K7_NPROF
+#define PCF_K7_NPROF 0     // per-phase cycles of team nodes (profiling builds only)
+#endif
 #define PCF_K7_NT 512
 namespace pcf { namespace k7n512 {
 #include "pcf_k7_body.cuh"

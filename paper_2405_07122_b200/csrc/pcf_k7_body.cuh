@@ -24,6 +24,7 @@ __host__ __device__ inline u32 k7_lsm_cap(u32 tau) { return k7_list_cap(tau) + K
 __host__ __device__ inline u32 k7_stk_cap(u32 tau) { return (u32)WCAP / tau > 0 ? (u32)WCAP / tau : 1u; }
 __host__ __device__ inline size_t k7_lists_bytes(u32 tau) { return 4ull * (k7_lsm_cap(tau) + (u64)K7_WARPS * k7_stk_cap(tau)); }
 constexpr int LBIG_CAP = 32;                       // nodes > WCAP keys of one task (<= 16)
+constexpr int TBIG_CAP = 16;                       // children > WCAP of one team node: <= 4096 / 257
 constexpr int STK_CAP = WCAP / 2;                  // per-warp DFS stack
 constexpr int BL_CAP = 128;                        // leaves > SMALL_MAX keys of one node: <= S_CAP / 65
 constexpr int BL_W = BL_CAP / K7_WARPS;            // per-warp slice (a warp's node has <= 7)
@@ -52,6 +53,10 @@ struct K7Smem {
     u16 hcol[TCOLS];   // bucket sizes of the current node (same slices)
     u16 LC[S_CAP];                // per position: bucket column of a B-leaf key, 0 otherwise
     u32 lbig[LBIG_CAP];           // nodes > WCAP keys
+    // children of > WCAP keys of a double / quad team's node (1024-thread builds: nodes of
+    // (1630, CTA_MIN] keys can have them), run next by the same team; per first warp
+    u32 tbig[K7_WARPS][TBIG_CAP];
+    u32 tbn[K7_WARPS];
     u32 bl[BL_CAP];               // leaves > SMALL_MAX keys of the current node (slices of the node's warps)
     u64 wmn[K7_WARPS], wmx[K7_WARPS];
     u32 wsum[K7_WARPS];
@@ -227,6 +232,17 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
     u32 *bl = S.bl + w0 * BL_W;
     const bool logging = c->rec != nullptr;
     const u32 tau = c->tau;
+    // PCF_K7_NPROF builds: cycles of each phase of the 4-warp team nodes (thread 0 of the
+    // team; slots 3, 14, 15, 20-23: minmax, samples, fit, classify, columns, placement, leaves)
+    constexpr bool NPROF = PCF_K7_NPROF && MODE == MODE_NODE && NW == GW;
+    long long np_t = (NPROF && t == 0 && c->k7_prof) ? clock64() : 0;
+    auto nmark = [&](int slot) {
+        if (NPROF && t == 0 && c->k7_prof) {
+            const long long x = clock64();
+            atomicAdd(&S.prof[slot], (unsigned long long)(x - np_t));
+            np_t = x;
+        }
+    };
 
     // ---- this thread's keys: warp wg owns [f0, f1), chunk q = 32 consecutive keys
     const u32 R = ((m + NT - 1) / NT) * 32;
@@ -272,6 +288,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         if (lane == 0) { S.wmn[w] = mn; S.wmx[w] = mx; }
         if (t == 0) { S.db[w0] = 0; S.dh[w0] = 0; S.ncnt[w0] = 0; S.nbl[w0] = 0; if (NW > 1 && !CTA) S.top[w0] = 0; }
         G.bar();
+        nmark(3);
         mn = S.wmn[G.w0];
         mx = S.wmx[G.w0];
 #pragma unroll
@@ -301,6 +318,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
             }
         }
         G.bar();
+        nmark(14);
         if (CTA && MODE == MODE_NODE) prof_mark(c, S, 3);
         // ---- fit: b = inclusive prefix over bins 1..P+1, T = floor(b*gamma/alpha)+1 (R7)
         {
@@ -333,6 +351,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
             }
         }
         G.bar();
+        nmark(15);
         // ---- classify (i(x) -> T) and count per (warp, column); unstable rank
         classify_slots<K>(key, pk, md);
 #pragma unroll
@@ -381,6 +400,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         }
     }
     G.bar();
+    nmark(20);
     if (CTA && MODE == MODE_NODE) prof_mark(c, S, 14);
 
     // ---- column pass: sizes, positions, Alg. 1 lines 160-167 dispatch, destinations per warp
@@ -417,9 +437,14 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
                     for (int ww = 0; ww < NW; ++ww) { const u32 o = Wg[ww * CCOLS + col]; Wg[ww * CCOLS + col] = (u16)d; d += o; }
                     if (!leaf) {
                         const u32 e = ent_make(pos + run, hh, rel + 1);
-                        if (CTA && hh > (u32)WCAP) {
-                            const u32 sl = atomicAdd(&S.btot, 1u);
-                            if (sl < (u32)LBIG_CAP) S.lbig[sl] = e; else atomicOr(c->err_flag, 2u);
+                        if (hh > (u32)WCAP) {   // too large for one warp: the CTA's big list / the team's own
+                            if (CTA) {
+                                const u32 sl = atomicAdd(&S.btot, 1u);
+                                if (sl < (u32)LBIG_CAP) S.lbig[sl] = e; else atomicOr(c->err_flag, 2u);
+                            } else {
+                                const u32 sl = atomicAdd(&S.tbn[w0], 1u);
+                                if (NW > 1 && sl < (u32)TBIG_CAP) S.tbig[w0][sl] = e; else atomicOr(c->err_flag, 2u);
+                            }
                         } else if (CTA) {
                             const u32 sl = atomicAdd(&S.stot, 1u);
                             if (sl < S.list_cap) S.lsm[sl] = e; else atomicOr(c->err_flag, 2u);
@@ -450,6 +475,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         }
     }
     G.bar();
+    nmark(21);
 
     // ---- placement (chunk order: stable re-rank of recursing keys)
 #pragma unroll
@@ -481,6 +507,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         }
     }
     G.bar();
+    nmark(22);
     if (CTA && MODE == MODE_NODE) prof_mark(c, S, 15);
     if (NW > 1 && !CTA) {   // team: publish the children (their keys are placed) to the small-node list
         const u32 nc = S.top[w0];
@@ -519,6 +546,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
                      cc & 1023u, (cc >> 10) & 1023u, cc >> 20);
     }
     G.bar();
+    nmark(23);
 }
 
 
@@ -631,12 +659,16 @@ __device__ __forceinline__ void run_tier(const DevCtx *c, K7Smem &S, const Grp<N
     for (;;) {
         if (G.t == 0) {
             u32 e = 0;
-            for (;;) {
-                const u32 i = atomicAdd(ctr, 1u);
-                if (i >= S.btot) break;
-                e = S.lbig[i];
-                if (ent_m(e) > lo && ent_m(e) <= hi) break;
-                e = 0;
+            if (S.tbn[G.w0] > 0) {   // the team's own children of > WCAP keys first (< delta(hi) keys: fit)
+                e = S.tbig[G.w0][--S.tbn[G.w0]];
+            } else {
+                for (;;) {
+                    const u32 i = atomicAdd(ctr, 1u);
+                    if (i >= S.btot) break;
+                    e = S.lbig[i];
+                    if (ent_m(e) > lo && ent_m(e) <= hi) break;
+                    e = 0;
+                }
             }
             cur[G.w0] = e;
         }
@@ -672,6 +704,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
     }
     __syncthreads();
     for (u32 i = threadIdx.x; i < S.lsm_cap; i += K7_THREADS) S.lsm[i] = 0;   // tickets read 0 until pushed
+    if (threadIdx.x < (u32)K7_WARPS) S.tbn[threadIdx.x] = 0;   // (each team empties its own list)
     if (c->k7_prof && threadIdx.x == 0) {
         for (int i = 0; i < K7_PROF_SLOTS; ++i) S.prof[i] = 0;
         S.prof_t = clock64();
@@ -786,7 +819,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
                     } else {
                         const u32 tk = atomicAdd(&S.snext, 1u);
                         volatile u32 *slot = &S.lsm[tk < S.lsm_cap ? tk : S.lsm_cap - 1];
-                        u32 ns = 32;
+                        u32 ns = PCF_K7_NS0;
                         for (;;) {   // wait (backing off, so the working teams keep the issue slots)
                             e = *slot;
                             if (e) { *slot = 0; break; }
@@ -797,7 +830,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
                                 break;
                             }
                             __nanosleep(ns);
-                            ns = ns < 2048 ? ns * 2 : ns;
+                            ns = ns < PCF_K7_NSMAX ? ns * 2 : ns;
                         }
                     }
                 }

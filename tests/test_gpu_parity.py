@@ -287,3 +287,30 @@ def test_r6_bin_edges_gpu(pcf):
         assert not np.array_equal(b_r6, b_ex)
         _, info = compare(pcf, x, sample_all=True)
         assert np.array_equal(info.level1_b[: beta + 1], b_r6), f"m={m}: GPU i(x) differs from reading R6"
+
+
+def _cluster_input(n0, k1, k2, seed, embedded):
+    """Uniform keys plus a cluster of k1 + k2 keys whose k2 keys sit in one tiny interval:
+    the node holding the cluster (the root when not embedded, else one level-2 node)
+    has a recursing bucket of ~k2 keys, larger than one warp's
+    register capacity in the 1024-thread K7 build."""
+    r = np.random.default_rng(seed)
+    if embedded:
+        beta = oracle.iroot34(n0 + k1 + k2)
+        parts = [r.random(n0), 0.25 + r.random(k1) * (0.5 / beta), 0.25 + 1e-5 + r.random(k2) * 1e-15]
+    else:
+        parts = [r.random(n0), 0.5 + r.random(k2) * 1e-9]
+    x = np.concatenate(parts)
+    r.shuffle(x)
+    return x
+
+
+@pytest.mark.parametrize("n0,k1,k2,embedded", [(1720, 0, 280, False), (3580, 0, 420, False), (2650, 0, 350, False),
+                                                (200_000, 2500, 300, True), (200_000, 1900, 250, True),
+                                                (200_000, 3500, 350, True)])
+def test_team_children_over_warp_capacity(pcf, n0, k1, k2, embedded):
+    """Nodes run by multi-warp groups whose recursing children exceed one warp's keys."""
+    x = _cluster_input(n0, k1, k2, 3, embedded)
+    ref, _ = compare(pcf, x)
+    nd = ref.nodes
+    assert ((nd["level"] >= 2) & (nd["m"] > 256)).any()

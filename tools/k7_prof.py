@@ -28,3 +28,8 @@ busy = cy[16] + cy[17] + cy[18]
 print(f"  warp-cycles in node steps: double teams {cy[16]:.3e}, teams {cy[17]:.3e}, warps {cy[18]:.3e}; "
       f"small-list waits {cy[19]:.3e}")
 print(f"  node-phase warp utilisation {busy / max(16 * nodes_cta, 1):.3f} (busy warp-cycles / (16 warps x node-phase cycles))")
+tp = [cy[i] for i in (3, 14, 15, 20, 21, 22, 23)]
+if sum(tp) and not cy[9] - cy[11]:   # PCF_K7_NPROF build: phases of the 4-warp team nodes
+    names = ["minmax", "samples", "fit", "classify+count", "columns", "placement", "leaves+record"]
+    print("  team-node phases (team-cycles, PCF_K7_NPROF): " + ", ".join(f"{n} {100 * v / sum(tp):.1f}%" for n, v in zip(names, tp))
+          + f"; total {sum(tp):.3e}")
