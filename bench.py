@@ -36,7 +36,7 @@ PASS_NOTE = {"minmax": "8 B/key read, once per global node", "fit": "8 B/sample 
              "classify_hist": "8 B/key read, once per bucketing level (SURVEY.md 8(d))",
              "scatter": "8 B/key read + 8 B/key write, once per bucketing level (SURVEY.md 8(d))",
              "smem_subtree": "8 B/key read + 8 B/key write per key handed to K7",
-             "fallback_sort": "16 B/key per merge pass"}
+             "log_records": "pass-log records of the global nodes (only with a log)"}
 
 
 def workload_config(name, n):
@@ -278,8 +278,9 @@ def run_gpu(args):
     peak, peak_src = load_peaks()
     passes = {}
     notes = {"other": "round plans, count-matrix scans, task generation",
-             "deep_batches": "device-driven batches of oversized recursing buckets (all phases; CUDA-graph loop)"}
-    for k in ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "deep_batches"]:
+             "deep_batches": "device-driven batches of oversized buckets: recursing ones (new global nodes) and "
+                             "Standard-Sort ones (MSD radix splits + K7 sorts); all phases, CUDA-graph loop"}
+    for k in ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "other", "deep_batches"]:
         ms = phase_ms.get(k, 0.0)
         by = phase_bytes.get(k, 0)
         if ms > 0 and by == 0:

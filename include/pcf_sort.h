@@ -99,10 +99,10 @@ typedef struct pcf_stats {
     uint64_t groups_smem;      /* bucket groups finished in shared memory (K7 tasks)         */
     uint64_t split_keys_moved; /* keys moved by the global digit-split rounds (all rounds)    */
     uint64_t global_nodes;     /* bucketing nodes run by the global (multi-CTA) path          */
-    uint64_t fallback_keys_global; /* keys sorted by the global fallback sort               */
+    uint64_t fallback_keys_global; /* keys of Standard-Sort buckets of > 8192 keys (radix splits) */
     /* PCF_FLAG_TIMING: milliseconds per phase, CUDA events on `stream`:
      * [0] min/max  [1] sample+fit  [2] classify+histogram  [3] stable scatter
-     * [4] smem subtree (K7)  [5] global fallback sort + pass-log records  [6] other
+     * [4] smem subtree (K7)  [5] pass-log records of the global nodes  [6] other
      * [7] total  [8] device-driven batches of oversized recursing buckets (all their
      * phases: the host cannot place events inside the device-driven loop) */
     float phase_ms[PCF_PHASES];
@@ -163,7 +163,8 @@ int pcf_sort_u64(const uint64_t *in, uint64_t *out, size_t n, const pcf_params *
  * The sort itself is unchanged (same buckets, same node records); every kernel that
  * moves keys also moves the key's source index: the stable split scatter (global
  * u32 indices), K7 (task-local u16 indices in shared memory, stable tie-break by
- * index in its leaf sorts) and K8 (u32 indices; (key, index) block sort).  Needs
+ * index in its leaf sorts; the stable radix splits of oversized Standard-Sort buckets
+ * keep input order among equal keys).  Needs
  * tau >= 16 (PCF_ERR_INVALID_ARG otherwise: shared-memory room for the indices).
  *
  * pcf_argsort_*: in/out as pcf_sort_*; perm: DEVICE uint32_t[n], 4-byte aligned,

@@ -18,7 +18,7 @@ __all__ = ["build", "lib", "sort", "argsort", "sort_pairs", "bucket_counts", "so
 KEY_F64, KEY_U64 = 0, 1
 KEY_ARGSORT, KEY_PAIRS = 0x10, 0x20   # or'ed into key_type for workspace_bytes
 FLAG_SYNC, FLAG_SAMPLE_ALL, FLAG_TIMING, FLAG_PROFILE, FLAG_EXACT_RANKS = 1, 2, 4, 8, 16
-PHASES = ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "fallback_sort", "other", "total",
+PHASES = ["minmax", "fit", "classify_hist", "scatter", "smem_subtree", "log_records", "other", "total",
           "deep_batches"]
 NPHASES = len(PHASES)
 STATUS = {0: "PCF_OK", 1: "PCF_ERR_INVALID_ARG", 2: "PCF_ERR_NAN", 3: "PCF_ERR_WORKSPACE_TOO_SMALL",

@@ -6,8 +6,9 @@
 //                       k_fit_sample -> k_fit_scan, then split rounds (count, scan,
 //                       scatter, taskgen) until every group fits a K7 CTA; oversized
 //                       recursing buckets become new global nodes (next round);
-//                       then one persistent K7 launch over all groups; K8 for buckets
-//                       that Alg. 1 sends to Standard-Sort and that exceed S_CAP.
+//                       then one persistent K7 launch over all groups.  Buckets that
+//                       Alg. 1 sends to Standard-Sort and that exceed S_CAP are sorted
+//                       by MSD radix splits (the same count / scatter rounds) + K7.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -20,7 +21,6 @@
 #include "pcf_common.cuh"
 #include "pcf_global.cuh"
 #include "pcf_k7.cuh"
-#include "pcf_k8.cuh"
 #include "pcf_bucketing.cuh"
 #include "pcf_shard.cuh"
 
@@ -83,7 +83,7 @@ static Caps caps_for(u64 n, u64 root_n = 0) {
 
 struct Layout {
     size_t ctx, counters, tmp, tidx, digs, tmap, k7_order, bpre_mm, bpre_fs, nodes, arena, k7, splits_a, splits_b, items, fb,
-        k8_tb, k8_mb, k8_flag, cmat, pmat, bsum, status, total;
+        cmat, pmat, bsum, status, total;
 };
 
 static Layout layout_for(const Caps &c, bool pr = false) {   // (caps_for(n, root_n))
@@ -106,11 +106,7 @@ static Layout layout_for(const Caps &c, bool pr = false) {   // (caps_for(n, roo
     L.splits_a = take((size_t)c.split_cap * sizeof(SplitTask));
     L.splits_b = take((size_t)c.split_cap * sizeof(SplitTask));
     L.items = take((size_t)c.items_cap * sizeof(SegItem));
-    L.fb = take((size_t)c.items_cap * sizeof(SegItem));   // fallback (K8) segments
-    L.k8_tb = take(((u64)c.items_cap + 1) * 4);
-    L.k8_mb = take(((u64)c.items_cap + 1) * 4);
-    L.k8_flag = take(((u64)c.items_cap + 1) * 4);
-    L.cmat = take(c.cmat_cap * 4);   // also the K8 merge-path splits (n / K8_MTILE + segments < cmat_cap)
+    L.cmat = take(c.cmat_cap * 4);
     L.pmat = take(c.cmat_cap * 4);
     L.bsum = take(c.bsum_cap * 4);
     L.total = off;
@@ -164,7 +160,7 @@ struct PhaseTimer {
     }
 };
 
-enum { PH_MINMAX = 0, PH_FIT = 1, PH_COUNT = 2, PH_SCATTER = 3, PH_K7 = 4, PH_K8 = 5, PH_OTHER = 6, PH_TOTAL = 7,
+enum { PH_MINMAX = 0, PH_FIT = 1, PH_COUNT = 2, PH_SCATTER = 3, PH_K7 = 4, PH_LOG = 5, PH_OTHER = 6, PH_TOTAL = 7,
        PH_BATCHES = 8 };
 
 // K7 dynamic shared memory: the struct, the node lists (sized for tau) and, in
@@ -255,10 +251,6 @@ static int configure_kernels() {
     CK(cudaFuncSetAttribute(k_split_scatter<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_scatter<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
-    CK(cudaFuncSetAttribute(k8_merge<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
-    CK(cudaFuncSetAttribute(k8_blocksort<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_SORT_SMEM));
-    CK(cudaFuncSetAttribute(k8_merge<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_MERGE_SMEM));
-    CK(cudaFuncSetAttribute(k8_blocksort<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K8_SORT_SMEM));
     done[d] = true;
     return PCF_OK;
 }
@@ -272,21 +264,17 @@ struct Launch {   // the kernel-launch configuration of this device and sort siz
     int count_grid;
     int tau_smem;
     u32 tile_grid;    // one CTA per split tile of a round (upper bound; idle CTAs exit)
-    u32 k8_tiles;     // one CTA per block-sort tile of all fallback segments (upper bound)
-    u32 k8_mtiles;    // one CTA per merge tile (upper bound)
 };
 
 // ---------------------------------------------------------------- device-driven tail (CUDA graph)
 // Everything after the host-launched first batch runs from one executable graph:
 //   k_items_to_nodes -> WHILE (more work) {
 //       batched min/max, sampling, fit of the new global nodes;
-//       two split rounds (plan, tile map, count, scan x3, scatter, taskgen);
+//       two split rounds (plan, tile map, count [model, radix], scan x3, scatter, taskgen);
 //       K7 (order, kernel, advance); k_items_to_nodes }
-//   [phase boundary]
-//   k8_plan -> IF (fallback segments) { k8_check, k8_blocksort }
-//           -> WHILE (merge passes left) { k8_partition, k8_merge, k8_pass_end }
-//           -> IF (pass log) { k_log_finalize }
-// A sort with no oversized bucket runs two kernels here (k_items_to_nodes, k8_plan).
+// k_items_to_nodes turns oversized recursing buckets into global nodes and oversized
+// Standard-Sort buckets into MSD radix splits.  A sort with no oversized bucket runs
+// one kernel here (k_items_to_nodes); with a pass log, k_log_finalize follows.
 // The loop conditions are set on the device (cudaGraphSetConditional), so the
 // recursion over oversized buckets needs no host round trip.
 // Graphs depend only on (device, key type, DevCtx address, tau); they are cached
@@ -297,9 +285,9 @@ struct TailGraph {
     const void *ctx;
     u32 tau;
     u64 n;    // grid bounds depend on it
-    cudaGraph_t g[2];
-    cudaGraphExec_t ex[2];
-    u32 body_kernels, parent_kernels[2], k8_body_kernels;
+    cudaGraph_t g;
+    cudaGraphExec_t ex;
+    u32 body_kernels;
 };
 
 static thread_local std::vector<TailGraph> g_tails;
@@ -310,12 +298,13 @@ static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32
     CK(launch_pdl(k_round_plan, 1, 1024, 0, cs, d_ctx));
     CK(launch_pdl(k_tile_map, lc.nsm * 2, 256, 0, cs, d_ctx));
     CK(launch_pdl(k_split_count_tile<K>, lc.tile_grid, SC_THREADS, 0, cs, d_ctx));
+    CK(launch_pdl(k_split_count_radix<K>, lc.nsm * 8, SC_THREADS, 0, cs, d_ctx));   // Standard-Sort splits
     CK(launch_pdl(k_scanp_partials, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_scanp_final, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_split_scatter<K, PR>, lc.tile_grid, SC_THREADS, split_smem_bytes(), cs, d_ctx));
     CK(launch_pdl(k_split_taskgen, lc.nsm * 2, TG_THREADS, 0, cs, d_ctx));
-    *nk += 8;
+    *nk += 9;
     return PCF_OK;
 }
 
@@ -362,13 +351,12 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
         if (!g_cap[i]) CK(cudaStreamCreateWithFlags(&g_cap[i], cudaStreamNonBlocking));
     cudaStream_t cs = g_cap[0];
     tg.body_kernels = 0;
-    tg.k8_body_kernels = 0;
-    // ---- graph 0: the device-driven batches of oversized recursing buckets
+    // ---- the device-driven batches of oversized buckets
     {
-        CK(cudaGraphCreate(&tg.g[0], 0));
+        CK(cudaGraphCreate(&tg.g, 0));
         cudaGraphConditionalHandle hb;
-        CK(cudaGraphConditionalHandleCreate(&hb, tg.g[0], 0, cudaGraphCondAssignDefault));
-        CK(cudaStreamBeginCaptureToGraph(cs, tg.g[0], nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        CK(cudaGraphConditionalHandleCreate(&hb, tg.g, 0, cudaGraphCondAssignDefault));
+        CK(cudaStreamBeginCaptureToGraph(cs, tg.g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         int rc = PCF_OK;
         auto cap = [&]() -> int {
             CK(launch_pdl(k_items_to_nodes<K>, 1, 1024, 0, cs, d_ctx, hb, 0u));
@@ -392,46 +380,8 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
         const cudaError_t e = cudaStreamEndCapture(cs, &out);
         if (rc) return rc;
         CK(e);
-        tg.parent_kernels[0] = 1;
     }
-    // ---- graph 1: the segmented fallback sort (K8) and the pass-log records
-    {
-        CK(cudaGraphCreate(&tg.g[1], 0));
-        cudaGraphConditionalHandle hs, hk, hl;
-        CK(cudaGraphConditionalHandleCreate(&hs, tg.g[1], 0, cudaGraphCondAssignDefault));
-        CK(cudaGraphConditionalHandleCreate(&hk, tg.g[1], 0, cudaGraphCondAssignDefault));
-        CK(cudaGraphConditionalHandleCreate(&hl, tg.g[1], 0, cudaGraphCondAssignDefault));
-        CK(cudaStreamBeginCaptureToGraph(cs, tg.g[1], nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        auto cap = [&]() -> int {
-            CK(launch_pdl(k8_plan, 1, 1024, 0, cs, d_ctx, hs, hk, hl));
-            int rc = add_cond(cs, hs, cudaGraphCondTypeIf, [&](cudaStream_t bs) -> int {
-                CK(launch_pdl(k8_check, lc.k8_tiles, 256, 0, bs, d_ctx));
-                CK(launch_pdl(k8_passes, 1, 1024, 0, bs, d_ctx, hk));
-                CK(launch_pdl(k8_blocksort<K, PR>, lc.k8_tiles, K8_THREADS, K8_SORT_SMEM, bs, d_ctx));
-                return PCF_OK;
-            });
-            if (rc) return rc;
-            rc = add_cond(cs, hk, cudaGraphCondTypeWhile, [&](cudaStream_t bs) -> int {
-                CK(launch_pdl(k8_partition<K>, (lc.k8_mtiles + 255) / 256, 256, 0, bs, d_ctx));
-                CK(launch_pdl(k8_merge<K, PR>, lc.nsm * 8, K8_MTHREADS, K8_MERGE_SMEM, bs, d_ctx));
-                CK(launch_pdl(k8_pass_end, 1, 1, 0, bs, d_ctx, hk));
-                tg.k8_body_kernels = 3;
-                return PCF_OK;
-            });
-            if (rc) return rc;
-            return add_cond(cs, hl, cudaGraphCondTypeIf, [&](cudaStream_t bs) -> int {
-                CK(launch_pdl(k_log_finalize<K>, lc.nsm * 4, 256, 0, bs, d_ctx));
-                return PCF_OK;
-            });
-        };
-        const int rc = cap();
-        cudaGraph_t out;
-        const cudaError_t e = cudaStreamEndCapture(cs, &out);
-        if (rc) return rc;
-        CK(e);
-        tg.parent_kernels[1] = 1;   // k8_plan; the IF bodies are counted from the device counters
-    }
-    for (int i = 0; i < 2; ++i) CK(cudaGraphInstantiate(&tg.ex[i], tg.g[i], 0));
+    CK(cudaGraphInstantiate(&tg.ex, tg.g, 0));
     return PCF_OK;
 }
 
@@ -444,7 +394,8 @@ static int get_tail(const DevCtx *d_ctx, u32 tau, u64 n, const Launch &lc, TailG
     constexpr size_t MAX_TAILS = 8;
     if (g_tails.size() >= MAX_TAILS) {   // evict the oldest
         TailGraph &o = g_tails.front();
-        for (int i = 0; i < 2; ++i) { cudaGraphExecDestroy(o.ex[i]); cudaGraphDestroy(o.g[i]); }
+        cudaGraphExecDestroy(o.ex);
+        cudaGraphDestroy(o.g);
         g_tails.erase(g_tails.begin());
     }
     TailGraph tg;
@@ -452,7 +403,8 @@ static int get_tail(const DevCtx *d_ctx, u32 tau, u64 n, const Launch &lc, TailG
     tg.dev = dev; tg.kt = kt; tg.ctx = d_ctx; tg.tau = tau; tg.n = n;
     const int rc = build_tail<K, PR>(tg, d_ctx, lc);
     if (rc) {
-        for (int i = 0; i < 2; ++i) { if (tg.ex[i]) cudaGraphExecDestroy(tg.ex[i]); if (tg.g[i]) cudaGraphDestroy(tg.g[i]); }
+        if (tg.ex) cudaGraphExecDestroy(tg.ex);
+        if (tg.g) cudaGraphDestroy(tg.g);
         return rc;
     }
     g_tails.push_back(tg);
@@ -610,12 +562,6 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.splits_cap = caps.split_cap;
         hc.items = (SegItem *)(ws + L.items);
         hc.items_cap = caps.items_cap;
-        hc.fb = (SegItem *)(ws + L.fb);
-        hc.fb_cap = caps.items_cap;
-        hc.k8_tb = (u32 *)(ws + L.k8_tb);
-        hc.k8_mb = (u32 *)(ws + L.k8_mb);
-        hc.k8_flag = (u32 *)(ws + L.k8_flag);
-        hc.k8_sp = (u32 *)(ws + L.cmat);   // free once the split rounds are done
         hc.cmat = (u32 *)(ws + L.cmat);
         hc.pmat = (u32 *)(ws + L.pmat);
         hc.bsum = (u32 *)(ws + L.bsum);
@@ -652,8 +598,6 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     lc.tau_smem = k7_smem_bytes(p.tau, PR);
     // fallback segments hold > S_CAP keys each: <= n / S_CAP partial tiles
     lc.tile_grid = (u32)std::min<u64>(n / SPLIT_TILE + 4096, 0x7fffffffull);
-    lc.k8_tiles = (u32)(n / K8_TILE + n / S_CAP + 2);
-    lc.k8_mtiles = (u32)(n / K8_MTILE + n / S_CAP + 2);
 
     // initial counters (host-built: the root node and its tables are carved here)
     Counters h0;
@@ -790,12 +734,15 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         rc = get_tail<K, PR>(d_ctx, p.tau, n, lc, &tail);
         if (rc) return rc;
         tm.begin(PH_BATCHES);
-        CK(cudaGraphLaunch(tail->ex[0], st));
+        CK(cudaGraphLaunch(tail->ex, st));
         tm.end();
-        tm.begin(PH_K8);
-        CK(cudaGraphLaunch(tail->ex[1], st));
-        tm.end();
-        launches += tail->parent_kernels[0] + tail->parent_kernels[1];
+        launches += 1;   // k_items_to_nodes; the loop bodies are counted from the device counters
+        if (logging) {   // the records of the global nodes (all levels)
+            tm.begin(PH_LOG);
+            CK(launch_pdl(k_log_finalize<K>, lc.nsm * 4, 256, 0, st, d_ctx));
+            tm.end();
+            launches += 1;
+        }
     }
     if (p.status_out) {
         k_status<<<1, 1, 0, st>>>(d_ctx, p.status_out);
@@ -821,8 +768,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         stats.split_keys_moved = hcnt.split_keys;
         stats.fallback_keys_global = hcnt.fb_keys;
         if (tail) {
-            launches += hcnt.iters * tail->body_kernels + hcnt.k8.max_merges * tail->k8_body_kernels
-                        + (hcnt.k8.nseg ? 3 : 0) + (logging ? 1 : 0);
+            launches += hcnt.iters * tail->body_kernels;
             stats.device_batches = hcnt.iters;
         }
         if (!small) {
@@ -832,7 +778,6 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             bytes[PH_COUNT] = 8ull * hcnt.global_keys;
             bytes[PH_SCATTER] = 16ull * hcnt.global_keys;
             bytes[PH_K7] = 16ull * hcnt.k7_keys;
-            bytes[PH_K8] = hcnt.k8_bytes;
             bytes[PH_MINMAX] = 8ull * hcnt.global_keys;
         }
     }

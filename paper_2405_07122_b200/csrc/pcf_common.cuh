@@ -252,7 +252,7 @@ struct K7Task {
     u32 level;      // K7_NODE: level of this node; K7_GROUP: level of `node`
     u32 node;
     u32 jlo, jhi;
-    u32 pad;
+    u32 pad;        // K7_SORT: 1 = the keys are all equal (copied, not sorted)
 };
 
 // A global split: stable partition of a segment by digit (j - jlo) >> shift.
@@ -299,16 +299,6 @@ struct BatchInfo {
     u64 a0, a1;
 };
 
-// Segmented fallback sort (K8) over every Standard-Sort bucket of > S_CAP keys.
-struct K8Plan {
-    u32 nseg;
-    u32 tiles;       // block-sort tiles over all segments
-    u32 mtiles;      // merge tiles over all segments
-    u32 max_merges;  // merge passes of the largest segment
-    u32 pass;        // current merge pass
-    u32 pad;
-};
-
 // Device counters of one sort (zeroed / initialised by the host at the start of
 // every call; read back only when the caller asks for a synchronous call).
 struct Counters {
@@ -316,10 +306,9 @@ struct Counters {
     u32 nsplits[2], nitems, k7_begin;
     unsigned long long rec_count, k7_keys, split_keys, global_keys;
     RoundPlan plan;
-    u32 round, node_count, fb_count, iters;   // iters: device-driven batches run
-    unsigned long long arena_used, k8_bytes, fb_keys;
+    u32 round, node_count, pad0, iters;   // iters: device-driven batches run
+    unsigned long long arena_used, fb_keys;   // fb_keys: keys of Standard-Sort buckets > S_CAP
     BatchInfo batch;
-    K8Plan k8;
     unsigned long long k7_prof[K7_PROF_SLOTS_DECL];
 };
 
@@ -369,11 +358,6 @@ struct DevCtx {
     u32 *arena;
     u64 arena_cap;
     u32 *bpre_mm, *bpre_fs;   // [node_cap + 1]
-    // fallback (K8) segments
-    SegItem *fb;
-    u32 fb_cap;
-    u32 *k8_tb, *k8_mb, *k8_flag;   // per segment: first tile, first merge tile, "two distinct keys"
-    u32 *k8_sp;                     // merge-path split of every merge tile
     // pass log
     NodeRec *rec;
     unsigned long long *rec_count;

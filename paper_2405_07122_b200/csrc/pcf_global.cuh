@@ -270,9 +270,24 @@ __global__ void __launch_bounds__(FSB_CHUNK) k_fit_sample_batch(const DevCtx *__
     }
 }
 
+constexpr u32 RADIX_BITS = 10;   // digit bits of a Standard-Sort (MSD radix) split: G <= 1024 = GMAX
+static_assert((1u << RADIX_BITS) <= (u32)GMAX, "radix digits");
+
+// The first MSD radix split of a Standard-Sort bucket of m > S_CAP keys:
+// the top RADIX_BITS bits of the ordered keys.
+__device__ __forceinline__ SplitTask radix_split(u64 off, u32 m, u32 src, u32 shift) {
+    SplitTask s;
+    s.off = off; s.m = m; s.node = 0xffffffffu; s.jlo = 0; s.jhi = 0;
+    s.shift = shift; s.G = 1u << (64u - shift < RADIX_BITS ? 64u - shift : RADIX_BITS);
+    s.src = src; s.dst = src == 1 ? 2 : 1;
+    s.tile_begin = 0; s.ntiles = 0; s.cbase = 0; s.mbase = 0;
+    return s;
+}
+__device__ __forceinline__ u32 radix_next_shift(u32 shift) { return shift >= RADIX_BITS ? shift - RADIX_BITS : 0u; }
+
 // Oversized recursing buckets (items of kind 0) -> new global nodes of the next
 // batch, with their tables carved from the arena and their first split appended
-// to the next round's list; Standard-Sort items (kind 1) -> the K8 segment list.
+// to the next round's list; Standard-Sort items (kind 1) -> an MSD radix split (same list).
 // One CTA; consumes every item and resets the item count.  This replaces the
 // host round trip of the previous design (recursion per bucket).
 template <class K>
@@ -358,10 +373,12 @@ __global__ void __launch_bounds__(1024) k_items_to_nodes(const DevCtx *__restric
             }
             atomicAdd(&C.global_keys, (unsigned long long)it.m);
         }
-        if (isf) {
-            const u32 k = nfb + ex_f, fi = C.fb_count + k;
-            if (fi < c->fb_cap) c->fb[fi] = it;
+        if (isf) {   // Standard-Sort of a bucket of > S_CAP keys: MSD radix splits
+            const SplitTask sp = radix_split(it.off, it.m, it.src, 64u - RADIX_BITS);
+            const u32 slot = atomicAdd(&C.nsplits[cur], 1u);
+            if (slot < c->splits_cap) c->splits[cur][slot] = sp;
             else atomicOr(c->err_flag, 1u);
+            atomicAdd(&C.fb_keys, (unsigned long long)it.m);
         }
         nb += tot_n; nfb += tot_f; cmm += tot_mm; cfs += tot_fs; arena += tot_a;
     }
@@ -375,7 +392,7 @@ __global__ void __launch_bounds__(1024) k_items_to_nodes(const DevCtx *__restric
         C.batch = bi;
         C.node_count = first + bi.nb;
         C.arena_used = bi.a1;
-        C.fb_count = min(C.fb_count + nfb, c->fb_cap);
+        (void)nfb;
         C.nitems = 0;
         // condition of the batch loop (a CUDA-graph WHILE node): another batch runs iff
         // this one made new global nodes or left unfinished splits (and no error)
@@ -454,6 +471,11 @@ __global__ void k_tile_map(const DevCtx *__restrict__ c) {
         for (u32 t = threadIdx.x; t < nt; t += blockDim.x) c->tmap[tb + t] = si;
     }
 }
+
+// A Standard-Sort split (jhi == 0; model splits have jhi >= 2): an MSD radix pass on
+// ordered-key bits [shift, shift + log2 G) of a bucket that Alg. 1 sends to Standard-Sort
+// (PAPER.md:162-163); jlo bit 0 is set by the count pass if the split holds two distinct keys.
+__host__ __device__ __forceinline__ bool is_radix(const SplitTask &st) { return st.jhi == 0; }
 
 template <class K>
 __device__ __forceinline__ u32 digit_of(u64 okey, const Model &md, const u32 *__restrict__ T, u32 jlo, u32 shift) {
@@ -667,16 +689,17 @@ __global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_tile(const DevCtx
     for (u32 tile = blockIdx.x; tile < pl.tiles; tile += gridDim.x) {
     const u32 s = c->tmap[tile];
     const SplitTask st = L[s];
+    if (is_radix(st)) continue;   // k_split_count_radix (uniform per CTA)
     const u32 lt = tile - st.tile_begin;
-    const GNode &g = c->nodes[st.node];
     if (tile != blockIdx.x) __syncthreads();   // the previous tile's histogram is written out
     for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) hist[d] = 0;
     const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
-    const bool deg = g.degenerate != 0;
+    const bool deg = c->nodes[st.node].degenerate != 0;
     __syncthreads();
     if (deg) {
         if (threadIdx.x == 0) hist[0] = k1 - k0;
     } else {
+        const GNode &g = c->nodes[st.node];
         const Model md = g.md;
         const u64 *x = c->buf[st.src] + st.off;
         const u32 *T = g.T;
@@ -714,6 +737,53 @@ __global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_tile(const DevCtx
     }
     __syncthreads();
     for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
+    }
+}
+
+// The count pass of the Standard-Sort (MSD radix) splits of a round: digit = ordered-key bits
+// [shift, shift + log2 G); also sets jlo bit 0 of a split that holds two distinct keys.
+// Grid-stride over the round's tiles; tiles of model splits are k_split_count_tile's.
+template <class K>
+__global__ void __launch_bounds__(SC_THREADS, 2) k_split_count_radix(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    __shared__ u32 hist[GMAX];
+    if (*c->nan_flag) return;
+    const RoundPlan pl = *c->plan;
+    SplitTask *L = c->splits[pl.cur];
+    u32 *__restrict__ C = c->cmat;
+    bool first_tile = true;
+    for (u32 tile = blockIdx.x; tile < pl.tiles; tile += gridDim.x) {
+        const u32 s = c->tmap[tile];
+        const SplitTask st = L[s];
+        if (!is_radix(st)) continue;
+        const u32 lt = tile - st.tile_begin;
+        if (!first_tile) __syncthreads();   // the previous tile's histogram is written out
+        first_tile = false;
+        for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) hist[d] = 0;
+        const u32 k0 = lt * SPLIT_TILE, k1 = min(st.m, k0 + SPLIT_TILE);
+        __syncthreads();
+        const u64 *x = c->buf[st.src] + st.off;
+        u16 *dg = c->digs + st.off;
+        const u64 first = K::to_okey(x[0]);
+        const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const u32 r0 = k0 + w * SC_PER_WARP + lane;
+        u64 ok[SC_KPL];
+#pragma unroll
+        for (u32 q = 0; q < SC_KPL; ++q) { const u32 k = r0 + q * 32; ok[q] = K::to_okey(k < k1 ? x[k] : x[k0]); }
+        bool diff = false;
+#pragma unroll
+        for (u32 q = 0; q < SC_KPL; ++q) {
+            const u32 k = r0 + q * 32;
+            if (k < k1) {
+                const u32 d = (u32)(ok[q] >> st.shift) & (st.G - 1u);
+                diff |= ok[q] != first;
+                dg[k] = (u16)d;
+                atomicAdd(&hist[d], 1u);
+            }
+        }
+        if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(&L[s].jlo, 1u);   // two distinct keys
+        __syncthreads();
+        for (u32 d = threadIdx.x; d < st.G; d += SC_THREADS) C[st.cbase + (u64)d * st.ntiles + lt] = hist[d];
     }
 }
 
@@ -962,7 +1032,7 @@ struct SplitScatterSmem {
 template <class K, bool FULL, bool PR>
 __device__ __forceinline__ void split_scatter_tile(const DevCtx *__restrict__ c, SplitScatterSmem &S, const SplitTask &st,
                                                    u32 lt, const u32 *__restrict__ P) {
-    const u32 deg = c->nodes[st.node].degenerate;   // checked after the tile's loads are issued
+    const u32 deg = !is_radix(st) && c->nodes[st.node].degenerate;   // checked after the tile's loads are issued
     const u64 *x = c->buf[st.src] + st.off;
     u64 *y = c->buf[st.dst] + st.off;
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1151,6 +1221,76 @@ __device__ __forceinline__ void make_run_task(const DevCtx *c, const SplitTask &
 }
 
 constexpr int TG_THREADS = 256;
+
+// Tasks of a Standard-Sort split after its scatter: runs of consecutive digit groups of
+// <= S_CAP keys become K7_SORT tasks (the groups are in key order, so sorting the run sorts
+// every group); larger groups become the next radix split (the next lower bits); a split
+// whose keys are all equal (count pass) or whose bits are exhausted is sorted as it lies,
+// in K7_SORT chunks of <= S_CAP keys.  A few warps' worth of work per split.
+__device__ void radix_taskgen(const DevCtx *__restrict__ c, const SplitTask &st, const u32 *__restrict__ P, u32 nxt,
+                              u32 *dcnt, u8 *dpack) {
+    const u32 lane = threadIdx.x & 31;
+    auto emit = [&](u64 off, u32 keys, u32 presorted) {
+        K7Task t;
+        t.off = off; t.size = keys; t.kind = K7_SORT; t.src = st.dst; t.level = 0; t.node = 0xffffffffu;
+        t.jlo = 0; t.jhi = 0; t.pad = presorted;
+        push_k7(c, t);
+    };
+    auto emit_chunks = [&](u64 off, u32 m, u32 t0, u32 nt) {   // keys all equal: sorted as they lie (copied)
+        for (u32 k = t0 * (u32)S_CAP; k < m; k += nt * (u32)S_CAP) emit(off + k, min((u32)S_CAP, m - k), 1u);
+    };
+    if (!(st.jlo & 1u)) {   // all keys of the split are equal
+        emit_chunks(st.off, st.m, threadIdx.x, TG_THREADS);
+        return;
+    }
+    for (u32 d = threadIdx.x; d < st.G; d += TG_THREADS) {
+        const u32 start = P[st.cbase + (u64)d * st.ntiles] - (u32)st.mbase;
+        const u32 end = d + 1 < st.G ? P[st.cbase + (u64)(d + 1) * st.ntiles] - (u32)st.mbase : st.m;
+        const u32 cn = end - start;
+        dcnt[d] = cn;
+        dpack[d] = cn <= (u32)S_CAP ? 1 : 0;
+        if (cn > (u32)S_CAP) {
+            if (st.shift == 0) {   // every bit consumed: the group's keys are equal
+                emit_chunks(st.off + start, cn, 0, 1);
+            } else {               // the next lower bits
+                const SplitTask nt = radix_split(st.off + start, cn, st.dst, radix_next_shift(st.shift));
+                const u32 slot = atomicAdd(&c->nsplits[nxt], 1u);
+                if (slot < c->splits_cap) c->splits[nxt][slot] = nt;
+                else atomicOr(c->err_flag, 1u);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    // warp 0, in digit order: greedy next-fit runs of packable groups of <= S_CAP keys
+    u32 run_start = 0, run_keys = 0, pos = 0;
+    for (u32 base = 0; base < st.G; base += 32) {
+        const u32 d = base + lane;
+        const u32 cn = d < st.G ? dcnt[d] : 0u;
+        const u32 pk = d < st.G ? (u32)dpack[d] : 1u;
+        const u32 nk = min(32u, st.G - base);
+        for (u32 k = 0; k < nk; ++k) {
+            const u32 ck = __shfl_sync(0xffffffffu, cn, k);
+            const bool pkk = __shfl_sync(0xffffffffu, pk, k) != 0;
+            if (!pkk) {
+                if (run_keys && lane == 0) emit(st.off + run_start, run_keys, 0u);
+                run_keys = 0;
+                pos += ck;
+                run_start = pos;
+            } else {
+                if (run_keys + ck > (u32)S_CAP) {
+                    if (run_keys && lane == 0) emit(st.off + run_start, run_keys, 0u);
+                    run_keys = 0;
+                    run_start = pos;
+                }
+                run_keys += ck;
+                pos += ck;
+            }
+        }
+    }
+    if (run_keys && lane == 0) emit(st.off + run_start, run_keys, 0u);
+}
+
 __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__restrict__ c) {
     pdl_entry();
     __shared__ u32 dcnt[GMAX];
@@ -1164,6 +1304,11 @@ __global__ void __launch_bounds__(TG_THREADS) k_split_taskgen(const DevCtx *__re
     const u32 lane = threadIdx.x & 31;
     for (u32 si = blockIdx.x; si < pl.ns; si += gridDim.x) {   // one CTA per split
         const SplitTask st = c->splits[cur][si];
+        if (is_radix(st)) {   // Standard-Sort split: its own task generation
+            __syncthreads();
+            radix_taskgen(c, st, P, nxt, dcnt, dpack);
+            continue;
+        }
         GNode &g = c->nodes[st.node];
         if (g.degenerate) continue;
         __syncthreads();

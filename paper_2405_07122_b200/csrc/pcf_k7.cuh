@@ -122,6 +122,93 @@ __device__ __forceinline__ u32 rank_in_leaf(const u64 *B, u32 st, u32 h, u64 v, 
     return h - r;
 }
 
+// ------------------------------------------------------------------ Standard-Sort of a whole task (R2)
+// Sort the NT * 8 ordered keys at X (keys-only; positions >= m are padding) into Y by
+// one CTA of NT threads: each thread sorts 8 keys with Batcher's 19-comparator network,
+// each warp merges its runs up to 256 keys in registers (bitonic merges over lane
+// shuffles), then log2(NT / 32) merge-path levels through shared memory (each thread
+// emits 8 consecutive outputs).  Padding (~0) sorts last.  X and Y are both written;
+// the result ends in Y.  Ends with __syncthreads().
+__device__ __forceinline__ void cx8(u64 &a, u64 &b) { const u64 x = a < b ? a : b; b = a < b ? b : a; a = x; }
+__device__ __forceinline__ u32 mp_split(const u64 *A, u32 la, const u64 *B, u32 lb, u32 d) {   // A first among equal keys
+    u32 lo = d > lb ? d - lb : 0, hi = d < la ? d : la;
+    while (lo < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (A[mid] <= B[d - 1 - mid]) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+template <int NT>
+__device__ void block_sort_tile(u64 *X, u64 *Y, u32 m) {
+    constexpr u32 IPT = 8, TILE = NT * IPT;
+    const u32 t = threadIdx.x, L = t & 31, t0 = t * IPT;
+    u64 r[IPT];
+#pragma unroll
+    for (u32 k = 0; k < IPT; ++k) {   // rotated loads (fewer bank conflicts); the network sorts them anyway
+        const u32 p = t0 + ((k + t) & (IPT - 1));
+        r[k] = p < m ? X[p] : ~0ull;
+    }
+    cx8(r[0], r[1]); cx8(r[2], r[3]); cx8(r[4], r[5]); cx8(r[6], r[7]);
+    cx8(r[0], r[2]); cx8(r[1], r[3]); cx8(r[4], r[6]); cx8(r[5], r[7]);
+    cx8(r[1], r[2]); cx8(r[5], r[6]);
+    cx8(r[0], r[4]); cx8(r[1], r[5]); cx8(r[2], r[6]); cx8(r[3], r[7]);
+    cx8(r[2], r[4]); cx8(r[3], r[5]);
+    cx8(r[1], r[2]); cx8(r[3], r[4]); cx8(r[5], r[6]);
+    // runs of 16 .. 256 keys inside the warp: element i = 8 lane + q; each stage compares i with
+    // its mirror i ^ (k - 1), then half-cleaners i ^ j
+#pragma unroll
+    for (u32 k = 16; k <= 32u * IPT; k <<= 1) {
+        {
+            const bool lo = (L & (k / (2 * IPT))) == 0;
+            u64 pv[IPT];
+#pragma unroll
+            for (int q = 0; q < (int)IPT; ++q) pv[q] = __shfl_xor_sync(0xffffffffu, r[IPT - 1 - q], k / IPT - 1);
+#pragma unroll
+            for (int q = 0; q < (int)IPT; ++q) r[q] = (lo == (pv[q] < r[q])) ? pv[q] : r[q];
+        }
+#pragma unroll
+        for (u32 j = k / 4; j >= 1; j >>= 1) {
+            if (j >= IPT) {
+                const bool lo = (L & (j / IPT)) == 0;
+#pragma unroll
+                for (int q = 0; q < (int)IPT; ++q) {
+                    const u64 pv = __shfl_xor_sync(0xffffffffu, r[q], j / IPT);
+                    r[q] = (lo == (pv < r[q])) ? pv : r[q];
+                }
+            } else {
+#pragma unroll
+                for (u32 q = 0; q < IPT; ++q)
+                    if (!(q & j)) cx8(r[q], r[q | j]);
+            }
+        }
+    }
+    // merge levels 256 -> TILE through shared memory; an odd number of levels starts in X
+    constexpr u32 LEVELS = NT >= 1024 ? 5 : NT >= 512 ? 4 : NT >= 256 ? 3 : NT >= 128 ? 2 : 1;
+    static_assert((32u << LEVELS) == (u32)NT, "NT must be a power of two >= 64");
+    u64 *sa = (LEVELS & 1) ? X : Y, *sb = (LEVELS & 1) ? Y : X;
+    __syncthreads();   // every thread's loads of X are done
+#pragma unroll
+    for (u32 k = 0; k < IPT; ++k) sa[t0 + k] = r[k];
+    __syncthreads();
+    for (u32 run = 32 * IPT; run < TILE; run <<= 1) {
+        const u32 p0 = (t0 / (2 * run)) * (2 * run), d = t0 - p0;
+        const u64 *A = sa + p0, *B = sa + p0 + run;
+        u32 ia = mp_split(A, run, B, run, d), ib = d - ia;
+        u64 xa = ia < run ? A[ia] : ~0ull, xb = ib < run ? B[ib] : ~0ull;
+#pragma unroll
+        for (u32 k = 0; k < IPT; ++k) {
+            const bool ta = ib >= run || (ia < run && xa <= xb);
+            r[k] = ta ? xa : xb;
+            if (ta) { ++ia; xa = ia < run ? A[ia] : ~0ull; }
+            else { ++ib; xb = ib < run ? B[ib] : ~0ull; }
+        }
+#pragma unroll
+        for (u32 k = 0; k < IPT; ++k) sb[t0 + k] = r[k];
+        __syncthreads();
+        u64 *tmp = sa; sa = sb; sb = tmp;
+    }
+}
+
 // ------------------------------------------------------------------ global I/O
 __device__ __forceinline__ ulonglong2 ld_stream2(const ulonglong2 *p) {
     ulonglong2 r;

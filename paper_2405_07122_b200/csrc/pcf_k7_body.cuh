@@ -735,7 +735,9 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
         const K7Task task = S.task;
         u64 *gout = c->buf[2] + task.off;
         const u32 M = task.size;
-        const bool sort_task = task.kind == K7_SORT || (task.kind == K7_NODE && M < c->tau);
+        // pad != 0: a K7_SORT chunk of equal keys (Standard-Sort split of one key value): copied
+        const bool presorted = task.kind == K7_SORT && task.pad != 0;
+        const bool sort_task = !presorted && (task.kind == K7_SORT || (task.kind == K7_NODE && M < c->tau));
         u64 *dst = sort_task ? S.B : S.A;
         bool nan_here = false;
         mbar_wait(&S.tbar, it & 1u);
@@ -770,8 +772,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
         __syncthreads();
         prof_mark(c, S, 1);
         if (threadIdx.x == 0 && c->k7_prof) { S.prof[11] += 1; S.prof[12] += M; }
-        if (sort_task) {
-            sort_range<K7_WARPS, PR>(S, 0, M, CT);
+        if (presorted) {
+        } else if (sort_task) {
+            if (!PR && K7_THREADS * 8 == S_CAP && M > SMALL_MAX) block_sort_tile<K7_THREADS>(S.B, S.A, M);   // B -> A
+            else sort_range<K7_WARPS, PR>(S, 0, M, CT);
             prof_mark(c, S, 6);
         } else {
             u32 Lb;

@@ -11,7 +11,7 @@
 // Buckets are then dealt out to ranks as contiguous ranges [J_r, J_{r+1}) of about
 // N / R keys, every rank sends its keys of range r to rank r in input (stable)
 // order, and rank r sorts its range -- the rest of Alg. 1 for those buckets --
-// with the single-GPU machinery (split rounds, K7, K8) at global offset
+// with the single-GPU machinery (split rounds, K7, the radix Standard-Sort) at global offset
 // O_r = sum_{j < J_r} H[j], so every deeper node has the single-GPU sampler key
 // and record.  The concatenation of the ranks' outputs is the single-GPU output.
 #pragma once

@@ -110,7 +110,7 @@ def test_argsort_patterns(pcf):
 
 @pytest.mark.gpu
 def test_argsort_full_size_c3(pcf):
-    """c3 at its BASELINE.json size (1e8, a 10^7-key duplicate bucket: K8 + stability)."""
+    """c3 at its BASELINE.json size (1e8, a 10^7-key duplicate bucket: the radix Standard-Sort + stability)."""
     check_argsort(pcf, synth.config("c3"))
 
 

@@ -202,7 +202,7 @@ def test_batched_degenerate_and_sample_all_nodes(pcf):
 def test_async_no_host_sync(pcf, name, n):
     """Without PCF_FLAG_SYNC the call never waits for the GPU: the recursion over
     oversized buckets and the fallback sort are decided on the
-    device.  c2 (one device batch), c4 (a ~10^8-key fallback bucket, the K8 loop)
+    device.  c2 (one device batch), c4 (a ~10^8-key Standard-Sort bucket: radix splits)
     and LogNormal 1e8 (thousands of oversized recursing buckets, several device
     batches); output and the status word must match the synchronous call / oracle."""
     x = synth.config(name, n=n)

@@ -16,7 +16,7 @@ cap c5f k_split_count_tile 0 k_split_count_tile_r2_c5f
 cap c5f k_split_scatter 0 k_split_scatter_r1_c5f
 cap c5f k_split_scatter 1 k_split_scatter_r2_c5f
 cap c2 k7_kernel 0 k7_kernel_c2
-# K8 runs inside CUDA-graph conditional nodes: its per-kernel times from a launch list of c4
+# the Standard-Sort radix rounds run inside CUDA-graph conditional nodes (not profiled per kernel); c4 launch list
 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $O/launches_c4.csv \
     python tools/prof_run.py --config c4 --reps 1 > $O/ncu_launch_c4.log 2>&1
 # summaries on the box (ncu -i), then drop the multi-MB reports (gpurun_out is capped at 64 MiB)

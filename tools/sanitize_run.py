@@ -1,7 +1,7 @@
 """Workload for compute-sanitizer: a few sorts through the C ABI
 that exercise every kernel family -- the single-task K7 path, the split rounds
 (bulk-copy count kernel, scatter, taskgen), K7's team / warp node lists and
-mbarrier bulk copies, the batched global nodes, K8 -- each checked against the
+mbarrier bulk copies, the batched global nodes, the radix Standard-Sort -- each checked against the
 oracle.  Sizes are kept small (sanitizers slow kernels down 10-1000x).
 
   python tools/sanitize_run.py [scale]     # scale 1.0 = default sizes
