@@ -182,10 +182,12 @@ static bool k7_wide(u32 tau, bool pr) {
 static int k7_smem_bytes(u32 tau, bool pr) {
     return (int)(k7_wide(tau, pr) ? k7w::Variant::smem(tau, pr) : k7s::Variant::smem(tau, pr));
 }
+// K7 instance: block size (wide: 1024 threads), key-value mode, pass log (the logging code
+// is compiled out of the benchmarked instance: fewer live registers, fewer spills)
 template <class K, bool PR>
-static void (*k7_fn(bool wide))(const DevCtx *) {
-    if constexpr (!PR) { if (wide) return k7w::k7_kernel<K, false>; }
-    return k7s::k7_kernel<K, PR>;
+static void (*k7_fn(bool wide, bool log))(const DevCtx *) {
+    if constexpr (!PR) { if (wide) return log ? k7w::k7_kernel<K, false, true> : k7w::k7_kernel<K, false, false>; }
+    return log ? k7s::k7_kernel<K, PR, true> : k7s::k7_kernel<K, PR, false>;
 }
 static int split_smem_bytes() { return (int)sizeof(SplitScatterSmem); }
 
@@ -222,7 +224,7 @@ static int k7_ctas_per_sm(bool wide) {   // resident K7 CTAs per SM (persistent 
         int b = 1;
         const int nt = wide ? k7w::Variant::threads : k7s::Variant::threads;
         const int sm = (int)(wide ? k7w::Variant::smem(K7W_MIN_TAU, false) : k7s::Variant::smem(PR ? PR_MIN_TAU : 2, PR));
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k7_fn<K, PR>(wide), nt, sm) != cudaSuccess || b < 1) b = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k7_fn<K, PR>(wide, false), nt, sm) != cudaSuccess || b < 1) b = 1;
         v[wide][d] = b;
     }
     return v[wide][d];
@@ -245,9 +247,11 @@ static int configure_kernels() {
     static thread_local bool done[MAX_DEVS] = {false};
     const int d = cur_dev();
     if (done[d]) return PCF_OK;
-    CK(cudaFuncSetAttribute(k7s::k7_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7s::Variant::smem(2, false)));
-    CK(cudaFuncSetAttribute(k7s::k7_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7s::Variant::smem(PR_MIN_TAU, true)));
-    CK(cudaFuncSetAttribute(k7w::k7_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7w::Variant::smem(K7W_MIN_TAU, false)));
+    for (int lg = 0; lg < 2; ++lg) {
+        CK(cudaFuncSetAttribute(k7_fn<K, false>(false, lg), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7s::Variant::smem(2, false)));
+        CK(cudaFuncSetAttribute(k7_fn<K, true>(false, lg), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7s::Variant::smem(PR_MIN_TAU, true)));
+        CK(cudaFuncSetAttribute(k7_fn<K, false>(true, lg), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k7w::Variant::smem(K7W_MIN_TAU, false)));
+    }
     CK(cudaFuncSetAttribute(k_split_scatter<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_scatter<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, split_smem_bytes()));
     CK(cudaFuncSetAttribute(k_split_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
@@ -261,6 +265,7 @@ struct Launch {   // the kernel-launch configuration of this device and sort siz
     int k7_grid;
     int k7_threads;
     bool k7_wide;
+    bool log;         // pass log on: the logging K7 instance
     int count_grid;
     int tau_smem;
     u32 tile_grid;    // one CTA per split tile of a round (upper bound; idle CTAs exit)
@@ -281,7 +286,7 @@ struct Launch {   // the kernel-launch configuration of this device and sort siz
 // per thread (a repeated sort with the same workspace reuses them).
 struct TailGraph {
     int dev;
-    int kt;   // key type * 2 + key-value mode
+    int kt;   // key type * 4 + key-value mode * 2 + pass log (selects the K7 instance)
     const void *ctx;
     u32 tau;
     u64 n;    // grid bounds depend on it
@@ -311,7 +316,7 @@ static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32
 template <class K, bool PR>
 static int add_k7(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32 *nk) {
     CK(launch_pdl(k_k7_order, 1, 1024, 0, cs, d_ctx));
-    CK(launch_pdl(k7_fn<K, PR>(lc.k7_wide), lc.k7_grid, lc.k7_threads, lc.tau_smem, cs, d_ctx));
+    CK(launch_pdl(k7_fn<K, PR>(lc.k7_wide, lc.log), lc.k7_grid, lc.k7_threads, lc.tau_smem, cs, d_ctx));
     CK(launch_pdl(k_k7_advance, 1, 1, 0, cs, d_ctx));
     *nk += 3;
     return PCF_OK;
@@ -388,7 +393,7 @@ static int build_tail(TailGraph &tg, const DevCtx *d_ctx, const Launch &lc) {
 template <class K, bool PR>
 static int get_tail(const DevCtx *d_ctx, u32 tau, u64 n, const Launch &lc, TailGraph **out) {
     const int dev = cur_dev();
-    const int kt = (K::is_f64 ? 0 : 2) + (PR ? 1 : 0);
+    const int kt = (K::is_f64 ? 0 : 4) + (PR ? 2 : 0) + (lc.log ? 1 : 0);
     for (auto &t : g_tails)
         if (t.dev == dev && t.kt == kt && t.ctx == d_ctx && t.tau == tau && t.n == n) { *out = &t; return PCF_OK; }
     constexpr size_t MAX_TAILS = 8;
@@ -592,6 +597,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     Launch lc;
     lc.nsm = nsm;
     lc.k7_wide = k7_wide(p.tau, PR);
+    lc.log = logging;
     lc.k7_threads = lc.k7_wide ? k7w::Variant::threads : k7s::Variant::threads;
     lc.k7_grid = nsm * k7_ctas_per_sm<K, PR>(lc.k7_wide);
     lc.count_grid = nsm * count_ctas_per_sm<K>();
@@ -614,7 +620,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         t.off = 0; t.size = (u32)n; t.kind = K7_NODE; t.src = 0; t.level = 1;
         CK(cudaMemcpyAsync(hc.k7, &t, sizeof t, cudaMemcpyHostToDevice, st));
         tm.begin(PH_K7);
-        k7_fn<K, PR>(lc.k7_wide)<<<1, lc.k7_threads, lc.tau_smem, st>>>(d_ctx);
+        k7_fn<K, PR>(lc.k7_wide, lc.log)<<<1, lc.k7_threads, lc.tau_smem, st>>>(d_ctx);
         CK(cudaGetLastError());
         tm.end();
         launches++;

@@ -89,7 +89,15 @@ struct Model {
 
 // Reading R6 evaluated exactly as written: d = x - x_min, q = d / r, t = q * beta,
 // every op binary64 round-to-nearest-even, i = floor(t) + 1.
-__device__ __noinline__ u32 interval_index_exact(double d, double r, double betad) {
+#ifndef PCF_EXACT_INLINE
+#define PCF_EXACT_INLINE 0
+#endif
+#if PCF_EXACT_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+u32 interval_index_exact(double d, double r, double betad) {
     const double q = __ddiv_rn(d, r);
     const double t = __dmul_rn(q, betad);
     return __double2uint_rz(t) + 1u;   // t in [0, beta]  (R6: no clamp needed)

@@ -228,6 +228,15 @@ __device__ __forceinline__ ulonglong2 ld_stream2(const ulonglong2 *p) {
 #ifndef PCF_K7_NSMAX
 #define PCF_K7_NSMAX 512   // small-list wait: largest back-off (ns; longer sleeps delay the task end)
 #endif
+#ifndef PCF_K7_LEAFB
+#define PCF_K7_LEAFB 1     // leaf sort: positions per thread whose loads are batched (2, 4: more spills, slower)
+#endif
+#ifndef PCF_K7_RELOAD
+#define PCF_K7_RELOAD 1    // re-read the node's keys before placement instead of keeping them live
+#endif
+#ifndef PCF_K7_RELOAD2
+#define PCF_K7_RELOAD2 0   // also re-read the keys before classify (not kept live through sampling and fit)
+#endif
 #ifndef PCF_K7_NPROF
 #define PCF_K7_NPROF 0     // per-phase cycles of team nodes (profiling builds only)
 #endif

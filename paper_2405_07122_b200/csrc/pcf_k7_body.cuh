@@ -210,7 +210,7 @@ __device__ __forceinline__ void classify_slots(const u64 (&key)[KPT], u32 (&pk)[
     }
 }
 
-template <class K, int NW, int MODE, bool PR>
+template <class K, int NW, int MODE, bool PR, bool LOG>
 __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos, u32 m, u32 L, u32 rel, u64 gbase,
                           const u64 *raw = nullptr) {   // MODE_GLOBAL: raw keys (bulk-copied task) instead of A
     constexpr u32 NT = NW * 32;
@@ -230,7 +230,7 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
     u16 *T16 = S.T16 + w0 * WCOLS;
     u16 *hc = S.hcol + w0 * WCOLS;
     u32 *bl = S.bl + w0 * BL_W;
-    const bool logging = c->rec != nullptr;
+    constexpr bool logging = LOG;   // pass log on (c->rec != NULL): a separate kernel instance
     const u32 tau = c->tau;
     // PCF_K7_NPROF builds: cycles of each phase of the 4-warp team nodes (thread 0 of the
     // team; slots 3, 14, 15, 20-23: minmax, samples, fit, classify, columns, placement, leaves)
@@ -353,6 +353,15 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         G.bar();
         nmark(15);
         // ---- classify (i(x) -> T) and count per (warp, column); unstable rank
+#if PCF_K7_RELOAD2
+        // the keys were dead through sampling and the fit: re-read them (X is unchanged until placement)
+#pragma unroll
+        for (int q = 0; q < KPT; ++q) {
+            const u32 f = f0 + q * 32 + lane;
+            key[q] = X[pos + (f < f1 ? f : 0u)];
+            pk[q] = f < f1 ? 0u : NONE;
+        }
+#endif
         classify_slots<K>(key, pk, md);
 #pragma unroll
         for (int q = 0; q < KPT; ++q) {
@@ -474,6 +483,16 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
             if (lane == 0) { atomicAdd(&S.dh[w0], dh); atomicAdd(&S.ncnt[w0], ncc); }
         }
     }
+#if PCF_K7_RELOAD
+    // the keys are dead from classify to placement: re-read them (still intact: nothing is
+    // written before the barrier below) instead of holding 2 x KPT registers across the column pass
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+        const u32 f = f0 + q * 32 + lane;
+        const u32 ff = f < f1 ? f : 0u;
+        key[q] = (MODE == MODE_GLOBAL && raw) ? K::to_okey(raw[ff]) : X[pos + ff];
+    }
+#endif
     G.bar();
     nmark(21);
 
@@ -521,17 +540,31 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
     }
 
     // ---- Standard-Sort of the leaves: <= SMALL_MAX keys key-parallel, larger ones by bitonic networks
-    for (u32 p = t; p < m; p += NT) {
-        const u32 cc = S.LC[pos + p];
-        if (!cc) continue;
-        const u32 hh = hc[cc];
-        if (hh > SMALL_MAX) continue;
-        const u32 st = pos + ((u32)Wg[cc] & POS_MASK);
-        const u64 v = S.B[pos + p];
-        const u32 r = st + rank_in_leaf<PR>(S.B, st, hh, v, tie_of<PR>(S.IB, pos + p), S.IB);
-        PCF_CHECK(c, r >= st && r < st + hh && st + hh <= pos + m);
-        S.A[r] = v;
-        if (PR) S.IA[r] = S.IB[pos + p];
+    // (a thread's positions p = t + q NT, q < KPT, in batches of LB: the dependent shared-memory
+    // loads of a batch -- leaf column, its size and start, the key -- are issued together)
+    constexpr int LB = PCF_K7_LEAFB;
+    for (int q0 = 0; q0 < KPT; q0 += LB) {
+        if (t + (u32)q0 * NT >= m) break;
+        u32 lc[LB], lh[LB], ls[LB];
+        u64 lv[LB];
+#pragma unroll
+        for (int q = 0; q < LB; ++q) { const u32 p = t + (u32)(q0 + q) * NT; lc[q] = p < m ? (u32)S.LC[pos + p] : 0u; }
+#pragma unroll
+        for (int q = 0; q < LB; ++q) {
+            const u32 p = t + (u32)(q0 + q) * NT;
+            lh[q] = lc[q] ? (u32)hc[lc[q]] : 0u;
+            ls[q] = pos + ((u32)Wg[lc[q]] & POS_MASK);
+            lv[q] = S.B[pos + (p < m ? p : 0u)];
+        }
+#pragma unroll
+        for (int q = 0; q < LB; ++q) {
+            const u32 p = t + (u32)(q0 + q) * NT;
+            if (!lc[q] || lh[q] > SMALL_MAX) continue;
+            const u32 r = ls[q] + rank_in_leaf<PR>(S.B, ls[q], lh[q], lv[q], tie_of<PR>(S.IB, pos + p), S.IB);
+            PCF_CHECK(c, r >= ls[q] && r < ls[q] + lh[q] && ls[q] + lh[q] <= pos + m);
+            S.A[r] = lv[q];
+            if (PR) S.IA[r] = S.IB[pos + p];
+        }
     }
     const u32 nb = S.nbl[w0];
     for (u32 i = 0; i < nb; ++i) {
@@ -653,7 +686,7 @@ __device__ __forceinline__ void push_root(const DevCtx *c, K7Smem &S, u32 e) {
 
 // One team tier: every set of NW warps claims nodes of (lo, hi] keys from the
 // task's big list and runs them until none is left.
-template <class K, int NW, bool PR>
+template <class K, int NW, bool PR, bool LOG>
 __device__ __forceinline__ void run_tier(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 *ctr, u32 *cur, u32 lo, u32 hi,
                                          u32 Lb, u64 gb, bool wprof, unsigned long long &wc) {
     for (;;) {
@@ -676,12 +709,12 @@ __device__ __forceinline__ void run_tier(const DevCtx *c, K7Smem &S, const Grp<N
         const u32 e = cur[G.w0];
         if (!e) break;
         const long long t0 = wprof ? clock64() : 0;
-        node_step<K, NW, MODE_NODE, PR>(c, S, G, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), gb);
+        node_step<K, NW, MODE_NODE, PR, LOG>(c, S, G, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), gb);
         if (wprof) wc += clock64() - t0;
     }
 }
 
-template <class K, bool PR>
+template <class K, bool PR, bool LOG>
 __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kernel(const DevCtx *__restrict__ c) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char k7_smem_raw[];
@@ -732,9 +765,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
         prof_mark(c, S, 0);
         u32 nclaim = 0;
         if (threadIdx.x == 0) nclaim = begin + atomicAdd(c->k7_next, 1u);   // used when this task is done
-        const K7Task task = S.task;
-        u64 *gout = c->buf[2] + task.off;
-        const u32 M = task.size;
+        const K7Task task = S.task;   // (task / M / offsets are re-read from S.task where they are used
+        const u32 M = task.size;      //  after the node phase: fewer registers live across it)
         // pad != 0: a K7_SORT chunk of equal keys (Standard-Sort split of one key value): copied
         const bool presorted = task.kind == K7_SORT && task.pad != 0;
         const bool sort_task = !presorted && (task.kind == K7_SORT || (task.kind == K7_NODE && M < c->tau));
@@ -787,7 +819,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
                 }
                 __syncthreads();
                 Lb = S.glevel;
-                node_step<K, K7_WARPS, MODE_GLOBAL, PR>(c, S, CT, 0, M, Lb, 0, c->gbase + task.off, raw_group ? S.B + S.lhead : nullptr);
+                node_step<K, K7_WARPS, MODE_GLOBAL, PR, LOG>(c, S, CT, 0, M, Lb, 0, c->gbase + task.off, raw_group ? S.B + S.lhead : nullptr);
                 prof_mark(c, S, 2);
             } else {   // K7_NODE: a fresh Learned-Sort call on the whole task
                 Lb = task.level;
@@ -800,17 +832,17 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
                 if (ent_m(e) > CTA_MIN) {
                     __syncthreads();
                     if (threadIdx.x == 0) S.lbig[i] = 0;
-                    node_step<K, K7_WARPS, MODE_NODE, PR>(c, S, CT, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), c->gbase + task.off);
+                    node_step<K, K7_WARPS, MODE_NODE, PR, LOG>(c, S, CT, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), c->gbase + S.task.off);
                 }
             }
-            const u64 gb = c->gbase + task.off;
+            const u64 gb = c->gbase + S.task.off;
             // quad teams (1024-thread builds): (2 GCAP, 4 GCAP]; double teams: (GCAP, 2 GCAP]
-            if constexpr (QUAD) run_tier<K, 4 * GW, PR>(c, S, GQ, &S.bnext4, S.cur4, 2u * GCAP, 4u * GCAP, Lb, gb, wprof, wcyc[0]);
-            run_tier<K, 2 * GW, PR>(c, S, GH, &S.bnext2, S.cur2, (u32)GCAP, 2u * GCAP, Lb, gb, wprof, wcyc[0]);
+            if constexpr (QUAD) run_tier<K, 4 * GW, PR, LOG>(c, S, GQ, &S.bnext4, S.cur4, 2u * GCAP, 4u * GCAP, Lb, gb, wprof, wcyc[0]);
+            run_tier<K, 2 * GW, PR, LOG>(c, S, GH, &S.bnext2, S.cur2, (u32)GCAP, 2u * GCAP, Lb, gb, wprof, wcyc[0]);
             prof_mark(c, S, 4);
             // teams of GW warps take the nodes of (WCAP, GCAP] keys (their children go to the small
             // list); then every warp runs small nodes and their whole subtrees on its own
-            run_tier<K, GW, PR>(c, S, GG, &S.bnext, S.cur, (u32)WCAP, (u32)GCAP, Lb, gb, wprof, wcyc[1]);
+            run_tier<K, GW, PR, LOG>(c, S, GG, &S.bnext, S.cur, (u32)WCAP, (u32)GCAP, Lb, gb, wprof, wcyc[1]);
             if (GG.t == 0) { __threadfence_block(); atomicSub(&S.big_active, 1u); }
             if (lane == 0) S.top[w] = 0;
             __syncwarp();
@@ -842,7 +874,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
                 const long long t0 = wprof ? clock64() : 0;
                 if (wprof) wcyc[3] += t0 - tw;
                 if (!e) break;
-                node_step<K, 1, MODE_NODE, PR>(c, S, GS, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), c->gbase + task.off);
+                node_step<K, 1, MODE_NODE, PR, LOG>(c, S, GS, ent_pos(e), ent_m(e), Lb + ent_rel(e), ent_rel(e), c->gbase + S.task.off);
                 if (wprof) wcyc[2] += clock64() - t0;
             }
             __syncthreads();
@@ -852,8 +884,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
             S.nidx = nclaim;
             if (nclaim < ntasks) { S.ntask = c->k7[c->k7_order ? c->k7_order[nclaim] : nclaim]; k7_issue(c, S, S.ntask); }
         }
-        store_task_idx<PR>(c, S, task, M);
-        store_task<K>(S, gout, M);
+        store_task_idx<PR>(c, S, S.task, S.task.size);
+        store_task<K>(S, c->buf[2] + S.task.off, S.task.size);
         prof_mark(c, S, 13);
         __syncthreads();
     }
