@@ -260,6 +260,9 @@ static int configure_kernels() {
 }
 
 // ---------------------------------------------------------------- launch helpers
+#ifndef PCF_TAIL_CTAS_PER_SM
+#define PCF_TAIL_CTAS_PER_SM 32   // grid bound of the tail graph's per-tile kernels (CTAs per SM)
+#endif
 struct Launch {   // the kernel-launch configuration of this device and sort size
     int nsm;
     int k7_grid;
@@ -268,7 +271,7 @@ struct Launch {   // the kernel-launch configuration of this device and sort siz
     bool log;         // pass log on: the logging K7 instance
     int count_grid;
     int tau_smem;
-    u32 tile_grid;    // one CTA per split tile of a round (upper bound; idle CTAs exit)
+    u32 tile_grid;    // tail graph: CTAs of the per-tile kernels (grid-stride over the round's tiles; idle CTAs exit)
 };
 
 // ---------------------------------------------------------------- device-driven tail (CUDA graph)
@@ -603,7 +606,9 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
     lc.count_grid = nsm * count_ctas_per_sm<K>();
     lc.tau_smem = k7_smem_bytes(p.tau, PR);
     // fallback segments hold > S_CAP keys each: <= n / S_CAP partial tiles
-    lc.tile_grid = (u32)std::min<u64>(n / SPLIT_TILE + 4096, 0x7fffffffull);
+    // (the tail graph's count / scatter kernels are grid-stride: a bounded grid keeps the cost of
+    // an almost empty batch -- c5f's few wide tail groups -- away from n / SPLIT_TILE idle CTAs)
+    lc.tile_grid = (u32)std::min<u64>(n / SPLIT_TILE + 4096, (u64)nsm * PCF_TAIL_CTAS_PER_SM);
 
     // initial counters (host-built: the root node and its tables are carved here)
     Counters h0;

@@ -74,6 +74,10 @@ struct K7Smem {
     const u32 *gT;
     u32 *gH;
     u32 gdelta, glevel, gjlo, gjhi;
+    Model ngmd;                   // the same for the claimed next task (K7_GROUP), fetched with the claim
+    const u32 *ngT;
+    u32 *ngH;
+    u32 ngdelta, nglevel;
     long long prof_t;                       // PCF_FLAG_PROFILE bookkeeping (thread 0)
     unsigned long long prof[K7_PROF_SLOTS];
     u16 *IA, *IB;                 // key-value mode (PR): task-local source index of every position
@@ -493,6 +497,8 @@ __device__ void node_step(const DevCtx *c, K7Smem &S, const Grp<NW> &G, u32 pos,
         key[q] = (MODE == MODE_GLOBAL && raw) ? K::to_okey(raw[ff]) : X[pos + ff];
     }
 #endif
+    // the K7_GROUP placement is the task's first write to A: the previous task's bulk store has read it
+    if (PCF_K7_BULKST && !PR && MODE == MODE_GLOBAL && threadIdx.x == 0) bulk_wait_read();
     G.bar();
     nmark(21);
 
@@ -653,6 +659,35 @@ __device__ __forceinline__ void store_task(const K7Smem &S, u64 *dst, u32 m) {
     if (m > head && ((m - head) & 1) && threadIdx.x == 0) dst[m - 1] = K::from_okey(S.A[m - 1]);
 }
 
+// The same by one bulk copy (PCF_K7_BULKST, keys-only): A is converted to raw keys in place --
+// shifted down by one key when dst is not 16-byte aligned, so that the shared and the global
+// address of the copied body are both aligned; the odd first / last key is stored directly --
+// and thread 0 issues the copy, which runs while the CTA starts its next task.  A must not be
+// written before thread 0 has waited for the copy's reads (bulk_wait_read) and a barrier.
+template <class K>
+__device__ __forceinline__ void store_task_bulk(K7Smem &S, u64 *dst, u32 m) {
+    const u32 sh = ((uintptr_t)dst & 15) ? 1u : 0u;
+    u64 r[KPT];
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+        const u32 i = threadIdx.x + q * K7_THREADS;
+        r[q] = i < m ? K::from_okey(S.A[i]) : 0ull;
+    }
+    const u32 body = (m - min(sh, m)) & ~1u;   // keys [sh, sh + body) go by the bulk copy
+    if (sh) __syncthreads();                    // in-place shift: every key is read before any is written
+#pragma unroll
+    for (int q = 0; q < KPT; ++q) {
+        const u32 i = threadIdx.x + q * K7_THREADS;
+        if (i < m) {
+            if (i < sh || i >= sh + body) dst[i] = r[q];
+            else S.A[i - sh] = r[q];
+        }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0 && body) bulk_s2g(dst + sh, S.A, body * 8u);
+}
+
 // ------------------------------------------------------------------ the kernel
 // Bulk copy of the raw keys of task t into B (issued while the previous task
 // is stored).  The copy covers the 16-byte aligned superset of the task; a task
@@ -670,6 +705,16 @@ __device__ __forceinline__ void k7_issue(const DevCtx *c, K7Smem &S, const K7Tas
         fence_proxy_async();
         mbar_arrive_tx(&S.tbar, (u32)(a1 - a0));
         bulk_g2s(S.B, (const void *)a0, (u32)(a1 - a0), &S.tbar);
+    }
+}
+
+// Thread 0, with the claim of the next task: the global node's model and tables of a K7_GROUP task
+// (read by its placement), so that the task does not start with a chain of global loads.
+__device__ __forceinline__ void k7_fetch_node(const DevCtx *c, K7Smem &S) {
+    if (S.ntask.kind == K7_GROUP) {
+        const GNode &gn = c->nodes[S.ntask.node];
+        S.ngmd = gn.md; S.ngT = gn.T; S.ngH = gn.H;
+        S.ngdelta = gn.delta; S.nglevel = gn.level;
     }
 }
 
@@ -720,6 +765,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
     extern __shared__ __align__(16) unsigned char k7_smem_raw[];
     K7Smem &S = *reinterpret_cast<K7Smem *>(k7_smem_raw);
     if (*c->nan_flag) return;
+    constexpr bool BULKST = PCF_K7_BULKST && !PR;   // the finished task leaves by an asynchronous bulk copy
     const u32 ntasks = *c->k7_count;
     const u32 begin = *c->k7_begin;
     const u32 w = warp_id(), lane = lane_id();
@@ -746,7 +792,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
         mbar_init(&S.tbar, 1);
         mbar_init_fence();
         S.nidx = begin + atomicAdd(c->k7_next, 1u);
-        if (S.nidx < ntasks) { S.ntask = c->k7[c->k7_order ? c->k7_order[S.nidx] : S.nidx]; k7_issue(c, S, S.ntask); }
+        if (S.nidx < ntasks) { S.ntask = c->k7[c->k7_order ? c->k7_order[S.nidx] : S.nidx]; k7_issue(c, S, S.ntask); k7_fetch_node(c, S); }
     }
     __syncthreads();
 #ifndef PCF_K7_WPROF
@@ -758,6 +804,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
         if (threadIdx.x == 0) {
             S.task_idx = S.nidx;
             S.task = S.ntask;
+            S.gmd = S.ngmd; S.gT = S.ngT; S.gH = S.ngH; S.gdelta = S.ngdelta; S.glevel = S.nglevel;
+            S.gjlo = S.ntask.jlo; S.gjhi = S.ntask.jhi;
             S.stot = 0; S.snext = 0; S.btot = 0; S.bnext = 0; S.bnext2 = 0; S.bnext4 = 0; S.big_active = NGRP;
         }
         __syncthreads();
@@ -775,6 +823,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
         mbar_wait(&S.tbar, it & 1u);
         // a K7_GROUP task's placement reads the raw bulk-copied keys itself (no pass over B)
         const bool raw_group = task.kind == K7_GROUP && !S.ldirect;
+        if (BULKST && !raw_group) {   // A is written next: the previous task's bulk store must have read it
+            if (threadIdx.x == 0) bulk_wait_read();
+            __syncthreads();
+        }
         if (raw_group) {
         } else if (S.ldirect) {
             nan_here = load_task<K, PR>(dst, sort_task ? S.IB : S.IA, c->buf[task.src] + task.off, M);
@@ -797,11 +849,14 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
                 }
             }
         }
-        if (K::is_f64 && task.level == 1 && __syncthreads_or(nan_here)) {
-            if (threadIdx.x == 0) atomicOr(c->nan_flag, 1u);
-            return;
+        if (K::is_f64 && task.level == 1) {   // (uniform) the NaN vote is this point's barrier
+            if (__syncthreads_or(nan_here)) {
+                if (threadIdx.x == 0) { atomicOr(c->nan_flag, 1u); if (BULKST) bulk_wait_all(); }
+                return;
+            }
+        } else {
+            __syncthreads();
         }
-        __syncthreads();
         prof_mark(c, S, 1);
         if (threadIdx.x == 0 && c->k7_prof) { S.prof[11] += 1; S.prof[12] += M; }
         if (presorted) {
@@ -812,12 +867,6 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
         } else {
             u32 Lb;
             if (task.kind == K7_GROUP) {   // finish the global node's placement for buckets [jlo, jhi)
-                if (threadIdx.x == 0) {
-                    const GNode &gn = c->nodes[task.node];
-                    S.gmd = gn.md; S.gT = gn.T; S.gH = gn.H;
-                    S.gdelta = gn.delta; S.glevel = gn.level; S.gjlo = task.jlo; S.gjhi = task.jhi;
-                }
-                __syncthreads();
                 Lb = S.glevel;
                 node_step<K, K7_WARPS, MODE_GLOBAL, PR, LOG>(c, S, CT, 0, M, Lb, 0, c->gbase + task.off, raw_group ? S.B + S.lhead : nullptr);
                 prof_mark(c, S, 2);
@@ -882,13 +931,18 @@ __global__ void __launch_bounds__(K7_THREADS, K7_THREADS >= 512 ? 1 : 2) k7_kern
         }
         if (threadIdx.x == 0) {   // B is free: the next task streams in while this one is stored
             S.nidx = nclaim;
-            if (nclaim < ntasks) { S.ntask = c->k7[c->k7_order ? c->k7_order[nclaim] : nclaim]; k7_issue(c, S, S.ntask); }
+            if (nclaim < ntasks) { S.ntask = c->k7[c->k7_order ? c->k7_order[nclaim] : nclaim]; k7_issue(c, S, S.ntask); k7_fetch_node(c, S); }
         }
-        store_task_idx<PR>(c, S, S.task, S.task.size);
-        store_task<K>(S, c->buf[2] + S.task.off, S.task.size);
+        if (BULKST) {
+            store_task_bulk<K>(S, c->buf[2] + S.task.off, S.task.size);
+        } else {
+            store_task_idx<PR>(c, S, S.task, S.task.size);
+            store_task<K>(S, c->buf[2] + S.task.off, S.task.size);
+        }
         prof_mark(c, S, 13);
         __syncthreads();
     }
+    if (BULKST && threadIdx.x == 0) bulk_wait_all();
     if (PCF_K7_WPROF) {
         if (wprof)
             for (int i = 0; i < 4; ++i) atomicAdd(&S.prof[16 + i], wcyc[i]);
