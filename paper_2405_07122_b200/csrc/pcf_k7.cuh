@@ -238,7 +238,7 @@ __device__ __forceinline__ ulonglong2 ld_stream2(const ulonglong2 *p) {
 #define PCF_K7_RELOAD2 0   // also re-read the keys before classify (not kept live through sampling and fit)
 #endif
 #ifndef PCF_K7_BULKST
-#define PCF_K7_BULKST 0    // keys-only: store the finished task by one asynchronous bulk copy (overlaps the next task)
+#define PCF_K7_BULKST 1    // keys-only: store the finished task by one asynchronous bulk copy (overlaps the next task)
 #endif
 #ifndef PCF_K7_NPROF
 #define PCF_K7_NPROF 0     // per-phase cycles of team nodes (profiling builds only)
