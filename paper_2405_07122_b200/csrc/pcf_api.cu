@@ -83,7 +83,7 @@ static Caps caps_for(u64 n, u64 root_n = 0) {
 
 struct Layout {
     size_t ctx, counters, tmp, tidx, digs, tmap, k7_order, bpre_mm, bpre_fs, nodes, arena, k7, splits_a, splits_b, items, fb,
-        cmat, pmat, bsum, status, total;
+        cmat, pmat, bsum, scan_status, status, total;
 };
 
 static Layout layout_for(const Caps &c, bool pr = false) {   // (caps_for(n, root_n))
@@ -109,6 +109,7 @@ static Layout layout_for(const Caps &c, bool pr = false) {   // (caps_for(n, roo
     L.cmat = take(c.cmat_cap * 4);
     L.pmat = take(c.cmat_cap * 4);
     L.bsum = take(c.bsum_cap * 4);
+    L.scan_status = take(c.bsum_cap * 8);
     L.total = off;
     return L;
 }
@@ -260,6 +261,9 @@ static int configure_kernels() {
 }
 
 // ---------------------------------------------------------------- launch helpers
+#ifndef PCF_SCAN_LOOKBACK
+#define PCF_SCAN_LOOKBACK 0   // count-matrix scan: one decoupled look-back kernel instead of partials / block sums / final
+#endif
 #ifndef PCF_TAIL_CTAS_PER_SM
 #define PCF_TAIL_CTAS_PER_SM 32   // grid bound of the tail graph's per-tile kernels (CTAs per SM)
 #endif
@@ -307,9 +311,14 @@ static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32
     CK(launch_pdl(k_tile_map, lc.nsm * 2, 256, 0, cs, d_ctx));
     CK(launch_pdl(k_split_count_tile<K>, lc.tile_grid, SC_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_split_count_radix<K>, lc.nsm * 8, SC_THREADS, 0, cs, d_ctx));   // Standard-Sort splits
+#if PCF_SCAN_LOOKBACK
+    CK(launch_pdl(k_scanp_lookback, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
+    *nk -= 2;
+#else
     CK(launch_pdl(k_scanp_partials, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_scanp_final, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
+#endif
     CK(launch_pdl(k_split_scatter<K, PR>, lc.tile_grid, SC_THREADS, split_smem_bytes(), cs, d_ctx));
     CK(launch_pdl(k_split_taskgen, lc.nsm * 2, TG_THREADS, 0, cs, d_ctx));
     *nk += 9;
@@ -573,6 +582,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
         hc.cmat = (u32 *)(ws + L.cmat);
         hc.pmat = (u32 *)(ws + L.pmat);
         hc.bsum = (u32 *)(ws + L.bsum);
+        hc.scan_status = (unsigned long long *)(ws + L.scan_status);
         hc.cmat_cap = caps.cmat_cap;
         hc.digs = (u16 *)(ws + L.digs);
         hc.tmap = (u32 *)(ws + L.tmap);
@@ -719,9 +729,13 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             else CK(launch_pdl(k_split_count<K>, lc.count_grid, CNT_THREADS, sizeof(CountSmem), st, dc));
             tm.end();
             tm.begin(PH_OTHER);
+#if PCF_SCAN_LOOKBACK
+            CK(launch_pdl(k_scanp_lookback, nsm * 2, SCAN_THREADS, 0, st, dc));
+#else
             CK(launch_pdl(k_scanp_partials, nsm * 2, SCAN_THREADS, 0, st, dc));
             CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, st, dc));
             CK(launch_pdl(k_scanp_final, nsm * 2, SCAN_THREADS, 0, st, dc));
+#endif
             tm.end();
             tm.begin(PH_SCATTER);
             CK(launch_pdl(k_split_scatter<K, PR>, tile_grid, SC_THREADS, split_smem_bytes(), st, dc));
@@ -729,7 +743,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             tm.begin(PH_OTHER);
             CK(launch_pdl(k_split_taskgen, nsm * 2, TG_THREADS, 0, st, dc));
             tm.end();
-            launches += 8;
+            launches += PCF_SCAN_LOOKBACK ? 6 : 8;
         }
         // K7 over every group produced so far (persistent grid; reads the task count on the device)
         tm.begin(PH_K7);

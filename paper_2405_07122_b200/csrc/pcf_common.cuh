@@ -290,8 +290,8 @@ struct RoundPlan {
     u32 ns;        // splits processed this round
     u32 tiles;     // total tiles
     u32 nblk;      // scan blocks over the count matrix
-    u32 next_count;   // dynamic tile claims of k_split_count
-    u32 next_scatter; // dynamic tile claims of k_split_scatter
+    u32 next_scan;    // block tickets of the count-matrix scan (k_scanp_lookback)
+    u32 pad_;
     u32 cur;       // split list this round consumes (splits[cur]); the next round's is cur ^ 1
     u64 ctot;      // count-matrix entries
     u64 mtot;      // keys moved
@@ -348,6 +348,7 @@ struct DevCtx {
     u32 splits_cap;
     struct RoundPlan *plan;
     u32 *cmat, *pmat, *bsum;
+    unsigned long long *scan_status;   // per scan block: flag << 32 | value (k_scanp_lookback; zeroed by k_round_plan)
     u64 cmat_cap;
     unsigned long long *split_keys;   // keys moved by split passes (byte accounting)
     unsigned long long *k7_prof;      // PCF_FLAG_PROFILE: K7 cycles per phase (NULL = off)

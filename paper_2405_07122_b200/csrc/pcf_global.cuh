@@ -876,6 +876,67 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_final(const DevCtx *__re
     }
 }
 
+// The same scan in one kernel (decoupled look-back): CTAs take block tickets in order; a block
+// publishes its aggregate (flag 1), sums its predecessors' aggregates back to the nearest
+// inclusive prefix (flag 2), publishes its own inclusive prefix and writes its slice of the
+// scanned matrix: one read and one write of the matrix instead of two reads and a write, one
+// launch instead of three.  A ticket's predecessors are held by CTAs that are already running,
+// so the waits always end.  Status words (flag << 32 | value, one 8-byte store) are zeroed and
+// the ticket counter reset by k_round_plan.
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_status(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__global__ void __launch_bounds__(SCAN_THREADS) k_scanp_lookback(const DevCtx *__restrict__ c) {
+    pdl_entry();
+    __shared__ u32 wsum[33];
+    __shared__ u32 s_b, s_pref;
+    const RoundPlan pl = *c->plan;
+    unsigned long long *st = c->scan_status;
+    const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (;;) {
+        if (threadIdx.x == 0) s_b = atomicAdd(&c->plan->next_scan, 1u);
+        __syncthreads();
+        const u32 b = s_b;
+        if (b >= pl.nblk) break;
+        const u64 base = (u64)b * SCAN_CHUNK + (u64)threadIdx.x * SCAN_ITEMS;
+        u32 v[SCAN_ITEMS];
+        u32 sum = 0;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) { v[k] = base + k < pl.ctot ? c->cmat[base + k] : 0; sum += v[k]; }
+        u32 total;
+        u32 e = block_excl_scan_1024(sum, wsum, total);   // (ends with a barrier: s_b may be rewritten after it)
+        if (w == 0) {
+            u32 acc = 0;
+            if (b > 0) {
+                if (lane == 0) st_status(&st[b], (1ull << 32) | total);
+                for (long long j = (long long)b - 1;; j -= 32) {   // windows of 32 predecessors, nearest first
+                    const long long idx = j - lane;
+                    unsigned long long x = idx >= 0 ? ld_status(&st[idx]) : (2ull << 32);
+                    while (__any_sync(0xffffffffu, (x >> 32) == 0)) {
+                        if ((x >> 32) == 0) x = ld_status(&st[idx]);
+                    }
+                    const u32 pm = __ballot_sync(0xffffffffu, (x >> 32) == 2);
+                    const u32 first = pm ? (u32)__ffs(pm) - 1u : 31u;
+                    u32 val = lane <= first ? (u32)x : 0u;
+                    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                    acc += val;
+                    if (pm) break;
+                }
+            }
+            if (lane == 0) { st_status(&st[b], (2ull << 32) | (u32)(acc + total)); s_pref = acc; }
+        }
+        __syncthreads();
+        e += s_pref;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) { if (base + k < pl.ctot) c->pmat[base + k] = e; e += v[k]; }
+    }
+}
+
 // Plan split round `cur`: tiles, count-matrix offsets and key offsets of every
 // split (one CTA).  Splits that do not fit the count matrix are carried over to
 // the next round's list; the next list's counter is reset here.
@@ -950,12 +1011,16 @@ __global__ void __launch_bounds__(1024) k_round_plan(const DevCtx *__restrict__ 
             pl.ctot = lst.cbase + (u64)lst.ntiles * lst.G; pl.mtot = lst.mbase + lst.m;
         }
         pl.nblk = (u32)((pl.ctot + SCAN_CHUNK - 1) / SCAN_CHUNK);
-        pl.next_count = 0; pl.next_scatter = 0;
+        pl.next_scan = 0; pl.pad_ = 0;
         pl.cur = cur;
         *c->plan = pl;
         atomicAdd(c->split_keys, (unsigned long long)pl.mtot);
         c->cnt->round += 1;   // every reader of this round takes cur from the plan
+        cut_s = pl.nblk;
     }
+    __syncthreads();
+    // status words of the round's scan blocks (k_scanp_lookback): none published yet
+    for (u32 i = threadIdx.x, nb = cut_s; i < nb; i += 1024) c->scan_status[i] = 0ull;
 }
 
 // b[i] = inclusive prefix of cnt[1..beta+1] (exclusive block offsets from the
