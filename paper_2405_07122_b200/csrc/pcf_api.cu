@@ -262,7 +262,7 @@ static int configure_kernels() {
 
 // ---------------------------------------------------------------- launch helpers
 #ifndef PCF_SCAN_LOOKBACK
-#define PCF_SCAN_LOOKBACK 0   // count-matrix scan: one decoupled look-back kernel instead of partials / block sums / final
+#define PCF_SCAN_LOOKBACK 2   // count-matrix scan by one decoupled look-back kernel: 0 never, 1 always, 2 sorts of n <= 2^25
 #endif
 #ifndef PCF_TAIL_CTAS_PER_SM
 #define PCF_TAIL_CTAS_PER_SM 32   // grid bound of the tail graph's per-tile kernels (CTAs per SM)
@@ -311,7 +311,7 @@ static int add_round(cudaStream_t cs, const DevCtx *d_ctx, const Launch &lc, u32
     CK(launch_pdl(k_tile_map, lc.nsm * 2, 256, 0, cs, d_ctx));
     CK(launch_pdl(k_split_count_tile<K>, lc.tile_grid, SC_THREADS, 0, cs, d_ctx));
     CK(launch_pdl(k_split_count_radix<K>, lc.nsm * 8, SC_THREADS, 0, cs, d_ctx));   // Standard-Sort splits
-#if PCF_SCAN_LOOKBACK
+#if PCF_SCAN_LOOKBACK == 1
     CK(launch_pdl(k_scanp_lookback, lc.nsm * 2, SCAN_THREADS, 0, cs, d_ctx));
     *nk -= 2;
 #else
@@ -729,13 +729,17 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             else CK(launch_pdl(k_split_count<K>, lc.count_grid, CNT_THREADS, sizeof(CountSmem), st, dc));
             tm.end();
             tm.begin(PH_OTHER);
-#if PCF_SCAN_LOOKBACK
-            CK(launch_pdl(k_scanp_lookback, nsm * 2, SCAN_THREADS, 0, st, dc));
-#else
-            CK(launch_pdl(k_scanp_partials, nsm * 2, SCAN_THREADS, 0, st, dc));
-            CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, st, dc));
-            CK(launch_pdl(k_scanp_final, nsm * 2, SCAN_THREADS, 0, st, dc));
-#endif
+            // the count-matrix scan (a6): one decoupled look-back kernel for small sorts (two launches
+            // less per round); for large matrices the three-phase scan is faster (ab_scan_lookback.txt)
+            const bool lookback = PCF_SCAN_LOOKBACK == 1 || (PCF_SCAN_LOOKBACK == 2 && n <= (1ull << 25));
+            if (lookback) {
+                CK(launch_pdl(k_scanp_lookback, nsm * 2, SCAN_THREADS, 0, st, dc));
+                launches -= 2;
+            } else {
+                CK(launch_pdl(k_scanp_partials, nsm * 2, SCAN_THREADS, 0, st, dc));
+                CK(launch_pdl(k_scanp_bsums, 1, SCAN_THREADS, 0, st, dc));
+                CK(launch_pdl(k_scanp_final, nsm * 2, SCAN_THREADS, 0, st, dc));
+            }
             tm.end();
             tm.begin(PH_SCATTER);
             CK(launch_pdl(k_split_scatter<K, PR>, tile_grid, SC_THREADS, split_smem_bytes(), st, dc));
@@ -743,7 +747,7 @@ static int sort_device(const u64 *in, u64 *out, size_t n, const pcf_params *pp, 
             tm.begin(PH_OTHER);
             CK(launch_pdl(k_split_taskgen, nsm * 2, TG_THREADS, 0, st, dc));
             tm.end();
-            launches += PCF_SCAN_LOOKBACK ? 6 : 8;
+            launches += 8;
         }
         // K7 over every group produced so far (persistent grid; reads the task count on the device)
         tm.begin(PH_K7);

@@ -891,23 +891,41 @@ __device__ __forceinline__ unsigned long long ld_status(const unsigned long long
 __device__ __forceinline__ void st_status(unsigned long long *p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+#ifndef PCF_LB_ITEMS
+#define PCF_LB_ITEMS 16   // matrix entries per thread and block of the look-back scan (4 x 16-byte loads)
+#endif
+constexpr int LB_ITEMS = PCF_LB_ITEMS;
+constexpr int LB_CHUNK = SCAN_THREADS * LB_ITEMS;
+static_assert(LB_ITEMS % 4 == 0 && LB_CHUNK % SCAN_CHUNK == 0, "look-back blocks are whole scan chunks (status words: one per SCAN_CHUNK)");
 __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_lookback(const DevCtx *__restrict__ c) {
     pdl_entry();
     __shared__ u32 wsum[33];
     __shared__ u32 s_b, s_pref;
     const RoundPlan pl = *c->plan;
+    const u32 nblk = (u32)((pl.ctot + LB_CHUNK - 1) / LB_CHUNK);   // (<= pl.nblk status words)
     unsigned long long *st = c->scan_status;
     const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (;;) {
         if (threadIdx.x == 0) s_b = atomicAdd(&c->plan->next_scan, 1u);
         __syncthreads();
         const u32 b = s_b;
-        if (b >= pl.nblk) break;
-        const u64 base = (u64)b * SCAN_CHUNK + (u64)threadIdx.x * SCAN_ITEMS;
-        u32 v[SCAN_ITEMS];
+        if (b >= nblk) break;
+        const u64 base = (u64)b * LB_CHUNK + (u64)threadIdx.x * LB_ITEMS;
+        const bool full = base + LB_ITEMS <= pl.ctot;
+        u32 v[LB_ITEMS];
         u32 sum = 0;
+        if (full) {
 #pragma unroll
-        for (int k = 0; k < SCAN_ITEMS; ++k) { v[k] = base + k < pl.ctot ? c->cmat[base + k] : 0; sum += v[k]; }
+            for (int k = 0; k < LB_ITEMS; k += 4) {
+                const uint4 q = *reinterpret_cast<const uint4 *>(c->cmat + base + k);
+                v[k] = q.x; v[k + 1] = q.y; v[k + 2] = q.z; v[k + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < LB_ITEMS; ++k) v[k] = base + k < pl.ctot ? c->cmat[base + k] : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < LB_ITEMS; ++k) sum += v[k];
         u32 total;
         u32 e = block_excl_scan_1024(sum, wsum, total);   // (ends with a barrier: s_b may be rewritten after it)
         if (w == 0) {
@@ -932,8 +950,17 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scanp_lookback(const DevCtx *_
         }
         __syncthreads();
         e += s_pref;
+        if (full) {
 #pragma unroll
-        for (int k = 0; k < SCAN_ITEMS; ++k) { if (base + k < pl.ctot) c->pmat[base + k] = e; e += v[k]; }
+            for (int k = 0; k < LB_ITEMS; k += 4) {
+                uint4 q;
+                q.x = e; e += v[k]; q.y = e; e += v[k + 1]; q.z = e; e += v[k + 2]; q.w = e; e += v[k + 3];
+                *reinterpret_cast<uint4 *>(c->pmat + base + k) = q;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < LB_ITEMS; ++k) { if (base + k < pl.ctot) c->pmat[base + k] = e; e += v[k]; }
+        }
     }
 }
 
