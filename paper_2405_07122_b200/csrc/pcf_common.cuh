@@ -126,12 +126,29 @@ __device__ __forceinline__ double key_offset_raw(u64 raw, const Model &md) {
     if (K::is_f64) return __dsub_rn(__longlong_as_double((long long)raw), md.xmin);
     return __ull2double_rn(raw - md.umin);
 }
+#ifndef PCF_FAST_FLOOR
+#define PCF_FAST_FLOOR 0
+#endif
 __device__ __forceinline__ u32 fast_from_offset(double d, const Model &md, bool &ok) {
     const double t = __dmul_rn(d, md.s);
+#if PCF_FAST_FLOOR
+    // floor(t') without the conversion pipe (FRND / F2I): m = RN(RN(t' - 0.5) + 1.5 * 2^52) holds the
+    // integer nearest to t' - 0.5 in its low mantissa bits (0 <= t' <= beta < 2^32; t' - 0.5 is exact
+    // for t' >= 0.5, and a tiny t' fails the band test below anyway), which is floor(t') whenever
+    // frac(t') is not 0; an integer t' (a tie) gives fl = t' or t' - 1, i.e. fr = 0 or 1, and the
+    // band test sends it to the exact path like every other key within eps of a bin edge.
+    const double MAGIC = 6755399441055744.0;   // 1.5 * 2^52
+    const double m = __dadd_rn(__dadd_rn(t, -0.5), MAGIC);
+    const double fl = __dsub_rn(m, MAGIC);
+    const double fr = __dsub_rn(t, fl);
+    ok = fr >= md.eps && fr <= 1.0 - md.eps;
+    return (u32)__double2loint(m) + 1u;
+#else
     const double fl = floor(t);
     const double fr = __dsub_rn(t, fl);
     ok = fr >= md.eps && fr <= 1.0 - md.eps;
     return (u32)fl + 1u;
+#endif
 }
 // Branch-free fast path: floor(t') + 1 and whether it is certified (ok); the
 // caller takes interval_index_exact for the rare uncertified keys.
